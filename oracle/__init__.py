@@ -1,0 +1,115 @@
+"""ctypes binding of the CPU oracle (liblocc_oracle.so).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this package.  It shares no code
+with the CUDA path (paper_2304_09439_b200/); see locc_oracle.h for what it computes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "liblocc_oracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "locc_oracle.cpp")
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+            os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "locc_oracle.h"))):
+        subprocess.check_call(["make", "-s", "-C", _HERE, "liblocc_oracle.so"])
+    return _LIB
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("M", C.c_int32), ("H", C.c_int32), ("F", C.c_int32), ("bf16_emul", C.c_int32),
+                ("n_threads", C.c_int32)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(_LIB)
+        vp = C.c_void_p
+        L.oracle_shape_prep.argtypes = [vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
+        L.oracle_rel_transform.argtypes = [vp] * 6
+        L.oracle_query.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, C.c_int32, C.c_int32, vp, vp,
+                                   C.c_int64] + [vp] * 7
+        L.oracle_load_weights.argtypes = [C.c_char_p, vp, C.c_size_t, vp, vp, vp]
+        L.oracle_load_weights.restype = C.c_int64
+        L.oracle_n_params.argtypes = [C.c_int32, C.c_int32]
+        L.oracle_n_params.restype = C.c_int64
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def n_params(H=256, F=64):
+    return int(lib().oracle_n_params(H, F))
+
+
+def shape_prep(points_k3, M=6):
+    """O0 for one shape -> (lo[3], hi[3], eps2, cell[K])."""
+    p = np.ascontiguousarray(points_k3, np.float32)
+    K = p.shape[0]
+    lo = np.zeros(3, np.float32)
+    hi = np.zeros(3, np.float32)
+    e2 = np.zeros(1, np.float32)
+    cell = np.zeros(K, np.int32)
+    rc = lib().oracle_shape_prep(_p(p), K, M, _p(lo), _p(hi), _p(e2), _p(cell))
+    if rc:
+        raise ValueError(f"oracle_shape_prep: {rc}")
+    return lo, hi, np.float32(e2[0]), cell
+
+
+def rel_transform(poseA, poseB):
+    """O1-O3 -> (R_BA[3,3], t_BA[3], R_AB[3,3], t_AB[3]) float32."""
+    a = np.ascontiguousarray(poseA, np.float32)
+    b = np.ascontiguousarray(poseB, np.float32)
+    out = [np.zeros(9, np.float32), np.zeros(3, np.float32), np.zeros(9, np.float32), np.zeros(3, np.float32)]
+    rc = lib().oracle_rel_transform(_p(a), _p(b), *[_p(o) for o in out])
+    if rc:
+        raise ValueError(f"oracle_rel_transform: {rc}")
+    return out[0].reshape(3, 3), out[1], out[2].reshape(3, 3), out[3]
+
+
+def query(weights_flat, points, pairs, poses, M=6, H=256, F=64, bf16_emul=False, n_threads=0):
+    """Whole query O0-O9.  Returns dict with probs, labels, logits (float64), kept, occ (int32 [N][2]),
+    masks (uint32 [N][2][ceil(K/32)]) and emb (float64 [N][2][F])."""
+    w = np.ascontiguousarray(weights_flat, np.float32)
+    pts = np.ascontiguousarray(points, np.float32)
+    pr = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+    po = np.ascontiguousarray(poses, np.float32).reshape(-1, 2, 7)
+    S, K = pts.shape[0], pts.shape[1]
+    N = pr.shape[0]
+    words = (K + 31) // 32
+    out = dict(probs=np.zeros(N), labels=np.zeros(N, np.uint8), logits=np.zeros(N),
+               kept=np.zeros((N, 2), np.int32), occ=np.zeros((N, 2), np.int32),
+               masks=np.zeros((N, 2, words), np.uint32), emb=np.zeros((N, 2, F)))
+    cfg = _Cfg(M, H, F, 1 if bf16_emul else 0, n_threads)
+    rc = lib().oracle_query(C.byref(cfg), _p(w), w.size, _p(pts), S, K, _p(pr), _p(po), N,
+                            _p(out["probs"]), _p(out["labels"]), _p(out["logits"]), _p(out["kept"]),
+                            _p(out["occ"]), _p(out["masks"]), _p(out["emb"]))
+    if rc:
+        raise ValueError(f"oracle_query: {rc}")
+    return out
+
+
+def load_weights(manifest):
+    cap = 1 << 24
+    buf = np.zeros(cap, np.float32)
+    M = np.zeros(1, np.int32)
+    H = np.zeros(1, np.int32)
+    F = np.zeros(1, np.int32)
+    n = lib().oracle_load_weights(manifest.encode(), _p(buf), cap, _p(M), _p(H), _p(F))
+    if n < 0:
+        raise ValueError(f"oracle_load_weights: {n}")
+    return buf[:n].copy(), (int(M[0]), int(H[0]), int(F[0]))

@@ -1,0 +1,495 @@
+// locc_oracle.cpp — plain CPU reference of the LOCC batched collision query.
+//
+// TEST INFRASTRUCTURE ONLY (see locc_oracle.h).  Shares nothing with the CUDA path.
+// Build: g++ -O2 -std=c++17 -ffp-contract=off -fPIC -shared -pthread (never -ffast-math:
+// the crop masks must come out of exactly the fp32 operations written below).
+//
+// Each step cites the passage it follows.  P:n = PAPER.md line n, S:n = SPEC.md line n,
+// and "O<k>" = the step of SURVEY.md §8(c) that fixes the reading used by this build.
+#include "locc_oracle.h"
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+constexpr int kP = 128;  // predictor MLP width: "3 layers of 128 neurons"
+
+// ------------------------------------------------------------------ parameters
+// Canonical order (SURVEY.md §8(c) "Parameter layout"), row-major [out][in], W then b.
+struct Layer {
+  const float* W;
+  const float* b;
+  int out, in;
+};
+struct Params {
+  Layer enc1, enc2, enc3, proj, obj1, obj2, obj3, pair1, pair2, pair3, out;
+};
+
+int64_t n_params(int H, int F) {
+  auto L = [](int64_t o, int64_t i) { return o * i + o; };
+  return L(H, 3) + L(H, H) + L(H, H) + L(F, H) + L(kP, F + 7) + 5 * L(kP, kP) + L(1, kP);
+}
+
+Params bind_params(const float* w, int H, int F) {
+  Params p;
+  const float* c = w;
+  auto take = [&c](int o, int i) {
+    Layer l{c, c + (int64_t)o * i, o, i};
+    c += (int64_t)o * i + o;
+    return l;
+  };
+  p.enc1 = take(H, 3);
+  p.enc2 = take(H, H);
+  p.enc3 = take(H, H);
+  p.proj = take(F, H);
+  p.obj1 = take(kP, F + 7);
+  p.obj2 = take(kP, kP);
+  p.obj3 = take(kP, kP);
+  p.pair1 = take(kP, kP);
+  p.pair2 = take(kP, kP);
+  p.pair3 = take(kP, kP);
+  p.out = take(1, kP);
+  return p;
+}
+
+// bf16 round-to-nearest-even of a double (8 significant bits), used only in bf16_emul mode.
+double bf16_rne(double x) {
+  if (x == 0.0 || !std::isfinite(x)) return x;
+  int e;
+  double m = std::frexp(x, &e);                // x = m * 2^e, 0.5 <= |m| < 1
+  double r = std::nearbyint(std::ldexp(m, 8));  // default rounding mode: ties to even
+  return std::ldexp(r, e - 8);
+}
+
+// y = act(W x + b) in fp64, plain dot products in index order.  `Wd` = the weights as
+// doubles (already bf16-rounded in bf16_emul mode); `round_in` rounds x to bf16 first.
+void dense(const Layer& L, const double* Wd, const double* x, double* y, bool relu, bool round_in) {
+  std::vector<double> xr(x, x + L.in);
+  if (round_in)
+    for (double& v : xr) v = bf16_rne(v);
+  for (int o = 0; o < L.out; ++o) {
+    double acc = 0.0;
+    for (int i = 0; i < L.in; ++i) acc += Wd[(int64_t)o * L.in + i] * xr[i];
+    acc += (double)L.b[o];
+    y[o] = relu ? (acc > 0.0 ? acc : 0.0) : acc;
+  }
+}
+void dense(const Layer& L, const double* x, double* y, bool relu) {
+  std::vector<double> Wd(L.W, L.W + (int64_t)L.out * L.in);
+  dense(L, Wd.data(), x, y, relu, false);
+}
+
+// Weights of one layer widened to fp64, optionally rounded to bf16 (bf16_emul mode).
+std::vector<double> widen(const Layer& L, bool round) {
+  std::vector<double> w(L.W, L.W + (int64_t)L.out * L.in);
+  if (round)
+    for (double& v : w) v = bf16_rne(v);
+  return w;
+}
+
+// ------------------------------------------------------------------ O0: shape precompute
+// AABB of the cloud ("compute the AABB of each object's mesh"; Q7: from the points),
+// M x M x M grid over it, eps = half the cell diagonal of this shape, used
+// when this shape is the *counter* object (P:424 eps = sqrt(a1^2+a2^2+a3^2)/2, a3^3 read
+// as the typo a3^2), cell binning floor((p-lo)*M/ext) clamped to M-1.
+struct ShapeInfo {
+  float lo[3], hi[3];
+  float eps2;
+  std::vector<int32_t> cell;  // per point, caller's order
+};
+
+bool shape_prep(const float* pts, int K, int M, ShapeInfo& s) {
+  if (K < 1 || M < 1) return false;
+  for (int d = 0; d < 3; ++d) {
+    s.lo[d] = pts[d];
+    s.hi[d] = pts[d];
+  }
+  for (int k = 0; k < K; ++k)
+    for (int d = 0; d < 3; ++d) {
+      float v = pts[3 * k + d];
+      if (!std::isfinite(v)) return false;
+      if (v < s.lo[d]) s.lo[d] = v;
+      if (v > s.hi[d]) s.hi[d] = v;
+    }
+  double ext[3], a[3];
+  for (int d = 0; d < 3; ++d) {
+    ext[d] = (double)s.hi[d] - (double)s.lo[d];
+    a[d] = ext[d] / (double)M;
+  }
+  s.eps2 = (float)(0.25 * ((a[0] * a[0] + a[1] * a[1]) + a[2] * a[2]));
+  s.cell.assign(K, 0);
+  for (int k = 0; k < K; ++k) {
+    int c[3];
+    for (int d = 0; d < 3; ++d) {
+      if (ext[d] == 0.0) {
+        c[d] = 0;
+        continue;
+      }
+      double u = (((double)pts[3 * k + d] - (double)s.lo[d]) * (double)M) / ext[d];
+      double f = std::floor(u);
+      c[d] = f >= (double)(M - 1) ? M - 1 : (int)f;
+    }
+    s.cell[k] = c[0] + M * (c[1] + M * c[2]);
+  }
+  return true;
+}
+
+// ------------------------------------------------------------------ O1-O3: relative pose
+struct Quat {
+  double w, x, y, z;
+};
+
+// O1: normalise in fp64 from the fp32 inputs.
+bool normalise(const float* q7, Quat& q) {
+  double w = q7[0], x = q7[1], y = q7[2], z = q7[3];
+  double n2 = ((w * w + x * x) + y * y) + z * z;
+  if (!(n2 >= 1e-12) || !std::isfinite(n2)) return false;
+  double s = std::sqrt(n2);
+  q = {w / s, x / s, y / s, z / s};
+  return true;
+}
+
+// O2: Hamilton product q1 (x) q2 = (w1w2 - v1.v2, w1 v2 + w2 v1 + v1 x v2), grouped so that
+// conj(q) (x) q has an exactly zero vector part.
+Quat hamilton(const Quat& a, const Quat& b) {
+  Quat r;
+  r.w = a.w * b.w - ((a.x * b.x + a.y * b.y) + a.z * b.z);
+  r.x = (a.w * b.x + b.w * a.x) + (a.y * b.z - a.z * b.y);
+  r.y = (a.w * b.y + b.w * a.y) + (a.z * b.x - a.x * b.z);
+  r.z = (a.w * b.z + b.w * a.z) + (a.x * b.y - a.y * b.x);
+  return r;
+}
+Quat conj(const Quat& q) { return {q.w, -q.x, -q.y, -q.z}; }
+
+// O3: rotation matrix of a quaternion (fp64).
+void rotmat(const Quat& q, double R[3][3]) {
+  const double w = q.w, x = q.x, y = q.y, z = q.z;
+  R[0][0] = 1.0 - 2.0 * (y * y + z * z);
+  R[0][1] = 2.0 * (x * y - w * z);
+  R[0][2] = 2.0 * (x * z + w * y);
+  R[1][0] = 2.0 * (x * y + w * z);
+  R[1][1] = 1.0 - 2.0 * (x * x + z * z);
+  R[1][2] = 2.0 * (y * z - w * x);
+  R[2][0] = 2.0 * (x * z - w * y);
+  R[2][1] = 2.0 * (y * z + w * x);
+  R[2][2] = 1.0 - 2.0 * (x * x + y * y);
+}
+
+// Frame of B seen from A: p_B = R_B^T (R_A p + t_A - t_B) = R(conj(qB) (x) qA) p + R_B^T (t_A - t_B)
+// ("create the OBB of shape embeddings of two objects by using their poses").
+void relative(const Quat& qA, const float* tA, const Quat& qB, const float* tB, float Rout[9],
+              float tout[3]) {
+  double R[3][3], RB[3][3];
+  rotmat(hamilton(conj(qB), qA), R);
+  rotmat(qB, RB);
+  double d[3] = {(double)tA[0] - (double)tB[0], (double)tA[1] - (double)tB[1],
+                 (double)tA[2] - (double)tB[2]};
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) Rout[3 * i + j] = (float)R[i][j];
+    tout[i] = (float)((RB[0][i] * d[0] + RB[1][i] * d[1]) + RB[2][i] * d[2]);
+  }
+}
+
+// ------------------------------------------------------------------ O4: crop
+// Keep point p of one object iff the Euclidean distance from its position in the other
+// object's frame to the other object's AABB is <= eps_other (S:359 applied
+// to points; reading Q8).  fp32, exactly these operations.
+int crop(const float* pts, int K, const float R[9], const float t[3], const ShapeInfo& other,
+         std::vector<uint8_t>& keep) {
+  keep.assign(K, 0);
+  int n = 0;
+  for (int k = 0; k < K; ++k) {
+    const float x = pts[3 * k], y = pts[3 * k + 1], z = pts[3 * k + 2];
+    float p[3];
+    for (int i = 0; i < 3; ++i)
+      p[i] = std::fmaf(R[3 * i], x, std::fmaf(R[3 * i + 1], y, std::fmaf(R[3 * i + 2], z, t[i])));
+    float dd[3];
+    for (int i = 0; i < 3; ++i) {
+      float a = other.lo[i] - p[i];
+      float b = p[i] - other.hi[i];
+      float m = std::fmaxf(a, b);
+      dd[i] = std::fmaxf(m, 0.0f);
+    }
+    float zz = dd[2] * dd[2];
+    float d2 = std::fmaf(dd[0], dd[0], std::fmaf(dd[1], dd[1], zz));
+    if (d2 <= other.eps2) {
+      keep[k] = 1;
+      ++n;
+    }
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------ O6-O7: encoder + pooling
+// Per kept point: 3 ReLU layers of width H ("3 layers of MLP with 256 neurons",
+// P:425 ReLU), input = the point's local-frame coordinates (reading Q6).  Cell-wise max over
+// the kept points of each cell, average over the occupied cells (P:335, P:424
+// "average pooling", reading Q11), then one linear layer to F (reading Q5).
+// Returns C (occupied cells); e = 0 when no point is kept.
+struct EncW {
+  std::vector<double> w1, w2, w3, wf;  // fp64 copies; w2, w3 bf16-rounded in bf16_emul mode
+};
+
+int encode(const Params& P, const EncW& W, const float* pts, int K, const ShapeInfo& s,
+           const std::vector<uint8_t>& keep, int M, int H, int F, bool emul, double* e) {
+  const int ncell = M * M * M;
+  std::vector<double> g((size_t)ncell * H, 0.0);
+  std::vector<uint8_t> occ(ncell, 0);
+  std::vector<double> x(3), h1(H), h2(H), h3(H);
+  int n = 0;
+  for (int k = 0; k < K; ++k) {
+    if (!keep[k]) continue;
+    ++n;
+    for (int d = 0; d < 3; ++d) x[d] = pts[3 * k + d];
+    dense(P.enc1, W.w1.data(), x.data(), h1.data(), true, false);
+    dense(P.enc2, W.w2.data(), h1.data(), h2.data(), true, emul);
+    dense(P.enc3, W.w3.data(), h2.data(), h3.data(), true, emul);
+    const int c = s.cell[k];
+    double* gc = &g[(size_t)c * H];
+    if (!occ[c]) {
+      occ[c] = 1;
+      for (int j = 0; j < H; ++j) gc[j] = h3[j];
+    } else {
+      for (int j = 0; j < H; ++j) gc[j] = h3[j] > gc[j] ? h3[j] : gc[j];
+    }
+  }
+  if (n == 0) {
+    for (int j = 0; j < F; ++j) e[j] = 0.0;
+    return 0;
+  }
+  std::vector<double> m(H, 0.0);
+  int C = 0;
+  for (int c = 0; c < ncell; ++c) {  // ascending cell order
+    if (!occ[c]) continue;
+    ++C;
+    for (int j = 0; j < H; ++j) m[j] += g[(size_t)c * H + j];
+  }
+  for (int j = 0; j < H; ++j) m[j] /= (double)C;
+  dense(P.proj, W.wf.data(), m.data(), e, false, false);
+  return C;
+}
+
+// ------------------------------------------------------------------ O8-O9: predictor
+// [e ; pose] -> 3x128 ReLU (shared by both objects) -> elementwise max across the pair ->
+// 3x128 ReLU -> linear -> sigmoid.  Pose = own world pose, unit quaternion with
+// the first non-zero component made positive, then translation (reading Q12).
+void object_mlp(const Params& P, const double* e, int F, const Quat& q, const float* t, double* u) {
+  std::vector<double> z(F + 7), a(kP), b(kP);
+  for (int j = 0; j < F; ++j) z[j] = e[j];
+  double qc[4] = {q.w, q.x, q.y, q.z};
+  double sgn = 1.0;
+  for (int i = 0; i < 4; ++i)
+    if (qc[i] != 0.0) {
+      sgn = qc[i] > 0.0 ? 1.0 : -1.0;
+      break;
+    }
+  for (int i = 0; i < 4; ++i) z[F + i] = sgn * qc[i];
+  for (int i = 0; i < 3; ++i) z[F + 4 + i] = t[i];
+  dense(P.obj1, z.data(), a.data(), true);
+  dense(P.obj2, a.data(), b.data(), true);
+  dense(P.obj3, b.data(), u, true);
+}
+
+double pair_head(const Params& P, const double* uA, const double* uB) {
+  std::vector<double> v(kP), a(kP), b(kP), c(kP);
+  for (int j = 0; j < kP; ++j) v[j] = uA[j] > uB[j] ? uA[j] : uB[j];
+  dense(P.pair1, v.data(), a.data(), true);
+  dense(P.pair2, a.data(), b.data(), true);
+  dense(P.pair3, b.data(), c.data(), true);
+  double logit;
+  dense(P.out, c.data(), &logit, false);
+  return logit;
+}
+
+bool finite_n(const float* p, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t oracle_n_params(int32_t H, int32_t F) { return n_params(H, F); }
+
+int oracle_shape_prep(const float* pts, int32_t K, int32_t M, float lo[3], float hi[3], float* eps2,
+                      int32_t* cell) {
+  ShapeInfo s;
+  if (!pts || !shape_prep(pts, K, M, s)) return -2;
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = s.lo[d];
+    hi[d] = s.hi[d];
+  }
+  *eps2 = s.eps2;
+  if (cell) std::memcpy(cell, s.cell.data(), sizeof(int32_t) * K);
+  return 0;
+}
+
+int oracle_rel_transform(const float poseA[7], const float poseB[7], float R_BA[9], float t_BA[3],
+                         float R_AB[9], float t_AB[3]) {
+  Quat qA, qB;
+  if (!normalise(poseA, qA) || !normalise(poseB, qB)) return -1;
+  relative(qA, poseA + 4, qB, poseB + 4, R_BA, t_BA);
+  relative(qB, poseB + 4, qA, poseA + 4, R_AB, t_AB);
+  return 0;
+}
+
+int oracle_query(const oracle_cfg* cfg, const float* weights, size_t n_weights, const float* points,
+                 int32_t S, int32_t K, const int32_t* pairs, const float* poses, int64_t N,
+                 double* probs, uint8_t* labels, double* logits, int32_t* kept, int32_t* occ,
+                 uint32_t* masks, double* emb) {
+  if (!cfg || cfg->M < 1 || cfg->H < 1 || cfg->F < 1 || N < 0) return -1;
+  const int M = cfg->M, H = cfg->H, F = cfg->F;
+  const bool emul = cfg->bf16_emul != 0;
+  if (!weights || (int64_t)n_weights != n_params(H, F) || !finite_n(weights, (int64_t)n_weights)) return -3;
+  if (!points || S < 1 || K < 1) return -2;
+  if (N > 0 && (!pairs || !poses)) return -1;
+  for (int64_t i = 0; i < 2 * N; ++i)
+    if (pairs[i] < 0 || pairs[i] >= S) return -1;
+  if (!finite_n(poses, 14 * N)) return -1;
+  Params P = bind_params(weights, H, F);
+  EncW EW{widen(P.enc1, false), widen(P.enc2, emul), widen(P.enc3, emul), widen(P.proj, false)};
+
+  std::vector<ShapeInfo> shapes(S);
+  for (int s = 0; s < S; ++s)
+    if (!shape_prep(points + (int64_t)s * K * 3, K, M, shapes[s])) return -2;
+  for (int64_t i = 0; i < 2 * N; ++i) {
+    Quat q;
+    if (!normalise(poses + 7 * i, q)) return -1;
+  }
+
+  const int words = (K + 31) / 32;
+  std::atomic<int64_t> next(0);
+  auto worker = [&]() {
+    std::vector<uint8_t> keepA, keepB;
+    std::vector<double> eA(F), eB(F), uA(kP), uB(kP);
+    for (;;) {
+      const int64_t i = next.fetch_add(1);
+      if (i >= N) break;
+      const int a = pairs[2 * i], b = pairs[2 * i + 1];
+      const float* pA = poses + 14 * i;
+      const float* pB = pA + 7;
+      Quat qA, qB;
+      normalise(pA, qA);
+      normalise(pB, qB);
+      float R_BA[9], t_BA[3], R_AB[9], t_AB[3];
+      relative(qA, pA + 4, qB, pB + 4, R_BA, t_BA);
+      relative(qB, pB + 4, qA, pA + 4, R_AB, t_AB);
+      const float* ptsA = points + (int64_t)a * K * 3;
+      const float* ptsB = points + (int64_t)b * K * 3;
+      const int nA = crop(ptsA, K, R_BA, t_BA, shapes[b], keepA);
+      const int nB = crop(ptsB, K, R_AB, t_AB, shapes[a], keepB);
+      if (kept) {
+        kept[2 * i] = nA;
+        kept[2 * i + 1] = nB;
+      }
+      if (masks) {
+        uint32_t* mA = masks + (2 * i) * words;
+        uint32_t* mB = mA + words;
+        std::memset(mA, 0, sizeof(uint32_t) * 2 * words);
+        for (int k = 0; k < K; ++k) {
+          if (keepA[k]) mA[k / 32] |= 1u << (k % 32);
+          if (keepB[k]) mB[k / 32] |= 1u << (k % 32);
+        }
+      }
+      // O5: both crops empty -> disjoint, short-circuit.
+      int CA = 0, CB = 0;
+      double logit, prob;
+      if (nA + nB == 0) {
+        for (int j = 0; j < F; ++j) eA[j] = eB[j] = 0.0;
+        logit = -INFINITY;
+        prob = 0.0;
+      } else {
+        CA = encode(P, EW, ptsA, K, shapes[a], keepA, M, H, F, emul, eA.data());
+        CB = encode(P, EW, ptsB, K, shapes[b], keepB, M, H, F, emul, eB.data());
+        object_mlp(P, eA.data(), F, qA, pA + 4, uA.data());
+        object_mlp(P, eB.data(), F, qB, pB + 4, uB.data());
+        logit = pair_head(P, uA.data(), uB.data());
+        prob = 1.0 / (1.0 + std::exp(-logit));
+      }
+      if (occ) {
+        occ[2 * i] = CA;
+        occ[2 * i + 1] = CB;
+      }
+      if (emb)
+        for (int j = 0; j < F; ++j) {
+          emb[(2 * i) * F + j] = eA[j];
+          emb[(2 * i + 1) * F + j] = eB[j];
+        }
+      if (probs) probs[i] = prob;
+      if (logits) logits[i] = logit;
+      if (labels) labels[i] = prob > 0.5 ? 1 : 0;  // ties negative
+    }
+  };
+  int nt = cfg->n_threads > 0 ? cfg->n_threads : (int)std::thread::hardware_concurrency();
+  if (nt < 1) nt = 1;
+  if (nt > N) nt = (int)(N > 0 ? N : 1);
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+  return 0;
+}
+
+int64_t oracle_load_weights(const char* manifest, float* out, size_t cap, int32_t* M, int32_t* H,
+                            int32_t* F) {
+  FILE* f = std::fopen(manifest, "r");
+  if (!f) return -3;
+  char magic[64];
+  int ver = 0;
+  if (std::fscanf(f, "%63s %d %d %d %d", magic, &ver, M, H, F) != 5 || std::string(magic) != "locc-weights" ||
+      ver != 1) {
+    std::fclose(f);
+    return -3;
+  }
+  const char* names[] = {"enc.l1", "enc.l2", "enc.l3", "enc.proj", "obj.l1", "obj.l2",
+                         "obj.l3", "pair.l1", "pair.l2", "pair.l3", "out"};
+  const int h = *H, fo = *F;
+  const int shp[11][2] = {{h, 3}, {h, h}, {h, h}, {fo, h}, {kP, fo + 7}, {kP, kP},
+                          {kP, kP}, {kP, kP}, {kP, kP}, {kP, kP}, {1, kP}};
+  std::string bin(manifest);
+  size_t dot = bin.find_last_of('.');
+  size_t slash = bin.find_last_of('/');
+  if (dot != std::string::npos && (slash == std::string::npos || dot > slash)) bin = bin.substr(0, dot);
+  bin += ".bin";
+  FILE* fb = std::fopen(bin.c_str(), "rb");
+  if (!fb) {
+    std::fclose(f);
+    return -3;
+  }
+  int64_t total = n_params(h, fo);
+  if ((int64_t)cap < total) {
+    std::fclose(f);
+    std::fclose(fb);
+    return -3;
+  }
+  int64_t pos = 0;
+  for (int l = 0; l < 11; ++l)
+    for (int wb = 0; wb < 2; ++wb) {
+      char name[128];
+      long long o, in, off;
+      if (std::fscanf(f, "%127s %lld %lld %lld", name, &o, &in, &off) != 4) goto bad;
+      std::string want = std::string(names[l]) + (wb == 0 ? ".W" : ".b");
+      long long eo = shp[l][0], ei = wb == 0 ? shp[l][1] : 1;
+      if (want != name || o != eo || in != ei) goto bad;
+      if (std::fseek(fb, (long)off, SEEK_SET) != 0) goto bad;
+      if ((long long)std::fread(out + pos, sizeof(float), (size_t)(o * in), fb) != o * in) goto bad;
+      pos += o * in;
+    }
+  std::fclose(f);
+  std::fclose(fb);
+  return pos;
+bad:
+  std::fclose(f);
+  std::fclose(fb);
+  return -3;
+}
+
+}  // extern "C"

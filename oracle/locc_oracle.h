@@ -1,0 +1,63 @@
+/* locc_oracle.h — plain, slow, CPU reference of the LOCC batched collision query.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2304_09439_b200/, include/locc.h) never links, imports or calls it, and
+ * this file shares no code, header, constant or helper with the CUDA path.
+ *
+ * What it computes is SURVEY.md §8(c) O0-O9 (the reading of PAPER.md §"Local
+ * object crop collision network" lines 325-345 and Appendix "Architecture
+ * Details" lines 420-425 adopted for this build; DESIGN.md lists every reading).
+ * Geometry (O0-O4) is prescribed fp32/fp64 arithmetic so crop masks can be
+ * compared bit-exactly; the network (O6-O9) is fp64.  `bf16_emul` = 1 rounds
+ * h1, W2, h2, W3 to bf16 (round-to-nearest-even) before their products — the
+ * arithmetic the bf16 tensor-core path is defined to perform.
+ *
+ * Parity pins: tests/test_oracle_*.py.  "parity unpinned": absolute
+ * probabilities of any trained LOCC (no trained weights exist).
+ *
+ * Return codes: 0 ok; -1 invalid argument; -2 bad shape table; -3 bad weights.
+ */
+#ifndef LOCC_ORACLE_H
+#define LOCC_ORACLE_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int32_t M, H, F;    /* voxel grid edge, point-feature width, cell-feature width */
+  int32_t bf16_emul;  /* 0: fp64 network; 1: bf16-operand emulation of layers 2-3 */
+  int32_t n_threads;  /* 0 = hardware_concurrency */
+} oracle_cfg;
+
+/* O0 for one shape: lo/hi (float3), eps2, per-point cell ids [K]. */
+int oracle_shape_prep(const float* pts /*[K][3]*/, int32_t K, int32_t M, float lo[3], float hi[3],
+                      float* eps2, int32_t* cell /*[K]*/);
+
+/* O1-O3 for one pair: R_BA (row-major 3x3), t_BA, R_AB, t_AB, each rounded once to fp32. */
+int oracle_rel_transform(const float poseA[7], const float poseB[7], float R_BA[9], float t_BA[3],
+                         float R_AB[9], float t_AB[3]);
+
+/* Whole query O0-O9.  Any output pointer may be NULL.  masks: [N][2][ceil(K/32)] bit k of
+ * word k/32 = caller's point k kept.  emb: [N][2][F].  Short-circuit: prob 0, label 0,
+ * logit -inf.  Returns nonzero on invalid input (ids out of range, |q|^2 < 1e-12, K < 1,
+ * non-finite values) without guaranteeing outputs. */
+int oracle_query(const oracle_cfg* cfg, const float* weights, size_t n_weights, const float* points,
+                 int32_t S, int32_t K, const int32_t* pairs, const float* poses, int64_t N,
+                 double* probs, uint8_t* labels, double* logits, int32_t* kept, int32_t* occ,
+                 uint32_t* masks, double* emb);
+
+/* Parse a weight manifest + .bin (format in include/locc.h) into `out` (canonical order).
+ * Returns the float count, or a negative code; writes M, H, F. */
+int64_t oracle_load_weights(const char* manifest, float* out, size_t cap, int32_t* M, int32_t* H,
+                            int32_t* F);
+
+/* Canonical parameter count for (H, F). */
+int64_t oracle_n_params(int32_t H, int32_t F);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
