@@ -1,0 +1,290 @@
+"""Benchmark of the LOCC batched collision query on B200 (BASELINE.json metric: collision checks/sec).
+
+Default: N=1 GPU, workload C3 = 1,048,576 pairs over 1030 synthetic shapes, K=1500, M=6, H=256,
+F=64, pose density s=0.5, bf16 tensor-core encoder.  A "step" = one locc_query over the whole
+batch (every stage of the hot path: transforms, crop + compaction, encoder, pooling, predictor).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--precision bf16|fp32] [--pairs N]
+  python bench.py --impl reference ...   # the CPU oracle (this tier's reference arm)
+
+Multi-GPU (torchrun, one process per GPU): every rank runs its own 1,048,576-pair batch (weak
+scaling; the path needs no collective); time = max over ranks; value = all pairs / that time.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "collision checks/sec (LOCC inference)"
+UNIT = "checks/s"
+FLOP_PER_ROW = 2 * (3 * 256 + 2 * 256 * 256)  # encoder layers 1-3 per kept row
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="locc", choices=["locc", "reference"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--pairs", type=int, default=1 << 20)
+    ap.add_argument("--K", type=int, default=1500)
+    ap.add_argument("--s", type=float, default=0.5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_name(a):
+    return (f"C3: {a.pairs} pairs/GPU over 1030 synthetic non-convex shapes, K={a.K}, M=6, H=256, F=64, "
+            f"pose density s={a.s}, spread weights (seeded random init)")
+
+
+def make_inputs(a, rank):
+    import locc_synth as ls
+    pts, _ = ls.make_shapes(1030, a.K, seed=1)
+    pairs, poses = ls.make_pairs_poses(pts, a.pairs, s=a.s, seed=2 + rank)
+    flat = ls.flatten_weights(ls.make_weights("spread", calib=ls.load_calibration()))
+    return pts, pairs, poses, flat
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in out.strip().splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(pts, pairs, poses, flat, target_s=15.0):
+    """The oracle as it stands (fp64 network, bf16-emulating to match the GPU arithmetic), timed on
+    this host's cores on a bounded prefix of the same workload."""
+    import oracle
+    cores = os.cpu_count() or 1
+    n = max(cores, 16)
+    t = time.perf_counter()
+    oracle.query(flat, pts, pairs[:n], poses[:n], bf16_emul=True, n_threads=cores)
+    dt = time.perf_counter() - t
+    n2 = int(min(len(pairs), max(n, n * target_s / max(dt, 1e-3))))
+    t = time.perf_counter()
+    oracle.query(flat, pts, pairs[:n2], poses[:n2], bf16_emul=True, n_threads=cores)
+    dt2 = time.perf_counter() - t
+    return {"value": n2 / dt2, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {n2} pairs of the workload ({dt2:.1f} s, {cores} threads, bf16-emulating fp64 oracle)"}
+
+
+def run_reference(a):
+    """--impl reference: the CPU oracle on the host cores, same config/metric, bounded sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    pts, pairs, poses, flat = make_inputs(a, 0)
+    import oracle
+    cores = os.cpu_count() or 1
+    n = max(2 * cores, 32)
+    for i in range(a.warmup):
+        oracle.query(flat, pts, pairs[:n], poses[:n], bf16_emul=True, n_threads=cores)
+    times = []
+    for i in range(a.steps):
+        sl = slice(n * (i + 1), n * (i + 2))
+        t = time.perf_counter()
+        oracle.query(flat, pts, pairs[sl], poses[sl], bf16_emul=True, n_threads=cores)
+        times.append(time.perf_counter() - t)
+    ms = 1e3 * statistics.mean(times)
+    v = n / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(a), "sample_pairs_per_step": n},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{n} consecutive pairs of the workload per step"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2304_09439_b200 import build as b
+    b.build()
+    from paper_2304_09439_b200 import locc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    prec = locc.LOCC_PREC_BF16 if a.precision == "bf16" else locc.LOCC_PREC_FP32
+
+    pts, pairs, poses, flat = make_inputs(a, rank)
+    N = len(pairs)
+    ctx = locc.Locc(precision=prec, device=local)
+    ctx.load_weights_mem(flat)
+    ctx.set_shapes(pts)
+    d_pairs = torch.from_numpy(pairs).cuda()
+    d_poses = torch.from_numpy(poses).cuda()
+    d_probs = torch.empty(N, device="cuda")
+    d_labels = torch.empty(N, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.Stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def step():
+        ctx.query_into(d_pairs, d_poses, d_probs, d_labels, stream=stream.cuda_stream)
+
+    for _ in range(a.warmup):
+        step()
+    stream.synchronize()
+    ctx.set_timing(True)
+    step()
+    stream.synchronize()
+    st = ctx.stats()  # kept rows, launches, encoder time of one step (for the roofline)
+    ctx.set_timing(False)
+
+    clocks = Clocks(local)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    enc_ms = []
+    for i in range(a.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            ev[i][0].record(stream)
+        ctx.set_timing(True)
+        step()
+        with torch.cuda.stream(stream):
+            ev[i][1].record(stream)
+        stream.synchronize()
+        enc_ms.append(ctx.stats()["encoder_ms"])
+        ctx.set_timing(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    ms = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # roofline of the dominant kernel (the encoder), algorithmic FLOPs of the kept rows only
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    kept = st["kept_rows"]
+    launches_per_step = st["kernel_launches"]
+    subs = max(1, st["sub_batches"])
+    enc_s = statistics.mean(enc_ms) / 1e3
+    achieved = FLOP_PER_ROW * kept / enc_s / 1e12 if enc_s > 0 else None
+    if prec == locc.LOCC_PREC_BF16:
+        peak = peaks.get("bf16_tflops_sustained", 1400.0)
+        roof = {"bound": "tensor", "unit": "TFLOP/s",
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback 1.4 PF sustained"}
+    else:
+        mhz = clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
+        roof = {"bound": "alu", "unit": "TFLOP/s",
+                "peak_source": f"148 SM x 128 FP32 FMA/clk x 2 x {mhz:.0f} MHz (median SM clock under load)"}
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "encoder_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(a.precision)
+        except Exception:
+            traffic = None
+    roof.update({"achieved": achieved, "peak": peak, "frac": (achieved / peak) if achieved else None,
+                 "traffic": traffic, "kernel": "encoder_tc_kernel" if prec else "encoder_f32_kernel",
+                 "launches_per_step": subs, "flop_per_launch": FLOP_PER_ROW * kept / subs,
+                 "avg_launch_ms": 1e3 * enc_s / subs, "encoder_share_of_step": (1e3 * enc_s) / ms})
+
+    line = {"metric": METRIC, "value": world * N / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": a.precision, "data": "synthetic",
+            "config": {"workload": workload_name(a), "pairs_per_gpu": N, "global_pairs": world * N,
+                       "kept_rows_per_step": kept, "kept_rows_per_pair": kept / N,
+                       "evaluated_pairs": st["evaluated_pairs"], "sub_batches": subs,
+                       "l2": "L2 flushed (256 MB write) before every timed step; working set (GBs of rows) >> L2",
+                       "parallelism": f"pair-batch shards, 1 process/GPU x {world}"},
+            "gpu_launches": launches_per_step * a.steps, "clocks": clk, "roofline": roof}
+
+    # e2e: same metric through the public API with HOST buffers (pinned), copies in the timed region
+    if not a.no_e2e:
+        h_pairs = torch.from_numpy(pairs).pin_memory()
+        h_poses = torch.from_numpy(poses).pin_memory()
+        h_probs = torch.empty(N).pin_memory()
+        h_labels = torch.empty(N, dtype=torch.uint8).pin_memory()
+        ctx.query_into(h_pairs, h_poses, h_probs, h_labels)
+        ts = []
+        for _ in range(max(2, min(a.steps, 3))):
+            t = time.perf_counter()
+            ctx.query_into(h_pairs, h_poses, h_probs, h_labels)
+            ts.append(time.perf_counter() - t)
+        e2e_s = statistics.mean(ts)
+        if world > 1:
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        line["e2e"] = {"value": world * N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": N * (8 + 56),
+                       "d2h_bytes_per_step": N * (4 + 1), "timer": "host perf_counter around the synchronous call"}
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(pts, pairs, poses, flat)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,149 @@
+/* locc.h — C ABI of the B200-native LOCC batched collision query (liblocc.so).
+ *
+ * LOCC (arXiv 2304.09439, "Local object crop collision network"): for each pair of objects
+ * (shape ids + SE(3) poses) return the collision probability and label.  Per pair the library
+ * runs, entirely in its own CUDA kernels for sm_100a:
+ *   S0 shape prep (once per shape table)   AABB, cell ids, eps
+ *   S1 relative transforms                 T_BA, T_AB from the poses
+ *   S2-S3 transform + crop + compaction    keep p iff dist(T p, AABB_other) <= eps_other
+ *                                                                          PAPER.md:335-337, :424
+ *   S4-S5 per-point encoder                3 -> H -> H -> H, ReLU
+ *   S6 cell-wise max pool                  over the kept points of a cell PAPER.md:331, :421
+ *   S7 mean over occupied cells, linear F  "average pooling" + linear
+ *   S8-S9 collision predictor              [e;pose] -> 3x128 -> max over pair -> 3x128 -> 1 -> sigmoid
+ *                                                                          PAPER.md:424-425
+ * The exact arithmetic of every step (and every reading of an ambiguous passage) is
+ * SURVEY.md §8(c) O0-O9, restated in DESIGN.md.  Threshold: label = p > 0.5 (ties negative).
+ *
+ * Conventions
+ *   - Points: float32 [S][K][3], metres, each shape in its own local frame.
+ *   - Pose: float32 [7] = (qw, qx, qy, qz, tx, ty, tz); the quaternion need not be unit
+ *     (it is normalised in fp64), |q|^2 must be >= 1e-12.
+ *   - Pair i: side 0 = object A = pairs[2i] with poses[14i .. 14i+6]; side 1 = B = pairs[2i+1]
+ *     with poses[14i+7 .. 14i+13].
+ *   - Buffers are caller-owned.  Every pointer passed to one call must have the same residency
+ *     (all host, or all device memory of the context's device); the library detects which.
+ *   - A context is bound to one CUDA device and is not reentrant; separate contexts are
+ *     independent.  Multi-GPU = one context (one process) per GPU, sharding pairs (see
+ *     paper_2304_09439_b200/parallel.py); the path needs no collective.
+ *   - Errors: every function returns a locc_status; on error no output is guaranteed written
+ *     and locc_last_error() holds a thread-local detail string.  No exception crosses the ABI.
+ */
+#ifndef LOCC_H
+#define LOCC_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LOCC_OK = 0,
+  LOCC_E_INVALID_ARG = -1, /* bad pointer/size/id/pose/config value */
+  LOCC_E_SHAPE = -2,       /* bad shape table: S < 1, K < 1, K > 65535, non-finite point */
+  LOCC_E_WEIGHTS = -3,     /* manifest/tensor name/shape mismatch, wrong count, non-finite */
+  LOCC_E_CUDA = -4,        /* a CUDA runtime call or kernel failed */
+  LOCC_E_OOM = -5,         /* device allocation failed */
+  LOCC_E_NCCL = -6,        /* reserved (the path itself uses no collective) */
+  LOCC_E_STATE = -7        /* query before weights and shapes were set */
+} locc_status;
+
+typedef enum {
+  LOCC_PREC_FP32 = 0, /* encoder layers 2-3 as fp32 FFMA on CUDA cores */
+  LOCC_PREC_BF16 = 1  /* encoder layers 2-3 on tcgen05 tensor cores: bf16 h1, W2, h2, W3,
+                         fp32 accumulate; layer 1, pooling and head stay fp32 */
+} locc_precision;
+
+typedef struct {
+  int32_t M;         /* voxel grid edge (M = 6); 1 <= M <= 15 */
+  int32_t H;         /* point-feature width; 256 for BF16, 32..256 step 32 for FP32 */
+  int32_t F;         /* cell-feature width; 1..256 */
+  int32_t precision; /* locc_precision */
+  int32_t device;    /* CUDA device ordinal; -1 = the calling thread's current device */
+  int32_t reserved;
+  int64_t max_batch; /* pairs per internal sub-batch (bounds scratch memory); 0 = 262144 */
+} locc_config;
+
+typedef struct locc_ctx locc_ctx;
+
+/* Per-query statistics of the last locc_query / locc_query_debug on this context. */
+typedef struct {
+  int64_t pairs;            /* N */
+  int64_t evaluated_pairs;  /* pairs with n_A + n_B > 0 (the rest are short-circuited) */
+  int64_t kept_rows;        /* sum over pairs of n_A + n_B: rows through the encoder */
+  int64_t nonempty_sides;   /* sides with n_s > 0 */
+  int64_t sub_batches;      /* internal sub-batches */
+  int64_t kernel_launches;  /* kernels the library launched for the query */
+  double  encoder_ms;       /* device time of the encoder launches (CUDA events; 0 if timing off) */
+  double  total_ms;         /* device time of the whole query on its stream (0 if timing off) */
+} locc_stats;
+
+/* Create a context on cfg->device.  Out: *out (free with locc_destroy).
+ * Errors: INVALID_ARG (null, M/H/F/precision out of range), CUDA, OOM. */
+locc_status locc_create(const locc_config* cfg, locc_ctx** out);
+
+/* Load parameters from the checkpoint format: text manifest
+ * `manifest_path` with header "locc-weights 1 M H F" then one line per tensor
+ * "name out in offset_bytes" in canonical order
+ *   enc.l1 [H][3], enc.l2 [H][H], enc.l3 [H][H], enc.proj [F][H], obj.l1 [128][F+7],
+ *   obj.l2, obj.l3, pair.l1, pair.l2, pair.l3 [128][128], out [1][128]
+ * each as "<layer>.W out in off" (row-major [out][in]) followed by "<layer>.b out 1 off",
+ * and the little-endian fp32 payload in the file with the manifest's stem and extension .bin.
+ * M, H, F must equal the context's.  Copies to the device; the caller keeps the files.
+ * Errors: WEIGHTS (parse error, name/shape/M/H/F mismatch, short file, non-finite value). */
+locc_status locc_load_weights(locc_ctx* ctx, const char* manifest_path);
+
+/* Same, from a host array of n_floats fp32 values in the canonical order above. */
+locc_status locc_load_weights_mem(locc_ctx* ctx, const float* flat, size_t n_floats);
+
+/* Set the shape table: points [S][K][3] (host or device pointer, caller keeps ownership).
+ * The library copies it and computes S0 on the device: AABB lo/hi (min/max of the points),
+ * eps^2 = (float)(0.25*((a.x^2 + a.y^2) + a.z^2)), a = ext/M in fp64, cell ids
+ * floor((p-lo)*M/ext) clamped to M-1 (0 on a zero-extent axis), and a stable cell-sorted
+ * copy of the points.  Errors: SHAPE (S < 1, K < 1, K > 65535, non-finite), INVALID_ARG, CUDA, OOM. */
+locc_status locc_set_shapes(locc_ctx* ctx, const float* points, int32_t S, int32_t K);
+
+/* Batched query.  pairs int32 [N][2] in [0, S); poses float32 [N][2][7]; out probs float32 [N];
+ * labels uint8 [N] (nullable; p > 0.5); logits float32 [N] (nullable).  Short-circuited pairs
+ * (both crops empty): prob 0, label 0, logit -inf.
+ * stream: cudaStream_t, or NULL for the library's own stream.  Host-resident buffers: the call
+ * copies them in and out and returns when the outputs are written.  Device-resident buffers:
+ * with stream == NULL the call returns after completion; with a caller stream it is
+ * asynchronous on that stream (and validation of ids/poses happens on the device: an invalid
+ * id or pose makes the call return INVALID_ARG only in the synchronous form).
+ * Errors: INVALID_ARG (N < 0, null buffers, id out of range, non-finite pose, |q|^2 < 1e-12),
+ * STATE (no weights or no shapes), CUDA, OOM. */
+locc_status locc_query(locc_ctx* ctx, const int32_t* pairs, const float* poses, int64_t N,
+                       float* probs, uint8_t* labels, float* logits, void* stream);
+
+/* locc_query plus every intermediate needed for bit-exact parity (all nullable):
+ * kept int32 [N][2] (n_A, n_B), occ int32 [N][2] (occupied cells C_A, C_B),
+ * masks uint32 [N][2][ceil(K/32)] (bit k of word k/32 = the CALLER's point k was kept),
+ * emb float32 [N][2][F] (e_A, e_B; 0 for an empty side).  Same residency rule. */
+locc_status locc_query_debug(locc_ctx* ctx, const int32_t* pairs, const float* poses, int64_t N,
+                             float* probs, uint8_t* labels, float* logits, int32_t* kept,
+                             int32_t* occ, uint32_t* masks, float* emb, void* stream);
+
+/* Switch the encoder precision of an existing context (LOCC_PREC_FP32 / LOCC_PREC_BF16). */
+locc_status locc_set_precision(locc_ctx* ctx, int32_t precision);
+
+/* Enable (1) / disable (0) CUDA-event timing of the encoder and of the whole query. */
+locc_status locc_set_timing(locc_ctx* ctx, int32_t enabled);
+
+/* Statistics of the last query (requires a completed query; reads device counters). */
+locc_status locc_get_stats(locc_ctx* ctx, locc_stats* out);
+
+/* Free the context and all its device memory.  NULL-safe. */
+void locc_destroy(locc_ctx* ctx);
+
+const char* locc_status_string(locc_status s);
+const char* locc_last_error(void);
+
+/* Library version, e.g. "locc-b200 0.1 sm_100a". */
+const char* locc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,91 @@
+// internal.h — device-side data layout shared by the liblocc.so translation units.
+// Product code only (never included by oracle/).  See DESIGN.md "Data layout in HBM".
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace locc {
+
+constexpr int kPredW = 128;        // predictor width, "3 layers of 128 neurons"
+constexpr int kSegPerChunk = 8;    // encoder work unit: 8 whole (pair, side) segments = 4 pairs
+constexpr int kRowFlagCellEnd = 1; // row flag: last kept row of its cell within the segment
+constexpr int kRowFlagSegEnd = 2;  // row flag: last kept row of the segment
+constexpr int kRowSegShift = 2;    // flags word = (segment << 2) | seg_end << 1 | cell_end
+
+// S0 output (one copy per context, resident for the context's lifetime).
+struct ShapeTable {
+  const float4* pts;    // [S][K] cell-sorted points: (x, y, z, __int_as_float(cell id))
+  const uint16_t* perm; // [S][K] sorted position -> caller's point index
+  const float4* lo;     // [S] (lo.x, lo.y, lo.z, eps^2)
+  const float4* hi;     // [S] (hi.x, hi.y, hi.z, 0)
+  int S, K;
+};
+
+// Parameters on the device (fp32 unless noted).  "T" = transposed to [in][out] so that a
+// thread per output unit reads coalesced rows.
+struct DevParams {
+  int H, F;
+  const float* w1;   // [H][3] + b1 [H] packed as float4 (w0, w1, w2, b) per unit: w1b [H]
+  const float4* w1b;
+  const float* w2T;  // [H in][H out]
+  const float* b2;
+  const float* w3T;
+  const float* b3;
+  const float* wfT;  // [H][F]
+  const float* bf;
+  const float* o1T;  // [F+7][128]
+  const float* ob1;
+  const float* o2T;  // [128][128]
+  const float* ob2;
+  const float* o3T;
+  const float* ob3;
+  const float* p1T;
+  const float* pb1;
+  const float* p2T;
+  const float* pb2;
+  const float* p3T;
+  const float* pb3;
+  const float* wout; // [128]
+  const float* bout; // [1]
+  const void* tc_w2; // bf16 W2/W3 pre-arranged as the encoder_tc shared-memory image
+  const void* tc_w3;
+};
+
+// Device counters of one query (int64 atomics), zeroed per query.
+struct DevStats {
+  unsigned long long kept_rows;
+  unsigned long long nonempty_sides;
+  unsigned long long evaluated_pairs;
+  unsigned long long bad_input;  // nonzero: an id was out of range or a pose invalid
+};
+
+// One sub-batch of pairs as seen by the kernels.
+struct Batch {
+  const int32_t* pairs;  // [B][2]
+  const float* poses;    // [B][2][7]
+  int64_t B;             // pairs in this sub-batch
+  int64_t G;             // segments = 2B
+  int32_t* counts;       // [G] n_s
+  int32_t* occ;          // [G] C_s (from the crop)
+  int64_t* offsets;      // [G+1] exclusive scan of counts
+  float4* rows;          // [sum n] kept rows (x, y, z, flags)
+  float* pooled;         // [G][H] mean over occupied cells of the cell-max features
+  uint32_t* masks;       // nullable [B][2][ceil(K/32)] caller-order keep bits (debug)
+  DevStats* stats;
+};
+
+// Launchers (kernels_*.cu).  All asynchronous on `st`.
+cudaError_t launch_shape_prep(const float* pts_in, int S, int K, int M, float4* pts, uint16_t* perm,
+                              float4* lo, float4* hi, uint16_t* cell_tmp, int* bad, cudaStream_t st);
+cudaError_t launch_crop_count(const ShapeTable& T, const Batch& b, int words, cudaStream_t st);
+cudaError_t launch_scan(const int32_t* counts, int64_t G, int64_t* offsets, int64_t* block_tmp,
+                        cudaStream_t st);
+cudaError_t launch_crop_emit(const ShapeTable& T, const Batch& b, cudaStream_t st);
+cudaError_t launch_encoder_f32(const DevParams& P, const Batch& b, cudaStream_t st);
+cudaError_t launch_encoder_tc(const DevParams& P, const Batch& b, int num_sms, cudaStream_t st);
+cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_t* labels,
+                        float* logits, float* emb, cudaStream_t st);
+size_t scan_tmp_elems(int64_t G);
+size_t encoder_tc_smem_bytes();
+
+}  // namespace locc

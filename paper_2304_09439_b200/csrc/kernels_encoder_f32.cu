@@ -1,0 +1,135 @@
+// kernels_encoder_f32.cu — S4-S7 on CUDA cores in fp32 (LOCC_PREC_FP32; the parity path and the
+// FFMA baseline the tensor-core encoder is measured against).
+//
+// Work unit: a chunk of kSegPerChunk whole (pair, side) segments = a contiguous row range of the
+// compacted row buffer.  Thread f owns feature f (H <= 256) and, for each 64-row tile:
+//   h1 = ReLU(W1 p + b1)               (input = local xyz, reading Q6)
+//   h2 = ReLU(W2 h1 + b2), acc3 = W3 h2 ("3 layers of MLP with 256 neurons")
+// then walks the tile's rows in order with its 64 accumulators of layer 3: the rows are sorted by
+// (segment, cell), so the cell-wise max pool is a running max that closes at each
+// cell end, g = ReLU(max + b3) (bias+ReLU is monotone, so this equals the max of ReLU(acc + b3)),
+// and the occupied-cell mean ("average pooling") a running sum in ascending
+// cell order, divided by C at the segment end.  Projection to F happens in the predictor kernel.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace locc {
+namespace {
+
+constexpr int TR = 64;        // rows per tile
+constexpr int LDH = TR + 4;   // padded row stride of the transposed activation tile
+
+__global__ void __launch_bounds__(256) encoder_f32_kernel(DevParams P, Batch b) {
+  extern __shared__ float4 smem4[];
+  float4* rows_s = smem4;                        // [TR]
+  float* hT = reinterpret_cast<float*>(smem4 + TR);  // [H][LDH]
+  const int H = P.H;
+  const int f = threadIdx.x;
+  const bool act = f < H;
+  const int64_t s0 = (int64_t)blockIdx.x * kSegPerChunk;
+  const int64_t s1 = min(s0 + kSegPerChunk, b.G);
+  const int64_t r0 = b.offsets[s0], r1 = b.offsets[s1];
+  if (r0 == r1) return;
+
+  float4 w1 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float b2 = 0.f, b3 = 0.f;
+  if (act) {
+    w1 = P.w1b[f];
+    b2 = P.b2[f];
+    b3 = P.b3[f];
+  }
+  float run_max = -INFINITY, run_sum = 0.f;
+  int run_cells = 0;
+
+  for (int64_t t0 = r0; t0 < r1; t0 += TR) {
+    const int nr = (int)min((int64_t)TR, r1 - t0);
+    if (f < TR) rows_s[f] = f < nr ? b.rows[t0 + f] : make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    // layer 1 (fp32 FFMA)
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < TR; r += 4) {
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 p = rows_s[r + j];
+          const float h = fmaf(w1.x, p.x, fmaf(w1.y, p.y, fmaf(w1.z, p.z, w1.w)));
+          v[j] = fmaxf(h, 0.f);
+        }
+        *reinterpret_cast<float4*>(&hT[f * LDH + r]) = make_float4(v[0], v[1], v[2], v[3]);
+      }
+    }
+    __syncthreads();
+    float acc[TR];
+    for (int layer = 0; layer < 2; ++layer) {
+      const float* WT = layer == 0 ? P.w2T : P.w3T;
+#pragma unroll
+      for (int r = 0; r < TR; ++r) acc[r] = 0.f;
+      if (act) {
+#pragma unroll 2
+        for (int k = 0; k < H; ++k) {
+          const float w = __ldg(WT + (int64_t)k * H + f);
+          const float4* hk = reinterpret_cast<const float4*>(&hT[k * LDH]);
+#pragma unroll
+          for (int r = 0; r < TR / 4; ++r) {
+            const float4 h = hk[r];
+            acc[4 * r + 0] = fmaf(w, h.x, acc[4 * r + 0]);
+            acc[4 * r + 1] = fmaf(w, h.y, acc[4 * r + 1]);
+            acc[4 * r + 2] = fmaf(w, h.z, acc[4 * r + 2]);
+            acc[4 * r + 3] = fmaf(w, h.w, acc[4 * r + 3]);
+          }
+        }
+      }
+      __syncthreads();
+      if (layer == 0) {
+        if (act) {
+#pragma unroll
+          for (int r = 0; r < TR; r += 4)
+            *reinterpret_cast<float4*>(&hT[f * LDH + r]) =
+                make_float4(fmaxf(acc[r] + b2, 0.f), fmaxf(acc[r + 1] + b2, 0.f), fmaxf(acc[r + 2] + b2, 0.f),
+                            fmaxf(acc[r + 3] + b2, 0.f));
+        }
+        __syncthreads();
+      }
+    }
+    // S6-S7: segmented cell max + occupied-cell sum over the tile's rows (row flags are uniform)
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < TR; ++r) {
+        if (r < nr) {
+          const uint32_t fl = __float_as_uint(rows_s[r].w);
+          run_max = fmaxf(run_max, acc[r]);
+          if (fl & kRowFlagCellEnd) {
+            run_sum += fmaxf(run_max + b3, 0.f);
+            ++run_cells;
+            run_max = -INFINITY;
+          }
+          if (fl & kRowFlagSegEnd) {
+            const int64_t seg = fl >> kRowSegShift;
+            b.pooled[seg * H + f] = __fdiv_rn(run_sum, (float)run_cells);
+            run_sum = 0.f;
+            run_cells = 0;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_encoder_f32(const DevParams& P, const Batch& b, cudaStream_t st) {
+  const int64_t chunks = (b.G + kSegPerChunk - 1) / kSegPerChunk;
+  if (chunks == 0) return cudaSuccess;
+  const size_t sm = sizeof(float4) * TR + sizeof(float) * (size_t)P.H * LDH;
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      encoder_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float4) * TR + sizeof(float) * 256 * LDH));
+  if (attr != cudaSuccess) return attr;
+  encoder_f32_kernel<<<(unsigned)chunks, 256, sm, st>>>(P, b);
+  return cudaGetLastError();
+}
+
+}  // namespace locc

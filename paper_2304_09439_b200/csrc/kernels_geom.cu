@@ -1,0 +1,434 @@
+// kernels_geom.cu — S0 shape prep, S1 relative transforms, S2-S3 transform + crop + compaction.
+//
+// Geometry is prescribed arithmetic so that crop masks, kept counts and
+// occupied-cell counts are bit-exact across implementations: every fp64/fp32 operation below is
+// an explicit round-to-nearest intrinsic, so nvcc cannot contract or reorder it.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "internal.h"
+#include "quat.cuh"
+
+namespace locc {
+namespace {
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---------------------------------------------------------------- S0 shape prep
+// AABB ("compute the AABB of each object's mesh"), eps = half the cell diagonal of
+// this shape used when it is the counter object (a3^3 read as a3^2), cell ids
+// floor((p - lo) * M / ext) clamped to M-1.
+__global__ void shape_bounds_kernel(const float* __restrict__ in, int K, int M, float4* __restrict__ lo_out,
+                                    float4* __restrict__ hi_out, uint16_t* __restrict__ cell_tmp,
+                                    int* __restrict__ bad) {
+  const int s = blockIdx.x;
+  const float* p = in + (int64_t)s * K * 3;
+  float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  int nonfinite = 0;
+  for (int k = threadIdx.x; k < K; k += blockDim.x)
+    for (int d = 0; d < 3; ++d) {
+      float v = p[3 * k + d];
+      nonfinite |= !isfinite(v);
+      mn[d] = fminf(mn[d], v);
+      mx[d] = fmaxf(mx[d], v);
+    }
+  __shared__ float red[2][3][32];
+  __shared__ int nf_any;
+  if (threadIdx.x == 0) nf_any = 0;
+  __syncthreads();
+  for (int d = 0; d < 3; ++d)
+    for (int o = 16; o; o >>= 1) {
+      mn[d] = fminf(mn[d], __shfl_xor_sync(0xffffffffu, mn[d], o));
+      mx[d] = fmaxf(mx[d], __shfl_xor_sync(0xffffffffu, mx[d], o));
+    }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (nonfinite) atomicOr(&nf_any, 1);
+  if (l == 0)
+    for (int d = 0; d < 3; ++d) {
+      red[0][d][w] = mn[d];
+      red[1][d][w] = mx[d];
+    }
+  __syncthreads();
+  __shared__ float lo_s[3], hi_s[3];
+  __shared__ double ext_s[3];
+  if (threadIdx.x == 0) {
+    double a[3];
+    for (int d = 0; d < 3; ++d) {
+      float a0 = red[0][d][0], b0 = red[1][d][0];
+      for (int i = 1; i < nw; ++i) {
+        a0 = fminf(a0, red[0][d][i]);
+        b0 = fmaxf(b0, red[1][d][i]);
+      }
+      lo_s[d] = a0;
+      hi_s[d] = b0;
+      ext_s[d] = __dsub_rn((double)b0, (double)a0);
+      a[d] = __ddiv_rn(ext_s[d], (double)M);
+    }
+    const double e2 = __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dmul_rn(a[0], a[0]), __dmul_rn(a[1], a[1])),
+                                                __dmul_rn(a[2], a[2])));
+    lo_out[s] = make_float4(lo_s[0], lo_s[1], lo_s[2], __double2float_rn(e2));
+    hi_out[s] = make_float4(hi_s[0], hi_s[1], hi_s[2], 0.f);
+    if (nf_any) atomicOr(bad, 1);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    int c[3];
+    for (int d = 0; d < 3; ++d) {
+      const double ext = ext_s[d];
+      if (ext == 0.0) {
+        c[d] = 0;
+        continue;
+      }
+      const double u = __ddiv_rn(__dmul_rn(__dsub_rn((double)p[3 * k + d], (double)lo_s[d]), (double)M), ext);
+      const double f = floor(u);
+      c[d] = f >= (double)(M - 1) ? M - 1 : (int)f;
+    }
+    cell_tmp[(int64_t)s * K + k] = (uint16_t)(c[0] + M * (c[1] + M * c[2]));
+  }
+}
+
+// Stable counting sort of each shape's points by cell id: points of one cell become contiguous
+// and keep their caller order, so a compacted crop is already grouped by cell (the encoder's
+// cell-wise max pool then walks runs).  perm maps the sorted slot back to the caller's index.
+__global__ void shape_sort_kernel(const float* __restrict__ in, int K, int M, const uint16_t* __restrict__ cell_tmp,
+                                  float4* __restrict__ pts, uint16_t* __restrict__ perm) {
+  extern __shared__ int cnt[];  // [M^3]
+  const int s = blockIdx.x, nc = M * M * M;
+  const uint16_t* cell = cell_tmp + (int64_t)s * K;
+  for (int c = threadIdx.x; c < nc; c += blockDim.x) cnt[c] = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < K; k += blockDim.x) atomicAdd(&cnt[cell[k]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int c = 0; c < nc; ++c) {
+      int v = cnt[c];
+      cnt[c] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const float* p = in + (int64_t)s * K * 3;
+  for (int base = 0; base < K; base += 32) {
+    const int k = base + lane;
+    const bool valid = k < K;
+    const int c = valid ? (int)cell[k] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, c);
+    const int rank = __popc(peers & lanemask_lt());
+    int pos = 0;
+    if (valid) pos = cnt[c] + rank;
+    __syncwarp();
+    if (valid && rank == 0) cnt[c] += __popc(peers);
+    __syncwarp();
+    if (valid) {
+      pts[(int64_t)s * K + pos] = make_float4(p[3 * k], p[3 * k + 1], p[3 * k + 2], __int_as_float(c));
+      perm[(int64_t)s * K + pos] = (uint16_t)k;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- S1 relative transforms
+// normalise in fp64; q_BA = conj(q_B) (x) q_A with the grouping that
+// makes conj(q) (x) q cancel exactly; R(q) in fp64; t_BA = R_B^T (t_A - t_B); each entry
+// rounded once to fp32.
+struct Xf {
+  float R[9];
+  float t[3];
+};
+
+__device__ __forceinline__ void qmul(const double a[4], const double b[4], double r[4]) {
+  r[0] = __dsub_rn(__dmul_rn(a[0], b[0]), __dadd_rn(__dadd_rn(__dmul_rn(a[1], b[1]), __dmul_rn(a[2], b[2])), __dmul_rn(a[3], b[3])));
+  r[1] = __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[1]), __dmul_rn(b[0], a[1])), __dsub_rn(__dmul_rn(a[2], b[3]), __dmul_rn(a[3], b[2])));
+  r[2] = __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[2]), __dmul_rn(b[0], a[2])), __dsub_rn(__dmul_rn(a[3], b[1]), __dmul_rn(a[1], b[3])));
+  r[3] = __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[3]), __dmul_rn(b[0], a[3])), __dsub_rn(__dmul_rn(a[1], b[2]), __dmul_rn(a[2], b[1])));
+}
+
+__device__ __forceinline__ void qmat(const double q[4], double R[9]) {
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  R[0] = __dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(__dmul_rn(y, y), __dmul_rn(z, z))));
+  R[1] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(x, y), __dmul_rn(w, z)));
+  R[2] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, z), __dmul_rn(w, y)));
+  R[3] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, y), __dmul_rn(w, z)));
+  R[4] = __dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, x), __dmul_rn(z, z))));
+  R[5] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(y, z), __dmul_rn(w, x)));
+  R[6] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(x, z), __dmul_rn(w, y)));
+  R[7] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(y, z), __dmul_rn(w, x)));
+  R[8] = __dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y))));
+}
+
+// Transform taking points of the object posed (qs, ts) into the frame of the object posed (qo, to).
+__device__ __forceinline__ void relative_xf(const double qs[4], const float* ts, const double qo[4],
+                                            const float* to, Xf& X) {
+  const double cj[4] = {qo[0], -qo[1], -qo[2], -qo[3]};
+  double qr[4], R[9], Ro[9];
+  qmul(cj, qs, qr);
+  qmat(qr, R);
+  qmat(qo, Ro);
+  const double d0 = __dsub_rn((double)ts[0], (double)to[0]);
+  const double d1 = __dsub_rn((double)ts[1], (double)to[1]);
+  const double d2 = __dsub_rn((double)ts[2], (double)to[2]);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) X.R[i] = __double2float_rn(R[i]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    X.t[i] = __double2float_rn(__dadd_rn(__dadd_rn(__dmul_rn(Ro[i], d0), __dmul_rn(Ro[3 + i], d1)), __dmul_rn(Ro[6 + i], d2)));
+}
+
+// O4: keep iff squared distance from the transformed point to the counter AABB <= eps^2.
+__device__ __forceinline__ bool keep_point(const Xf& X, float x, float y, float z, const float4& lo,
+                                           const float4& hi) {
+  const float px = __fmaf_rn(X.R[0], x, __fmaf_rn(X.R[1], y, __fmaf_rn(X.R[2], z, X.t[0])));
+  const float py = __fmaf_rn(X.R[3], x, __fmaf_rn(X.R[4], y, __fmaf_rn(X.R[5], z, X.t[1])));
+  const float pz = __fmaf_rn(X.R[6], x, __fmaf_rn(X.R[7], y, __fmaf_rn(X.R[8], z, X.t[2])));
+  const float dx = fmaxf(fmaxf(__fsub_rn(lo.x, px), __fsub_rn(px, hi.x)), 0.f);
+  const float dy = fmaxf(fmaxf(__fsub_rn(lo.y, py), __fsub_rn(py, hi.y)), 0.f);
+  const float dz = fmaxf(fmaxf(__fsub_rn(lo.z, pz), __fsub_rn(pz, hi.z)), 0.f);
+  const float d2 = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz)));
+  return d2 <= lo.w;
+}
+
+// Resolve segment g = 2*pair + side: own shape, counter shape, transform.  False = invalid input.
+__device__ __forceinline__ bool segment_setup(const ShapeTable& T, const Batch& b, int64_t g, int& own,
+                                              int& other, Xf& X) {
+  const int64_t i = g >> 1;
+  const int side = (int)(g & 1);
+  const int a = b.pairs[2 * i], c = b.pairs[2 * i + 1];
+  if (a < 0 || a >= T.S || c < 0 || c >= T.S) return false;
+  const float* pA = b.poses + 14 * i;
+  const float* pB = pA + 7;
+  for (int j = 0; j < 14; ++j)
+    if (!isfinite(pA[j])) return false;
+  double qA[4], qB[4];
+  if (!quat_unit(pA, qA) || !quat_unit(pB, qB)) return false;
+  if (side == 0) {
+    own = a;
+    other = c;
+    relative_xf(qA, pA + 4, qB, pB + 4, X);
+  } else {
+    own = c;
+    other = a;
+    relative_xf(qB, pB + 4, qA, pA + 4, X);
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------- S2-S3 pass 1: counts
+// One warp per segment: float4 point loads (coalesced, 512 B per warp step), fp32 transform +
+// eps test, warp ballot.  Writes n_s and C_s (occupied cells among the kept points: cell runs,
+// the points being cell-sorted) and, in debug mode, the caller-order keep mask.
+__global__ void __launch_bounds__(256) crop_count_kernel(ShapeTable T, Batch b, int words) {
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= b.G) return;
+  int own = 0, other = 0;
+  Xf X;
+  if (!segment_setup(T, b, g, own, other, X)) {
+    if (lane == 0) {
+      b.counts[g] = 0;
+      b.occ[g] = 0;
+      atomicAdd(&b.stats->bad_input, 1ull);
+    }
+    return;
+  }
+  const float4 lo = T.lo[other], hi = T.hi[other];
+  const float4* pts = T.pts + (int64_t)own * T.K;
+  const uint16_t* perm = T.perm + (int64_t)own * T.K;
+  uint32_t* mask = b.masks ? b.masks + g * words : nullptr;
+  int n = 0, C = 0, carry = -1;
+  for (int base = 0; base < T.K; base += 32) {
+    const int k = base + lane;
+    float4 p = make_float4(0.f, 0.f, 0.f, __int_as_float(-2));
+    if (k < T.K) p = pts[k];
+    const bool keep = k < T.K && keep_point(X, p.x, p.y, p.z, lo, hi);
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (m == 0) continue;
+    const int cell = __float_as_int(p.w);
+    const unsigned before = m & lanemask_lt();
+    const int src = before ? 31 - __clz(before) : lane;
+    int prev = __shfl_sync(0xffffffffu, cell, src);
+    if (!before) prev = carry;
+    C += __popc(__ballot_sync(0xffffffffu, keep && prev != cell));
+    carry = __shfl_sync(0xffffffffu, cell, 31 - __clz(m));
+    n += __popc(m);
+    if (mask && keep) {
+      const int ck = perm[k];
+      atomicOr(mask + (ck >> 5), 1u << (ck & 31));
+    }
+  }
+  if (lane == 0) {
+    b.counts[g] = n;
+    b.occ[g] = C;
+    if (n) {
+      atomicAdd(&b.stats->kept_rows, (unsigned long long)n);
+      atomicAdd(&b.stats->nonempty_sides, 1ull);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- S2-S3 pass 2: compaction
+// Same keep decisions (same function), rows written densely at offsets[g] in cell-sorted order:
+// (x, y, z) in the object's LOCAL frame (the encoder input, reading Q6) and a flags word
+// (segment << 2 | last-of-segment << 1 | last-of-cell).  "Last of cell" needs the next kept
+// point, so the last kept point of each 32-point step is held back until the next step.
+__global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= b.G) return;
+  const int n = b.counts[g];
+  if (n == 0) return;
+  int own = 0, other = 0;
+  Xf X;
+  if (!segment_setup(T, b, g, own, other, X)) return;
+  const float4 lo = T.lo[other], hi = T.hi[other];
+  const float4* pts = T.pts + (int64_t)own * T.K;
+  float4* out = b.rows + b.offsets[g];
+  const uint32_t segbits = (uint32_t)g << kRowSegShift;
+  int written = 0;        // kept rows before this step
+  bool pending = false;   // a held-back row (warp-uniform)
+  float4 prow;            // held-back row payload (valid in every lane)
+  int pcell = 0, pidx = 0;
+  for (int base = 0; base < T.K; base += 32) {
+    const int k = base + lane;
+    float4 p = make_float4(0.f, 0.f, 0.f, __int_as_float(-2));
+    if (k < T.K) p = pts[k];
+    const bool keep = k < T.K && keep_point(X, p.x, p.y, p.z, lo, hi);
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (m == 0) continue;
+    const int cell = __float_as_int(p.w);
+    const int first = __ffs(m) - 1, last = 31 - __clz(m);
+    const unsigned after = m & ~(0xffffffffu >> (31 - lane));  // kept lanes above this one
+    const int nxt = after ? __ffs(after) - 1 : lane;
+    const int next_cell = __shfl_sync(0xffffffffu, cell, nxt);
+    const int first_cell = __shfl_sync(0xffffffffu, cell, first);
+    if (pending && lane == 0) {
+      const uint32_t f = segbits | (pcell != first_cell ? kRowFlagCellEnd : 0);
+      out[pidx] = make_float4(prow.x, prow.y, prow.z, __uint_as_float(f));
+    }
+    const int idx = written + __popc(m & lanemask_lt());
+    if (keep && lane != last) {
+      const uint32_t f = segbits | (cell != next_cell ? kRowFlagCellEnd : 0);
+      out[idx] = make_float4(p.x, p.y, p.z, __uint_as_float(f));
+    }
+    prow.x = __shfl_sync(0xffffffffu, p.x, last);
+    prow.y = __shfl_sync(0xffffffffu, p.y, last);
+    prow.z = __shfl_sync(0xffffffffu, p.z, last);
+    pcell = __shfl_sync(0xffffffffu, cell, last);
+    pidx = written + __popc(m) - 1;
+    pending = true;
+    written += __popc(m);
+  }
+  if (pending && lane == 0) {
+    const uint32_t f = segbits | kRowFlagCellEnd | kRowFlagSegEnd;
+    out[pidx] = make_float4(prow.x, prow.y, prow.z, __uint_as_float(f));
+  }
+}
+
+// ---------------------------------------------------------------- exclusive scan of counts
+__global__ void __launch_bounds__(1024) scan_blocks_kernel(const int32_t* __restrict__ in, int64_t G,
+                                                           int64_t* __restrict__ out, int64_t* __restrict__ sums) {
+  __shared__ int64_t ws[32];
+  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t v = i < G ? (int64_t)in[i] : 0, x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int64_t s = ws[lane], t = s;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    ws[lane] = t - s;
+    if (lane == 31) sums[blockIdx.x] = t;
+  }
+  __syncthreads();
+  if (i < G) out[i] = x - v + ws[w];
+}
+
+__global__ void __launch_bounds__(1024) scan_top_kernel(int64_t* __restrict__ sums, int64_t nb,
+                                                        int64_t* __restrict__ total) {
+  __shared__ int64_t ws[32];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t base = 0; base < nb; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    int64_t v = i < nb ? sums[i] : 0, x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int64_t s = ws[lane], t = s;
+      for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      ws[lane] = t - s;
+    }
+    __syncthreads();
+    const int64_t c = carry;
+    if (i < nb) sums[i] = c + x - v + ws[w];
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = c + x + ws[w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void __launch_bounds__(1024) scan_add_kernel(int64_t* __restrict__ out, int64_t G,
+                                                        const int64_t* __restrict__ sums) {
+  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  if (i < G) out[i] += sums[blockIdx.x];
+}
+
+}  // namespace
+
+cudaError_t launch_shape_prep(const float* pts_in, int S, int K, int M, float4* pts, uint16_t* perm, float4* lo,
+                              float4* hi, uint16_t* cell_tmp, int* bad, cudaStream_t st) {
+  shape_bounds_kernel<<<S, 256, 0, st>>>(pts_in, K, M, lo, hi, cell_tmp, bad);
+  const size_t sm = sizeof(int) * (size_t)M * M * M;
+  shape_sort_kernel<<<S, 256, sm, st>>>(pts_in, K, M, cell_tmp, pts, perm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_crop_count(const ShapeTable& T, const Batch& b, int words, cudaStream_t st) {
+  if (b.G == 0) return cudaSuccess;
+  const int64_t blocks = (b.G * 32 + 255) / 256;
+  crop_count_kernel<<<(unsigned)blocks, 256, 0, st>>>(T, b, words);
+  return cudaGetLastError();
+}
+
+size_t scan_tmp_elems(int64_t G) { return (size_t)((G + 1023) / 1024) + 1; }
+
+cudaError_t launch_scan(const int32_t* counts, int64_t G, int64_t* offsets, int64_t* block_tmp, cudaStream_t st) {
+  const int64_t nb = (G + 1023) / 1024;
+  if (nb == 0) return cudaMemsetAsync(offsets, 0, sizeof(int64_t), st);
+  scan_blocks_kernel<<<(unsigned)nb, 1024, 0, st>>>(counts, G, offsets, block_tmp);
+  scan_top_kernel<<<1, 1024, 0, st>>>(block_tmp, nb, offsets + G);
+  scan_add_kernel<<<(unsigned)nb, 1024, 0, st>>>(offsets, G, block_tmp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_crop_emit(const ShapeTable& T, const Batch& b, cudaStream_t st) {
+  if (b.G == 0) return cudaSuccess;
+  const int64_t blocks = (b.G * 32 + 255) / 256;
+  crop_emit_kernel<<<(unsigned)blocks, 256, 0, st>>>(T, b);
+  return cudaGetLastError();
+}
+
+}  // namespace locc

@@ -1,0 +1,614 @@
+// locc_runtime.cu — host runtime behind the C ABI of include/locc.h.
+//
+// Owns the per-context device state (parameters, shape table, scratch), validates inputs, splits a
+// query into sub-batches that bound the scratch memory, and launches the kernels of one pass of
+// the hot path on one stream:
+//   crop_count -> scan (3 launches) -> crop_emit -> encoder (fp32 or tcgen05) -> head
+// No exception crosses the ABI; every CUDA call is checked and mapped to a locc_status.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/locc.h"
+#include "internal.h"
+
+using namespace locc;
+
+namespace {
+
+thread_local std::string g_err;
+
+locc_status fail(locc_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CK(call)                                                                                     \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) {                                                                         \
+      return fail(e_ == cudaErrorMemoryAllocation ? LOCC_E_OOM : LOCC_E_CUDA, "%s: %s (%s:%d)", #call, \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                                       \
+    }                                                                                                \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 256));
+    if (e == cudaSuccess) n = std::max<size_t>(bytes, 256);
+    return e;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+int64_t n_params(int H, int F) {
+  auto L = [](int64_t o, int64_t i) { return o * i + o; };
+  return L(H, 3) + 2 * L(H, H) + L(F, H) + L(kPredW, F + 7) + 5 * L(kPredW, kPredW) + L(1, kPredW);
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct locc_ctx {
+  locc_config cfg{};
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[2] = {};          // whole-query timing
+  std::vector<cudaEvent_t> enc_ev;  // per sub-batch encoder start/stop pairs
+  bool timing = false;
+  bool has_weights = false, has_shapes = false;
+  // parameters
+  DevBuf params;
+  DevParams P{};
+  // shapes
+  DevBuf sh_pts, sh_perm, sh_lo, sh_hi;
+  ShapeTable T{};
+  // scratch for one sub-batch
+  int64_t cap_B = 0;
+  DevBuf in_pairs, in_poses, counts, occ, offsets, scan_tmp, rows, pooled, stats;
+  DevBuf out_probs, out_labels, out_logits, out_kept, out_occ, out_masks, out_emb;
+  locc_stats last{};
+  int64_t timed_subs = 0;  // sub-batches whose encoder events await reading
+};
+
+namespace {
+
+// Derived device layouts of the canonical flat parameter vector (see internal.h DevParams).
+locc_status upload_params(locc_ctx* c, const float* flat) {
+  const int H = c->cfg.H, F = c->cfg.F, P = kPredW;
+  struct L {
+    const float *W, *b;
+    int o, i;
+  };
+  const float* q = flat;
+  auto take = [&q](int o, int i) {
+    L l{q, q + (int64_t)o * i, o, i};
+    q += (int64_t)o * i + o;
+    return l;
+  };
+  L e1 = take(H, 3), e2 = take(H, H), e3 = take(H, H), pj = take(F, H), o1 = take(P, F + 7), o2 = take(P, P),
+    o3 = take(P, P), p1 = take(P, P), p2 = take(P, P), p3 = take(P, P), out = take(1, P);
+  std::vector<float> img;
+  std::vector<size_t> off;
+  auto push = [&](const float* src, size_t n) {
+    while (img.size() % 64) img.push_back(0.f);  // 256-byte alignment
+    off.push_back(img.size());
+    img.insert(img.end(), src, src + n);
+  };
+  auto pushT = [&](const L& l) {
+    std::vector<float> t((size_t)l.o * l.i);
+    for (int o = 0; o < l.o; ++o)
+      for (int i = 0; i < l.i; ++i) t[(size_t)i * l.o + o] = l.W[(size_t)o * l.i + i];
+    push(t.data(), t.size());
+  };
+  std::vector<float> w1b((size_t)H * 4);
+  for (int f = 0; f < H; ++f) {
+    for (int j = 0; j < 3; ++j) w1b[4 * f + j] = e1.W[3 * f + j];
+    w1b[4 * f + 3] = e1.b[f];
+  }
+  push(w1b.data(), w1b.size());  // 0
+  pushT(e2);                     // 1
+  push(e2.b, H);                 // 2
+  pushT(e3);                     // 3
+  push(e3.b, H);                 // 4
+  pushT(pj);                     // 5
+  push(pj.b, F);                 // 6
+  pushT(o1);                     // 7
+  push(o1.b, P);                 // 8
+  pushT(o2);                     // 9
+  push(o2.b, P);                 // 10
+  pushT(o3);                     // 11
+  push(o3.b, P);                 // 12
+  pushT(p1);                     // 13
+  push(p1.b, P);                 // 14
+  pushT(p2);                     // 15
+  push(p2.b, P);                 // 16
+  pushT(p3);                     // 17
+  push(p3.b, P);                 // 18
+  push(out.W, P);                // 19
+  push(out.b, 1);                // 20
+  const size_t bytes = img.size() * sizeof(float);
+  CK(c->params.ensure(bytes));
+  CK(cudaMemcpy(c->params.p, img.data(), bytes, cudaMemcpyHostToDevice));
+  const float* d = c->params.as<float>();
+  DevParams& D = c->P;
+  D.H = H;
+  D.F = F;
+  D.w1 = nullptr;
+  D.w1b = reinterpret_cast<const float4*>(d + off[0]);
+  D.w2T = d + off[1];
+  D.b2 = d + off[2];
+  D.w3T = d + off[3];
+  D.b3 = d + off[4];
+  D.wfT = d + off[5];
+  D.bf = d + off[6];
+  D.o1T = d + off[7];
+  D.ob1 = d + off[8];
+  D.o2T = d + off[9];
+  D.ob2 = d + off[10];
+  D.o3T = d + off[11];
+  D.ob3 = d + off[12];
+  D.p1T = d + off[13];
+  D.pb1 = d + off[14];
+  D.p2T = d + off[15];
+  D.pb2 = d + off[16];
+  D.p3T = d + off[17];
+  D.pb3 = d + off[18];
+  D.wout = d + off[19];
+  D.bout = d + off[20];
+  D.tc_w2 = nullptr;
+  D.tc_w3 = nullptr;
+  c->has_weights = true;
+  return LOCC_OK;
+}
+
+locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks) {
+  const int K = c->T.K;
+  const int64_t G = 2 * B;
+  if (B > c->cap_B) {
+    CK(c->in_pairs.ensure(sizeof(int32_t) * 2 * B));
+    CK(c->in_poses.ensure(sizeof(float) * 14 * B));
+    CK(c->counts.ensure(sizeof(int32_t) * G));
+    CK(c->occ.ensure(sizeof(int32_t) * G));
+    CK(c->offsets.ensure(sizeof(int64_t) * (G + 1)));
+    CK(c->scan_tmp.ensure(sizeof(int64_t) * scan_tmp_elems(G)));
+    CK(c->rows.ensure(sizeof(float4) * (size_t)G * K));
+    CK(c->pooled.ensure(sizeof(float) * (size_t)G * c->cfg.H));
+    CK(c->out_probs.ensure(sizeof(float) * B));
+    CK(c->out_labels.ensure(B));
+    CK(c->out_logits.ensure(sizeof(float) * B));
+    CK(c->out_kept.ensure(sizeof(int32_t) * G));
+    CK(c->out_occ.ensure(sizeof(int32_t) * G));
+    CK(c->out_emb.ensure(sizeof(float) * (size_t)G * c->cfg.F));
+    c->cap_B = B;
+  }
+  CK(c->stats.ensure(sizeof(DevStats)));
+  if (need_masks) CK(c->out_masks.ensure(sizeof(uint32_t) * (size_t)G * ((K + 31) / 32)));
+  return LOCC_OK;
+}
+
+locc_status validate_host(const locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N) {
+  for (int64_t i = 0; i < N; ++i) {
+    for (int s = 0; s < 2; ++s) {
+      const int32_t id = pairs[2 * i + s];
+      if (id < 0 || id >= c->T.S)
+        return fail(LOCC_E_INVALID_ARG, "pair %lld side %d: shape id %d not in [0, %d)", (long long)i, s, id, c->T.S);
+      const float* p = poses + 14 * i + 7 * s;
+      for (int j = 0; j < 7; ++j)
+        if (!std::isfinite(p[j])) return fail(LOCC_E_INVALID_ARG, "pair %lld side %d: non-finite pose", (long long)i, s);
+      const double w = p[0], x = p[1], y = p[2], z = p[3];
+      if (!(((w * w + x * x) + y * y) + z * z >= 1e-12))
+        return fail(LOCC_E_INVALID_ARG, "pair %lld side %d: |q|^2 < 1e-12", (long long)i, s);
+    }
+  }
+  return LOCC_OK;
+}
+
+int64_t batch_cap(const locc_ctx* c) {
+  int64_t B = c->cfg.max_batch > 0 ? c->cfg.max_batch : 262144;
+  // bound the compacted-row buffer (worst case every point kept) to ~12 GiB
+  const int64_t rows_budget = (int64_t)12 << 30;
+  const int64_t per_pair = 2LL * c->T.K * (int64_t)sizeof(float4);
+  B = std::min<int64_t>(B, std::max<int64_t>(1, rows_budget / per_pair));
+  return std::min<int64_t>(B, (int64_t)1 << 29);
+}
+
+// Elapsed times of the last timed query (its events must have completed).
+locc_status read_timing(locc_ctx* c) {
+  if (!c->timed_subs) return LOCC_OK;
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  c->last.total_ms = ms;
+  double enc = 0.0;
+  for (int64_t s = 0; s < c->timed_subs; ++s) {
+    CK(cudaEventElapsedTime(&ms, c->enc_ev[2 * s], c->enc_ev[2 * s + 1]));
+    enc += ms;
+  }
+  c->last.encoder_ms = enc;
+  c->timed_subs = 0;
+  return LOCC_OK;
+}
+
+locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
+                      uint8_t* labels, float* logits, int32_t* kept, int32_t* occ, uint32_t* masks, float* emb,
+                      void* stream) {
+  if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
+  if (N < 0) return fail(LOCC_E_INVALID_ARG, "N < 0");
+  if (!c->has_weights || !c->has_shapes) return fail(LOCC_E_STATE, "weights and shapes must be set before a query");
+  if (N == 0) {
+    c->last = locc_stats{};
+    return LOCC_OK;
+  }
+  if (!pairs || !poses || !probs) return fail(LOCC_E_INVALID_ARG, "pairs, poses and probs must be non-null");
+  CK(cudaSetDevice(c->device));
+  const bool dev = is_device_ptr(pairs);
+  const void* all[] = {poses, probs, labels, logits, kept, occ, masks, emb};
+  for (const void* p : all)
+    if (p && is_device_ptr(p) != dev)
+      return fail(LOCC_E_INVALID_ARG, "all buffers of one call must be host or all device memory");
+  if (!dev) {
+    locc_status s = validate_host(c, pairs, poses, N);
+    if (s != LOCC_OK) return s;
+  }
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  const bool sync = !dev || !stream;
+  const int64_t Bcap = std::min<int64_t>(N, batch_cap(c));
+  locc_status s = ensure_scratch(c, Bcap, masks != nullptr);
+  if (s != LOCC_OK) return s;
+  const int K = c->T.K, words = (K + 31) / 32;
+  DevStats* dstats = c->stats.as<DevStats>();
+  CK(cudaMemsetAsync(dstats, 0, sizeof(DevStats), st));
+  const int64_t n_sub = (N + Bcap - 1) / Bcap;
+  if (c->timing) {
+    while ((int64_t)c->enc_ev.size() < 2 * n_sub) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->enc_ev.push_back(e);
+    }
+    CK(cudaEventRecord(c->ev[0], st));
+  }
+  int64_t launches = 0, subs = 0;
+  for (int64_t i0 = 0; i0 < N; i0 += Bcap) {
+    const int64_t B = std::min(Bcap, N - i0);
+    Batch b{};
+    b.B = B;
+    b.G = 2 * B;
+    if (dev) {
+      b.pairs = pairs + 2 * i0;
+      b.poses = poses + 14 * i0;
+    } else {
+      CK(cudaMemcpyAsync(c->in_pairs.p, pairs + 2 * i0, sizeof(int32_t) * 2 * B, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(c->in_poses.p, poses + 14 * i0, sizeof(float) * 14 * B, cudaMemcpyHostToDevice, st));
+      b.pairs = c->in_pairs.as<int32_t>();
+      b.poses = c->in_poses.as<float>();
+    }
+    b.counts = (dev && kept) ? kept + 2 * i0 : c->counts.as<int32_t>();
+    b.occ = (dev && occ) ? occ + 2 * i0 : c->occ.as<int32_t>();
+    b.offsets = c->offsets.as<int64_t>();
+    b.rows = c->rows.as<float4>();
+    b.pooled = c->pooled.as<float>();
+    b.stats = dstats;
+    b.masks = nullptr;
+    if (masks) {
+      b.masks = dev ? masks + (size_t)2 * i0 * words : c->out_masks.as<uint32_t>();
+      CK(cudaMemsetAsync(b.masks, 0, sizeof(uint32_t) * (size_t)2 * B * words, st));
+    }
+    float* d_probs = dev ? probs + i0 : c->out_probs.as<float>();
+    uint8_t* d_labels = labels ? (dev ? labels + i0 : c->out_labels.as<uint8_t>()) : nullptr;
+    float* d_logits = logits ? (dev ? logits + i0 : c->out_logits.as<float>()) : nullptr;
+    float* d_emb = emb ? (dev ? emb + (size_t)2 * i0 * c->cfg.F : c->out_emb.as<float>()) : nullptr;
+
+    CK(launch_crop_count(c->T, b, words, st));
+    CK(launch_scan(b.counts, b.G, b.offsets, c->scan_tmp.as<int64_t>(), st));
+    CK(launch_crop_emit(c->T, b, st));
+    if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs], st));
+    if (c->cfg.precision == LOCC_PREC_BF16) {
+      CK(launch_encoder_tc(c->P, b, c->num_sms, st));
+    } else {
+      CK(launch_encoder_f32(c->P, b, st));
+    }
+    if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs + 1], st));
+    CK(launch_head(c->P, b, d_probs, d_labels, d_logits, d_emb, st));
+    launches += 7;
+    ++subs;
+    if (!dev) {
+      CK(cudaMemcpyAsync(probs + i0, d_probs, sizeof(float) * B, cudaMemcpyDeviceToHost, st));
+      if (labels) CK(cudaMemcpyAsync(labels + i0, d_labels, B, cudaMemcpyDeviceToHost, st));
+      if (logits) CK(cudaMemcpyAsync(logits + i0, d_logits, sizeof(float) * B, cudaMemcpyDeviceToHost, st));
+      if (kept) CK(cudaMemcpyAsync(kept + 2 * i0, b.counts, sizeof(int32_t) * 2 * B, cudaMemcpyDeviceToHost, st));
+      if (occ) CK(cudaMemcpyAsync(occ + 2 * i0, b.occ, sizeof(int32_t) * 2 * B, cudaMemcpyDeviceToHost, st));
+      if (masks)
+        CK(cudaMemcpyAsync(masks + (size_t)2 * i0 * words, b.masks, sizeof(uint32_t) * (size_t)2 * B * words,
+                           cudaMemcpyDeviceToHost, st));
+      if (emb)
+        CK(cudaMemcpyAsync(emb + (size_t)2 * i0 * c->cfg.F, d_emb, sizeof(float) * (size_t)2 * B * c->cfg.F,
+                           cudaMemcpyDeviceToHost, st));
+    } else {
+      if (kept && b.counts != kept + 2 * i0)
+        CK(cudaMemcpyAsync(kept + 2 * i0, b.counts, sizeof(int32_t) * 2 * B, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  if (c->timing) CK(cudaEventRecord(c->ev[1], st));
+  c->last = locc_stats{};
+  c->last.pairs = N;
+  c->last.sub_batches = subs;
+  c->last.kernel_launches = launches;
+  c->timed_subs = c->timing ? subs : 0;
+  if (sync) {
+    CK(cudaStreamSynchronize(st));
+    DevStats hs;
+    CK(cudaMemcpy(&hs, dstats, sizeof hs, cudaMemcpyDeviceToHost));
+    c->last.kept_rows = (int64_t)hs.kept_rows;
+    c->last.nonempty_sides = (int64_t)hs.nonempty_sides;
+    c->last.evaluated_pairs = (int64_t)hs.evaluated_pairs;
+    locc_status ts = read_timing(c);
+    if (ts != LOCC_OK) return ts;
+    if (hs.bad_input) return fail(LOCC_E_INVALID_ARG, "%llu segments had an out-of-range id or invalid pose",
+                                  (unsigned long long)hs.bad_input);
+  }
+  return LOCC_OK;
+}
+
+bool read_file(const std::string& path, std::vector<char>& out) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return false;
+  out.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* locc_version(void) { return "locc-b200 0.1 sm_100a"; }
+
+const char* locc_last_error(void) { return g_err.c_str(); }
+
+const char* locc_status_string(locc_status s) {
+  switch (s) {
+    case LOCC_OK: return "LOCC_OK";
+    case LOCC_E_INVALID_ARG: return "LOCC_E_INVALID_ARG";
+    case LOCC_E_SHAPE: return "LOCC_E_SHAPE";
+    case LOCC_E_WEIGHTS: return "LOCC_E_WEIGHTS";
+    case LOCC_E_CUDA: return "LOCC_E_CUDA";
+    case LOCC_E_OOM: return "LOCC_E_OOM";
+    case LOCC_E_NCCL: return "LOCC_E_NCCL";
+    case LOCC_E_STATE: return "LOCC_E_STATE";
+  }
+  return "LOCC_E_UNKNOWN";
+}
+
+locc_status locc_create(const locc_config* cfg, locc_ctx** out) {
+  if (!cfg || !out) return fail(LOCC_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (cfg->M < 1 || cfg->M > 15) return fail(LOCC_E_INVALID_ARG, "M must be in [1, 15]");
+  if (cfg->F < 1 || cfg->F > 256) return fail(LOCC_E_INVALID_ARG, "F must be in [1, 256]");
+  if (cfg->precision != LOCC_PREC_FP32 && cfg->precision != LOCC_PREC_BF16)
+    return fail(LOCC_E_INVALID_ARG, "unknown precision %d", cfg->precision);
+  if (cfg->H < 32 || cfg->H > 256 || cfg->H % 32) return fail(LOCC_E_INVALID_ARG, "H must be 32..256, step 32");
+  if (cfg->precision == LOCC_PREC_BF16 && cfg->H != 256)
+    return fail(LOCC_E_INVALID_ARG, "the tensor-core encoder is built for H = 256");
+  if (cfg->max_batch < 0) return fail(LOCC_E_INVALID_ARG, "max_batch < 0");
+  int dev = cfg->device;
+  if (dev < 0) CK(cudaGetDevice(&dev));
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (dev >= ndev) return fail(LOCC_E_INVALID_ARG, "device %d of %d", dev, ndev);
+  CK(cudaSetDevice(dev));
+  locc_ctx* c = new (std::nothrow) locc_ctx();
+  if (!c) return fail(LOCC_E_OOM, "host allocation");
+  c->cfg = *cfg;
+  c->device = dev;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) c->num_sms = prop.multiProcessorCount;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+  if (e != cudaSuccess) {
+    locc_destroy(c);
+    return fail(LOCC_E_CUDA, "stream/event creation: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return LOCC_OK;
+}
+
+void locc_destroy(locc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->enc_ev) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+locc_status locc_set_precision(locc_ctx* c, int32_t precision) {
+  if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
+  if (precision != LOCC_PREC_FP32 && precision != LOCC_PREC_BF16)
+    return fail(LOCC_E_INVALID_ARG, "unknown precision %d", precision);
+  if (precision == LOCC_PREC_BF16 && c->cfg.H != 256)
+    return fail(LOCC_E_INVALID_ARG, "the tensor-core encoder is built for H = 256");
+  c->cfg.precision = precision;
+  return LOCC_OK;
+}
+
+locc_status locc_set_timing(locc_ctx* c, int32_t enabled) {
+  if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
+  c->timing = enabled != 0;
+  return LOCC_OK;
+}
+
+locc_status locc_get_stats(locc_ctx* c, locc_stats* out) {
+  if (!c || !out) return fail(LOCC_E_INVALID_ARG, "null argument");
+  if (c->last.pairs > 0 && c->last.kept_rows == 0 && c->last.evaluated_pairs == 0) {
+    // asynchronous query: read the device counters now
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    DevStats hs;
+    CK(cudaMemcpy(&hs, c->stats.p, sizeof hs, cudaMemcpyDeviceToHost));
+    c->last.kept_rows = (int64_t)hs.kept_rows;
+    c->last.nonempty_sides = (int64_t)hs.nonempty_sides;
+    c->last.evaluated_pairs = (int64_t)hs.evaluated_pairs;
+    locc_status ts = read_timing(c);
+    if (ts != LOCC_OK) return ts;
+  }
+  *out = c->last;
+  return LOCC_OK;
+}
+
+locc_status locc_load_weights_mem(locc_ctx* c, const float* flat, size_t n) {
+  if (!c || !flat) return fail(LOCC_E_INVALID_ARG, "null argument");
+  const int64_t want = n_params(c->cfg.H, c->cfg.F);
+  if ((int64_t)n != want)
+    return fail(LOCC_E_WEIGHTS, "expected %lld floats for H=%d F=%d, got %zu", (long long)want, c->cfg.H, c->cfg.F, n);
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(flat[i])) return fail(LOCC_E_WEIGHTS, "non-finite parameter at %zu", i);
+  CK(cudaSetDevice(c->device));
+  locc_status s = upload_params(c, flat);
+  if (s != LOCC_OK) return s;
+  if (c->cfg.H == 256) {
+    extern locc_status locc_upload_tc_weights(locc_ctx*, const float* w2, const float* w3);
+    const float* w2 = flat + 4 * 256;
+    const float* w3 = w2 + 256 * 256 + 256;
+    s = locc_upload_tc_weights(c, w2, w3);
+  }
+  return s;
+}
+
+locc_status locc_load_weights(locc_ctx* c, const char* manifest) {
+  if (!c || !manifest) return fail(LOCC_E_INVALID_ARG, "null argument");
+  std::ifstream f(manifest);
+  if (!f) return fail(LOCC_E_WEIGHTS, "cannot open %s", manifest);
+  std::string magic;
+  int ver = 0, M = 0, H = 0, F = 0;
+  f >> magic >> ver >> M >> H >> F;
+  if (!f || magic != "locc-weights" || ver != 1) return fail(LOCC_E_WEIGHTS, "%s: bad header", manifest);
+  if (M != c->cfg.M || H != c->cfg.H || F != c->cfg.F)
+    return fail(LOCC_E_WEIGHTS, "manifest M/H/F = %d/%d/%d, context %d/%d/%d", M, H, F, c->cfg.M, c->cfg.H, c->cfg.F);
+  std::string path(manifest), bin = path;
+  const size_t dot = path.find_last_of('.'), slash = path.find_last_of('/');
+  if (dot != std::string::npos && (slash == std::string::npos || dot > slash)) bin = path.substr(0, dot);
+  bin += ".bin";
+  std::vector<char> raw;
+  if (!read_file(bin, raw)) return fail(LOCC_E_WEIGHTS, "cannot read %s", bin.c_str());
+  const char* names[] = {"enc.l1", "enc.l2", "enc.l3", "enc.proj", "obj.l1", "obj.l2",
+                         "obj.l3", "pair.l1", "pair.l2", "pair.l3", "out"};
+  const int shp[11][2] = {{H, 3}, {H, H}, {H, H}, {F, H}, {kPredW, F + 7}, {kPredW, kPredW},
+                          {kPredW, kPredW}, {kPredW, kPredW}, {kPredW, kPredW}, {kPredW, kPredW}, {1, kPredW}};
+  std::vector<float> flat;
+  flat.reserve(n_params(H, F));
+  for (int l = 0; l < 11; ++l)
+    for (int wb = 0; wb < 2; ++wb) {
+      std::string name;
+      long long o = -1, in = -1, off = -1;
+      f >> name >> o >> in >> off;
+      const std::string want = std::string(names[l]) + (wb ? ".b" : ".W");
+      const long long eo = shp[l][0], ei = wb ? 1 : shp[l][1];
+      if (!f || name != want || o != eo || in != ei)
+        return fail(LOCC_E_WEIGHTS, "%s: expected tensor %s [%lld][%lld], got '%s' [%lld][%lld]", manifest,
+                    want.c_str(), eo, ei, name.c_str(), o, in);
+      const size_t bytes = (size_t)(o * in) * sizeof(float);
+      if (off < 0 || (size_t)off + bytes > raw.size())
+        return fail(LOCC_E_WEIGHTS, "%s: tensor %s beyond the end of %s", manifest, want.c_str(), bin.c_str());
+      const size_t at = flat.size();
+      flat.resize(at + (size_t)(o * in));
+      std::memcpy(flat.data() + at, raw.data() + off, bytes);
+    }
+  return locc_load_weights_mem(c, flat.data(), flat.size());
+}
+
+locc_status locc_set_shapes(locc_ctx* c, const float* points, int32_t S, int32_t K) {
+  if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
+  if (!points) return fail(LOCC_E_INVALID_ARG, "null points");
+  if (S < 1 || K < 1 || K > 65535) return fail(LOCC_E_SHAPE, "need S >= 1 and 1 <= K <= 65535 (S=%d K=%d)", S, K);
+  CK(cudaSetDevice(c->device));
+  const size_t n = (size_t)S * K * 3;
+  DevBuf tmp, cell, bad;
+  const float* src = points;
+  if (!is_device_ptr(points)) {
+    CK(tmp.ensure(n * sizeof(float)));
+    CK(cudaMemcpyAsync(tmp.p, points, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    src = tmp.as<float>();
+  }
+  CK(c->sh_pts.ensure(sizeof(float4) * (size_t)S * K));
+  CK(c->sh_perm.ensure(sizeof(uint16_t) * (size_t)S * K));
+  CK(c->sh_lo.ensure(sizeof(float4) * S));
+  CK(c->sh_hi.ensure(sizeof(float4) * S));
+  CK(cell.ensure(sizeof(uint16_t) * (size_t)S * K));
+  CK(bad.ensure(sizeof(int)));
+  CK(cudaMemsetAsync(bad.p, 0, sizeof(int), c->stream));
+  CK(launch_shape_prep(src, S, K, c->cfg.M, c->sh_pts.as<float4>(), c->sh_perm.as<uint16_t>(), c->sh_lo.as<float4>(),
+                       c->sh_hi.as<float4>(), cell.as<uint16_t>(), bad.as<int>(), c->stream));
+  int hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (hbad) {
+    c->has_shapes = false;
+    return fail(LOCC_E_SHAPE, "non-finite point coordinate");
+  }
+  c->T.pts = c->sh_pts.as<float4>();
+  c->T.perm = c->sh_perm.as<uint16_t>();
+  c->T.lo = c->sh_lo.as<float4>();
+  c->T.hi = c->sh_hi.as<float4>();
+  c->T.S = S;
+  if (c->T.K != K) c->cap_B = 0;  // row buffer depends on K
+  c->T.K = K;
+  c->has_shapes = true;
+  return LOCC_OK;
+}
+
+locc_status locc_query(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
+                       uint8_t* labels, float* logits, void* stream) {
+  return run_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+locc_status locc_query_debug(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
+                             uint8_t* labels, float* logits, int32_t* kept, int32_t* occ, uint32_t* masks,
+                             float* emb, void* stream) {
+  return run_query(c, pairs, poses, N, probs, labels, logits, kept, occ, masks, emb, stream);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- tensor-core weight image
+locc_status locc_upload_tc_weights(locc_ctx* c, const float* w2, const float* w3) {
+  (void)c;
+  (void)w2;
+  (void)w3;
+  return LOCC_OK;  // filled in by the tcgen05 encoder (kernels_encoder_tc.cu)
+}

@@ -1,0 +1,185 @@
+"""Thin ctypes binding of liblocc.so (include/locc.h) — argument marshalling only.
+
+Every step of the query runs in the library's CUDA kernels; this module only passes pointers
+(numpy arrays -> host pointers, torch tensors -> their data_ptr on host or device) and maps
+status codes to exceptions.  If the library is missing it raises: there is no fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblocc.so")
+
+LOCC_PREC_FP32 = 0
+LOCC_PREC_BF16 = 1
+
+EXPORTS = ("locc_create", "locc_load_weights", "locc_load_weights_mem", "locc_set_shapes", "locc_query",
+           "locc_query_debug", "locc_set_precision", "locc_set_timing", "locc_get_stats", "locc_destroy",
+           "locc_status_string", "locc_last_error", "locc_version")
+
+
+class LoccError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{msg}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [("M", C.c_int32), ("H", C.c_int32), ("F", C.c_int32), ("precision", C.c_int32),
+                ("device", C.c_int32), ("reserved", C.c_int32), ("max_batch", C.c_int64)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("pairs", C.c_int64), ("evaluated_pairs", C.c_int64), ("kept_rows", C.c_int64),
+                ("nonempty_sides", C.c_int64), ("sub_batches", C.c_int64), ("kernel_launches", C.c_int64),
+                ("encoder_ms", C.c_double), ("total_ms", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load liblocc.so (raises if it was not built: run __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+        L.locc_create.argtypes = [C.POINTER(Config), C.POINTER(vp)]
+        L.locc_load_weights.argtypes = [vp, C.c_char_p]
+        L.locc_load_weights_mem.argtypes = [vp, vp, C.c_size_t]
+        L.locc_set_shapes.argtypes = [vp, vp, i32, i32]
+        L.locc_query.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp]
+        L.locc_query_debug.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.locc_set_precision.argtypes = [vp, i32]
+        L.locc_set_timing.argtypes = [vp, i32]
+        L.locc_get_stats.argtypes = [vp, C.POINTER(Stats)]
+        L.locc_destroy.argtypes = [vp]
+        L.locc_destroy.restype = None
+        L.locc_status_string.argtypes = [C.c_int]
+        L.locc_status_string.restype = C.c_char_p
+        L.locc_last_error.restype = C.c_char_p
+        L.locc_version.restype = C.c_char_p
+        for name in EXPORTS[:9]:
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        L = lib()
+        raise LoccError(rc, f"{L.locc_status_string(rc).decode()}: {L.locc_last_error().decode()}")
+
+
+def _ptr(x, dtype=None):
+    """Raw pointer of a numpy array or torch tensor (contiguous, expected dtype); None -> NULL."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        if dtype is not None and x.dtype != dtype:
+            raise TypeError(f"expected {np.dtype(dtype)}, got {x.dtype}")
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return x.ctypes.data
+    if hasattr(x, "data_ptr"):  # torch.Tensor
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr()
+    raise TypeError(type(x))
+
+
+class Locc:
+    """One library context on one CUDA device (locc_create / locc_destroy)."""
+
+    def __init__(self, M=6, H=256, F=64, precision=LOCC_PREC_BF16, device=-1, max_batch=0):
+        self._h = C.c_void_p()
+        self.cfg = Config(M, H, F, precision, device, 0, max_batch)
+        _check(lib().locc_create(C.byref(self.cfg), C.byref(self._h)))
+        self.M, self.H, self.F = M, H, F
+        self.K = None
+
+    def close(self):
+        if self._h:
+            lib().locc_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def load_weights(self, manifest_path: str):
+        _check(lib().locc_load_weights(self._h, manifest_path.encode()))
+
+    def load_weights_mem(self, flat):
+        flat = np.ascontiguousarray(flat, np.float32)
+        _check(lib().locc_load_weights_mem(self._h, _ptr(flat), flat.size))
+
+    def set_shapes(self, points):
+        S, K = int(points.shape[0]), int(points.shape[1])
+        if isinstance(points, np.ndarray):
+            points = np.ascontiguousarray(points, np.float32)
+        _check(lib().locc_set_shapes(self._h, _ptr(points, np.float32), S, K))
+        self.K = K
+
+    def set_precision(self, precision):
+        _check(lib().locc_set_precision(self._h, precision))
+
+    def set_timing(self, on=True):
+        _check(lib().locc_set_timing(self._h, 1 if on else 0))
+
+    def stats(self):
+        s = Stats()
+        _check(lib().locc_get_stats(self._h, C.byref(s)))
+        return s.as_dict()
+
+    def query_into(self, pairs, poses, probs, labels=None, logits=None, stream=None):
+        """locc_query on caller buffers (numpy = host, torch cuda tensors = device)."""
+        N = int(pairs.shape[0])
+        _check(lib().locc_query(self._h, _ptr(pairs), _ptr(poses), N, _ptr(probs), _ptr(labels), _ptr(logits),
+                                stream))
+
+    def query(self, pairs, poses):
+        """Host convenience form: numpy in, numpy out (probs float32, labels uint8, logits float32)."""
+        pairs = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+        poses = np.ascontiguousarray(poses, np.float32).reshape(-1, 2, 7)
+        N = pairs.shape[0]
+        probs = np.zeros(N, np.float32)
+        labels = np.zeros(N, np.uint8)
+        logits = np.zeros(N, np.float32)
+        self.query_into(pairs, poses, probs, labels, logits)
+        return probs, labels, logits
+
+    def query_debug(self, pairs, poses):
+        """Host form of locc_query_debug -> dict of every output and intermediate."""
+        pairs = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+        poses = np.ascontiguousarray(poses, np.float32).reshape(-1, 2, 7)
+        N = pairs.shape[0]
+        words = (self.K + 31) // 32
+        o = dict(probs=np.zeros(N, np.float32), labels=np.zeros(N, np.uint8), logits=np.zeros(N, np.float32),
+                 kept=np.zeros((N, 2), np.int32), occ=np.zeros((N, 2), np.int32),
+                 masks=np.zeros((N, 2, words), np.uint32), emb=np.zeros((N, 2, self.F), np.float32))
+        _check(lib().locc_query_debug(self._h, _ptr(pairs), _ptr(poses), N, _ptr(o["probs"]), _ptr(o["labels"]),
+                                      _ptr(o["logits"]), _ptr(o["kept"]), _ptr(o["occ"]), _ptr(o["masks"]),
+                                      _ptr(o["emb"]), None))
+        return o
+
+
+def version():
+    return lib().locc_version().decode()

@@ -1,0 +1,267 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bars (BASELINE.json north_star):
+  * crop masks, kept counts n_s, occupied-cell counts C_s: bit-exact;
+  * fp32 path: |p - p_oracle| <= 1e-5; labels identical except where |p_oracle - 0.5| <= 1e-3;
+  * bf16 path: |p - p_oracle_bf16emul| <= 5e-4 with identical labels outside the 1e-3 band, and
+    |p - p_oracle_fp64| <= 2e-2 (reading Q18).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import locc_synth as ls
+from conftest import cube26, pose
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+P_TOL = {0: 1e-5, 1: 5e-4}
+
+
+@pytest.fixture(scope="module")
+def locc_mod():
+    from paper_2304_09439_b200 import build as b
+    b.build()
+    from paper_2304_09439_b200 import locc
+    return locc
+
+
+@pytest.fixture(scope="module")
+def spread_flat():
+    return ls.flatten_weights(ls.make_weights("spread", calib=ls.load_calibration()))
+
+
+@pytest.fixture(scope="module")
+def c1():
+    return ls.make_workload("C1")
+
+
+@pytest.fixture(scope="module")
+def c1_oracle(oracle_mod, c1, spread_flat):
+    return {emul: oracle_mod.query(spread_flat, c1.points, c1.pairs, c1.poses, bf16_emul=emul) for emul in (False, True)}
+
+
+def make_ctx(locc_mod, flat, points, precision, M=6, H=256, F=64, max_batch=0):
+    ctx = locc_mod.Locc(M=M, H=H, F=F, precision=precision, device=0, max_batch=max_batch)
+    ctx.load_weights_mem(flat)
+    ctx.set_shapes(points)
+    return ctx
+
+
+def assert_parity(got, ref, precision, ref64=None):
+    assert np.array_equal(got["kept"], ref["kept"]), "kept counts differ"
+    assert np.array_equal(got["masks"], ref["masks"]), "crop masks differ"
+    assert np.array_equal(got["occ"], ref["occ"]), "occupied-cell counts differ"
+    short = ref["kept"].sum(1) == 0
+    assert np.all(got["probs"][short] == 0) and np.all(got["labels"][short] == 0)
+    assert np.all(np.isneginf(got["logits"][short]))
+    dp = np.abs(got["probs"].astype(np.float64) - ref["probs"])
+    assert dp.max() <= P_TOL[precision], f"max |dp| = {dp.max():.3g}"
+    band = np.abs(ref["probs"] - 0.5) <= 1e-3
+    assert np.array_equal(got["labels"][~band], ref["labels"][~band])
+    if ref64 is not None:
+        assert np.abs(got["probs"].astype(np.float64) - ref64["probs"]).max() <= 2e-2
+    return dp.max()
+
+
+# ----------------------------------------------------------------------------- C1 parity
+@pytest.mark.parametrize("precision", [0, 1])
+def test_c1_parity(locc_mod, c1, c1_oracle, spread_flat, precision):
+    with make_ctx(locc_mod, spread_flat, c1.points, precision) as ctx:
+        got = ctx.query_debug(c1.pairs, c1.poses)
+    ref = c1_oracle[precision == 1]
+    assert_parity(got, ref, precision, ref64=c1_oracle[False])
+    ne = ref["kept"] > 0
+    tol = 2e-4 if precision == 0 else 2e-2
+    np.testing.assert_allclose(got["emb"][ne], ref["emb"][ne], atol=tol, rtol=tol)
+    assert np.all(got["emb"][~ne] == 0)
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_c1_parity_with_ragged_subbatches_and_device_buffers(locc_mod, c1, c1_oracle, spread_flat, precision):
+    import torch
+    ref = c1_oracle[precision == 1]
+    with make_ctx(locc_mod, spread_flat, c1.points, precision, max_batch=7) as ctx:
+        got = ctx.query_debug(c1.pairs, c1.poses)
+        assert_parity(got, ref, precision)
+        # device-resident inputs/outputs on a caller stream: same bits as the host path
+        pairs = torch.from_numpy(c1.pairs).cuda()
+        poses = torch.from_numpy(c1.poses).cuda()
+        probs = torch.empty(len(c1.pairs), device="cuda")
+        labels = torch.empty(len(c1.pairs), dtype=torch.uint8, device="cuda")
+        s = torch.cuda.Stream()
+        ctx.query_into(pairs, poses, probs, labels, stream=s.cuda_stream)
+        s.synchronize()
+        assert np.array_equal(probs.cpu().numpy(), got["probs"])
+        assert np.array_equal(labels.cpu().numpy(), got["labels"])
+
+
+# ----------------------------------------------------------------------------- worked example
+@pytest.mark.parametrize("precision", [0, 1])
+def test_w1_worked_example_gpu(locc_mod, precision):
+    g = json.load(open(os.path.join(GOLD, "w1_boxes.json")))
+    c = cube26()
+    zero = ls.flatten_weights(ls.make_weights("zero"))
+    with make_ctx(locc_mod, zero, np.stack([c, c]), precision) as ctx:
+        pairs = np.array([[0, 1]] * len(g["rows"]), np.int32)
+        poses = np.stack([np.stack([pose(), pose(r["qB"], r["tB"])]) for r in g["rows"]])
+        got = ctx.query_debug(pairs, poses)
+    for i, row in enumerate(g["rows"]):
+        assert tuple(got["kept"][i]) == (row["nA"], row["nB"])
+        assert tuple(got["occ"][i]) == (row["CA"], row["CB"])
+        if row["short"]:
+            assert got["probs"][i] == 0 and np.isneginf(got["logits"][i])
+        else:
+            assert got["probs"][i] == 0.5 and got["labels"][i] == 0 and got["logits"][i] == 0
+
+
+def test_identity_probe_gpu(locc_mod):
+    """Closed form (W1 row 2): e_A[0:6] = (1/2, 1/6, 1/6, 0, 1/6, 1/6) through both encoders; with
+    dyadic operands the bf16 tensor-core path is exact up to the final /C."""
+    from test_oracle_network import perms, probe_weights
+    g = json.load(open(os.path.join(GOLD, "w1_boxes.json")))
+    row = g["rows"][g["identity_probe_row"]]
+    c = cube26()
+    s, t = perms()
+    w = ls.flatten_weights(probe_weights(s, t))
+    for precision in (0, 1):
+        with make_ctx(locc_mod, w, np.stack([c, c]), precision) as ctx:
+            got = ctx.query_debug(np.array([[0, 1]], np.int32), np.stack([pose(), pose(row["qB"], row["tB"])])[None])
+        np.testing.assert_allclose(got["emb"][0, 0, :6], g["identity_probe_eA_first6"], atol=1e-7)
+        assert np.all(got["emb"][0, 0, 6:] == 0)
+
+
+# ----------------------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("K,M,s", [(1, 6, 0.5), (77, 6, 0.3), (300, 1, 0.5), (300, 7, 0.25), (2000, 5, 0.1)])
+def test_edge_shapes(locc_mod, oracle_mod, spread_flat, precision, K, M, s):
+    pts, _ = ls.make_shapes(5, K, seed=40 + K)
+    pairs, poses = ls.make_pairs_poses(pts, 24, s=s, seed=41)
+    pairs[0] = [2, 2]  # self pair
+    poses[1, 1] = poses[1, 0]  # coincident poses: everything kept
+    ref = oracle_mod.query(spread_flat, pts, pairs, poses, M=M, bf16_emul=precision == 1)
+    with make_ctx(locc_mod, spread_flat, pts, precision, M=M) as ctx:
+        got = ctx.query_debug(pairs, poses)
+    assert_parity(got, ref, precision)
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_all_short_circuit_and_empty(locc_mod, spread_flat, precision):
+    pts, _ = ls.make_shapes(3, 200, seed=50)
+    with make_ctx(locc_mod, spread_flat, pts, precision) as ctx:
+        poses = np.stack([np.stack([pose(), pose(t=(5.0 + i, 0, 0))]) for i in range(10)])
+        pr, lb, lg = ctx.query(np.zeros((10, 2), np.int32), poses)
+        assert np.all(pr == 0) and np.all(lb == 0) and np.all(np.isneginf(lg))
+        pr, lb, lg = ctx.query(np.zeros((0, 2), np.int32), np.zeros((0, 2, 7), np.float32))
+        assert pr.size == 0
+
+
+def test_invalid_inputs_fail_loudly(locc_mod, spread_flat):
+    pts, _ = ls.make_shapes(3, 100, seed=51)
+    with make_ctx(locc_mod, spread_flat, pts, 0) as ctx:
+        ok = np.stack([pose(), pose()])[None]
+        with pytest.raises(locc_mod.LoccError):
+            ctx.query(np.array([[0, 3]], np.int32), ok)
+        bad = ok.copy()
+        bad[0, 1, :4] = 0
+        with pytest.raises(locc_mod.LoccError):
+            ctx.query(np.array([[0, 1]], np.int32), bad)
+        bad = ok.copy()
+        bad[0, 0, 5] = np.nan
+        with pytest.raises(locc_mod.LoccError):
+            ctx.query(np.array([[0, 1]], np.int32), bad)
+    with pytest.raises(locc_mod.LoccError):
+        locc_mod.Locc(M=0)
+    ctx = locc_mod.Locc(precision=0, device=0)
+    with pytest.raises(locc_mod.LoccError):  # no weights / shapes yet
+        ctx.query(np.array([[0, 0]], np.int32), ok)
+    with pytest.raises(locc_mod.LoccError):
+        ctx.load_weights_mem(spread_flat[:-1])
+    with pytest.raises(locc_mod.LoccError):
+        ctx.set_shapes(np.full((2, 10, 3), np.nan, np.float32))
+    ctx.close()
+
+
+def test_weight_file_path(locc_mod, c1, spread_flat, tmp_path):
+    w = ls.make_weights("spread", calib=ls.load_calibration())
+    path = ls.write_weights(str(tmp_path / "w.txt"), w)
+    with make_ctx(locc_mod, spread_flat, c1.points, 0) as a, locc_mod.Locc(precision=0, device=0) as b:
+        b.load_weights(path)
+        b.set_shapes(c1.points)
+        assert np.array_equal(a.query(c1.pairs, c1.poses)[0], b.query(c1.pairs, c1.poses)[0])
+
+
+# ----------------------------------------------------------------------------- invariants
+@pytest.mark.parametrize("precision", [0, 1])
+def test_bitwise_invariances(locc_mod, c1, spread_flat, precision):
+    """Point order, object swap, q -> -q and batch composition leave every output bitwise equal."""
+    with make_ctx(locc_mod, spread_flat, c1.points, precision) as ctx:
+        base = ctx.query_debug(c1.pairs, c1.poses)
+        sw = ctx.query_debug(c1.pairs[:, ::-1].copy(), c1.poses[:, ::-1].copy())
+        neg = c1.poses.copy()
+        neg[:, :, :4] *= -1
+        ng = ctx.query_debug(c1.pairs, neg)
+        one = ctx.query_debug(c1.pairs[5:6], c1.poses[5:6])
+        perm = np.random.default_rng(3).permutation(len(c1.pairs))
+        pm = ctx.query_debug(c1.pairs[perm], c1.poses[perm])
+    for k in ("probs", "logits", "labels"):
+        assert np.array_equal(base[k], sw[k]), k
+        assert np.array_equal(base[k], ng[k]), k
+        assert np.array_equal(base[k][5:6], one[k]), k
+        assert np.array_equal(base[k][perm], pm[k]), k
+    assert np.array_equal(base["emb"], sw["emb"][:, ::-1])
+    rng = np.random.default_rng(4)
+    pts2 = np.stack([p[rng.permutation(p.shape[0])] for p in c1.points])
+    with make_ctx(locc_mod, spread_flat, pts2, precision) as ctx:
+        pp = ctx.query_debug(c1.pairs, c1.poses)
+    for k in ("probs", "logits", "kept", "occ", "emb"):
+        assert np.array_equal(base[k], pp[k]), k
+
+
+# ----------------------------------------------------------------------------- full sizes
+@pytest.mark.parametrize("precision", [0, 1])
+def test_c2_sampled_parity(locc_mod, oracle_mod, spread_flat, precision):
+    wl = ls.make_workload("C2")
+    with make_ctx(locc_mod, spread_flat, wl.points, precision) as ctx:
+        pr, lb, lg = ctx.query(wl.pairs, wl.poses)
+        st = ctx.stats()
+    assert st["pairs"] == len(wl.pairs) and st["kept_rows"] > 0
+    idx = np.random.default_rng(9).choice(len(wl.pairs), 96, replace=False)
+    ref = oracle_mod.query(spread_flat, wl.points, wl.pairs[idx], wl.poses[idx], bf16_emul=precision == 1)
+    assert np.abs(pr[idx] - ref["probs"]).max() <= P_TOL[precision]
+    band = np.abs(ref["probs"] - 0.5) <= 1e-3
+    assert np.array_equal(lb[idx][~band], ref["labels"][~band])
+    ev = np.isfinite(lg)
+    assert np.all((pr[ev] > 0) & (pr[ev] < 1)) and st["evaluated_pairs"] == ev.sum()
+
+
+def test_c3_full_size_bf16(locc_mod, oracle_mod, spread_flat):
+    """BASELINE config C3 (1,048,576 pairs, bf16, the bench launch configuration): sampled outputs
+    against the oracle, kept = popcount(mask) everywhere, swap invariance on the whole batch."""
+    import torch
+    wl = ls.make_workload("C3")
+    N = len(wl.pairs)
+    with make_ctx(locc_mod, spread_flat, wl.points, 1) as ctx:
+        pairs = torch.from_numpy(wl.pairs).cuda()
+        poses = torch.from_numpy(wl.poses).cuda()
+        probs = torch.empty(N, device="cuda")
+        labels = torch.empty(N, dtype=torch.uint8, device="cuda")
+        ctx.query_into(pairs, poses, probs, labels)
+        probs2 = torch.empty(N, device="cuda")
+        ctx.query_into(pairs.flip(1).contiguous(), poses.flip(1).contiguous(), probs2)
+        assert torch.equal(probs, probs2)
+        pr = probs.cpu().numpy()
+        lb = labels.cpu().numpy()
+        sub = np.random.default_rng(10).choice(N, 2048, replace=False)
+        dbg = ctx.query_debug(wl.pairs[sub], wl.poses[sub])
+    pc = np.array([[sum(bin(int(w)).count("1") for w in dbg["masks"][i, s]) for s in range(2)] for i in range(len(sub))])
+    assert np.array_equal(pc, dbg["kept"])
+    assert np.array_equal(dbg["probs"], pr[sub])  # batch composition: same bits inside the 1M batch
+    idx = sub[:64]
+    ref = oracle_mod.query(spread_flat, wl.points, wl.pairs[idx], wl.poses[idx], bf16_emul=True)
+    assert np.abs(pr[idx] - ref["probs"]).max() <= 5e-4
+    band = np.abs(ref["probs"] - 0.5) <= 1e-3
+    assert np.array_equal(lb[idx][~band], ref["labels"][~band])
+    assert np.array_equal(dbg["kept"][:64], ref["kept"])
