@@ -247,7 +247,18 @@ int encode(const Params& P, const EncW& W, const float* pts, int K, const ShapeI
     if (!keep[k]) continue;
     ++n;
     for (int d = 0; d < 3; ++d) x[d] = pts[3 * k + d];
-    dense(P.enc1, W.w1.data(), x.data(), h1.data(), true, false);
+    if (emul) {
+      // bf16 mode: layer 1 is fp32 arithmetic by definition of the bf16 path, and
+      // its bf16 rounding is a quantisation decision taken in the kernel's precision, so h1 is
+      // formed exactly as fp32 fma(w0, x, fma(w1, y, fma(w2, z, b))) before rounding.
+      for (int o = 0; o < H; ++o) {
+        const float* w = P.enc1.W + 3 * o;
+        float h = std::fmaf(w[0], pts[3 * k], std::fmaf(w[1], pts[3 * k + 1], std::fmaf(w[2], pts[3 * k + 2], P.enc1.b[o])));
+        h1[o] = h > 0.0f ? (double)h : 0.0;
+      }
+    } else {
+      dense(P.enc1, W.w1.data(), x.data(), h1.data(), true, false);
+    }
     dense(P.enc2, W.w2.data(), h1.data(), h2.data(), true, emul);
     dense(P.enc3, W.w3.data(), h2.data(), h3.data(), true, emul);
     const int c = s.cell[k];

@@ -74,6 +74,13 @@ struct Batch {
   DevStats* stats;
 };
 
+// Layer-1 weights and layer-2 bias of the tensor-core encoder, passed by value as kernel
+// parameters (constant bank) so every FFMA/FADD reads them as a uniform operand.
+struct TcL1 {
+  float4 w1b[256];  // (w0, w1, w2, b1) per feature of encoder layer 1
+  float b2[256];
+};
+
 // Launchers (kernels_*.cu).  All asynchronous on `st`.
 cudaError_t launch_shape_prep(const float* pts_in, int S, int K, int M, float4* pts, uint16_t* perm,
                               float4* lo, float4* hi, uint16_t* cell_tmp, int* bad, cudaStream_t st);
@@ -82,7 +89,7 @@ cudaError_t launch_scan(const int32_t* counts, int64_t G, int64_t* offsets, int6
                         cudaStream_t st);
 cudaError_t launch_crop_emit(const ShapeTable& T, const Batch& b, cudaStream_t st);
 cudaError_t launch_encoder_f32(const DevParams& P, const Batch& b, cudaStream_t st);
-cudaError_t launch_encoder_tc(const DevParams& P, const Batch& b, int num_sms, cudaStream_t st);
+cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b, int num_sms, cudaStream_t st);
 cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_t* labels,
                         float* logits, float* emb, cudaStream_t st);
 size_t scan_tmp_elems(int64_t G);

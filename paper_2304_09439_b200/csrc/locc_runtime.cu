@@ -19,8 +19,12 @@
 
 #include "../../include/locc.h"
 #include "internal.h"
+#include "tc_ptx.cuh"
 
 using namespace locc;
+
+struct locc_ctx;
+locc_status locc_upload_tc_weights(locc_ctx* c, const float* flat);
 
 namespace {
 
@@ -93,8 +97,9 @@ struct locc_ctx {
   bool timing = false;
   bool has_weights = false, has_shapes = false;
   // parameters
-  DevBuf params;
+  DevBuf params, tc_img;
   DevParams P{};
+  TcL1 tc_l1{};
   // shapes
   DevBuf sh_pts, sh_perm, sh_lo, sh_hi;
   ShapeTable T{};
@@ -338,7 +343,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     CK(launch_crop_emit(c->T, b, st));
     if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs], st));
     if (c->cfg.precision == LOCC_PREC_BF16) {
-      CK(launch_encoder_tc(c->P, b, c->num_sms, st));
+      CK(launch_encoder_tc(c->P, c->tc_l1, b, c->num_sms, st));
     } else {
       CK(launch_encoder_f32(c->P, b, st));
     }
@@ -501,12 +506,7 @@ locc_status locc_load_weights_mem(locc_ctx* c, const float* flat, size_t n) {
   CK(cudaSetDevice(c->device));
   locc_status s = upload_params(c, flat);
   if (s != LOCC_OK) return s;
-  if (c->cfg.H == 256) {
-    extern locc_status locc_upload_tc_weights(locc_ctx*, const float* w2, const float* w3);
-    const float* w2 = flat + 4 * 256;
-    const float* w3 = w2 + 256 * 256 + 256;
-    s = locc_upload_tc_weights(c, w2, w3);
-  }
+  if (c->cfg.H == 256) s = locc_upload_tc_weights(c, flat);
   return s;
 }
 
@@ -606,9 +606,50 @@ locc_status locc_query_debug(locc_ctx* c, const int32_t* pairs, const float* pos
 }  // extern "C"
 
 // ---------------------------------------------------------------- tensor-core weight image
-locc_status locc_upload_tc_weights(locc_ctx* c, const float* w2, const float* w3) {
-  (void)c;
-  (void)w2;
-  (void)w3;
-  return LOCC_OK;  // filled in by the tcgen05 encoder (kernels_encoder_tc.cu)
+namespace {
+uint16_t bf16_rne(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+}  // namespace
+
+// W2 as the B operand of layer 2: per CTA rank r its output features [128r, 128r+128), K-major,
+// 4 K blocks of [128 rows x 128 B] with the 128-byte swizzle (16-byte chunk j of row i stored at
+// chunk j ^ (i & 7)) — the exact shared-memory image, so one bulk copy places it.
+// W3 as the TMEM A operand of layer 3: row f = 128 columns of bf16x2 (K = 2c low, 2c+1 high).
+// Also keeps layer 1 (w, b) and b2 for the kernel-parameter block.
+locc_status locc_upload_tc_weights(locc_ctx* c, const float* flat) {
+  const int H = 256;
+  const float* w1 = flat;
+  const float* b1 = w1 + 3 * H;
+  const float* w2 = b1 + H;
+  const float* b2 = w2 + H * H;
+  const float* w3 = b2 + H;
+  for (int f = 0; f < H; ++f) {
+    c->tc_l1.w1b[f] = make_float4(w1[3 * f], w1[3 * f + 1], w1[3 * f + 2], b1[f]);
+    c->tc_l1.b2[f] = b2[f];
+  }
+  std::vector<uint8_t> img(2 * 65536 + (size_t)H * 128 * 4);
+  for (int r = 0; r < 2; ++r)
+    for (int i = 0; i < 128; ++i)
+      for (int kb = 0; kb < 4; ++kb)
+        for (int j = 0; j < 8; ++j) {
+          uint8_t* dst = img.data() + r * 65536 + kb * 16384 + locc::tc::sw128_off(i, j);
+          for (int e = 0; e < 8; ++e) {
+            const uint16_t v = bf16_rne(w2[(size_t)(128 * r + i) * H + 64 * kb + 8 * j + e]);
+            std::memcpy(dst + 2 * e, &v, 2);
+          }
+        }
+  uint32_t* w3img = reinterpret_cast<uint32_t*>(img.data() + 2 * 65536);
+  for (int f = 0; f < H; ++f)
+    for (int cc = 0; cc < 128; ++cc)
+      w3img[(size_t)f * 128 + cc] =
+          (uint32_t)bf16_rne(w3[(size_t)f * H + 2 * cc]) | ((uint32_t)bf16_rne(w3[(size_t)f * H + 2 * cc + 1]) << 16);
+  CK(c->tc_img.ensure(img.size()));
+  CK(cudaMemcpy(c->tc_img.p, img.data(), img.size(), cudaMemcpyHostToDevice));
+  c->P.tc_w2 = c->tc_img.p;
+  c->P.tc_w3 = static_cast<uint8_t*>(c->tc_img.p) + 2 * 65536;
+  return LOCC_OK;
 }
