@@ -89,7 +89,8 @@ cudaError_t launch_scan(const int32_t* counts, int64_t G, int64_t* offsets, int6
                         cudaStream_t st);
 cudaError_t launch_crop_emit(const ShapeTable& T, const Batch& b, cudaStream_t st);
 cudaError_t launch_encoder_f32(const DevParams& P, const Batch& b, cudaStream_t st);
-cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b, int num_sms, cudaStream_t st);
+cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b, int num_sms, cudaStream_t st,
+                              long long* trace = nullptr);
 cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_t* labels,
                         float* logits, float* emb, cudaStream_t st);
 size_t scan_tmp_elems(int64_t G);

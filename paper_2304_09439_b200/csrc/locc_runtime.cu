@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <sstream>
@@ -105,6 +106,7 @@ struct locc_ctx {
   ShapeTable T{};
   // scratch for one sub-batch
   int64_t cap_B = 0;
+  DevBuf trace;
   DevBuf in_pairs, in_poses, counts, occ, offsets, scan_tmp, rows, pooled, stats;
   DevBuf out_probs, out_labels, out_logits, out_kept, out_occ, out_masks, out_emb;
   locc_stats last{};
@@ -343,7 +345,32 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     CK(launch_crop_emit(c->T, b, st));
     if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs], st));
     if (c->cfg.precision == LOCC_PREC_BF16) {
-      CK(launch_encoder_tc(c->P, c->tc_l1, b, c->num_sms, st));
+      long long* trace = nullptr;
+      if (getenv("LOCC_TC_TRACE") && subs == 0) {
+        CK(c->trace.ensure(sizeof(long long) * 2 * 64 * 16));
+        CK(cudaMemsetAsync(c->trace.p, 0, sizeof(long long) * 2 * 64 * 16, st));
+        trace = c->trace.as<long long>();
+      }
+      CK(launch_encoder_tc(c->P, c->tc_l1, b, c->num_sms, st, trace));
+      if (trace) {
+        std::vector<long long> h(2 * 64 * 16);
+        CK(cudaMemcpyAsync(h.data(), trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int rk = 0; rk < 2; ++rk) {
+          long long t0 = 0;
+          for (long long v : h) if (v && (!t0 || v < t0)) t0 = v;
+          t0 = 0;
+          for (int e = 0; e < 16; ++e) if (h[(rk * 64) * 16 + e] && (!t0 || h[(rk * 64) * 16 + e] < t0)) t0 = h[(rk * 64) * 16 + e];
+          for (int t = 0; t < 64; ++t) {
+            fprintf(stderr, "trace r%d t%02d", rk, t);
+            for (int e = 0; e < 16; ++e) {
+              long long v = h[(rk * 64 + t) * 16 + e];
+              fprintf(stderr, " %7lld", v ? v - t0 : -1);
+            }
+            fprintf(stderr, "\n");
+          }
+        }
+      }
     } else {
       CK(launch_encoder_f32(c->P, b, st));
     }
