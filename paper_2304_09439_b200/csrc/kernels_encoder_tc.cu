@@ -23,8 +23,8 @@
 // produces layer 3's operand in place and layer 3's epilogue sees each feature's rows in one
 // thread — the segmented cell max needs no cross-lane reduction.
 //
-// Roles (13 warps): warp 0 = TMEM allocation + MMA issue (leader CTA), warps 1-4 = epi L3,
-// warps 5-12 = epi L2 of tile t then layer 1 of tile t+1.  mbarriers link the roles across both
+// Roles (13 warps): warps 0-7 = epi L2 of tile t then layer 1 of tile t+1, warps 8-11 = epi L3,
+// warp 12 = TMEM allocation + MMA issue (leader CTA).  mbarriers link the roles across both
 // CTAs; layer 3 starts per 32-feature K chunk as soon as epi L2 has written it; TMEM regions rotate
 // between tiles so the MMAs of one tile overlap the layer-3 epilogue of the previous one.
 #include <cuda_runtime.h>
@@ -43,9 +43,12 @@ using namespace tc;
 // TMEM-reading group covers the four quarters.
 constexpr int kWarps = 13;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kWarpE3 = 1;  // warps 1..4: epilogue of L3 (thread = output feature)
-constexpr int kWarpW = 5;   // warps 5..12: epilogue of L2 (thread = row, half the features each),
-                            // then layer 1 of the next tile (thread = 4 features x 32 rows)
+// The warp scheduler favours higher warp ids, so the sequential layer-3 walk and the MMA issuer get
+// the high ids.
+constexpr int kWarpW = 0;    // warps 0..7: epilogue of L2 (thread = row, half the features each),
+                             // then layer 1 of the next tile (thread = 4 features x 32 rows)
+constexpr int kWarpE3 = 8;   // warps 8..11: epilogue of L3 (thread = output feature)
+constexpr int kWarpMMA = 12; // warp 12: TMEM allocation + MMA issue (leader CTA)
 constexpr int kTileRows = 256;
 constexpr uint32_t kTmemCols = 512;
 // TMEM columns: W3 (A of L3: this CTA's 128 features as bf16x2) and three 128-column regions that
@@ -188,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       bulk_g2s(S.w2 + kb * 16384, a.w2img + (size_t)rank * 65536 + kb * 16384, 16384, &S.bar[B_WLOAD]);
   }
   for (int i = threadIdx.x; i < 256; i += kThreads) S.b2[i] = a.b2[i];
-  if (warp == 0) tmem_alloc_2cta(&S.tmem_base, kTmemCols);
+  if (warp == kWarpMMA) tmem_alloc_2cta(&S.tmem_base, kTmemCols);
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
@@ -210,7 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
   tc_fence_after();
 
   // ---------------------------------------------------------------- roles
-  if (warp == 0) {
+  if (warp == kWarpMMA) {
     // ============ MMA issuer (leader CTA, one thread) ============
     if (rank == 0 && lane == 0) {
       TileIter iter(a, cid, ncl);
@@ -281,7 +284,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         ++it;
       }
     }
-  } else if (warp >= kWarpW) {
+  } else if (warp < kWarpE3) {
     // ============ workers: epi L2 of tile t, then layer 1 of tile t+1 ============
     const uint32_t q = warp & 3;                 // TMEM lane quarter (epi L2 rows 32q..32q+31)
     const uint32_t half = (warp - kWarpW) >> 2;  // epi L2 features [128 half, +128)
@@ -380,7 +383,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       ++it;
       if (iter_l1.next(l1_row0, l1_nrows)) layer1(it, l1_row0, l1_nrows);
     }
-  } else if (warp >= kWarpE3) {
+  } else {
     // ============ epi L3: thread = output feature; walk rows: cell max, occupied-cell mean ============
     const uint32_t q = warp & 3;
     const uint32_t eg = warp - kWarpE3;  // 0..3: which 32-row chunks this warp flags
@@ -442,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
-  if (warp == 0) tmem_dealloc_2cta(tmem, kTmemCols);
+  if (warp == kWarpMMA) tmem_dealloc_2cta(tmem, kTmemCols);
 }
 
 }  // namespace
