@@ -26,7 +26,8 @@ def deps():
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(p) for p in deps()):
         return LIB
-    cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB + ".tmp"] + sources()
+    extra = os.environ.get("LOCC_NVCC_FLAGS", "").split()  # experiment switches, e.g. -DLOCC_E3_TWO_WALKERS=1
+    cmd = [NVCC] + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB + ".tmp"] + sources()
     subprocess.check_call(cmd, cwd=HERE)
     os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -5,33 +5,40 @@
 // row buffer (rows sorted by segment, then cell), cut into 256-row tiles; CTA r of the pair owns
 // the tile rows {64r..64r+63} and {128+64r..128+64r+63}.  Per tile:
 //
-//   L1 (CUDA cores, fp32 FFMA)  h1 = ReLU(W1 p + b1) -> bf16, written as the A operand of L2
-//                               (K-major, 128-byte swizzle) — PAPER.md:331, :421, :425
-//   L2 (tcgen05, SS)            D2[256 rows x 256 features] = h1 * W2^T; A = h1 (each CTA its 128
-//                               rows), B = W2 (each CTA 128 of the 256 output features, resident
-//                               in shared memory for the whole launch)
-//   epi L2 (TMEM -> regs)       h2 = ReLU(D2 + b2) -> bf16, written row-major (K-major) as the B
-//                               operand of L3 — each CTA keeps its own rows: no exchange
-//   L3 (tcgen05, TS)            D3[256 features x 128 rows] = W3 * h2^T, twice per tile (rows
-//                               0-127, 128-255); A = W3 resident in TMEM (each CTA 128 features),
-//                               B = h2 (each CTA 64 of the 128 rows)
-//   epi L3 (TMEM -> regs)       thread = output feature, walking the rows in order: cell-wise max
-//                               (PAPER.md:331), g = ReLU(max + b3), running sum over occupied cells
-//                               in ascending order, mean at the segment end
+//   L1 (CUDA cores, fp32 FFMA2)  h1 = ReLU(W1 p + b1) -> bf16, written as the A operand of L2
+//                                (K-major, 128-byte swizzle) — PAPER.md:331, :421, :425
+//   L2 (tcgen05, SS)             D2[256 rows x 256 features] = h1 * W2^T; A = h1 (each CTA its 128
+//                                rows), B = W2 (each CTA 128 of the 256 output features, resident
+//                                in shared memory for the whole launch)
+//   epi L2 (TMEM -> regs)        h2 = ReLU(D2 + b2) -> bf16, written row-major (K-major) as the B
+//                                operand of L3 — each CTA keeps its own rows: no exchange
+//   L3 (tcgen05, TS)             D3[256 features x 128 rows] = W3 * h2^T, twice per tile (rows
+//                                0-127, 128-255); A = W3 resident in TMEM (each CTA 128 features),
+//                                B = h2 (each CTA 64 of the 128 rows)
+//   epi L3 (TMEM -> regs)        thread = output feature, walking the rows in order: cell-wise max
+//                                (PAPER.md:331), g = ReLU(max + b3), running sum over occupied cells,
+//                                mean at the segment end
 //
 // Layer 2 is computed "rows x features" and layer 3 "features x rows" so that layer 2's epilogue
 // produces layer 3's operand in place and layer 3's epilogue sees each feature's rows in one
 // thread — the segmented cell max needs no cross-lane reduction.
 //
-// Roles (13 warps): warps 0-7 = epi L2 of tile t then layer 1 of tile t+1, warps 8-11 = epi L3,
-// warp 12 = TMEM allocation + MMA issue (leader CTA).  mbarriers link the roles across both
-// CTAs; layer 3 starts per 32-feature K chunk as soon as epi L2 has written it; TMEM regions rotate
-// between tiles so the MMAs of one tile overlap the layer-3 epilogue of the previous one.
+// Roles (17 warps): warps 0-3 = layer 1, warps 4-11 = epi L2, warps 12-15 = epi L3, warp 16 = TMEM
+// allocation + MMA issue (leader CTA).  mbarriers link the roles across both CTAs.  h1 is handed
+// over per 64-feature K block in both directions (layer 1 of tile t+1 overwrites K block kb as soon
+// as L2 of tile t has consumed it; L2 of tile t+1 starts on K block 0 while layer 1 still writes
+// the others); layer 3 starts per 32-feature K chunk as soon as epi L2 has written it; TMEM
+// regions rotate between tiles so the MMAs of one tile overlap the layer-3 epilogue of the
+// previous one.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "internal.h"
 #include "tc_ptx.cuh"
+
+#ifndef LOCC_E3_TWO_WALKERS
+#define LOCC_E3_TWO_WALKERS 0
+#endif
 
 namespace locc {
 
@@ -39,16 +46,16 @@ namespace {
 
 using namespace tc;
 
-// Warp roles (13 warps).  TMEM lane access is restricted to lane quarter (warp % 4), so each
-// TMEM-reading group covers the four quarters.
-constexpr int kWarps = 13;
+// Warp roles.  TMEM lane access is restricted to lane quarter (warp % 4), so each TMEM-reading
+// group starts at a multiple of 4.  The warp scheduler favours higher warp ids, so the sequential
+// layer-3 walk and the MMA issuer get the high ids and layer 1 (which has the most slack) the low.
+// 17 warps = at most 5 per scheduler, which leaves 96 registers per thread.
+constexpr int kWarpL1 = 0;    // warps 0..3: layer 1 (thread = 4 features x 16 rows per K block)
+constexpr int kWarpE2 = 4;    // warps 4..11: epi L2 (thread = row, half the features each)
+constexpr int kWarpE3 = 12;   // warps 12..15: epi L3 (thread = output feature)
+constexpr int kWarpMMA = 16;  // warp 16: TMEM allocation + MMA issue (leader CTA)
+constexpr int kWarps = 17;
 constexpr int kThreads = 32 * kWarps;
-// The warp scheduler favours higher warp ids, so the sequential layer-3 walk and the MMA issuer get
-// the high ids.
-constexpr int kWarpW = 0;    // warps 0..7: epilogue of L2 (thread = row, half the features each),
-                             // then layer 1 of the next tile (thread = 4 features x 32 rows)
-constexpr int kWarpE3 = 8;   // warps 8..11: epilogue of L3 (thread = output feature)
-constexpr int kWarpMMA = 12; // warp 12: TMEM allocation + MMA issue (leader CTA)
 constexpr int kTileRows = 256;
 constexpr uint32_t kTmemCols = 512;
 // TMEM columns: W3 (A of L3: this CTA's 128 features as bf16x2) and three 128-column regions that
@@ -68,17 +75,17 @@ struct alignas(1024) Smem {
   uint8_t w2[65536];  // B of L2: this CTA's 128 W2 rows, 4 K blocks x [128 rows x 128 B], SW128
   uint8_t h1[65536];  // A of L2: this CTA's 128 rows of h1, same layout
   uint8_t h2[65536];  // B of L3: this CTA's 128 rows of h2, same layout
-  float px[128], py[128], pz[128];  // this CTA's rows of the tile (layer-1 input), SoA
+  float px[2][128], py[2][128], pz[2][128];  // this CTA's rows of a tile (layer-1 input), double buffered
+  float4 w1b[256];                            // (w0, w1, w2, b1) per layer-1 feature
   float b2[256];
   uint32_t flags[kTileRows];  // row flags of the whole tile (epi L3)
   uint32_t masks[16];         // cell-end bits [0..7], segment-end bits [8..15] per 32-row chunk
-  uint64_t bar[13];
+  uint64_t bar[19];
   uint32_t tmem_base;
 };
 
 enum {
-  B_H1_FULL = 0, B_H1_EMPTY, B_D2_FULL, B_E2K0, B_E2K1, B_E2K2, B_E2K3, B_H2_EMPTY, B_D3F0, B_D3F1, B_D3E0,
-  B_D3E1, B_WLOAD
+  B_H1F0 = 0, B_H1E0 = 4, B_D2_FULL = 8, B_E2K0 = 9, B_H2_EMPTY = 13, B_D3F0, B_D3F1, B_D3E0, B_D3E1, B_WLOAD
 };
 
 struct TcArgs {
@@ -109,7 +116,9 @@ struct TileIter {
   int64_t r1 = 0, t0 = 0;
   __device__ TileIter(const TcArgs& a, int64_t first, int64_t stride)
       : off(a.offsets), G(a.G), n_chunks(a.n_chunks), chunk(first - stride), step(stride), spc(a.seg_per_chunk) {}
-  __device__ bool next(int64_t& row0, int& nrows) {
+  // first = true for the first tile of a chunk (a chunk starts on a segment boundary)
+  __device__ bool next(int64_t& row0, int& nrows, bool& first) {
+    first = false;
     while (t0 >= r1) {
       chunk += step;
       if (chunk >= n_chunks) return false;
@@ -117,11 +126,16 @@ struct TileIter {
       const int64_t s1 = min(s0 + spc, G);
       t0 = off[s0];
       r1 = off[s1];
+      first = true;
     }
     row0 = t0;
     nrows = (int)min((int64_t)kTileRows, r1 - t0);
     t0 += kTileRows;
     return true;
+  }
+  __device__ bool next(int64_t& row0, int& nrows) {
+    bool f;
+    return next(row0, nrows, f);
   }
 };
 
@@ -129,40 +143,170 @@ __device__ __forceinline__ uint32_t tile_row_of_local(uint32_t rank, uint32_t i)
   return i < 64 ? 64 * rank + i : 128 + 64 * rank + (i - 64);
 }
 
-// One 32-column chunk of the layer-3 walk for this thread's feature.  Columns are tile rows in
-// order; `ce`/`se` flag the last row of a cell / of a segment (uniform across the warp).  The common
-// chunk (32 valid rows, no segment end) runs branch-free: per row one max, and at a cell end the
-// cell's pooled value g = ReLU(max + b3) is added (fma with 0/1) and the running max reset.
-__device__ __forceinline__ void walk_chunk(const uint32_t (&v)[32], int n, uint32_t ce, uint32_t se,
-                                           const uint32_t* flags, float b3, float& run_max, float& run_sum,
-                                           int& run_cells, float* pooled, uint32_t f) {
-  if (n == 32 && se == 0) {
-    run_cells += __popc(ce);
+// Layer-3 walk state of one output feature.  m runs from -b3 so that ReLU(max + b3) = m + b3 at a
+// cell end (max(x, -b3) + b3 rounds to exactly the same value as ReLU(x + b3)); s sums m over the
+// occupied cells of the open segment and the mean is (s + c b3) / c.
+struct Walk {
+  float m, s;
+  int c;
+};
+// A walker that starts in the middle of the row sequence (the second half of a layer-3 part) runs
+// without the state before it: the rows up to its first cell end ("head") continue the cell left
+// open by its predecessor and its first segment end closes the predecessor's segment, so both are
+// kept aside (hm; s1, c1, seg1) and folded in by merge() once the predecessor has finished.
+struct Tail {
+  Walk w;
+  float hm, s1;
+  int c1;
+  uint32_t seg1;
+  bool ce, se;  // seen a cell end / a segment end (warp-uniform)
+};
+
+__device__ __forceinline__ void store_mean(float* pooled, uint32_t seg, uint32_t f, float s, int c, float b3) {
+  pooled[(int64_t)seg * 256 + f] = __fdividef(fmaf((float)c, b3, s), (float)c);
+}
+
+// Both walkers over 16 rows without a segment end (and, for the tail walker, not its first cell
+// end): per row one max and, at a cell end, one add; the two dependency chains interleave.
+__device__ __forceinline__ void walk_fast2(const uint32_t (&vx)[16], const uint32_t (&vy)[16], uint32_t cex,
+                                           uint32_t cey, Walk& x, Walk& y, float nb3) {
+  x.c += __popc(cex);
+  y.c += __popc(cey);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    x.m = fmaxf(x.m, __uint_as_float(vx[j]));
+    y.m = fmaxf(y.m, __uint_as_float(vy[j]));
+    if ((cex >> j) & 1u) {
+      x.s += x.m;
+      x.m = nb3;
+    }
+    if ((cey >> j) & 1u) {
+      y.s += y.m;
+      y.m = nb3;
+    }
+  }
+}
+
+// General 16 rows for the carried walker: segment ends write the mean.
+__device__ __forceinline__ void walk_slow_x(const uint32_t (&v)[16], uint32_t ce, uint32_t se, const uint32_t* flags,
+                                            Walk& w, float nb3, float b3, float* pooled, uint32_t f) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    w.m = fmaxf(w.m, __uint_as_float(v[j]));
+    if ((ce >> j) & 1u) {
+      w.s += w.m;
+      w.c += 1;
+      w.m = nb3;
+      if ((se >> j) & 1u) {
+        store_mean(pooled, flags[j] >> kRowSegShift, f, w.s, w.c, b3);
+        w.s = 0.f;
+        w.c = 0;
+      }
+    }
+  }
+}
+
+// General 16 rows for the tail walker.
+__device__ __forceinline__ void walk_slow_y(const uint32_t (&v)[16], uint32_t ce, uint32_t se, const uint32_t* flags,
+                                            Tail& t, float nb3, float b3, float* pooled, uint32_t f) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    t.w.m = fmaxf(t.w.m, __uint_as_float(v[j]));
+    if ((ce >> j) & 1u) {
+      if (t.ce) {
+        t.w.s += t.w.m;
+        t.w.c += 1;
+      } else {
+        t.hm = t.w.m;
+        t.ce = true;
+      }
+      t.w.m = nb3;
+      if ((se >> j) & 1u) {
+        const uint32_t seg = flags[j] >> kRowSegShift;
+        if (t.se) {
+          store_mean(pooled, seg, f, t.w.s, t.w.c, b3);
+        } else {
+          t.s1 = t.w.s;
+          t.c1 = t.w.c;
+          t.seg1 = seg;
+          t.se = true;
+        }
+        t.w.s = 0.f;
+        t.w.c = 0;
+      }
+    }
+  }
+}
+
+// x <- x followed by the tail walker's rows.
+__device__ __forceinline__ void merge(Walk& x, const Tail& t, float b3, float* pooled, uint32_t f) {
+  if (!t.ce) {
+    x.m = fmaxf(x.m, t.w.m);
+    return;
+  }
+  const float hv = fmaxf(x.m, t.hm);  // the cell open across the boundary
+  if (t.se) {
+    store_mean(pooled, t.seg1, f, x.s + hv + t.s1, x.c + 1 + t.c1, b3);
+    x = t.w;
+  } else {
+    x.s = x.s + hv + t.w.s;
+    x.c = x.c + 1 + t.w.c;
+    x.m = t.w.m;
+  }
+}
+
+// Step C (0..3) of a layer-3 part: rows 16C..16C+15 (carried walker) and 64+16C.. (tail walker);
+// the next step's columns are loaded into (nx, ny) while this one is walked.
+// One 32-column chunk of the single-walker layer-3 walk (rows in order).
+__device__ __forceinline__ void walk_chunk32(const uint32_t (&v)[32], uint32_t ce, uint32_t se, const uint32_t* flags,
+                                             Walk& w, float nb3, float b3, float* pooled, uint32_t f) {
+  if (se == 0) {
+    w.c += __popc(ce);
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const bool e = (ce >> j) & 1u;
-      run_max = fmaxf(run_max, __uint_as_float(v[j]));
-      run_sum = fmaf(e ? 1.f : 0.f, fmaxf(run_max + b3, 0.f), run_sum);
-      run_max = e ? -INFINITY : run_max;
+      w.m = fmaxf(w.m, __uint_as_float(v[j]));
+      if ((ce >> j) & 1u) {
+        w.s += w.m;
+        w.m = nb3;
+      }
     }
     return;
   }
-#pragma unroll 1
-  for (int j = 0; j < n; ++j) {
-    float x = 0.f;
 #pragma unroll
-    for (int t = 0; t < 32; ++t) x = t == j ? __uint_as_float(v[t]) : x;
-    run_max = fmaxf(run_max, x);
+  for (int j = 0; j < 32; ++j) {
+    w.m = fmaxf(w.m, __uint_as_float(v[j]));
     if ((ce >> j) & 1u) {
-      run_sum += fmaxf(run_max + b3, 0.f);
-      ++run_cells;
-      run_max = -INFINITY;
+      w.s += w.m;
+      w.c += 1;
+      w.m = nb3;
       if ((se >> j) & 1u) {
-        pooled[(int64_t)(flags[j] >> kRowSegShift) * 256 + f] = __fdiv_rn(run_sum, (float)run_cells);
-        run_sum = 0.f;
-        run_cells = 0;
+        store_mean(pooled, flags[j] >> kRowSegShift, f, w.s, w.c, b3);
+        w.s = 0.f;
+        w.c = 0;
       }
     }
+  }
+}
+
+template <int C>
+__device__ __forceinline__ void e3_step(uint32_t tbase, uint32_t (&vx)[16], uint32_t (&vy)[16], uint32_t (&nx)[16],
+                                        uint32_t (&ny)[16], const uint32_t* mk, const uint32_t* fl, Walk& w, Tail& t,
+                                        float nb3, float b3, float* pooled, uint32_t f) {
+  tmem_ld_wait();
+  if (C < 3) {
+    tmem_ld16(tbase + 16 * (C + 1), nx);
+    tmem_ld16(tbase + 64 + 16 * (C + 1), ny);
+  }
+  constexpr int sh = 16 * (C & 1);
+  const uint32_t cex = (mk[C >> 1] >> sh) & 0xffffu;
+  const uint32_t sex = (mk[8 + (C >> 1)] >> sh) & 0xffffu;
+  const uint32_t cey = (mk[2 + (C >> 1)] >> sh) & 0xffffu;
+  const uint32_t sey = (mk[8 + 2 + (C >> 1)] >> sh) & 0xffffu;
+  if ((sex | sey) == 0 && (t.ce || cey == 0)) {
+    walk_fast2(vx, vy, cex, cey, w, t.w, nb3);
+  } else {
+    walk_slow_x(vx, cex, sex, fl + 16 * C, w, nb3, b3, pooled, f);
+    walk_slow_y(vy, cey, sey, fl + 64 + 16 * C, t, nb3, b3, pooled, f);
   }
 }
 
@@ -175,10 +319,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
 
   // ---------------------------------------------------------------- setup
   if (threadIdx.x == 0) {
-    mbar_init(&S.bar[B_H1_FULL], 16);  // 8 worker warps x 2 CTAs (the leader's copy is used)
-    mbar_init(&S.bar[B_H1_EMPTY], 1);  // MMA commits
+    for (int kb = 0; kb < 4; ++kb) {
+      mbar_init(&S.bar[B_H1F0 + kb], 8);  // 4 layer-1 warps x 2 CTAs (the leader's copy is used)
+      mbar_init(&S.bar[B_H1E0 + kb], 1);   // MMA commits
+    }
     mbar_init(&S.bar[B_D2_FULL], 1);
-    for (int j = 0; j < 4; ++j) mbar_init(&S.bar[B_E2K0 + j], 16);  // 8 worker warps x 2 CTAs
+    for (int j = 0; j < 4; ++j) mbar_init(&S.bar[B_E2K0 + j], 16);  // 8 epi-L2 warps x 2 CTAs
     mbar_init(&S.bar[B_H2_EMPTY], 1);
     mbar_init(&S.bar[B_D3F0], 1);
     mbar_init(&S.bar[B_D3F1], 1);
@@ -190,7 +336,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     for (int kb = 0; kb < 4; ++kb)
       bulk_g2s(S.w2 + kb * 16384, a.w2img + (size_t)rank * 65536 + kb * 16384, 16384, &S.bar[B_WLOAD]);
   }
-  for (int i = threadIdx.x; i < 256; i += kThreads) S.b2[i] = a.b2[i];
+  for (int i = threadIdx.x; i < 256; i += kThreads) {
+    S.b2[i] = a.b2[i];
+    S.w1b[i] = a.w1b[i];
+  }
   if (warp == kWarpMMA) tmem_alloc_2cta(&S.tmem_base, kTmemCols);
   cluster_sync();
   tc_fence_after();
@@ -224,20 +373,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       const uint32_t a_h1 = smem_u32(S.h1), b_w2 = smem_u32(S.w2), b_h2 = smem_u32(S.h2);
       while (iter.next(row0, nrows)) {
         const uint32_t par = it & 1;
-        mbar_wait(&S.bar[B_H1_FULL], par);
-        trace_ev(a, rank, cid, it, 0);
         // D2 = [RA|RB] (even) or [RB|RC] (odd): RA resp. RC last held L3p0 of the previous tile;
         // RB held the previous D2, drained before that tile's L3 could start.
         if (it > 0) mbar_wait(&S.bar[B_D3E0], (n0 - 1) & 1);
         trace_ev(a, rank, cid, it, 1);
-        tc_fence_after();
         const uint32_t dcol = tmem + d2_col(par);
 #pragma unroll 1
-        for (int k = 0; k < 16; ++k) {
-          const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32;
-          mma_ss_2cta(dcol, smem_desc_sw128(a_h1 + koff, 1024), smem_desc_sw128(b_w2 + koff, 1024), kIdescL2, k > 0);
+        for (int kb = 0; kb < 4; ++kb) {
+          mbar_wait(&S.bar[B_H1F0 + kb], par);
+          if (kb == 0) trace_ev(a, rank, cid, it, 0);
+          tc_fence_after();
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            const uint32_t koff = kb * 16384 + s * 32;
+            mma_ss_2cta(dcol, smem_desc_sw128(a_h1 + koff, 1024), smem_desc_sw128(b_w2 + koff, 1024), kIdescL2,
+                        (kb | s) != 0);
+          }
+          mma_commit_2cta(&S.bar[B_H1E0 + kb], 3);
         }
-        mma_commit_2cta(&S.bar[B_H1_EMPTY], 3);
         mma_commit_2cta(&S.bar[B_D2_FULL], 3);
         trace_ev(a, rank, cid, it, 2);
         // L3p0 -> RC (even) / RA (odd): last held L3p1 of the previous tile, if it had one
@@ -284,68 +437,84 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         ++it;
       }
     }
-  } else if (warp < kWarpE3) {
-    // ============ workers: epi L2 of tile t, then layer 1 of tile t+1 ============
-    const uint32_t q = warp & 3;                 // TMEM lane quarter (epi L2 rows 32q..32q+31)
-    const uint32_t half = (warp - kWarpW) >> 2;  // epi L2 features [128 half, +128)
-    const uint32_t row = 32 * q + lane;
-    const uint32_t lt = threadIdx.x - 32 * kWarpW;  // 0..255
-    const uint32_t fq = lt & 63, rq = lt >> 6;      // layer 1: features 4fq..4fq+3, rows 32rq..32rq+31
-    unsigned long long wx[4], wy[4], wz[4], wb[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float4 w = a.w1b[4 * fq + k];
-      wx[k] = f2(w.x, w.x);
-      wy[k] = f2(w.y, w.y);
-      wz[k] = f2(w.z, w.z);
-      wb[k] = f2(w.w, w.w);
-    }
-    const uint32_t l1_base = smem_u32(S.h1) + ((4 * fq) >> 6) * 16384 + (((4 * fq) & 7) << 1);
-    const uint32_t l1_chunk = ((4 * fq) & 63) >> 3;
-    const uint32_t h2 = smem_u32(S.h2);
-
-    auto layer1 = [&](uint32_t t, int64_t r0, int nr) {
-      asm volatile("bar.sync 2, 256;" ::: "memory");  // previous tile's rows no longer read
-      if (lt < 128) {
+  } else if (warp < kWarpE2) {
+    // ============ layer 1: K block kb -> thread = features 64kb + 4fq..+3, rows 8rq + {0..7, 64..71} ====
+    const uint32_t lt = threadIdx.x - 32 * kWarpL1;  // 0..127
+    const uint32_t fq = lt & 15, rq = lt >> 4;
+    const uint32_t h1 = smem_u32(S.h1) + rq * 1024 + ((4 * fq) & 7) * 2;
+    const uint32_t chunk = (4 * fq) >> 3;  // 16-byte chunk of the 128-byte row (same in every K block)
+    TileIter iter(a, cid, ncl), ahead(a, cid, ncl);
+    int64_t row0, nrow0;
+    int nrows, nnrows;
+    auto stage = [&](float4 p, uint32_t buf) {
+      S.px[buf][lt] = p.x;
+      S.py[buf][lt] = p.y;
+      S.pz[buf][lt] = p.z;
+    };
+    auto fetch = [&](bool ok, int64_t r0, int nr) {
+      float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ok) {
         const uint32_t trow = tile_row_of_local(rank, lt);
-        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
         if ((int)trow < nr) p = a.rows[r0 + trow];
-        S.px[lt] = p.x;
-        S.py[lt] = p.y;
-        S.pz[lt] = p.z;
       }
-      asm volatile("bar.sync 2, 256;" ::: "memory");
-      mbar_wait(&S.bar[B_H1_EMPTY], (t & 1) ^ 1);
-      if (lt == 0) trace_ev(a, rank, cid, t, 6);
+      return p;
+    };
+    bool have_next = ahead.next(nrow0, nnrows);
+    stage(fetch(have_next, nrow0, nnrows), 0);
+    uint32_t it = 0;
+    while (iter.next(row0, nrows)) {
+      const uint32_t buf = it & 1;
+      asm volatile("bar.sync 2, 128;" ::: "memory");  // rows of tile it staged; buffer buf^1 free
+      have_next = ahead.next(nrow0, nnrows);
+      const float4 pf = fetch(have_next, nrow0, nnrows);  // next tile's row, in flight during this tile
 #pragma unroll 1
-      for (uint32_t r8 = 32 * rq; r8 < 32 * rq + 32; r8 += 8) {
+      for (uint32_t kb = 0; kb < 4; ++kb) {
+        unsigned long long wx[4], wy[4], wz[4], wb[4];
 #pragma unroll
-        for (uint32_t v = 0; v < 8; v += 2) {
-          const uint32_t r = r8 + v;
-          const unsigned long long x2 = *reinterpret_cast<const unsigned long long*>(&S.px[r]);
-          const unsigned long long y2 = *reinterpret_cast<const unsigned long long*>(&S.py[r]);
-          const unsigned long long z2 = *reinterpret_cast<const unsigned long long*>(&S.pz[r]);
+        for (int k = 0; k < 4; ++k) {
+          const float4 w = S.w1b[64 * kb + 4 * fq + k];
+          wx[k] = f2(w.x, w.x);
+          wy[k] = f2(w.y, w.y);
+          wz[k] = f2(w.z, w.z);
+          wb[k] = f2(w.w, w.w);
+        }
+        mbar_wait(&S.bar[B_H1E0 + kb], (it & 1) ^ 1);
+        if (lt == 0 && kb == 0) trace_ev(a, rank, cid, it, 6);
+#pragma unroll
+        for (uint32_t v = 0; v < 8; ++v) {
+          const uint32_t lr = 64 * (v >> 2) + 8 * rq + 2 * (v & 3);  // local rows lr, lr + 1
+          const unsigned long long x2 = *reinterpret_cast<const unsigned long long*>(&S.px[buf][lr]);
+          const unsigned long long y2 = *reinterpret_cast<const unsigned long long*>(&S.py[buf][lr]);
+          const unsigned long long z2 = *reinterpret_cast<const unsigned long long*>(&S.pz[buf][lr]);
           unsigned long long h[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) h[k] = ffma2(wx[k], x2, ffma2(wy[k], y2, ffma2(wz[k], z2, wb[k])));
-          const uint32_t base = l1_base + (r8 >> 3) * 1024;
-          st_shared_v2(base + v * 128 + ((l1_chunk ^ v) << 4), pack_relu_bf16x2(f2_lo(h[0]), f2_lo(h[1])),
+          const uint32_t base = h1 + kb * 16384 + (v >> 2) * 8192;
+          const uint32_t r = 2 * (v & 3);  // row within the 8-row group
+          st_shared_v2(base + r * 128 + ((chunk ^ r) << 4), pack_relu_bf16x2(f2_lo(h[0]), f2_lo(h[1])),
                        pack_relu_bf16x2(f2_lo(h[2]), f2_lo(h[3])));
-          st_shared_v2(base + (v + 1) * 128 + ((l1_chunk ^ (v + 1)) << 4), pack_relu_bf16x2(f2_hi(h[0]), f2_hi(h[1])),
+          st_shared_v2(base + (r + 1) * 128 + ((chunk ^ (r + 1)) << 4), pack_relu_bf16x2(f2_hi(h[0]), f2_hi(h[1])),
                        pack_relu_bf16x2(f2_hi(h[2]), f2_hi(h[3])));
         }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&S.bar[B_H1F0 + kb], 0);
       }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&S.bar[B_H1_FULL], 0);
-      if (lt == 0) trace_ev(a, rank, cid, t, 7);
-    };
-
-    TileIter iter_l1(a, cid, ncl), iter(a, cid, ncl);
-    int64_t row0, l1_row0;
-    int nrows, l1_nrows;
+      if (lt == 0) trace_ev(a, rank, cid, it, 7);
+      stage(pf, buf ^ 1);
+      ++it;
+    }
+  } else if (warp < kWarpE3) {
+    // ============ epi L2: thread = row, features [128 half, +128) ============
+    const uint32_t q = warp & 3;                 // TMEM lane quarter (rows 32q..32q+31)
+    const uint32_t half = (warp - kWarpE2) >> 2;
+    const uint32_t row = 32 * q + lane;
+    const uint32_t lt = threadIdx.x - 32 * kWarpE2;
+    const uint32_t h2 = smem_u32(S.h2);
+    TileIter iter(a, cid, ncl);
+    int64_t row0;
+    int nrows;
     uint32_t it = 0;
-    if (iter_l1.next(l1_row0, l1_nrows)) layer1(0, l1_row0, l1_nrows);
     while (iter.next(row0, nrows)) {
       mbar_wait(&S.bar[B_D2_FULL], it & 1);
       if (lt == 0) trace_ev(a, rank, cid, it, 8);
@@ -381,21 +550,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       }
       if (lt == 0) trace_ev(a, rank, cid, it, 10);
       ++it;
-      if (iter_l1.next(l1_row0, l1_nrows)) layer1(it, l1_row0, l1_nrows);
     }
   } else {
     // ============ epi L3: thread = output feature; walk rows: cell max, occupied-cell mean ============
     const uint32_t q = warp & 3;
     const uint32_t eg = warp - kWarpE3;  // 0..3: which 32-row chunks this warp flags
     const uint32_t f = 128 * rank + 32 * q + lane;
-    const float b3 = a.b3[f];
-    float run_max = -INFINITY, run_sum = 0.f;
-    int run_cells = 0;
+    const float b3 = a.b3[f], nb3 = -b3;
+    Walk w{nb3, 0.f, 0};
     TileIter iter(a, cid, ncl);
     int64_t row0;
     int nrows;
+    bool first;
     uint32_t it = 0, c0 = 0, c1 = 0;
-    while (iter.next(row0, nrows)) {
+    while (iter.next(row0, nrows, first)) {
+      if (first) w.m = nb3;  // drop padding rows after the previous chunk's last segment end
       asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's flags no longer read
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -416,6 +585,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         mbar_wait(&S.bar[p ? B_D3F1 : B_D3F0], (p ? c1 : c0) & 1);
         if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 12 + 2 * p);
         tc_fence_after();
+#if LOCC_E3_TWO_WALKERS
+        // columns [0, 64) continue w; columns [64, 128) run as a tail walker, merged at the end.
+        // Columns past the valid rows follow the chunk's last segment end (or are skipped with the
+        // whole part), so they only touch m.
+        const uint32_t tbase = tmem + ((32 * q) << 16) + d3_col(it & 1, p);
+        Tail t;
+        t.w = Walk{nb3, 0.f, 0};
+        t.hm = nb3;
+        t.s1 = 0.f;
+        t.c1 = 0;
+        t.seg1 = 0;
+        t.ce = false;
+        t.se = false;
+        uint32_t xa[16], ya[16], xb[16], yb[16];
+        tmem_ld16(tbase, xa);
+        tmem_ld16(tbase + 64, ya);
+        const uint32_t* fl = S.flags + 128 * p;
+        const uint32_t* mk = S.masks + 4 * p;
+        e3_step<0>(tbase, xa, ya, xb, yb, mk, fl, w, t, nb3, b3, a.pooled, f);
+        e3_step<1>(tbase, xb, yb, xa, ya, mk, fl, w, t, nb3, b3, a.pooled, f);
+        e3_step<2>(tbase, xa, ya, xb, yb, mk, fl, w, t, nb3, b3, a.pooled, f);
+        e3_step<3>(tbase, xb, yb, xa, ya, mk, fl, w, t, nb3, b3, a.pooled, f);
+        merge(w, t, b3, a.pooled, f);
+#else
         const uint32_t tbase = tmem + ((32 * q) << 16) + d3_col(it & 1, p);
         const int ncols = min(128, nrows - 128 * p);
         uint32_t va[32], vb[32];
@@ -427,10 +620,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
             uint32_t(&nx)[32] = (c & 1) ? va : vb;
             tmem_ld_wait();
             if (c < 3 && 32 * (c + 1) < ncols) tmem_ld32(tbase + 32 * (c + 1), nx);
-            walk_chunk(v, min(32, ncols - 32 * c), S.masks[4 * p + c], S.masks[8 + 4 * p + c],
-                       S.flags + 128 * p + 32 * c, b3, run_max, run_sum, run_cells, a.pooled, f);
+            walk_chunk32(v, S.masks[4 * p + c], S.masks[8 + 4 * p + c], S.flags + 128 * p + 32 * c, w, nb3, b3,
+                         a.pooled, f);
           }
         }
+#endif
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&S.bar[p ? B_D3E1 : B_D3E0], 0);
