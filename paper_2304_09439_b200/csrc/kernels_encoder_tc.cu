@@ -72,12 +72,13 @@ __device__ __forceinline__ uint32_t d3_col(uint32_t par, int p) {
 }
 
 struct alignas(1024) Smem {
-  uint8_t w2[65536];  // B of L2: this CTA's 128 W2 rows, 4 K blocks x [128 rows x 128 B], SW128
+  uint8_t w2[5 * 16384];  // B of L2: this CTA's 128 W2 rows, 4 K blocks x [128 rows x 128 B], SW128,
+                          // + a block whose K = 0..2 hold b2 split into three bf16 terms
+  uint8_t ones[1024];     // A of the bias MMA: one 8-row SW128 atom with K = 0..2 = 1 (all rows alike)
   uint8_t h1[65536];  // A of L2: this CTA's 128 rows of h1, same layout
   uint8_t h2[65536];  // B of L3: this CTA's 128 rows of h2, same layout
   float px[2][128], py[2][128], pz[2][128];  // this CTA's rows of a tile (layer-1 input), double buffered
   float4 w1b[256];                            // (w0, w1, w2, b1) per layer-1 feature
-  float b2[256];
   uint32_t flags[kTileRows];  // row flags of the whole tile (epi L3)
   uint32_t masks[16];         // cell-end bits [0..7], segment-end bits [8..15] per 32-row chunk
   uint64_t bar[19];
@@ -90,9 +91,8 @@ enum {
 
 struct TcArgs {
   const float4* w1b;      // [256] (w0, w1, w2, b1)
-  const float* b2;
   const float* b3;
-  const uint8_t* w2img;   // [2 ranks][65536 B] pre-swizzled
+  const uint8_t* w2img;   // [2 ranks][5 x 16384 B] pre-swizzled (W2 + bias block)
   const uint32_t* w3img;  // [256 rows][128] bf16x2
   const float4* rows;
   const int64_t* offsets;
@@ -138,6 +138,14 @@ struct TileIter {
     return next(row0, nrows, f);
   }
 };
+
+// One warp of a role group polls the mbarrier; the others wait on a named barrier (no issue slots).
+template <int ID, int NTHREADS>
+__device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool poller) {
+  if (poller) mbar_wait(bar, parity);
+  __syncwarp();
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(NTHREADS) : "memory");
+}
 
 __device__ __forceinline__ uint32_t tile_row_of_local(uint32_t rank, uint32_t i) {
   return i < 64 ? 64 * rank + i : 128 + 64 * rank + (i - 64);
@@ -332,14 +340,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     mbar_init(&S.bar[B_D3E1], 8);
     mbar_init(&S.bar[B_WLOAD], 1);
     fence_mbar_init();
-    mbar_arrive_expect_tx(&S.bar[B_WLOAD], 65536);
-    for (int kb = 0; kb < 4; ++kb)
-      bulk_g2s(S.w2 + kb * 16384, a.w2img + (size_t)rank * 65536 + kb * 16384, 16384, &S.bar[B_WLOAD]);
+    mbar_arrive_expect_tx(&S.bar[B_WLOAD], 5 * 16384);
+    for (int kb = 0; kb < 5; ++kb)
+      bulk_g2s(S.w2 + kb * 16384, a.w2img + (size_t)rank * 5 * 16384 + kb * 16384, 16384, &S.bar[B_WLOAD]);
   }
-  for (int i = threadIdx.x; i < 256; i += kThreads) {
-    S.b2[i] = a.b2[i];
-    S.w1b[i] = a.w1b[i];
+  for (int i = threadIdx.x; i < 256; i += kThreads) S.w1b[i] = a.w1b[i];
+  for (int i = threadIdx.x; i < 256; i += kThreads) {  // ones atom: row i>>5, 4-byte word i&31
+    const uint32_t row = i >> 5, word = i & 31;
+    const uint32_t chunk = (word >> 2) ^ row;  // logical 16-byte chunk of this physical word
+    uint32_t v = 0;
+    if (chunk == 0 && (word & 3) == 0) v = 0x3F803F80u;  // K = 0, 1
+    if (chunk == 0 && (word & 3) == 1) v = 0x00003F80u;  // K = 2
+    reinterpret_cast<uint32_t*>(S.ones)[i] = v;
   }
+  fence_proxy_async_smem();
   if (warp == kWarpMMA) tmem_alloc_2cta(&S.tmem_base, kTmemCols);
   cluster_sync();
   tc_fence_after();
@@ -370,7 +384,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       int nrows;
       uint32_t it = 0, n0 = 0, n1 = 0;
       bool prev_p1 = false;
-      const uint32_t a_h1 = smem_u32(S.h1), b_w2 = smem_u32(S.w2), b_h2 = smem_u32(S.h2);
+      const uint32_t a_h1 = smem_u32(S.h1), b_w2 = smem_u32(S.w2), b_h2 = smem_u32(S.h2), a_one = smem_u32(S.ones);
       while (iter.next(row0, nrows)) {
         const uint32_t par = it & 1;
         // D2 = [RA|RB] (even) or [RB|RC] (odd): RA resp. RC last held L3p0 of the previous tile;
@@ -378,6 +392,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         if (it > 0) mbar_wait(&S.bar[B_D3E0], (n0 - 1) & 1);
         trace_ev(a, rank, cid, it, 1);
         const uint32_t dcol = tmem + d2_col(par);
+        tc_fence_after();
+        // D2 = 1 * b2 (hi + mid + lo): independent of h1, issued before layer 1 has finished
+        mma_ss_2cta(dcol, smem_desc_sw128(a_one, 0), smem_desc_sw128(b_w2 + 4 * 16384, 1024), kIdescL2, 0);
 #pragma unroll 1
         for (int kb = 0; kb < 4; ++kb) {
           mbar_wait(&S.bar[B_H1F0 + kb], par);
@@ -386,8 +403,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
             const uint32_t koff = kb * 16384 + s * 32;
-            mma_ss_2cta(dcol, smem_desc_sw128(a_h1 + koff, 1024), smem_desc_sw128(b_w2 + koff, 1024), kIdescL2,
-                        (kb | s) != 0);
+            mma_ss_2cta(dcol, smem_desc_sw128(a_h1 + koff, 1024), smem_desc_sw128(b_w2 + koff, 1024), kIdescL2, 1);
           }
           mma_commit_2cta(&S.bar[B_H1E0 + kb], 3);
         }
@@ -478,7 +494,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           wz[k] = f2(w.z, w.z);
           wb[k] = f2(w.w, w.w);
         }
-        mbar_wait(&S.bar[B_H1E0 + kb], (it & 1) ^ 1);
+        group_wait<2, 128>(&S.bar[B_H1E0 + kb], (it & 1) ^ 1, warp == kWarpL1);
         if (lt == 0 && kb == 0) trace_ev(a, rank, cid, it, 6);
 #pragma unroll
         for (uint32_t v = 0; v < 8; ++v) {
@@ -516,10 +532,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     int nrows;
     uint32_t it = 0;
     while (iter.next(row0, nrows)) {
-      mbar_wait(&S.bar[B_D2_FULL], it & 1);
-      if (lt == 0) trace_ev(a, rank, cid, it, 8);
-      mbar_wait(&S.bar[B_H2_EMPTY], (it & 1) ^ 1);
-      if (lt == 0) trace_ev(a, rank, cid, it, 9);
+      if (warp == kWarpE2) {  // one warp polls; the group waits on a named barrier
+        mbar_wait(&S.bar[B_D2_FULL], it & 1);
+        if (lt == 0) trace_ev(a, rank, cid, it, 8);
+        mbar_wait(&S.bar[B_H2_EMPTY], (it & 1) ^ 1);
+        if (lt == 0) trace_ev(a, rank, cid, it, 9);
+      }
+      __syncwarp();
+      asm volatile("bar.sync 3, 256;" ::: "memory");
       tc_fence_after();
       const uint32_t tbase = tmem + ((32 * q) << 16) + d2_col(it & 1) + 128 * half;
       uint32_t va[32], vb[32];
@@ -532,15 +552,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         if (c < 3) tmem_ld32(tbase + 32 * (c + 1), nx);
         const int cc = 4 * half + c;  // feature chunk (32 features)
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const float* bp = &S.b2[32 * cc + 8 * g];
-          const unsigned long long* b2p = reinterpret_cast<const unsigned long long*>(bp);
+        for (int g = 0; g < 4; ++g) {  // D2 already holds the bias (see the MMA issuer)
           uint32_t w[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const unsigned long long s = fadd2(f2(__uint_as_float(v[8 * g + 2 * e]), __uint_as_float(v[8 * g + 2 * e + 1])), b2p[e]);
-            w[e] = pack_relu_bf16x2(f2_lo(s), f2_hi(s));
-          }
+          for (int e = 0; e < 4; ++e)
+            w[e] = pack_relu_bf16x2(__uint_as_float(v[8 * g + 2 * e]), __uint_as_float(v[8 * g + 2 * e + 1]));
           st_shared_v4(h2 + (cc >> 1) * 16384 + sw128_off(row, (cc & 1) * 4 + g), w[0], w[1], w[2], w[3]);
         }
         fence_proxy_async_smem();
@@ -582,7 +598,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 11);
       const int np = nrows > 128 ? 2 : 1;
       for (int p = 0; p < np; ++p) {
-        mbar_wait(&S.bar[p ? B_D3F1 : B_D3F0], (p ? c1 : c0) & 1);
+        group_wait<1, 128>(&S.bar[p ? B_D3F1 : B_D3F0], (p ? c1 : c0) & 1, warp == kWarpE3);
         if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 12 + 2 * p);
         tc_fence_after();
 #if LOCC_E3_TWO_WALKERS
@@ -655,7 +671,6 @@ cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b
   (void)l1;
   TcArgs args;
   args.w1b = P.w1b;
-  args.b2 = P.b2;
   args.b3 = P.b3;
   args.w2img = static_cast<const uint8_t*>(P.tc_w2);
   args.w3img = static_cast<const uint32_t*>(P.tc_w3);

@@ -640,13 +640,22 @@ uint16_t bf16_rne(float x) {
   u += 0x7FFFu + ((u >> 16) & 1u);
   return (uint16_t)(u >> 16);
 }
+float bf16_to_float(uint16_t h) {
+  const uint32_t u = (uint32_t)h << 16;
+  float x;
+  std::memcpy(&x, &u, 4);
+  return x;
+}
 }  // namespace
 
 // W2 as the B operand of layer 2: per CTA rank r its output features [128r, 128r+128), K-major,
 // 4 K blocks of [128 rows x 128 B] with the 128-byte swizzle (16-byte chunk j of row i stored at
-// chunk j ^ (i & 7)) — the exact shared-memory image, so one bulk copy places it.
+// chunk j ^ (i & 7)) — the exact shared-memory image, so one bulk copy places it.  A fifth block
+// holds b2 as the K = 0..2 entries (b2 = hi + mid + lo, each bf16, exact), which the kernel
+// multiplies with a column of ones so that the first layer-2 MMA initialises D2 with the bias.
 // W3 as the TMEM A operand of layer 3: row f = 128 columns of bf16x2 (K = 2c low, 2c+1 high).
 // Also keeps layer 1 (w, b) and b2 for the kernel-parameter block.
+constexpr size_t kTcW2Bytes = 5 * 16384;  // per CTA rank
 locc_status locc_upload_tc_weights(locc_ctx* c, const float* flat) {
   const int H = 256;
   const float* w1 = flat;
@@ -658,18 +667,28 @@ locc_status locc_upload_tc_weights(locc_ctx* c, const float* flat) {
     c->tc_l1.w1b[f] = make_float4(w1[3 * f], w1[3 * f + 1], w1[3 * f + 2], b1[f]);
     c->tc_l1.b2[f] = b2[f];
   }
-  std::vector<uint8_t> img(2 * 65536 + (size_t)H * 128 * 4);
+  std::vector<uint8_t> img(2 * kTcW2Bytes + (size_t)H * 128 * 4, 0);
   for (int r = 0; r < 2; ++r)
-    for (int i = 0; i < 128; ++i)
+    for (int i = 0; i < 128; ++i) {
       for (int kb = 0; kb < 4; ++kb)
         for (int j = 0; j < 8; ++j) {
-          uint8_t* dst = img.data() + r * 65536 + kb * 16384 + locc::tc::sw128_off(i, j);
+          uint8_t* dst = img.data() + r * kTcW2Bytes + kb * 16384 + locc::tc::sw128_off(i, j);
           for (int e = 0; e < 8; ++e) {
             const uint16_t v = bf16_rne(w2[(size_t)(128 * r + i) * H + 64 * kb + 8 * j + e]);
             std::memcpy(dst + 2 * e, &v, 2);
           }
         }
-  uint32_t* w3img = reinterpret_cast<uint32_t*>(img.data() + 2 * 65536);
+      const float b = b2[128 * r + i];
+      const uint16_t hi = bf16_rne(b);
+      const float r1 = b - bf16_to_float(hi);
+      const uint16_t mid = bf16_rne(r1);
+      const uint16_t lo = bf16_rne(r1 - bf16_to_float(mid));
+      uint8_t* dst = img.data() + r * kTcW2Bytes + 4 * 16384 + locc::tc::sw128_off(i, 0);
+      std::memcpy(dst + 0, &hi, 2);
+      std::memcpy(dst + 2, &mid, 2);
+      std::memcpy(dst + 4, &lo, 2);
+    }
+  uint32_t* w3img = reinterpret_cast<uint32_t*>(img.data() + 2 * kTcW2Bytes);
   for (int f = 0; f < H; ++f)
     for (int cc = 0; cc < 128; ++cc)
       w3img[(size_t)f * 128 + cc] =
@@ -677,6 +696,6 @@ locc_status locc_upload_tc_weights(locc_ctx* c, const float* flat) {
   CK(c->tc_img.ensure(img.size()));
   CK(cudaMemcpy(c->tc_img.p, img.data(), img.size(), cudaMemcpyHostToDevice));
   c->P.tc_w2 = c->tc_img.p;
-  c->P.tc_w3 = static_cast<uint8_t*>(c->tc_img.p) + 2 * 65536;
+  c->P.tc_w3 = static_cast<uint8_t*>(c->tc_img.p) + 2 * kTcW2Bytes;
   return LOCC_OK;
 }
