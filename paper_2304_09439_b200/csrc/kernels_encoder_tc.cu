@@ -78,7 +78,7 @@ struct alignas(1024) Smem {
   uint8_t h1[65536];  // A of L2: this CTA's 128 rows of h1, same layout
   uint8_t h2[65536];  // B of L3: this CTA's 128 rows of h2, same layout
   float px[2][128], py[2][128], pz[2][128];  // this CTA's rows of a tile (layer-1 input), double buffered
-  float4 w1b[256];                            // (w0, w1, w2, b1) per layer-1 feature
+  float4 w1b[256];  // (w0, w1, w2, b1) of feature 64kb + 4fq + k at [(4kb + k) 16 + fq] (conflict-free reads)
   uint32_t flags[kTileRows];  // row flags of the whole tile (epi L3)
   uint32_t masks[16];         // cell-end bits [0..7], segment-end bits [8..15] per 32-row chunk
   uint64_t bar[19];
@@ -344,7 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     for (int kb = 0; kb < 5; ++kb)
       bulk_g2s(S.w2 + kb * 16384, a.w2img + (size_t)rank * 5 * 16384 + kb * 16384, 16384, &S.bar[B_WLOAD]);
   }
-  for (int i = threadIdx.x; i < 256; i += kThreads) S.w1b[i] = a.w1b[i];
+  for (int i = threadIdx.x; i < 256; i += kThreads) S.w1b[((i >> 6) * 4 + (i & 3)) * 16 + ((i & 63) >> 2)] = a.w1b[i];
   for (int i = threadIdx.x; i < 256; i += kThreads) {  // ones atom: row i>>5, 4-byte word i&31
     const uint32_t row = i >> 5, word = i & 31;
     const uint32_t chunk = (word >> 2) ^ row;  // logical 16-byte chunk of this physical word
@@ -377,45 +377,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
 
   // ---------------------------------------------------------------- roles
   if (warp == kWarpMMA) {
-    // ============ MMA issuer (leader CTA, one thread) ============
-    if (rank == 0 && lane == 0) {
+    // ============ MMA issuer (leader CTA, whole warp; one elected lane issues) ============
+    if (rank == 0) {
       TileIter iter(a, cid, ncl);
       int64_t row0;
       int nrows;
       uint32_t it = 0, n0 = 0, n1 = 0;
       bool prev_p1 = false;
-      const uint32_t a_h1 = smem_u32(S.h1), b_w2 = smem_u32(S.w2), b_h2 = smem_u32(S.h2), a_one = smem_u32(S.ones);
+      // descriptors are fixed for the launch: K step k of a K-major SW128 operand is +32 B (+2 in
+      // the descriptor's address field) within a K block and +16384 B (+1024) per K block
+      const uint64_t dA1 = smem_desc_sw128(smem_u32(S.h1), 1024), dW2 = smem_desc_sw128(smem_u32(S.w2), 1024);
+      const uint64_t dH2 = smem_desc_sw128(smem_u32(S.h2), 1024), dOne = smem_desc_sw128(smem_u32(S.ones), 0);
+      const uint64_t dB2 = dW2 + 4 * 1024;
       while (iter.next(row0, nrows)) {
         const uint32_t par = it & 1;
         // D2 = [RA|RB] (even) or [RB|RC] (odd): RA resp. RC last held L3p0 of the previous tile;
         // RB held the previous D2, drained before that tile's L3 could start.
         if (it > 0) mbar_wait(&S.bar[B_D3E0], (n0 - 1) & 1);
-        trace_ev(a, rank, cid, it, 1);
+        if (lane == 0) trace_ev(a, rank, cid, it, 1);
         const uint32_t dcol = tmem + d2_col(par);
         tc_fence_after();
         // D2 = 1 * b2 (hi + mid + lo): independent of h1, issued before layer 1 has finished
-        mma_ss_2cta(dcol, smem_desc_sw128(a_one, 0), smem_desc_sw128(b_w2 + 4 * 16384, 1024), kIdescL2, 0);
-#pragma unroll 1
+        if (elect_one()) mma_ss_2cta(dcol, dOne, dB2, kIdescL2, 0);
+#pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
           mbar_wait(&S.bar[B_H1F0 + kb], par);
-          if (kb == 0) trace_ev(a, rank, cid, it, 0);
+          if (kb == 0 && lane == 0) trace_ev(a, rank, cid, it, 0);
           tc_fence_after();
 #pragma unroll
           for (int s = 0; s < 4; ++s) {
-            const uint32_t koff = kb * 16384 + s * 32;
-            mma_ss_2cta(dcol, smem_desc_sw128(a_h1 + koff, 1024), smem_desc_sw128(b_w2 + koff, 1024), kIdescL2, 1);
+            const uint32_t koff = kb * 1024 + s * 2;
+            if (elect_one()) mma_ss_2cta(dcol, dA1 + koff, dW2 + koff, kIdescL2, 1);
           }
-          mma_commit_2cta(&S.bar[B_H1E0 + kb], 3);
+          if (elect_one()) mma_commit_2cta(&S.bar[B_H1E0 + kb], 3);
         }
-        mma_commit_2cta(&S.bar[B_D2_FULL], 3);
-        trace_ev(a, rank, cid, it, 2);
+        if (elect_one()) mma_commit_2cta(&S.bar[B_D2_FULL], 3);
+        if (lane == 0) trace_ev(a, rank, cid, it, 2);
         // L3p0 -> RC (even) / RA (odd): last held L3p1 of the previous tile, if it had one
         if (prev_p1) mbar_wait(&S.bar[B_D3E1], (n1 - 1) & 1);
-        trace_ev(a, rank, cid, it, 3);
+        if (lane == 0) trace_ev(a, rank, cid, it, 3);
         const int np = nrows > 128 ? 2 : 1;
         {
           const uint32_t d3 = tmem + d3_col(par, 0);
-#pragma unroll 1
+#pragma unroll
           for (int j = 0; j < 4; ++j) {  // K chunk j = features {32j..32j+31} and {128+32j..}
             mbar_wait(&S.bar[B_E2K0 + j], par);
             tc_fence_after();
@@ -424,29 +428,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
 #pragma unroll
               for (int s = 0; s < 2; ++s) {
                 const int k = 8 * h + 2 * j + s;
-                const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32;
-                mma_ts_2cta(d3, tmem + kColW3 + 8 * k, smem_desc_sw128(b_h2 + koff, 1024), kIdescL3, (j | h | s) != 0);
+                const uint32_t koff = (k >> 2) * 1024 + (k & 3) * 2;
+                if (elect_one()) mma_ts_2cta(d3, tmem + kColW3 + 8 * k, dH2 + koff, kIdescL3, (j | h | s) != 0);
               }
           }
-          mma_commit_2cta(&S.bar[B_D3F0], 3);
-          trace_ev(a, rank, cid, it, 4);
+          if (elect_one()) mma_commit_2cta(&S.bar[B_D3F0], 3);
+          if (lane == 0) trace_ev(a, rank, cid, it, 4);
         }
         if (np == 2) {
           const uint32_t d3 = tmem + d3_col(par, 1);
-#pragma unroll 1
+#pragma unroll
           for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
               for (int s = 0; s < 2; ++s) {
                 const int k = 8 * h + 2 * j + s;
-                const uint32_t koff = (k >> 2) * 16384 + (k & 3) * 32 + 8192;
-                mma_ts_2cta(d3, tmem + kColW3 + 8 * k, smem_desc_sw128(b_h2 + koff, 1024), kIdescL3, (j | h | s) != 0);
+                const uint32_t koff = (k >> 2) * 1024 + (k & 3) * 2 + 512;
+                if (elect_one()) mma_ts_2cta(d3, tmem + kColW3 + 8 * k, dH2 + koff, kIdescL3, (j | h | s) != 0);
               }
-          mma_commit_2cta(&S.bar[B_D3F1], 3);
-          trace_ev(a, rank, cid, it, 5);
+          if (elect_one()) mma_commit_2cta(&S.bar[B_D3F1], 3);
+          if (lane == 0) trace_ev(a, rank, cid, it, 5);
         }
-        mma_commit_2cta(&S.bar[B_H2_EMPTY], 3);
+        if (elect_one()) mma_commit_2cta(&S.bar[B_H2_EMPTY], 3);
         ++n0;
         if (np == 2) ++n1;
         prev_p1 = np == 2;
@@ -488,7 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         unsigned long long wx[4], wy[4], wz[4], wb[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const float4 w = S.w1b[64 * kb + 4 * fq + k];
+          const float4 w = S.w1b[(4 * kb + k) * 16 + fq];
           wx[k] = f2(w.x, w.x);
           wy[k] = f2(w.y, w.y);
           wz[k] = f2(w.z, w.z);
@@ -497,20 +501,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         group_wait<2, 128>(&S.bar[B_H1E0 + kb], (it & 1) ^ 1, warp == kWarpL1);
         if (lt == 0 && kb == 0) trace_ev(a, rank, cid, it, 6);
 #pragma unroll
-        for (uint32_t v = 0; v < 8; ++v) {
-          const uint32_t lr = 64 * (v >> 2) + 8 * rq + 2 * (v & 3);  // local rows lr, lr + 1
-          const unsigned long long x2 = *reinterpret_cast<const unsigned long long*>(&S.px[buf][lr]);
-          const unsigned long long y2 = *reinterpret_cast<const unsigned long long*>(&S.py[buf][lr]);
-          const unsigned long long z2 = *reinterpret_cast<const unsigned long long*>(&S.pz[buf][lr]);
-          unsigned long long h[4];
+        for (uint32_t g = 0; g < 2; ++g) {  // local rows 64g + 8rq .. +7
+          const uint32_t lr = 64 * g + 8 * rq;
+          const float4 xa = *reinterpret_cast<const float4*>(&S.px[buf][lr]);
+          const float4 xb = *reinterpret_cast<const float4*>(&S.px[buf][lr + 4]);
+          const float4 ya = *reinterpret_cast<const float4*>(&S.py[buf][lr]);
+          const float4 yb = *reinterpret_cast<const float4*>(&S.py[buf][lr + 4]);
+          const float4 za = *reinterpret_cast<const float4*>(&S.pz[buf][lr]);
+          const float4 zb = *reinterpret_cast<const float4*>(&S.pz[buf][lr + 4]);
+          const unsigned long long x2[4] = {f2(xa.x, xa.y), f2(xa.z, xa.w), f2(xb.x, xb.y), f2(xb.z, xb.w)};
+          const unsigned long long y2[4] = {f2(ya.x, ya.y), f2(ya.z, ya.w), f2(yb.x, yb.y), f2(yb.z, yb.w)};
+          const unsigned long long z2[4] = {f2(za.x, za.y), f2(za.z, za.w), f2(zb.x, zb.y), f2(zb.z, zb.w)};
+          const uint32_t base = h1 + kb * 16384 + g * 8192;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) h[k] = ffma2(wx[k], x2, ffma2(wy[k], y2, ffma2(wz[k], z2, wb[k])));
-          const uint32_t base = h1 + kb * 16384 + (v >> 2) * 8192;
-          const uint32_t r = 2 * (v & 3);  // row within the 8-row group
-          st_shared_v2(base + r * 128 + ((chunk ^ r) << 4), pack_relu_bf16x2(f2_lo(h[0]), f2_lo(h[1])),
-                       pack_relu_bf16x2(f2_lo(h[2]), f2_lo(h[3])));
-          st_shared_v2(base + (r + 1) * 128 + ((chunk ^ (r + 1)) << 4), pack_relu_bf16x2(f2_hi(h[0]), f2_hi(h[1])),
-                       pack_relu_bf16x2(f2_hi(h[2]), f2_hi(h[3])));
+          for (uint32_t v = 0; v < 4; ++v) {  // rows lr + 2v, lr + 2v + 1
+            unsigned long long h[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) h[k] = ffma2(wx[k], x2[v], ffma2(wy[k], y2[v], ffma2(wz[k], z2[v], wb[k])));
+            const uint32_t r = 2 * v;  // row within the 8-row group
+            st_shared_v2(base + r * 128 + ((chunk ^ r) << 4), pack_relu_bf16x2(f2_lo(h[0]), f2_lo(h[1])),
+                         pack_relu_bf16x2(f2_lo(h[2]), f2_lo(h[3])));
+            st_shared_v2(base + (r + 1) * 128 + ((chunk ^ (r + 1)) << 4), pack_relu_bf16x2(f2_hi(h[0]), f2_hi(h[1])),
+                         pack_relu_bf16x2(f2_hi(h[2]), f2_hi(h[3])));
+          }
         }
         fence_proxy_async_smem();
         __syncwarp();
