@@ -10,7 +10,12 @@ constexpr int kPredW = 128;        // predictor width, "3 layers of
 constexpr int kSegPerChunk = 8;    // encoder work unit: 8 whole (pair, side) segments = 4 pairs
 constexpr int kRowFlagCellEnd = 1; // row flag: last kept row of its cell within the segment
 constexpr int kRowFlagSegEnd = 2;  // row flag: last kept row of the segment
-constexpr int kRowSegShift = 2;    // flags word = (segment << 2) | seg_end << 1 | cell_end
+constexpr int kRowFlagPad = 4;     // row flag: padding row after the segment's last kept row
+constexpr int kRowSegShift = 3;    // flags word = (segment << 3) | pad << 2 | seg_end << 1 | cell_end
+// Each segment's rows are padded to a multiple of kSegAlign, so a segment starts on a 16-row step
+// of the encoder's layer-3 walk and a segment end is followed only by padding within its step.
+constexpr int kSegAlign = 16;
+__host__ __device__ constexpr int64_t seg_rows(int64_t kept) { return (kept + kSegAlign - 1) / kSegAlign * kSegAlign; }
 
 // S0 output (one copy per context, resident for the context's lifetime).
 struct ShapeTable {

@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(256) encoder_f32_kernel(DevParams P, Batch b) 
     if (act) {
 #pragma unroll
       for (int r = 0; r < TR; ++r) {
-        if (r < nr) {
-          const uint32_t fl = __float_as_uint(rows_s[r].w);
+        const uint32_t fl = __float_as_uint(rows_s[r].w);
+        if (r < nr && !(fl & kRowFlagPad)) {
           run_max = fmaxf(run_max, acc[r]);
           if (fl & kRowFlagCellEnd) {
             run_sum += fmaxf(run_max + b3, 0.f);

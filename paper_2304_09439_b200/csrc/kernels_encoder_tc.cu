@@ -35,16 +35,15 @@
 
 #include "internal.h"
 #include "tc_ptx.cuh"
+#include "e3_walk.cuh"
 
-#ifndef LOCC_E3_TWO_WALKERS
-#define LOCC_E3_TWO_WALKERS 0
-#endif
 
 namespace locc {
 
 namespace {
 
 using namespace tc;
+using namespace e3;
 
 // Warp roles.  TMEM lane access is restricted to lane quarter (warp % 4), so each TMEM-reading
 // group starts at a multiple of 4.  The warp scheduler favours higher warp ids, so the sequential
@@ -80,7 +79,7 @@ struct alignas(1024) Smem {
   float px[2][128], py[2][128], pz[2][128];  // this CTA's rows of a tile (layer-1 input), double buffered
   float4 w1b[256];  // (w0, w1, w2, b1) of feature 64kb + 4fq + k at [(4kb + k) 16 + fq] (conflict-free reads)
   uint32_t flags[kTileRows];  // row flags of the whole tile (epi L3)
-  uint32_t masks[16];         // cell-end bits [0..7], segment-end bits [8..15] per 32-row chunk
+  alignas(16) uint32_t masks[16];  // per part p: [8p + C] cell ends, [8p + 4 + C] segment ends of step C (interleaved)
   uint64_t bar[19];
   uint32_t tmem_base;
 };
@@ -151,171 +150,18 @@ __device__ __forceinline__ uint32_t tile_row_of_local(uint32_t rank, uint32_t i)
   return i < 64 ? 64 * rank + i : 128 + 64 * rank + (i - 64);
 }
 
-// Layer-3 walk state of one output feature.  m runs from -b3 so that ReLU(max + b3) = m + b3 at a
-// cell end (max(x, -b3) + b3 rounds to exactly the same value as ReLU(x + b3)); s sums m over the
-// occupied cells of the open segment and the mean is (s + c b3) / c.
-struct Walk {
-  float m, s;
-  int c;
-};
-// A walker that starts in the middle of the row sequence (the second half of a layer-3 part) runs
-// without the state before it: the rows up to its first cell end ("head") continue the cell left
-// open by its predecessor and its first segment end closes the predecessor's segment, so both are
-// kept aside (hm; s1, c1, seg1) and folded in by merge() once the predecessor has finished.
-struct Tail {
-  Walk w;
-  float hm, s1;
-  int c1;
-  uint32_t seg1;
-  bool ce, se;  // seen a cell end / a segment end (warp-uniform)
-};
-
-__device__ __forceinline__ void store_mean(float* pooled, uint32_t seg, uint32_t f, float s, int c, float b3) {
-  pooled[(int64_t)seg * 256 + f] = __fdividef(fmaf((float)c, b3, s), (float)c);
-}
-
-// Both walkers over 16 rows without a segment end (and, for the tail walker, not its first cell
-// end): per row one max and, at a cell end, one add; the two dependency chains interleave.
-__device__ __forceinline__ void walk_fast2(const uint32_t (&vx)[16], const uint32_t (&vy)[16], uint32_t cex,
-                                           uint32_t cey, Walk& x, Walk& y, float nb3) {
-  x.c += __popc(cex);
-  y.c += __popc(cey);
+// Layer-3 MMAs of K chunk j (features {32j..32j+31} and {128+32j..}): K steps 2j, 2j+1, 8+2j, 9+2j.
+// A = W3 columns in TMEM (8 columns of bf16x2 per K step), B = h2 (+rowoff: descriptor offset of the
+// part's 64 rows), accumulate from the first K step of the part on.
+__device__ __forceinline__ void l3_chunk(uint32_t d3, uint32_t w3, uint64_t dH2, int j, uint32_t rowoff) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    x.m = fmaxf(x.m, __uint_as_float(vx[j]));
-    y.m = fmaxf(y.m, __uint_as_float(vy[j]));
-    if ((cex >> j) & 1u) {
-      x.s += x.m;
-      x.m = nb3;
-    }
-    if ((cey >> j) & 1u) {
-      y.s += y.m;
-      y.m = nb3;
-    }
-  }
-}
-
-// General 16 rows for the carried walker: segment ends write the mean.
-__device__ __forceinline__ void walk_slow_x(const uint32_t (&v)[16], uint32_t ce, uint32_t se, const uint32_t* flags,
-                                            Walk& w, float nb3, float b3, float* pooled, uint32_t f) {
+  for (int h = 0; h < 2; ++h)
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    w.m = fmaxf(w.m, __uint_as_float(v[j]));
-    if ((ce >> j) & 1u) {
-      w.s += w.m;
-      w.c += 1;
-      w.m = nb3;
-      if ((se >> j) & 1u) {
-        store_mean(pooled, flags[j] >> kRowSegShift, f, w.s, w.c, b3);
-        w.s = 0.f;
-        w.c = 0;
-      }
+    for (int s = 0; s < 2; ++s) {
+      const int k = 8 * h + 2 * j + s;
+      const uint32_t koff = (k >> 2) * 1024 + (k & 3) * 2 + rowoff;
+      mma_ts_2cta(d3, w3 + 8 * k, dH2 + koff, kIdescL3, (j | h | s) != 0);
     }
-  }
-}
-
-// General 16 rows for the tail walker.
-__device__ __forceinline__ void walk_slow_y(const uint32_t (&v)[16], uint32_t ce, uint32_t se, const uint32_t* flags,
-                                            Tail& t, float nb3, float b3, float* pooled, uint32_t f) {
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    t.w.m = fmaxf(t.w.m, __uint_as_float(v[j]));
-    if ((ce >> j) & 1u) {
-      if (t.ce) {
-        t.w.s += t.w.m;
-        t.w.c += 1;
-      } else {
-        t.hm = t.w.m;
-        t.ce = true;
-      }
-      t.w.m = nb3;
-      if ((se >> j) & 1u) {
-        const uint32_t seg = flags[j] >> kRowSegShift;
-        if (t.se) {
-          store_mean(pooled, seg, f, t.w.s, t.w.c, b3);
-        } else {
-          t.s1 = t.w.s;
-          t.c1 = t.w.c;
-          t.seg1 = seg;
-          t.se = true;
-        }
-        t.w.s = 0.f;
-        t.w.c = 0;
-      }
-    }
-  }
-}
-
-// x <- x followed by the tail walker's rows.
-__device__ __forceinline__ void merge(Walk& x, const Tail& t, float b3, float* pooled, uint32_t f) {
-  if (!t.ce) {
-    x.m = fmaxf(x.m, t.w.m);
-    return;
-  }
-  const float hv = fmaxf(x.m, t.hm);  // the cell open across the boundary
-  if (t.se) {
-    store_mean(pooled, t.seg1, f, x.s + hv + t.s1, x.c + 1 + t.c1, b3);
-    x = t.w;
-  } else {
-    x.s = x.s + hv + t.w.s;
-    x.c = x.c + 1 + t.w.c;
-    x.m = t.w.m;
-  }
-}
-
-// Step C (0..3) of a layer-3 part: rows 16C..16C+15 (carried walker) and 64+16C.. (tail walker);
-// the next step's columns are loaded into (nx, ny) while this one is walked.
-// One 32-column chunk of the single-walker layer-3 walk (rows in order).
-__device__ __forceinline__ void walk_chunk32(const uint32_t (&v)[32], uint32_t ce, uint32_t se, const uint32_t* flags,
-                                             Walk& w, float nb3, float b3, float* pooled, uint32_t f) {
-  if (se == 0) {
-    w.c += __popc(ce);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      w.m = fmaxf(w.m, __uint_as_float(v[j]));
-      if ((ce >> j) & 1u) {
-        w.s += w.m;
-        w.m = nb3;
-      }
-    }
-    return;
-  }
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    w.m = fmaxf(w.m, __uint_as_float(v[j]));
-    if ((ce >> j) & 1u) {
-      w.s += w.m;
-      w.c += 1;
-      w.m = nb3;
-      if ((se >> j) & 1u) {
-        store_mean(pooled, flags[j] >> kRowSegShift, f, w.s, w.c, b3);
-        w.s = 0.f;
-        w.c = 0;
-      }
-    }
-  }
-}
-
-template <int C>
-__device__ __forceinline__ void e3_step(uint32_t tbase, uint32_t (&vx)[16], uint32_t (&vy)[16], uint32_t (&nx)[16],
-                                        uint32_t (&ny)[16], const uint32_t* mk, const uint32_t* fl, Walk& w, Tail& t,
-                                        float nb3, float b3, float* pooled, uint32_t f) {
-  tmem_ld_wait();
-  if (C < 3) {
-    tmem_ld16(tbase + 16 * (C + 1), nx);
-    tmem_ld16(tbase + 64 + 16 * (C + 1), ny);
-  }
-  constexpr int sh = 16 * (C & 1);
-  const uint32_t cex = (mk[C >> 1] >> sh) & 0xffffu;
-  const uint32_t sex = (mk[8 + (C >> 1)] >> sh) & 0xffffu;
-  const uint32_t cey = (mk[2 + (C >> 1)] >> sh) & 0xffffu;
-  const uint32_t sey = (mk[8 + 2 + (C >> 1)] >> sh) & 0xffffu;
-  if ((sex | sey) == 0 && (t.ce || cey == 0)) {
-    walk_fast2(vx, vy, cex, cey, w, t.w, nb3);
-  } else {
-    walk_slow_x(vx, cex, sex, fl + 16 * C, w, nb3, b3, pooled, f);
-    walk_slow_y(vy, cey, sey, fl + 64 + 16 * C, t, nb3, b3, pooled, f);
-  }
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder_tc_kernel(const __grid_constant__ TcArgs a) {
@@ -399,17 +245,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         tc_fence_after();
         // D2 = 1 * b2 (hi + mid + lo): independent of h1, issued before layer 1 has finished
         if (elect_one()) mma_ss_2cta(dcol, dOne, dB2, kIdescL2, 0);
-#pragma unroll
+#pragma unroll 1
         for (int kb = 0; kb < 4; ++kb) {
           mbar_wait(&S.bar[B_H1F0 + kb], par);
           if (kb == 0 && lane == 0) trace_ev(a, rank, cid, it, 0);
           tc_fence_after();
+          if (elect_one()) {
+            const uint32_t koff = kb * 1024;
 #pragma unroll
-          for (int s = 0; s < 4; ++s) {
-            const uint32_t koff = kb * 1024 + s * 2;
-            if (elect_one()) mma_ss_2cta(dcol, dA1 + koff, dW2 + koff, kIdescL2, 1);
+            for (int s = 0; s < 4; ++s) mma_ss_2cta(dcol, dA1 + koff + 2 * s, dW2 + koff + 2 * s, kIdescL2, 1);
+            mma_commit_2cta(&S.bar[B_H1E0 + kb], 3);
           }
-          if (elect_one()) mma_commit_2cta(&S.bar[B_H1E0 + kb], 3);
+          __syncwarp();
         }
         if (elect_one()) mma_commit_2cta(&S.bar[B_D2_FULL], 3);
         if (lane == 0) trace_ev(a, rank, cid, it, 2);
@@ -419,34 +266,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         const int np = nrows > 128 ? 2 : 1;
         {
           const uint32_t d3 = tmem + d3_col(par, 0);
-#pragma unroll
+#pragma unroll 1
           for (int j = 0; j < 4; ++j) {  // K chunk j = features {32j..32j+31} and {128+32j..}
             mbar_wait(&S.bar[B_E2K0 + j], par);
             tc_fence_after();
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-              for (int s = 0; s < 2; ++s) {
-                const int k = 8 * h + 2 * j + s;
-                const uint32_t koff = (k >> 2) * 1024 + (k & 3) * 2;
-                if (elect_one()) mma_ts_2cta(d3, tmem + kColW3 + 8 * k, dH2 + koff, kIdescL3, (j | h | s) != 0);
-              }
+            if (elect_one()) l3_chunk(d3, tmem + kColW3, dH2, j, 0);
+            __syncwarp();
           }
           if (elect_one()) mma_commit_2cta(&S.bar[B_D3F0], 3);
           if (lane == 0) trace_ev(a, rank, cid, it, 4);
         }
         if (np == 2) {
           const uint32_t d3 = tmem + d3_col(par, 1);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-              for (int s = 0; s < 2; ++s) {
-                const int k = 8 * h + 2 * j + s;
-                const uint32_t koff = (k >> 2) * 1024 + (k & 3) * 2 + 512;
-                if (elect_one()) mma_ts_2cta(d3, tmem + kColW3 + 8 * k, dH2 + koff, kIdescL3, (j | h | s) != 0);
-              }
+          if (elect_one()) {
+#pragma unroll 1
+            for (int j = 0; j < 4; ++j) l3_chunk(d3, tmem + kColW3, dH2, j, 512);
+          }
+          __syncwarp();
           if (elect_one()) mma_commit_2cta(&S.bar[B_D3F1], 3);
           if (lane == 0) trace_ev(a, rank, cid, it, 5);
         }
@@ -583,7 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
   } else {
     // ============ epi L3: thread = output feature; walk rows: cell max, occupied-cell mean ============
     const uint32_t q = warp & 3;
-    const uint32_t eg = warp - kWarpE3;  // 0..3: which 32-row chunks this warp flags
+    const uint32_t eg = warp - kWarpE3;  // 0..3: flags of rows 32eg.. and the masks of step eg
     const uint32_t f = 128 * rank + 32 * q + lane;
     const float b3 = a.b3[f], nb3 = -b3;
     Walk w{nb3, 0.f, 0};
@@ -598,62 +434,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = 128 * h + 32 * eg + lane;
-        const uint32_t fl = r < nrows ? __float_as_uint(a.rows[row0 + r].w) : 0u;
-        S.flags[r] = fl;
+        S.flags[r] = r < nrows ? __float_as_uint(a.rows[row0 + r].w) : 0u;
+        const int r2 = interleaved_row(h, eg, lane);  // interleaved masks of step eg of part h
+        const uint32_t fl = r2 < nrows ? __float_as_uint(a.rows[row0 + r2].w) : 0u;
         const uint32_t ce = __ballot_sync(0xffffffffu, fl & kRowFlagCellEnd);
         const uint32_t se = __ballot_sync(0xffffffffu, fl & kRowFlagSegEnd);
         if (lane == 0) {
-          S.masks[4 * h + eg] = ce;
-          S.masks[8 + 4 * h + eg] = se;
+          S.masks[8 * h + eg] = ce;
+          S.masks[8 * h + 4 + eg] = se;
         }
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 11);
       const int np = nrows > 128 ? 2 : 1;
+#pragma unroll 1
       for (int p = 0; p < np; ++p) {
         group_wait<1, 128>(&S.bar[p ? B_D3F1 : B_D3F0], (p ? c1 : c0) & 1, warp == kWarpE3);
         if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 12 + 2 * p);
         tc_fence_after();
-#if LOCC_E3_TWO_WALKERS
-        // columns [0, 64) continue w; columns [64, 128) run as a tail walker, merged at the end.
-        // Columns past the valid rows follow the chunk's last segment end (or are skipped with the
-        // whole part), so they only touch m.
-        const uint32_t tbase = tmem + ((32 * q) << 16) + d3_col(it & 1, p);
-        Tail t;
-        t.w = Walk{nb3, 0.f, 0};
-        t.hm = nb3;
-        t.s1 = 0.f;
-        t.c1 = 0;
-        t.seg1 = 0;
-        t.ce = false;
-        t.se = false;
-        uint32_t xa[16], ya[16], xb[16], yb[16];
-        tmem_ld16(tbase, xa);
-        tmem_ld16(tbase + 64, ya);
-        const uint32_t* fl = S.flags + 128 * p;
-        const uint32_t* mk = S.masks + 4 * p;
-        e3_step<0>(tbase, xa, ya, xb, yb, mk, fl, w, t, nb3, b3, a.pooled, f);
-        e3_step<1>(tbase, xb, yb, xa, ya, mk, fl, w, t, nb3, b3, a.pooled, f);
-        e3_step<2>(tbase, xa, ya, xb, yb, mk, fl, w, t, nb3, b3, a.pooled, f);
-        e3_step<3>(tbase, xb, yb, xa, ya, mk, fl, w, t, nb3, b3, a.pooled, f);
-        merge(w, t, b3, a.pooled, f);
-#else
-        const uint32_t tbase = tmem + ((32 * q) << 16) + d3_col(it & 1, p);
-        const int ncols = min(128, nrows - 128 * p);
-        uint32_t va[32], vb[32];
-        tmem_ld32(tbase, va);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (32 * c < ncols) {
-            uint32_t(&v)[32] = (c & 1) ? vb : va;
-            uint32_t(&nx)[32] = (c & 1) ? va : vb;
-            tmem_ld_wait();
-            if (c < 3 && 32 * (c + 1) < ncols) tmem_ld32(tbase + 32 * (c + 1), nx);
-            walk_chunk32(v, S.masks[4 * p + c], S.masks[8 + 4 * p + c], S.flags + 128 * p + 32 * c, w, nb3, b3,
-                         a.pooled, f);
-          }
-        }
-#endif
+        e3_part2(tmem + ((32 * q) << 16) + d3_col(it & 1, p), S.masks + 8 * p, S.flags + 128 * p, w, nb3, b3,
+                 a.pooled, f);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&S.bar[p ? B_D3E1 : B_D3E0], 0);

@@ -328,15 +328,18 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
     const uint32_t f = segbits | kRowFlagCellEnd | kRowFlagSegEnd;
     out[pidx] = make_float4(prow.x, prow.y, prow.z, __uint_as_float(f));
   }
+  // padding up to the next multiple of kSegAlign rows
+  const int pad_end = (int)seg_rows(n);
+  if (n + lane < pad_end) out[n + lane] = make_float4(0.f, 0.f, 0.f, __uint_as_float(segbits | kRowFlagPad));
 }
 
-// ---------------------------------------------------------------- exclusive scan of counts
+// ---------------------------------------------------------------- exclusive scan of segment footprints
 __global__ void __launch_bounds__(1024) scan_blocks_kernel(const int32_t* __restrict__ in, int64_t G,
                                                            int64_t* __restrict__ out, int64_t* __restrict__ sums) {
   __shared__ int64_t ws[32];
   const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int64_t v = i < G ? (int64_t)in[i] : 0, x = v;
+  int64_t v = i < G ? seg_rows(in[i]) : 0, x = v;  // segment footprint: kept rows + padding
   for (int o = 1; o < 32; o <<= 1) {
     int64_t y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;

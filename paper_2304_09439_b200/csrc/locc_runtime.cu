@@ -214,7 +214,7 @@ locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks) {
     CK(c->occ.ensure(sizeof(int32_t) * G));
     CK(c->offsets.ensure(sizeof(int64_t) * (G + 1)));
     CK(c->scan_tmp.ensure(sizeof(int64_t) * scan_tmp_elems(G)));
-    CK(c->rows.ensure(sizeof(float4) * (size_t)G * K));
+    CK(c->rows.ensure(sizeof(float4) * (size_t)G * seg_rows(K)));
     CK(c->pooled.ensure(sizeof(float) * (size_t)G * c->cfg.H));
     CK(c->out_probs.ensure(sizeof(float) * B));
     CK(c->out_labels.ensure(B));
@@ -250,7 +250,7 @@ int64_t batch_cap(const locc_ctx* c) {
   int64_t B = c->cfg.max_batch > 0 ? c->cfg.max_batch : 262144;
   // bound the compacted-row buffer (worst case every point kept) to ~12 GiB
   const int64_t rows_budget = (int64_t)12 << 30;
-  const int64_t per_pair = 2LL * c->T.K * (int64_t)sizeof(float4);
+  const int64_t per_pair = 2LL * seg_rows(c->T.K) * (int64_t)sizeof(float4);
   B = std::min<int64_t>(B, std::max<int64_t>(1, rows_budget / per_pair));
   return std::min<int64_t>(B, (int64_t)1 << 29);
 }
