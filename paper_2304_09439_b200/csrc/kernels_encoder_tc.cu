@@ -7,29 +7,29 @@
 //
 //   L1 (CUDA cores, fp32 FFMA2)  h1 = ReLU(W1 p + b1) -> bf16, written as the A operand of L2
 //                                (K-major, 128-byte swizzle) — PAPER.md:331, :421, :425
-//   L2 (tcgen05, SS)             D2[256 rows x 256 features] = h1 * W2^T; A = h1 (each CTA its 128
-//                                rows), B = W2 (each CTA 128 of the 256 output features, resident
-//                                in shared memory for the whole launch)
-//   epi L2 (TMEM -> regs)        h2 = ReLU(D2 + b2) -> bf16, written row-major (K-major) as the B
-//                                operand of L3 — each CTA keeps its own rows: no exchange
+//   L2 (tcgen05, SS)             D2 = 1 * b2 + h1 * W2^T [256 rows x 256 features] as two N = 128
+//                                halves (L2a, L2b); A = h1 (each CTA its 128 rows), B = W2 (each CTA
+//                                64 rows of each half, resident in shared memory with a bias block:
+//                                the first MMA of a half multiplies a column of ones with b2)
+//   epi L2 (TMEM -> regs)        h2 = ReLU(D2) -> bf16, written row-major (K-major) as the B operand
+//                                of L3 — each CTA keeps its own rows: no exchange
 //   L3 (tcgen05, TS)             D3[256 features x 128 rows] = W3 * h2^T, twice per tile (rows
 //                                0-127, 128-255); A = W3 resident in TMEM (each CTA 128 features),
 //                                B = h2 (each CTA 64 of the 128 rows)
 //   epi L3 (TMEM -> regs)        thread = output feature, walking the rows in order: cell-wise max
 //                                (PAPER.md:331), g = ReLU(max + b3), running sum over occupied cells,
-//                                mean at the segment end
+//                                mean at the segment end — e3_walk.cuh
 //
 // Layer 2 is computed "rows x features" and layer 3 "features x rows" so that layer 2's epilogue
 // produces layer 3's operand in place and layer 3's epilogue sees each feature's rows in one
 // thread — the segmented cell max needs no cross-lane reduction.
 //
-// Roles (17 warps): warps 0-3 = layer 1, warps 4-11 = epi L2, warps 12-15 = epi L3, warp 16 = TMEM
-// allocation + MMA issue (leader CTA).  mbarriers link the roles across both CTAs.  h1 is handed
-// over per 64-feature K block in both directions (layer 1 of tile t+1 overwrites K block kb as soon
-// as L2 of tile t has consumed it; L2 of tile t+1 starts on K block 0 while layer 1 still writes
-// the others); layer 3 starts per 32-feature K chunk as soon as epi L2 has written it; TMEM
-// regions rotate between tiles so the MMAs of one tile overlap the layer-3 epilogue of the
-// previous one.
+// Roles (17 warps): warps 0-3 = layer 1, warps 4-11 = epi L2 (4 per half), warps 12-15 = epi L3,
+// warp 16 = TMEM allocation + MMA issue (leader CTA).  mbarriers link the roles across both CTAs.
+// h1 is handed over per 64-feature K block in both directions (layer 1 of tile t+1 overwrites K
+// block kb as soon as L2 of tile t has consumed it); layer 3 accumulates per 32-feature K chunk as
+// epi L2 writes them; accumulators rotate over three TMEM regions (struct Regions) so that the
+// tensor core runs the next tile's first layer-2 half while the epilogues still drain this one.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -57,18 +57,31 @@ constexpr int kWarps = 17;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kTileRows = 256;
 constexpr uint32_t kTmemCols = 512;
-// TMEM columns: W3 (A of L3: this CTA's 128 features as bf16x2) and three 128-column regions that
-// rotate between the accumulators: even tiles D2 = [RA|RB], D3p0 = RC, D3p1 = RA; odd tiles
-// D2 = [RB|RC], D3p0 = RA, D3p1 = RC.  A region is rewritten only one full layer after its
-// previous consumer started, so the MMAs never wait for a layer-3 epilogue in steady state.
-constexpr uint32_t kColW3 = 0, kColRA = 128, kColRB = 256, kColRC = 384;
-constexpr uint32_t kIdescL2 = idesc_bf16_f32(256, 256);
-constexpr uint32_t kIdescL3 = idesc_bf16_f32(256, 128);
+// TMEM columns: W3 (A of L3: this CTA's 128 features as bf16x2) and three 128-column regions
+// R(i) = 128 + 128 i, assigned per tile as described at struct Regions.
+constexpr uint32_t kColW3 = 0, kColR0 = 128;
+constexpr uint32_t kIdescN128 = idesc_bf16_f32(256, 128);
 
-__device__ __forceinline__ uint32_t d2_col(uint32_t par) { return par ? kColRB : kColRA; }
-__device__ __forceinline__ uint32_t d3_col(uint32_t par, int p) {
-  return p == 0 ? (par ? kColRA : kColRC) : (par ? kColRC : kColRA);
-}
+__device__ __forceinline__ uint32_t region_col(uint32_t i) { return kColR0 + 128 * i; }
+
+// Layer 2 runs as two N = 128 halves (L2a: features 0-127, L2b: 128-255), layer 3 as two 128-row
+// parts; a tile's region pair (P, Q) takes L2a -> P, L2b -> Q, then L3p0 -> P and L3p1 -> Q once
+// epi L2 has drained them.  The next tile takes P' = the third region (last used by L3p1 two tiles
+// back) and Q' = P (its L3p0, the part the layer-3 epilogue walks first), so the tensor core can run
+// L2a of the next tile while the epilogue still walks this tile's parts.
+struct Regions {
+  uint32_t P = 0, Q = 1;
+  __device__ void next() {
+    const uint32_t t = 3 - P - Q;
+    Q = P;
+    P = t;
+  }
+};
+
+enum {
+  B_H1F0 = 0, B_H1E0 = 4, B_D2AF = 8, B_D2BF, B_E2K0, B_H2_EMPTY = B_E2K0 + 8, B_D3F0, B_D3F1, B_D3E0, B_D3E1, B_WLOAD,
+  kNumBars
+};
 
 struct alignas(1024) Smem {
   uint8_t w2[5 * 16384];  // B of L2: this CTA's 128 W2 rows, 4 K blocks x [128 rows x 128 B], SW128,
@@ -80,13 +93,10 @@ struct alignas(1024) Smem {
   float4 w1b[256];  // (w0, w1, w2, b1) of feature 64kb + 4fq + k at [(4kb + k) 16 + fq] (conflict-free reads)
   uint32_t flags[kTileRows];  // row flags of the whole tile (epi L3)
   alignas(16) uint32_t masks[16];  // per part p: [8p + C] cell ends, [8p + 4 + C] segment ends of step C (interleaved)
-  uint64_t bar[19];
+  uint64_t bar[kNumBars];
   uint32_t tmem_base;
 };
 
-enum {
-  B_H1F0 = 0, B_H1E0 = 4, B_D2_FULL = 8, B_E2K0 = 9, B_H2_EMPTY = 13, B_D3F0, B_D3F1, B_D3E0, B_D3E1, B_WLOAD
-};
 
 struct TcArgs {
   const float4* w1b;      // [256] (w0, w1, w2, b1)
@@ -150,18 +160,16 @@ __device__ __forceinline__ uint32_t tile_row_of_local(uint32_t rank, uint32_t i)
   return i < 64 ? 64 * rank + i : 128 + 64 * rank + (i - 64);
 }
 
-// Layer-3 MMAs of K chunk j (features {32j..32j+31} and {128+32j..}): K steps 2j, 2j+1, 8+2j, 9+2j.
+// Layer-3 MMAs of K chunk j (features 32j..32j+31, written by epi L2 as one chunk): K steps 2j, 2j+1.
 // A = W3 columns in TMEM (8 columns of bf16x2 per K step), B = h2 (+rowoff: descriptor offset of the
-// part's 64 rows), accumulate from the first K step of the part on.
+// part's 64 rows); the part's first K step overwrites the accumulator.
 __device__ __forceinline__ void l3_chunk(uint32_t d3, uint32_t w3, uint64_t dH2, int j, uint32_t rowoff) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int k = 8 * h + 2 * j + s;
-      const uint32_t koff = (k >> 2) * 1024 + (k & 3) * 2 + rowoff;
-      mma_ts_2cta(d3, w3 + 8 * k, dH2 + koff, kIdescL3, (j | h | s) != 0);
-    }
+  for (int s = 0; s < 2; ++s) {
+    const int k = 2 * j + s;
+    const uint32_t koff = (k >> 2) * 1024 + (k & 3) * 2 + rowoff;
+    mma_ts_2cta(d3, w3 + 8 * k, dH2 + koff, kIdescN128, (j | s) != 0);
+  }
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder_tc_kernel(const __grid_constant__ TcArgs a) {
@@ -177,8 +185,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       mbar_init(&S.bar[B_H1F0 + kb], 8);  // 4 layer-1 warps x 2 CTAs (the leader's copy is used)
       mbar_init(&S.bar[B_H1E0 + kb], 1);   // MMA commits
     }
-    mbar_init(&S.bar[B_D2_FULL], 1);
-    for (int j = 0; j < 4; ++j) mbar_init(&S.bar[B_E2K0 + j], 16);  // 8 epi-L2 warps x 2 CTAs
+    mbar_init(&S.bar[B_D2AF], 1);
+    mbar_init(&S.bar[B_D2BF], 1);
+    for (int j = 0; j < 8; ++j) mbar_init(&S.bar[B_E2K0 + j], 8);  // 4 epi-L2 warps (one half) x 2 CTAs
     mbar_init(&S.bar[B_H2_EMPTY], 1);
     mbar_init(&S.bar[B_D3F0], 1);
     mbar_init(&S.bar[B_D3F1], 1);
@@ -229,22 +238,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       int64_t row0;
       int nrows;
       uint32_t it = 0, n0 = 0, n1 = 0;
-      bool prev_p1 = false;
+      int p1n[3] = {-1, -1, -1};  // per tile (mod 3): index of its layer-3 part 1 among all part-1s
+      Regions R;
       // descriptors are fixed for the launch: K step k of a K-major SW128 operand is +32 B (+2 in
-      // the descriptor's address field) within a K block and +16384 B (+1024) per K block
+      // the descriptor's address field) within a K block and +16384 B (+1024) per K block; the
+      // second 64-row half of an operand image is +8192 B (+512)
       const uint64_t dA1 = smem_desc_sw128(smem_u32(S.h1), 1024), dW2 = smem_desc_sw128(smem_u32(S.w2), 1024);
       const uint64_t dH2 = smem_desc_sw128(smem_u32(S.h2), 1024), dOne = smem_desc_sw128(smem_u32(S.ones), 0);
       const uint64_t dB2 = dW2 + 4 * 1024;
       while (iter.next(row0, nrows)) {
         const uint32_t par = it & 1;
-        // D2 = [RA|RB] (even) or [RB|RC] (odd): RA resp. RC last held L3p0 of the previous tile;
-        // RB held the previous D2, drained before that tile's L3 could start.
-        if (it > 0) mbar_wait(&S.bar[B_D3E0], (n0 - 1) & 1);
+        const int np = nrows > 128 ? 2 : 1;
+        const uint32_t rp = tmem + region_col(R.P), rq = tmem + region_col(R.Q);
+        // L2a -> P: last held L3p1 of tile it-2 (or its L2b, drained); waited for at the end of the
+        // previous iteration
         if (lane == 0) trace_ev(a, rank, cid, it, 1);
-        const uint32_t dcol = tmem + d2_col(par);
         tc_fence_after();
-        // D2 = 1 * b2 (hi + mid + lo): independent of h1, issued before layer 1 has finished
-        if (elect_one()) mma_ss_2cta(dcol, dOne, dB2, kIdescL2, 0);
+        if (elect_one()) mma_ss_2cta(rp, dOne, dB2, kIdescN128, 0);  // D = 1 * b2 (hi + mid + lo)
+        __syncwarp();
 #pragma unroll 1
         for (int kb = 0; kb < 4; ++kb) {
           mbar_wait(&S.bar[B_H1F0 + kb], par);
@@ -253,43 +264,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           if (elect_one()) {
             const uint32_t koff = kb * 1024;
 #pragma unroll
-            for (int s = 0; s < 4; ++s) mma_ss_2cta(dcol, dA1 + koff + 2 * s, dW2 + koff + 2 * s, kIdescL2, 1);
-            mma_commit_2cta(&S.bar[B_H1E0 + kb], 3);
+            for (int s = 0; s < 4; ++s) mma_ss_2cta(rp, dA1 + koff + 2 * s, dW2 + koff + 2 * s, kIdescN128, 1);
           }
           __syncwarp();
         }
-        if (elect_one()) mma_commit_2cta(&S.bar[B_D2_FULL], 3);
+        if (elect_one()) mma_commit_2cta(&S.bar[B_D2AF], 3);
+        __syncwarp();
+        // L2b -> Q: last held L3p0 of the previous tile
+        if (it > 0) mbar_wait(&S.bar[B_D3E0], (n0 - 1) & 1);
         if (lane == 0) trace_ev(a, rank, cid, it, 2);
-        // L3p0 -> RC (even) / RA (odd): last held L3p1 of the previous tile, if it had one
-        if (prev_p1) mbar_wait(&S.bar[B_D3E1], (n1 - 1) & 1);
-        if (lane == 0) trace_ev(a, rank, cid, it, 3);
-        const int np = nrows > 128 ? 2 : 1;
-        {
-          const uint32_t d3 = tmem + d3_col(par, 0);
+        tc_fence_after();
+        if (elect_one()) {
+          mma_ss_2cta(rq, dOne, dB2 + 512, kIdescN128, 0);
 #pragma unroll 1
-          for (int j = 0; j < 4; ++j) {  // K chunk j = features {32j..32j+31} and {128+32j..}
-            mbar_wait(&S.bar[B_E2K0 + j], par);
-            tc_fence_after();
-            if (elect_one()) l3_chunk(d3, tmem + kColW3, dH2, j, 0);
-            __syncwarp();
+          for (int kb = 0; kb < 4; ++kb) {
+            const uint32_t koff = kb * 1024;
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+              mma_ss_2cta(rq, dA1 + koff + 2 * s, dW2 + koff + 512 + 2 * s, kIdescN128, 1);
+            mma_commit_2cta(&S.bar[B_H1E0 + kb], 3);  // h1 K block kb read by both halves
           }
-          if (elect_one()) mma_commit_2cta(&S.bar[B_D3F0], 3);
-          if (lane == 0) trace_ev(a, rank, cid, it, 4);
+          mma_commit_2cta(&S.bar[B_D2BF], 3);
         }
-        if (np == 2) {
-          const uint32_t d3 = tmem + d3_col(par, 1);
+        __syncwarp();
+        // L3p0 -> P once epi L2 has drained all of it (K chunks 0-3), then K chunks 4-7 as they come
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) mbar_wait(&S.bar[B_E2K0 + j], par);
+        if (lane == 0) trace_ev(a, rank, cid, it, 3);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll 1
+          for (int j = 0; j < 4; ++j) l3_chunk(rp, tmem + kColW3, dH2, j, 0);
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int j = 4; j < 8; ++j) {
+          mbar_wait(&S.bar[B_E2K0 + j], par);
+          tc_fence_after();
+          if (elect_one()) l3_chunk(rp, tmem + kColW3, dH2, j, 0);
+          __syncwarp();
+        }
+        if (elect_one()) mma_commit_2cta(&S.bar[B_D3F0], 3);
+        __syncwarp();
+        if (lane == 0) trace_ev(a, rank, cid, it, 4);
+        if (np == 2) {  // L3p1 -> Q, drained likewise (all K chunks were waited for)
           if (elect_one()) {
 #pragma unroll 1
-            for (int j = 0; j < 4; ++j) l3_chunk(d3, tmem + kColW3, dH2, j, 512);
+            for (int j = 0; j < 8; ++j) l3_chunk(rq, tmem + kColW3, dH2, j, 512);
+            mma_commit_2cta(&S.bar[B_D3F1], 3);
           }
           __syncwarp();
-          if (elect_one()) mma_commit_2cta(&S.bar[B_D3F1], 3);
           if (lane == 0) trace_ev(a, rank, cid, it, 5);
         }
         if (elect_one()) mma_commit_2cta(&S.bar[B_H2_EMPTY], 3);
+        __syncwarp();
+        p1n[it % 3] = np == 2 ? (int)n1 : -1;
+        // The next tile's L2a overwrites the region of L3p1 of tile it-1.  Waited for here, right
+        // after issuing this tile's L3p1: the epilogue cannot have completed that one yet, so the
+        // barrier is never two phases ahead of the parity we wait for.
+        if (it >= 1 && p1n[(it + 2) % 3] >= 0) mbar_wait(&S.bar[B_D3E1], p1n[(it + 2) % 3] & 1);
+        R.next();
         ++n0;
         if (np == 2) ++n1;
-        prev_p1 = np == 2;
         ++it;
       }
     }
@@ -380,17 +416,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     int64_t row0;
     int nrows;
     uint32_t it = 0;
+    Regions R;
     while (iter.next(row0, nrows)) {
-      if (warp == kWarpE2) {  // one warp polls; the group waits on a named barrier
-        mbar_wait(&S.bar[B_D2_FULL], it & 1);
+      if ((warp & 3) == 0) {  // one warp per half polls; the half waits on a named barrier
+        mbar_wait(&S.bar[half ? B_D2BF : B_D2AF], it & 1);
         if (lt == 0) trace_ev(a, rank, cid, it, 8);
         mbar_wait(&S.bar[B_H2_EMPTY], (it & 1) ^ 1);
         if (lt == 0) trace_ev(a, rank, cid, it, 9);
       }
       __syncwarp();
-      asm volatile("bar.sync 3, 256;" ::: "memory");
+      if (half)
+        asm volatile("bar.sync 4, 128;" ::: "memory");
+      else
+        asm volatile("bar.sync 3, 128;" ::: "memory");
       tc_fence_after();
-      const uint32_t tbase = tmem + ((32 * q) << 16) + d2_col(it & 1) + 128 * half;
+      const uint32_t tbase = tmem + ((32 * q) << 16) + region_col(half ? R.Q : R.P);
       uint32_t va[32], vb[32];
       tmem_ld32(tbase, va);
 #pragma unroll
@@ -411,10 +451,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&S.bar[B_E2K0 + c], 0);
+        if (lane == 0) mbar_arrive_cluster(&S.bar[B_E2K0 + 4 * half + c], 0);
       }
       if (lt == 0) trace_ev(a, rank, cid, it, 10);
       ++it;
+      R.next();
     }
   } else {
     // ============ epi L3: thread = output feature; walk rows: cell max, occupied-cell mean ============
@@ -428,6 +469,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     int nrows;
     bool first;
     uint32_t it = 0, c0 = 0, c1 = 0;
+    Regions R;
     while (iter.next(row0, nrows, first)) {
       if (first) w.m = nb3;  // drop padding rows after the previous chunk's last segment end
       asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's flags no longer read
@@ -452,7 +494,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         group_wait<1, 128>(&S.bar[p ? B_D3F1 : B_D3F0], (p ? c1 : c0) & 1, warp == kWarpE3);
         if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 12 + 2 * p);
         tc_fence_after();
-        e3_part2(tmem + ((32 * q) << 16) + d3_col(it & 1, p), S.masks + 8 * p, S.flags + 128 * p, w, nb3, b3,
+        e3_part2(tmem + ((32 * q) << 16) + region_col(p ? R.Q : R.P), S.masks + 8 * p, S.flags + 128 * p, w, nb3, b3,
                  a.pooled, f);
         tc_fence_before();
         __syncwarp();
@@ -461,6 +503,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         if (p) ++c1; else ++c0;
       }
       ++it;
+      R.next();
     }
   }
 

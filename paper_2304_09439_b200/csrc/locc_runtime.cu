@@ -648,8 +648,9 @@ float bf16_to_float(uint16_t h) {
 }
 }  // namespace
 
-// W2 as the B operand of layer 2: per CTA rank r its output features [128r, 128r+128), K-major,
-// 4 K blocks of [128 rows x 128 B] with the 128-byte swizzle (16-byte chunk j of row i stored at
+// W2 as the B operand of layer 2, computed as two N = 128 halves: per CTA rank r the 64 output
+// features [64r, 64r+64) of half 0 (image rows 0-63) and [128+64r, +64) of half 1 (rows 64-127),
+// K-major, 4 K blocks of [128 rows x 128 B] with the 128-byte swizzle (16-byte chunk j of row i stored at
 // chunk j ^ (i & 7)) — the exact shared-memory image, so one bulk copy places it.  A fifth block
 // holds b2 as the K = 0..2 entries (b2 = hi + mid + lo, each bf16, exact), which the kernel
 // multiplies with a column of ones so that the first layer-2 MMA initialises D2 with the bias.
@@ -670,15 +671,17 @@ locc_status locc_upload_tc_weights(locc_ctx* c, const float* flat) {
   std::vector<uint8_t> img(2 * kTcW2Bytes + (size_t)H * 128 * 4, 0);
   for (int r = 0; r < 2; ++r)
     for (int i = 0; i < 128; ++i) {
+      // image row i: layer-2 half i / 64 (features 0-127 or 128-255), of which CTA r supplies 64 rows
+      const int n = 128 * (i >> 6) + 64 * r + (i & 63);
       for (int kb = 0; kb < 4; ++kb)
         for (int j = 0; j < 8; ++j) {
           uint8_t* dst = img.data() + r * kTcW2Bytes + kb * 16384 + locc::tc::sw128_off(i, j);
           for (int e = 0; e < 8; ++e) {
-            const uint16_t v = bf16_rne(w2[(size_t)(128 * r + i) * H + 64 * kb + 8 * j + e]);
+            const uint16_t v = bf16_rne(w2[(size_t)n * H + 64 * kb + 8 * j + e]);
             std::memcpy(dst + 2 * e, &v, 2);
           }
         }
-      const float b = b2[128 * r + i];
+      const float b = b2[n];
       const uint16_t hi = bf16_rne(b);
       const float r1 = b - bf16_to_float(hi);
       const uint16_t mid = bf16_rne(r1);
