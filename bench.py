@@ -103,7 +103,8 @@ def cpu_baseline(pts, pairs, poses, flat, target_s=15.0):
     this host's cores on a bounded prefix of the same workload."""
     import oracle
     cores = os.cpu_count() or 1
-    n = max(cores, 16)
+    n = max(4 * cores, 64)
+    oracle.query(flat, pts, pairs[:cores], poses[:cores], bf16_emul=True, n_threads=cores)  # warm-up
     t = time.perf_counter()
     oracle.query(flat, pts, pairs[:n], poses[:n], bf16_emul=True, n_threads=cores)
     dt = time.perf_counter() - t
