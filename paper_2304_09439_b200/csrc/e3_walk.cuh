@@ -118,6 +118,10 @@ __device__ __forceinline__ void merge2(Walk& x, const Tail& t, float b3, float* 
   }
 }
 
+__device__ __forceinline__ uint32_t sel4(const uint4& v, int c) {
+  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+
 // A 128-row part: four straight-line steps with a register double buffer of TMEM columns.
 // mk[0..3] = interleaved cell ends of steps 0..3, mk[4..7] = interleaved segment ends.
 __device__ __forceinline__ void e3_part2(uint32_t tbase, const uint32_t* mk, const uint32_t* fl, Walk& w, float nb3,
@@ -132,12 +136,11 @@ __device__ __forceinline__ void e3_part2(uint32_t tbase, const uint32_t* mk, con
   t.se = false;
   const uint4 ce = *reinterpret_cast<const uint4*>(mk);
   const uint4 se = *reinterpret_cast<const uint4*>(mk + 4);
-  const uint32_t cm[4] = {ce.x, ce.y, ce.z, ce.w}, sm[4] = {se.x, se.y, se.z, se.w};
   uint32_t xa[16], ya[16], xb[16], yb[16];
   tmem_ld16(tbase, xa);
   tmem_ld16(tbase + 64, ya);
-  if (cm[0] & kOdd) {  // Y's head ends in step 0 (~97%): straight-line steps
-    const uint32_t yc = cm[0] & kOdd;
+  if (ce.x & kOdd) {  // Y's head ends in step 0 (~97%): straight-line steps
+    const uint32_t yc = ce.x & kOdd;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       uint32_t(&vx)[16] = (c & 1) ? xb : xa;
@@ -150,10 +153,10 @@ __device__ __forceinline__ void e3_part2(uint32_t tbase, const uint32_t* mk, con
         tmem_ld16(tbase + 64 + 16 * (c + 1), ny);
       }
       if (c == 0)
-        step2<true>(vx, vy, cm[c], yc & (0u - yc), w, t, nb3);
+        step2<true>(vx, vy, sel4(ce, c), yc & (0u - yc), w, t, nb3);
       else
-        step2<false>(vx, vy, cm[c], 0u, w, t, nb3);
-      if (sm[c]) seg_close(sm[c], fl + 16 * c, fl + 64 + 16 * c, w, t, nb3, b3, pooled, f);
+        step2<false>(vx, vy, sel4(ce, c), 0u, w, t, nb3);
+      if (sel4(se, c)) seg_close(sel4(se, c), fl + 16 * c, fl + 64 + 16 * c, w, t, nb3, b3, pooled, f);
     }
   } else {
 #pragma unroll 1
@@ -163,12 +166,13 @@ __device__ __forceinline__ void e3_part2(uint32_t tbase, const uint32_t* mk, con
         tmem_ld16(tbase + 64 + 16 * c, ya);
       }
       tmem_ld_wait();
-      const uint32_t yc = cm[c] & kOdd;
+      const uint32_t cec = sel4(ce, c), sec = sel4(se, c);
+      const uint32_t yc = cec & kOdd;
       if (!t.ce && yc != 0)
-        step2<true>(xa, ya, cm[c], yc & (0u - yc), w, t, nb3);
+        step2<true>(xa, ya, cec, yc & (0u - yc), w, t, nb3);
       else
-        step2<false>(xa, ya, cm[c], 0u, w, t, nb3);
-      if (sm[c]) seg_close(sm[c], fl + 16 * c, fl + 64 + 16 * c, w, t, nb3, b3, pooled, f);
+        step2<false>(xa, ya, cec, 0u, w, t, nb3);
+      if (sec) seg_close(sec, fl + 16 * c, fl + 64 + 16 * c, w, t, nb3, b3, pooled, f);
     }
   }
   merge2(w, t, b3, pooled, f);

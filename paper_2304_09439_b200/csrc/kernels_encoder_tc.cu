@@ -49,8 +49,15 @@ using namespace e3;
 // group starts at a multiple of 4.  The warp scheduler favours higher warp ids, so the sequential
 // layer-3 walk and the MMA issuer get the high ids and layer 1 (which has the most slack) the low.
 // 17 warps = at most 5 per scheduler, which leaves 96 registers per thread.
-constexpr int kWarpL1 = 0;    // warps 0..3: layer 1 (thread = 4 features x 16 rows per K block)
-constexpr int kWarpE2 = 4;    // warps 4..11: epi L2 (thread = row, half the features each)
+#ifndef LOCC_L1_WARPS
+#define LOCC_L1_WARPS 8
+#endif
+constexpr int kL1Warps = LOCC_L1_WARPS;  // 8: layer 1 on warps 0-7, epi L2 on 8-11 (both halves)
+                                         // 4: layer 1 on warps 0-3, epi L2 on 4-11 (one half each)
+constexpr int kL1Threads = 32 * kL1Warps;
+constexpr int kE2Warps = 12 - kL1Warps;
+constexpr int kWarpL1 = 0;            // layer 1: thread = 4 features x (8 or 16) rows per K block
+constexpr int kWarpE2 = kL1Warps;     // epi L2: thread = row
 constexpr int kWarpE3 = 12;   // warps 12..15: epi L3 (thread = output feature)
 constexpr int kWarpMMA = 16;  // warp 16: TMEM allocation + MMA issue (leader CTA)
 constexpr int kWarps = 17;
@@ -79,7 +86,7 @@ struct Regions {
 };
 
 enum {
-  B_H1F0 = 0, B_H1E0 = 4, B_D2AF = 8, B_D2BF, B_E2K0, B_H2_EMPTY = B_E2K0 + 8, B_D3F0, B_D3F1, B_D3E0, B_D3E1, B_WLOAD,
+  B_H1F0 = 0, B_H1E0 = 4, B_D2AF = 8, B_D2BF, B_E2K0, B_H2_EMPTY = B_E2K0 + 8, B_D3F0, B_D3F1, B_D3E0, B_D3E1, B_WLOAD, B_PROBE,
   kNumBars
 };
 
@@ -95,6 +102,7 @@ struct alignas(1024) Smem {
   alignas(16) uint32_t masks[16];  // per part p: [8p + C] cell ends, [8p + 4 + C] segment ends of step C (interleaved)
   uint64_t bar[kNumBars];
   uint32_t tmem_base;
+  uint32_t issue_seq;  // LOCC_TC_TRACE: issuer trace points (written remotely into CTA 1)
 };
 
 
@@ -113,28 +121,41 @@ struct TcArgs {
 };
 
 constexpr int kTraceTiles = 64;
+// Issuer trace points are also signalled to CTA 1's idle MMA warp, which timestamps them in the same
+// clock domain as the tensor-core completion probes.
+__device__ __forceinline__ void trace_issue(const TcArgs& a, uint32_t* seq, int64_t cid) {
+  if (a.trace && cid == 0) {
+    const uint32_t v = *seq + 1;  // the issuer's local copy counts its trace points
+    *seq = v;
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, 1;\n\t"
+        "st.shared::cluster.u32 [ra], %1;\n\t}" ::"r"(smem_u32(seq)), "r"(v)
+        : "memory");
+  }
+}
+
 __device__ __forceinline__ void trace_ev(const TcArgs& a, uint32_t rank, int64_t cid, uint32_t tile, int ev) {
   if (a.trace && cid == 0 && tile < kTraceTiles) a.trace[(rank * kTraceTiles + tile) * 16 + ev] = clock64();
 }
 
-// Iterates the (chunk, tile) sequence of this cluster; every role walks the same sequence.
+// Iterates the (chunk, tile) sequence of this cluster; every role walks the same sequence.  Only
+// the cursor lives in registers (the launch constants stay in the parameter bank).
 struct TileIter {
-  const int64_t* off;
-  int64_t G, n_chunks, chunk, step;
-  int spc;
+  const TcArgs& a;
+  int chunk;
   int64_t r1 = 0, t0 = 0;
-  __device__ TileIter(const TcArgs& a, int64_t first, int64_t stride)
-      : off(a.offsets), G(a.G), n_chunks(a.n_chunks), chunk(first - stride), step(stride), spc(a.seg_per_chunk) {}
+  __device__ TileIter(const TcArgs& args, int first, int stride) : a(args), chunk(first - stride) {}
   // first = true for the first tile of a chunk (a chunk starts on a segment boundary)
   __device__ bool next(int64_t& row0, int& nrows, bool& first) {
     first = false;
     while (t0 >= r1) {
-      chunk += step;
-      if (chunk >= n_chunks) return false;
-      const int64_t s0 = chunk * spc;
-      const int64_t s1 = min(s0 + spc, G);
-      t0 = off[s0];
-      r1 = off[s1];
+      chunk += (int)nclusters_x();
+      if (chunk >= a.n_chunks) return false;
+      const int64_t s0 = (int64_t)chunk * a.seg_per_chunk;
+      const int64_t s1 = min(s0 + a.seg_per_chunk, a.G);
+      t0 = a.offsets[s0];
+      r1 = a.offsets[s1];
       first = true;
     }
     row0 = t0;
@@ -182,18 +203,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
   // ---------------------------------------------------------------- setup
   if (threadIdx.x == 0) {
     for (int kb = 0; kb < 4; ++kb) {
-      mbar_init(&S.bar[B_H1F0 + kb], 8);  // 4 layer-1 warps x 2 CTAs (the leader's copy is used)
+      mbar_init(&S.bar[B_H1F0 + kb], 2 * kL1Warps);  // layer-1 warps x 2 CTAs (the leader's copy is used)
       mbar_init(&S.bar[B_H1E0 + kb], 1);   // MMA commits
     }
     mbar_init(&S.bar[B_D2AF], 1);
     mbar_init(&S.bar[B_D2BF], 1);
-    for (int j = 0; j < 8; ++j) mbar_init(&S.bar[B_E2K0 + j], 8);  // 4 epi-L2 warps (one half) x 2 CTAs
+    for (int j = 0; j < 8; ++j) mbar_init(&S.bar[B_E2K0 + j], 8);  // the 4 epi-L2 warps of a half x 2 CTAs
     mbar_init(&S.bar[B_H2_EMPTY], 1);
     mbar_init(&S.bar[B_D3F0], 1);
     mbar_init(&S.bar[B_D3F1], 1);
     mbar_init(&S.bar[B_D3E0], 8);  // 4 epi-L3 warps x 2 CTAs
     mbar_init(&S.bar[B_D3E1], 8);
     mbar_init(&S.bar[B_WLOAD], 1);
+    mbar_init(&S.bar[B_PROBE], 1);  // LOCC_TC_TRACE: tensor-core completion probes
+    S.issue_seq = 0;
     fence_mbar_init();
     mbar_arrive_expect_tx(&S.bar[B_WLOAD], 5 * 16384);
     for (int kb = 0; kb < 5; ++kb)
@@ -231,14 +254,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
   tc_fence_after();
 
   // ---------------------------------------------------------------- roles
-  if (warp == kWarpMMA) {
+  if (warp == kWarpMMA && rank == 1) {
+    if (a.trace && cid == 0 && lane == 0) {  // debug: tensor-core completion times
+      TileIter iter(a, (int)cid, (int)ncl);
+      int64_t row0;
+      int nrows;
+      uint32_t ph = 0;
+      for (uint32_t it = 0; iter.next(row0, nrows); ++it) {
+        const int ng = nrows > 128 ? 5 : 4;
+        for (int g = 0; g < ng; ++g) {
+          mbar_wait_spin(&S.bar[B_PROBE], ph & 1);
+          ++ph;
+          if (it < kTraceTiles) a.trace[(2 * kTraceTiles + it) * 16 + g] = clock64();
+        }
+      }
+    } else if (a.trace && cid == 0 && lane == 1) {  // issuer trace points, same clock
+      TileIter iter(a, (int)cid, (int)ncl);
+      int64_t row0;
+      int nrows;
+      uint32_t seen = 0;
+      for (uint32_t it = 0; iter.next(row0, nrows); ++it) {
+        const uint32_t ng = nrows > 128 ? 6 : 5;
+        const uint32_t target = seen + ng;
+        while (seen < target) {
+          const uint32_t v = *reinterpret_cast<volatile uint32_t*>(&S.issue_seq);
+          const long long now = clock64();
+          for (; seen < v && seen < target; ++seen)
+            if (it < kTraceTiles) a.trace[(2 * kTraceTiles + it) * 16 + 8 + (seen + ng - target)] = now;
+        }
+      }
+    }
+  } else if (warp == kWarpMMA) {
     // ============ MMA issuer (leader CTA, whole warp; one elected lane issues) ============
     if (rank == 0) {
-      TileIter iter(a, cid, ncl);
+      TileIter iter(a, (int)cid, (int)ncl);
       int64_t row0;
       int nrows;
       uint32_t it = 0, n0 = 0, n1 = 0;
-      int p1n[3] = {-1, -1, -1};  // per tile (mod 3): index of its layer-3 part 1 among all part-1s
+      int prev_p1 = -1;  // index of the previous tile's layer-3 part 1 among all part-1s (-1: none)
       Regions R;
       // descriptors are fixed for the launch: K step k of a K-major SW128 operand is +32 B (+2 in
       // the descriptor's address field) within a K block and +16384 B (+1024) per K block; the
@@ -252,14 +305,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         const uint32_t rp = tmem + region_col(R.P), rq = tmem + region_col(R.Q);
         // L2a -> P: last held L3p1 of tile it-2 (or its L2b, drained); waited for at the end of the
         // previous iteration
-        if (lane == 0) trace_ev(a, rank, cid, it, 1);
+        if (lane == 0) { trace_ev(a, rank, cid, it, 1); trace_issue(a, &S.issue_seq, cid); }
         tc_fence_after();
         if (elect_one()) mma_ss_2cta(rp, dOne, dB2, kIdescN128, 0);  // D = 1 * b2 (hi + mid + lo)
         __syncwarp();
 #pragma unroll 1
         for (int kb = 0; kb < 4; ++kb) {
-          mbar_wait(&S.bar[B_H1F0 + kb], par);
-          if (kb == 0 && lane == 0) trace_ev(a, rank, cid, it, 0);
+          mbar_wait_spin(&S.bar[B_H1F0 + kb], par);
+          if (kb == 0 && lane == 0) { trace_ev(a, rank, cid, it, 0); trace_issue(a, &S.issue_seq, cid); }
           tc_fence_after();
           if (elect_one()) {
             const uint32_t koff = kb * 1024;
@@ -268,15 +321,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           }
           __syncwarp();
         }
-        if (elect_one()) mma_commit_2cta(&S.bar[B_D2AF], 3);
+        if (elect_one()) {
+          mma_commit_2cta(&S.bar[B_D2AF], 3);
+          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE], 3);
+        }
         __syncwarp();
         // L2b -> Q: last held L3p0 of the previous tile
-        if (it > 0) mbar_wait(&S.bar[B_D3E0], (n0 - 1) & 1);
-        if (lane == 0) trace_ev(a, rank, cid, it, 2);
+        if (it > 0) mbar_wait_spin(&S.bar[B_D3E0], (n0 - 1) & 1);
+        if (lane == 0) { trace_ev(a, rank, cid, it, 2); trace_issue(a, &S.issue_seq, cid); }
         tc_fence_after();
         if (elect_one()) {
           mma_ss_2cta(rq, dOne, dB2 + 512, kIdescN128, 0);
-#pragma unroll 1
+#pragma unroll
           for (int kb = 0; kb < 4; ++kb) {
             const uint32_t koff = kb * 1024;
 #pragma unroll
@@ -285,67 +341,75 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
             mma_commit_2cta(&S.bar[B_H1E0 + kb], 3);  // h1 K block kb read by both halves
           }
           mma_commit_2cta(&S.bar[B_D2BF], 3);
+          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE], 3);
         }
         __syncwarp();
         // L3p0 -> P once epi L2 has drained all of it (K chunks 0-3), then K chunks 4-7 as they come
 #pragma unroll 1
-        for (int j = 0; j < 4; ++j) mbar_wait(&S.bar[B_E2K0 + j], par);
-        if (lane == 0) trace_ev(a, rank, cid, it, 3);
+        for (int j = 0; j < 4; ++j) mbar_wait_spin(&S.bar[B_E2K0 + j], par);
+        if (lane == 0) { trace_ev(a, rank, cid, it, 3); trace_issue(a, &S.issue_seq, cid); }
         tc_fence_after();
         if (elect_one()) {
-#pragma unroll 1
+#pragma unroll
           for (int j = 0; j < 4; ++j) l3_chunk(rp, tmem + kColW3, dH2, j, 0);
+          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE], 3);
         }
         __syncwarp();
 #pragma unroll 1
         for (int j = 4; j < 8; ++j) {
-          mbar_wait(&S.bar[B_E2K0 + j], par);
+          mbar_wait_spin(&S.bar[B_E2K0 + j], par);
           tc_fence_after();
           if (elect_one()) l3_chunk(rp, tmem + kColW3, dH2, j, 0);
           __syncwarp();
         }
-        if (elect_one()) mma_commit_2cta(&S.bar[B_D3F0], 3);
+        if (elect_one()) {
+          mma_commit_2cta(&S.bar[B_D3F0], 3);
+          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE], 3);
+        }
         __syncwarp();
-        if (lane == 0) trace_ev(a, rank, cid, it, 4);
+        if (lane == 0) { trace_ev(a, rank, cid, it, 4); trace_issue(a, &S.issue_seq, cid); }
         if (np == 2) {  // L3p1 -> Q, drained likewise (all K chunks were waited for)
           if (elect_one()) {
-#pragma unroll 1
+#pragma unroll
             for (int j = 0; j < 8; ++j) l3_chunk(rq, tmem + kColW3, dH2, j, 512);
             mma_commit_2cta(&S.bar[B_D3F1], 3);
+            if (a.trace) mma_commit_2cta(&S.bar[B_PROBE], 3);
           }
           __syncwarp();
-          if (lane == 0) trace_ev(a, rank, cid, it, 5);
+          if (lane == 0) { trace_ev(a, rank, cid, it, 5); trace_issue(a, &S.issue_seq, cid); }
         }
         if (elect_one()) mma_commit_2cta(&S.bar[B_H2_EMPTY], 3);
         __syncwarp();
-        p1n[it % 3] = np == 2 ? (int)n1 : -1;
         // The next tile's L2a overwrites the region of L3p1 of tile it-1.  Waited for here, right
         // after issuing this tile's L3p1: the epilogue cannot have completed that one yet, so the
         // barrier is never two phases ahead of the parity we wait for.
-        if (it >= 1 && p1n[(it + 2) % 3] >= 0) mbar_wait(&S.bar[B_D3E1], p1n[(it + 2) % 3] & 1);
+        if (prev_p1 >= 0) mbar_wait_spin(&S.bar[B_D3E1], prev_p1 & 1);
+        prev_p1 = np == 2 ? (int)n1 : -1;
         R.next();
         ++n0;
         if (np == 2) ++n1;
         ++it;
       }
     }
-  } else if (warp < kWarpE2) {
+  } else if (warp < kWarpL1 + kL1Warps) {
     // ============ layer 1: K block kb -> thread = features 64kb + 4fq..+3, rows 8rq + {0..7, 64..71} ====
-    const uint32_t lt = threadIdx.x - 32 * kWarpL1;  // 0..127
-    const uint32_t fq = lt & 15, rq = lt >> 4;
+    const uint32_t lt = threadIdx.x - 32 * kWarpL1;  // 0..kL1Threads-1
+    const uint32_t fq = lt & 15, rq = lt >> 4;  // 8 warps: rows 8rq..8rq+7; 4 warps: also 64 + 8rq..
     const uint32_t h1 = smem_u32(S.h1) + rq * 1024 + ((4 * fq) & 7) * 2;
     const uint32_t chunk = (4 * fq) >> 3;  // 16-byte chunk of the 128-byte row (same in every K block)
-    TileIter iter(a, cid, ncl), ahead(a, cid, ncl);
+    TileIter iter(a, (int)cid, (int)ncl), ahead(a, (int)cid, (int)ncl);
     int64_t row0, nrow0;
     int nrows, nnrows;
     auto stage = [&](float4 p, uint32_t buf) {
-      S.px[buf][lt] = p.x;
-      S.py[buf][lt] = p.y;
-      S.pz[buf][lt] = p.z;
+      if (lt < 128) {
+        S.px[buf][lt] = p.x;
+        S.py[buf][lt] = p.y;
+        S.pz[buf][lt] = p.z;
+      }
     };
     auto fetch = [&](bool ok, int64_t r0, int nr) {
       float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (ok) {
+      if (ok && lt < 128) {
         const uint32_t trow = tile_row_of_local(rank, lt);
         if ((int)trow < nr) p = a.rows[r0 + trow];
       }
@@ -356,7 +420,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     uint32_t it = 0;
     while (iter.next(row0, nrows)) {
       const uint32_t buf = it & 1;
-      asm volatile("bar.sync 2, 128;" ::: "memory");  // rows of tile it staged; buffer buf^1 free
+      asm volatile("bar.sync 2, %0;" ::"n"(kL1Threads) : "memory");  // rows of tile it staged; buffer buf^1 free
       have_next = ahead.next(nrow0, nnrows);
       const float4 pf = fetch(have_next, nrow0, nnrows);  // next tile's row, in flight during this tile
 #pragma unroll 1
@@ -370,10 +434,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           wz[k] = f2(w.z, w.z);
           wb[k] = f2(w.w, w.w);
         }
-        group_wait<2, 128>(&S.bar[B_H1E0 + kb], (it & 1) ^ 1, warp == kWarpL1);
+        group_wait<2, kL1Threads>(&S.bar[B_H1E0 + kb], (it & 1) ^ 1, warp == kWarpL1);
         if (lt == 0 && kb == 0) trace_ev(a, rank, cid, it, 6);
 #pragma unroll
-        for (uint32_t g = 0; g < 2; ++g) {  // local rows 64g + 8rq .. +7
+        for (uint32_t g = 0; g < 128 / (8 * (kL1Threads / 16)); ++g) {  // local rows 64g + 8rq .. +7
           const uint32_t lr = 64 * g + 8 * rq;
           const float4 xa = *reinterpret_cast<const float4*>(&S.px[buf][lr]);
           const float4 xb = *reinterpret_cast<const float4*>(&S.px[buf][lr + 4]);
@@ -406,52 +470,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       ++it;
     }
   } else if (warp < kWarpE3) {
-    // ============ epi L2: thread = row, features [128 half, +128) ============
-    const uint32_t q = warp & 3;                 // TMEM lane quarter (rows 32q..32q+31)
-    const uint32_t half = (warp - kWarpE2) >> 2;
+    // ============ epi L2: thread = row; 8 warps: one half each, 4 warps: both halves in turn ============
+    const uint32_t q = warp & 3;  // TMEM lane quarter (rows 32q..32q+31)
     const uint32_t row = 32 * q + lane;
     const uint32_t lt = threadIdx.x - 32 * kWarpE2;
     const uint32_t h2 = smem_u32(S.h2);
-    TileIter iter(a, cid, ncl);
+    TileIter iter(a, (int)cid, (int)ncl);
     int64_t row0;
     int nrows;
     uint32_t it = 0;
     Regions R;
     while (iter.next(row0, nrows)) {
-      if ((warp & 3) == 0) {  // one warp per half polls; the half waits on a named barrier
-        mbar_wait(&S.bar[half ? B_D2BF : B_D2AF], it & 1);
-        if (lt == 0) trace_ev(a, rank, cid, it, 8);
-        mbar_wait(&S.bar[B_H2_EMPTY], (it & 1) ^ 1);
-        if (lt == 0) trace_ev(a, rank, cid, it, 9);
-      }
-      __syncwarp();
-      if (half)
-        asm volatile("bar.sync 4, 128;" ::: "memory");
-      else
-        asm volatile("bar.sync 3, 128;" ::: "memory");
-      tc_fence_after();
-      const uint32_t tbase = tmem + ((32 * q) << 16) + region_col(half ? R.Q : R.P);
-      uint32_t va[32], vb[32];
-      tmem_ld32(tbase, va);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t(&v)[32] = (c & 1) ? vb : va;
-        uint32_t(&nx)[32] = (c & 1) ? va : vb;
-        tmem_ld_wait();
-        if (c < 3) tmem_ld32(tbase + 32 * (c + 1), nx);
-        const int cc = 4 * half + c;  // feature chunk (32 features)
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {  // D2 already holds the bias (see the MMA issuer)
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            w[e] = pack_relu_bf16x2(__uint_as_float(v[8 * g + 2 * e]), __uint_as_float(v[8 * g + 2 * e + 1]));
-          st_shared_v4(h2 + (cc >> 1) * 16384 + sw128_off(row, (cc & 1) * 4 + g), w[0], w[1], w[2], w[3]);
+#pragma unroll 1
+      for (uint32_t hh = 0; hh < (kE2Warps == 4 ? 2u : 1u); ++hh) {
+        const uint32_t half = kE2Warps == 4 ? hh : (warp - kWarpE2) >> 2;
+        if ((warp & 3) == 0) {  // one warp per group polls; the group waits on a named barrier
+          mbar_wait(&S.bar[half ? B_D2BF : B_D2AF], it & 1);
+          if (lt == 0 && half == 0) trace_ev(a, rank, cid, it, 8);
+          if (hh == 0) mbar_wait(&S.bar[B_H2_EMPTY], (it & 1) ^ 1);
+          if (lt == 0 && half == 0) trace_ev(a, rank, cid, it, 9);
         }
-        fence_proxy_async_smem();
-        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&S.bar[B_E2K0 + 4 * half + c], 0);
+        if (half && kE2Warps == 8)
+          asm volatile("bar.sync 4, 128;" ::: "memory");
+        else
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+        tc_fence_after();
+        const uint32_t tbase = tmem + ((32 * q) << 16) + region_col(half ? R.Q : R.P);
+        uint32_t va[32], vb[32];
+        tmem_ld32(tbase, va);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t(&v)[32] = (c & 1) ? vb : va;
+          uint32_t(&nx)[32] = (c & 1) ? va : vb;
+          tmem_ld_wait();
+          if (c < 3) tmem_ld32(tbase + 32 * (c + 1), nx);
+          const int cc = 4 * half + c;  // feature chunk (32 features)
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {  // D2 already holds the bias (see the MMA issuer)
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              w[e] = pack_relu_bf16x2(__uint_as_float(v[8 * g + 2 * e]), __uint_as_float(v[8 * g + 2 * e + 1]));
+            st_shared_v4(h2 + (cc >> 1) * 16384 + sw128_off(row, (cc & 1) * 4 + g), w[0], w[1], w[2], w[3]);
+          }
+          fence_proxy_async_smem();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(&S.bar[B_E2K0 + 4 * half + c], 0);
+        }
       }
       if (lt == 0) trace_ev(a, rank, cid, it, 10);
       ++it;
@@ -464,7 +531,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     const uint32_t f = 128 * rank + 32 * q + lane;
     const float b3 = a.b3[f], nb3 = -b3;
     Walk w{nb3, 0.f, 0};
-    TileIter iter(a, cid, ncl);
+    TileIter iter(a, (int)cid, (int)ncl);
     int64_t row0;
     int nrows;
     bool first;

@@ -33,6 +33,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (NW + 1), 1) k(
   fence_proxy_async_smem();
   if (threadIdx.x == 0) {
     mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
     S.stop = 0;
     fence_mbar_init();
   }
@@ -64,14 +65,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (NW + 1), 1) k(
     if (acc == 0x1234567u) out[127] = acc;
   } else if (rank == 0 && lane == 0) {
     const uint32_t sa = smem_u32(S.a), sb = smem_u32(S.b);
-    const uint32_t id = SHAPE == 0 ? idesc_bf16_f32(256, 256) : idesc_bf16_f32(256, 128);
+    const uint32_t id = SHAPE == 0 ? idesc_bf16_f32(256, 256) : idesc_bf16_f32(256, 128);  // SHAPE 1, 3-5: N128
     // warm up, then time
     long long t0 = 0;
     for (int r = 0; r < reps + 4; ++r) {
       if (r == 4) t0 = clock64();
       for (int kk = 0; kk < 16; ++kk) {
         const uint32_t koff = (kk >> 2) * 16384 + (kk & 3) * 32;
-        if (SHAPE < 2)
+        if (SHAPE == 4) {  // SS N128 with a commit (to a spare barrier) after every 4 MMAs
+          mma_ss_2cta(tm + 128, smem_desc_sw128(sa + koff, 1024), smem_desc_sw128(sb + koff, 1024), id, kk > 0);
+          if ((kk & 3) == 3) mma_commit_2cta(&S.bar[1], 3);
+        } else if (SHAPE == 5) {  // SS N128 with a commit after every MMA
+          mma_ss_2cta(tm + 128, smem_desc_sw128(sa + koff, 1024), smem_desc_sw128(sb + koff, 1024), id, kk > 0);
+          mma_commit_2cta(&S.bar[1], 3);
+        } else if (SHAPE == 3)
+          mma_ss_2cta(tm + 128, smem_desc_sw128(sa, 0), smem_desc_sw128(sb + koff, 1024), id, kk > 0);
+        else if (SHAPE < 2)
           mma_ss_2cta(tm + 128, smem_desc_sw128(sa + koff, 1024), smem_desc_sw128(sb + koff, 1024), id, kk > 0);
         else
           mma_ts_2cta(tm + 256, tm + 8 * kk, smem_desc_sw128(sb + koff, 1024), id, kk > 0);
@@ -112,6 +121,9 @@ void run(const char* name) {
 }
 
 int main() {
+  run<3, 0, 1>("SS N128 A-desc SBO=0 (bias MMA), quiet");
+  run<4, 0, 1>("SS N128 + commit every 4 MMAs");
+  run<5, 0, 1>("SS N128 + commit every MMA");
   run<0, 0, 1>("SS N256, quiet");
   run<1, 0, 1>("SS N128, quiet");
   run<2, 0, 1>("TS N128, quiet");
