@@ -124,7 +124,13 @@ def run_reference(a):
     pts, pairs, poses, flat = make_inputs(a, 0)
     import oracle
     cores = os.cpu_count() or 1
-    n = max(2 * cores, 32)
+    # size the per-step sample to ~8 s of host work (a warm probe first), so K + W steps take minutes
+    oracle.query(flat, pts, pairs[:cores], poses[:cores], bf16_emul=True, n_threads=cores)
+    n0 = max(4 * cores, 64)
+    t = time.perf_counter()
+    oracle.query(flat, pts, pairs[:n0], poses[:n0], bf16_emul=True, n_threads=cores)
+    dt = time.perf_counter() - t
+    n = int(max(n0, min(len(pairs) // (a.steps + 2), n0 * 8.0 / max(dt, 1e-3))))
     for i in range(a.warmup):
         oracle.query(flat, pts, pairs[:n], poses[:n], bf16_emul=True, n_threads=cores)
     times = []
