@@ -72,22 +72,24 @@ constexpr uint32_t kIdescN128 = idesc_bf16_f32(256, 128);
 __device__ __forceinline__ uint32_t region_col(uint32_t i) { return kColR0 + 128 * i; }
 
 // Layer 2 runs as two N = 128 halves (L2a: features 0-127, L2b: 128-255), layer 3 as two 128-row
-// parts; a tile's region pair (P, Q) takes L2a -> P, L2b -> Q, then L3p0 -> P and L3p1 -> Q once
-// epi L2 has drained them.  The next tile takes P' = the third region (last used by L3p1 two tiles
-// back) and Q' = P (its L3p0, the part the layer-3 epilogue walks first), so the tensor core can run
-// L2a of the next tile while the epilogue still walks this tile's parts.
+// parts.  Regions: a tile's pair (P, Q) takes L2a -> P and L2b -> Q; L3p0 then reuses P once epi L2
+// has drained it, and L3p1 always goes to the third region R(2), so it can start on the first K half
+// (written by epi L2 from L2a) while L2b is still being drained.  The next tile swaps P and Q: its
+// L2a reuses this tile's L2b region (drained before this tile's L3 finished) and its L2b the region
+// of this tile's L3p0 (freed by the layer-3 epilogue).
+constexpr uint32_t kRegionP1 = 2;
 struct Regions {
   uint32_t P = 0, Q = 1;
   __device__ void next() {
-    const uint32_t t = 3 - P - Q;
-    Q = P;
-    P = t;
+    const uint32_t t = P;
+    P = Q;
+    Q = t;
   }
 };
 
 enum {
-  B_H1F0 = 0, B_H1E0 = 4, B_D2AF = 8, B_D2BF, B_E2K0, B_H2_EMPTY = B_E2K0 + 8, B_D3F0, B_D3F1, B_D3E0, B_D3E1, B_WLOAD, B_PROBE,
-  kNumBars
+  B_H1F0 = 0, B_H1E0 = 4, B_D2AF = 8, B_D2BF, B_E2K0, B_H2_EMPTY = B_E2K0 + 8, B_D3F0, B_D3F1, B_D3E0, B_D3E1, B_WLOAD, B_PROBE, B_PROBE_END = B_PROBE + 5,
+  kNumBars = B_PROBE_END
 };
 
 struct alignas(1024) Smem {
@@ -215,7 +217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     mbar_init(&S.bar[B_D3E0], 8);  // 4 epi-L3 warps x 2 CTAs
     mbar_init(&S.bar[B_D3E1], 8);
     mbar_init(&S.bar[B_WLOAD], 1);
-    mbar_init(&S.bar[B_PROBE], 1);  // LOCC_TC_TRACE: tensor-core completion probes
+    for (int g = 0; g < 5; ++g) mbar_init(&S.bar[B_PROBE + g], 1);  // LOCC_TC_TRACE: completion probes
     S.issue_seq = 0;
     fence_mbar_init();
     mbar_arrive_expect_tx(&S.bar[B_WLOAD], 5 * 16384);
@@ -255,32 +257,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
 
   // ---------------------------------------------------------------- roles
   if (warp == kWarpMMA && rank == 1) {
-    if (a.trace && cid == 0 && lane == 0) {  // debug: tensor-core completion times
-      TileIter iter(a, (int)cid, (int)ncl);
-      int64_t row0;
-      int nrows;
-      uint32_t ph = 0;
-      for (uint32_t it = 0; iter.next(row0, nrows); ++it) {
-        const int ng = nrows > 128 ? 5 : 4;
-        for (int g = 0; g < ng; ++g) {
-          mbar_wait_spin(&S.bar[B_PROBE], ph & 1);
-          ++ph;
-          if (it < kTraceTiles) a.trace[(2 * kTraceTiles + it) * 16 + g] = clock64();
+    if (a.trace && cid == 0 && lane == 0) {
+      // debug: one thread timestamps tensor-core completions (probe barriers) and issuer trace points
+      // (sequence numbers stored remotely by the issuer) in this SM's clock
+      TileIter pit(a, (int)cid, (int)ncl), iit(a, (int)cid, (int)ncl);
+      int64_t r0;
+      int pn = 0, in_ = 0;
+      bool pmore = pit.next(r0, pn), imore = iit.next(r0, in_);
+      uint32_t ptile = 0, pg = 0, np1 = 0, itile = 0, ig = 0, seen = 0;
+      while (pmore || imore) {
+        if (pmore) {
+          const uint32_t ng = pn > 128 ? 5 : 4;  // L2a, L2b, L3p0 first K half, L3p0, L3p1
+          if (mbar_try_wait(&S.bar[B_PROBE + pg], (pg == 4 ? np1 : ptile) & 1)) {
+            if (ptile < kTraceTiles) a.trace[(2 * kTraceTiles + ptile) * 16 + pg] = clock64();
+            if (++pg == ng) {
+              if (ng == 5) ++np1;
+              pg = 0;
+              ++ptile;
+              pmore = pit.next(r0, pn);
+            }
+          }
         }
-      }
-    } else if (a.trace && cid == 0 && lane == 1) {  // issuer trace points, same clock
-      TileIter iter(a, (int)cid, (int)ncl);
-      int64_t row0;
-      int nrows;
-      uint32_t seen = 0;
-      for (uint32_t it = 0; iter.next(row0, nrows); ++it) {
-        const uint32_t ng = nrows > 128 ? 6 : 5;
-        const uint32_t target = seen + ng;
-        while (seen < target) {
+        if (imore) {
+          const uint32_t ng = in_ > 128 ? 6 : 5;
           const uint32_t v = *reinterpret_cast<volatile uint32_t*>(&S.issue_seq);
           const long long now = clock64();
-          for (; seen < v && seen < target; ++seen)
-            if (it < kTraceTiles) a.trace[(2 * kTraceTiles + it) * 16 + 8 + (seen + ng - target)] = now;
+          while (imore && seen < v) {
+            if (itile < kTraceTiles) a.trace[(2 * kTraceTiles + itile) * 16 + 8 + ig] = now;
+            ++seen;
+            if (++ig == ng) {
+              ig = 0;
+              ++itile;
+              imore = iit.next(r0, in_);
+            }
+          }
         }
       }
     }
@@ -291,7 +301,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       int64_t row0;
       int nrows;
       uint32_t it = 0, n0 = 0, n1 = 0;
-      int prev_p1 = -1;  // index of the previous tile's layer-3 part 1 among all part-1s (-1: none)
+      int last_p1 = -1;  // index (among all part-1s) of the last L3p1 issued: R(2)'s previous user
       Regions R;
       // descriptors are fixed for the launch: K step k of a K-major SW128 operand is +32 B (+2 in
       // the descriptor's address field) within a K block and +16384 B (+1024) per K block; the
@@ -299,12 +309,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       const uint64_t dA1 = smem_desc_sw128(smem_u32(S.h1), 1024), dW2 = smem_desc_sw128(smem_u32(S.w2), 1024);
       const uint64_t dH2 = smem_desc_sw128(smem_u32(S.h2), 1024), dOne = smem_desc_sw128(smem_u32(S.ones), 0);
       const uint64_t dB2 = dW2 + 4 * 1024;
+      const uint32_t r3 = tmem + region_col(kRegionP1);
       while (iter.next(row0, nrows)) {
         const uint32_t par = it & 1;
-        const int np = nrows > 128 ? 2 : 1;
+        const bool p1 = nrows > 128;
         const uint32_t rp = tmem + region_col(R.P), rq = tmem + region_col(R.Q);
-        // L2a -> P: last held L3p1 of tile it-2 (or its L2b, drained); waited for at the end of the
-        // previous iteration
+        // L2a -> P: the previous tile's L2b region, drained before that tile's L3 was issued
         if (lane == 0) { trace_ev(a, rank, cid, it, 1); trace_issue(a, &S.issue_seq, cid); }
         tc_fence_after();
         if (elect_one()) mma_ss_2cta(rp, dOne, dB2, kIdescN128, 0);  // D = 1 * b2 (hi + mid + lo)
@@ -323,10 +333,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         }
         if (elect_one()) {
           mma_commit_2cta(&S.bar[B_D2AF], 3);
-          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE], 3);
+          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE + 0], 3);
         }
         __syncwarp();
-        // L2b -> Q: last held L3p0 of the previous tile
+        // L2b -> Q: the previous tile's L3p0 region
         if (it > 0) mbar_wait_spin(&S.bar[B_D3E0], (n0 - 1) & 1);
         if (lane == 0) { trace_ev(a, rank, cid, it, 2); trace_issue(a, &S.issue_seq, cid); }
         tc_fence_after();
@@ -341,10 +351,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
             mma_commit_2cta(&S.bar[B_H1E0 + kb], 3);  // h1 K block kb read by both halves
           }
           mma_commit_2cta(&S.bar[B_D2BF], 3);
-          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE], 3);
+          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE + 1], 3);
         }
         __syncwarp();
-        // L3p0 -> P once epi L2 has drained all of it (K chunks 0-3), then K chunks 4-7 as they come
+        // Layer 3, first K half (features 0-127, from L2a): L3p0 -> P once epi L2 has drained all of
+        // it, L3p1 -> R(2) once the layer-3 epilogue has walked its previous part there
 #pragma unroll 1
         for (int j = 0; j < 4; ++j) mbar_wait_spin(&S.bar[B_E2K0 + j], par);
         if (lane == 0) { trace_ev(a, rank, cid, it, 3); trace_issue(a, &S.issue_seq, cid); }
@@ -352,42 +363,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         if (elect_one()) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) l3_chunk(rp, tmem + kColW3, dH2, j, 0);
-          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE], 3);
+          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE + 2], 3);
         }
         __syncwarp();
+        if (p1) {
+          if (last_p1 >= 0) mbar_wait_spin(&S.bar[B_D3E1], last_p1 & 1);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) l3_chunk(r3, tmem + kColW3, dH2, j, 512);
+          }
+          __syncwarp();
+        }
+        // second K half (features 128-255) chunk by chunk as epi L2 writes it
 #pragma unroll 1
         for (int j = 4; j < 8; ++j) {
           mbar_wait_spin(&S.bar[B_E2K0 + j], par);
           tc_fence_after();
-          if (elect_one()) l3_chunk(rp, tmem + kColW3, dH2, j, 0);
-          __syncwarp();
-        }
-        if (elect_one()) {
-          mma_commit_2cta(&S.bar[B_D3F0], 3);
-          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE], 3);
-        }
-        __syncwarp();
-        if (lane == 0) { trace_ev(a, rank, cid, it, 4); trace_issue(a, &S.issue_seq, cid); }
-        if (np == 2) {  // L3p1 -> Q, drained likewise (all K chunks were waited for)
           if (elect_one()) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) l3_chunk(rq, tmem + kColW3, dH2, j, 512);
-            mma_commit_2cta(&S.bar[B_D3F1], 3);
-            if (a.trace) mma_commit_2cta(&S.bar[B_PROBE], 3);
+            l3_chunk(rp, tmem + kColW3, dH2, j, 0);
+            if (j == 7) {
+              mma_commit_2cta(&S.bar[B_D3F0], 3);
+              if (a.trace) mma_commit_2cta(&S.bar[B_PROBE + 3], 3);
+            }
+            if (p1) l3_chunk(r3, tmem + kColW3, dH2, j, 512);
           }
           __syncwarp();
-          if (lane == 0) { trace_ev(a, rank, cid, it, 5); trace_issue(a, &S.issue_seq, cid); }
         }
-        if (elect_one()) mma_commit_2cta(&S.bar[B_H2_EMPTY], 3);
+        if (lane == 0) { trace_ev(a, rank, cid, it, 4); trace_issue(a, &S.issue_seq, cid); }
+        if (elect_one()) {
+          if (p1) {
+            mma_commit_2cta(&S.bar[B_D3F1], 3);
+            if (a.trace) mma_commit_2cta(&S.bar[B_PROBE + 4], 3);
+          }
+          mma_commit_2cta(&S.bar[B_H2_EMPTY], 3);
+        }
         __syncwarp();
-        // The next tile's L2a overwrites the region of L3p1 of tile it-1.  Waited for here, right
-        // after issuing this tile's L3p1: the epilogue cannot have completed that one yet, so the
-        // barrier is never two phases ahead of the parity we wait for.
-        if (prev_p1 >= 0) mbar_wait_spin(&S.bar[B_D3E1], prev_p1 & 1);
-        prev_p1 = np == 2 ? (int)n1 : -1;
+        if (p1) {
+          if (lane == 0) { trace_ev(a, rank, cid, it, 5); trace_issue(a, &S.issue_seq, cid); }
+          last_p1 = (int)n1;
+          ++n1;
+        }
         R.next();
         ++n0;
-        if (np == 2) ++n1;
         ++it;
       }
     }
@@ -561,7 +579,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         group_wait<1, 128>(&S.bar[p ? B_D3F1 : B_D3F0], (p ? c1 : c0) & 1, warp == kWarpE3);
         if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 12 + 2 * p);
         tc_fence_after();
-        e3_part2(tmem + ((32 * q) << 16) + region_col(p ? R.Q : R.P), S.masks + 8 * p, S.flags + 128 * p, w, nb3, b3,
+        e3_part2(tmem + ((32 * q) << 16) + region_col(p ? kRegionP1 : R.P), S.masks + 8 * p, S.flags + 128 * p, w, nb3, b3,
                  a.pooled, f);
         tc_fence_before();
         __syncwarp();
