@@ -6,9 +6,11 @@
 // across object pairs"); 3x128 ReLU; linear; sigmoid; label = p > 0.5.  Both crops empty ->
 // short-circuit: p = 0, label 0, logit -inf.
 //
-// A block of 128 threads evaluates PB = 16 pairs (32 sides).  Activations live in shared memory
-// transposed, [feature][row] with rows contiguous, so a thread computing output unit o for all rows
-// reads 4 rows per LDS.128 and updates 2 rows per packed FFMA2; weights are coalesced rows of W^T.
+// head_tile_kernel: one 256-thread block per 64 pairs (128 sides), all layers fused.  Activations
+// stay in shared memory, transposed ([feature][row]); every layer is a small fp32 GEMM with a
+// register tile of RT rows x 8 outputs per thread (64 or 32 independent FFMAs per k) and the
+// layer's weights streamed through shared memory in 32-row chunks (register double buffer), so a
+// weight is fetched once per 128 (or 64) rows.  head_kernel is the generic fallback (any H, F).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -25,6 +27,219 @@ using tc::f2_hi;
 using tc::f2_lo;
 using tc::ffma2;
 
+// ------------------------------------------------------------------ fused tile kernel (H = 256, F = 64)
+constexpr int kTP = 64;           // pairs per block
+constexpr int kTS = 2 * kTP;      // sides per block
+constexpr int kLD = kTS + 4;      // row stride (floats) of the transposed activation buffers
+constexpr int kKC = 32;           // weight rows per staged chunk
+constexpr int kHeadThreads = 256;
+
+struct HeadSmem {
+  float u[128][kLD];   // activations, ping (u and v together: the projection's 256-feature input)
+  float v[128][kLD];   // activations, pong
+  float z[72][kLD];    // z = [e ; q ; t] per side
+  float w[2][kKC][128];  // weight chunks
+  int nside[kTS];
+};
+
+// out[n][r] = act(sum_k W[k][n] in[k][r] + b[n]), r < ROWS, n < N; W = transposed weights [K][N]
+// (global, row-major).  in / out: [feature][kLD] shared buffers.  RT rows x 8 outputs per thread.
+template <int ROWS, int N, bool kRelu>
+__device__ __forceinline__ void dense(const float* __restrict__ W, const float* __restrict__ bias, int K,
+                                      const float (*in)[kLD], float (*out)[kLD], float (*ws)[kKC][128]) {
+  constexpr int CG = N / 8;                  // column groups
+  constexpr int RG = kHeadThreads / CG;      // row groups
+  constexpr int RT = ROWS / RG;              // rows per thread
+  static_assert(RT % 4 == 0 && RT * RG == ROWS, "tile");
+  const int tid = threadIdx.x;
+  const int c0 = (tid % CG) * 8, r0 = (tid / CG) * RT;
+  unsigned long long acc[RT][4];  // (column 2j, column 2j+1) per row, packed for FFMA2
+#pragma unroll
+  for (int r = 0; r < RT; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0ull;
+  // weight chunk kc: rows [32kc, 32kc+32) x N floats, N / 4 float4 per row
+  constexpr int F4 = kKC * N / 4;            // float4 per chunk
+  constexpr int PER = (F4 + kHeadThreads - 1) / kHeadThreads;
+  const int nchunks = (K + kKC - 1) / kKC;
+  float4 pre[PER];
+  auto fetch = [&](int kc) {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = tid + i * kHeadThreads;
+      const int row = e / (N / 4), col4 = e % (N / 4);
+      const int k = kc * kKC + row;
+      pre[i] = (e < F4 && k < K) ? __ldg(reinterpret_cast<const float4*>(W + (int64_t)k * N) + col4)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int e = tid + i * kHeadThreads;
+      if (e < F4) *reinterpret_cast<float4*>(&ws[buf][e / (N / 4)][4 * (e % (N / 4))]) = pre[i];
+    }
+  };
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  for (int kc = 0; kc < nchunks; ++kc) {
+    const int buf = kc & 1;
+    if (kc + 1 < nchunks) fetch(kc + 1);  // in flight while this chunk is consumed
+    const int kn = min(kKC, K - kc * kKC);
+    // operands of step kk + 1 are loaded while step kk is multiplied (shared-memory latency hidden)
+    float4 xa[RT / 4], wa, wb;
+    auto load = [&](int kk) {
+      const int k = kc * kKC + kk;
+#pragma unroll
+      for (int r = 0; r < RT; r += 4) xa[r / 4] = *reinterpret_cast<const float4*>(&in[k][r0 + r]);
+      wa = *reinterpret_cast<const float4*>(&ws[buf][kk][c0]);
+      wb = *reinterpret_cast<const float4*>(&ws[buf][kk][c0 + 4]);
+    };
+    load(0);
+#pragma unroll 2
+    for (int kk = 0; kk < kn; ++kk) {
+      float a[RT];
+#pragma unroll
+      for (int r = 0; r < RT; r += 4) {
+        a[r] = xa[r / 4].x;
+        a[r + 1] = xa[r / 4].y;
+        a[r + 2] = xa[r / 4].z;
+        a[r + 3] = xa[r / 4].w;
+      }
+      const unsigned long long w2[4] = {f2(wa.x, wa.y), f2(wa.z, wa.w), f2(wb.x, wb.y), f2(wb.z, wb.w)};
+      if (kk + 1 < kn) load(kk + 1);
+#pragma unroll
+      for (int r = 0; r < RT; ++r) {
+        const unsigned long long a2 = f2(a[r], a[r]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = ffma2(a2, w2[c], acc[r][c]);
+      }
+    }
+    if (kc + 1 < nchunks) stash(buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float b = bias[c0 + c];
+#pragma unroll
+    for (int r = 0; r < RT; r += 4) {
+      float v4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v4[q] = ((c & 1) ? f2_hi(acc[r + q][c >> 1]) : f2_lo(acc[r + q][c >> 1])) + b;
+      float4 y = make_float4(v4[0], v4[1], v4[2], v4[3]);
+      if (kRelu) y = make_float4(fmaxf(y.x, 0.f), fmaxf(y.y, 0.f), fmaxf(y.z, 0.f), fmaxf(y.w, 0.f));
+      *reinterpret_cast<float4*>(&out[c0 + c][r0 + r]) = y;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kHeadThreads, 1) head_tile_kernel(DevParams P, Batch b, float* __restrict__ probs,
+                                                                    uint8_t* __restrict__ labels,
+                                                                    float* __restrict__ logits, float* __restrict__ emb) {
+  extern __shared__ float4 smem4[];
+  HeadSmem& S = *reinterpret_cast<HeadSmem*>(smem4);
+  const int tid = threadIdx.x;
+  const int64_t i0 = (int64_t)blockIdx.x * kTP;
+  const int npairs = (int)min((int64_t)kTP, b.B - i0);
+  if (tid < kTS) S.nside[tid] = tid < 2 * npairs ? b.counts[2 * i0 + tid] : 0;
+  // z rows F..F+6: canonical unit quaternion and translation per side (fp64 normalisation, Q12)
+  if (tid < kTS) {
+    const int s = tid;
+    float zq[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (s < 2 * npairs) {
+      const float* pose = b.poses + (2 * i0 + s) * 7;
+      double q[4] = {1.0, 0.0, 0.0, 0.0};
+      quat_unit(pose, q);
+      double sg = 1.0;
+      for (int c = 0; c < 4; ++c)
+        if (q[c] != 0.0) {
+          sg = q[c] > 0.0 ? 1.0 : -1.0;
+          break;
+        }
+      for (int c = 0; c < 4; ++c) zq[c] = __double2float_rn(sg * q[c]);
+      for (int c = 0; c < 3; ++c) zq[4 + c] = pose[4 + c];
+    }
+    for (int c = 0; c < 7; ++c) S.z[64 + c][s] = zq[c];
+    S.z[71][s] = 0.f;
+  }
+  // S7 projection e = W_F m + b_F: the pooled rows (256 features) are staged transposed into u..v
+  // (contiguous: one [256][kLD] buffer); empty and padding sides read as 0
+  {
+    float (*m)[kLD] = reinterpret_cast<float (*)[kLD]>(&S.u[0][0]);  // u and v are contiguous
+    __syncthreads();  // nside
+#pragma unroll 1
+    for (int e0 = 0; e0 < kTS * 64; e0 += 8 * kHeadThreads) {  // 8 loads in flight per thread
+      float4 x[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = e0 + i * kHeadThreads + tid, s = e / 64, j4 = e % 64;
+        x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (S.nside[s] > 0) x[i] = __ldg(reinterpret_cast<const float4*>(b.pooled + (2 * i0 + s) * (int64_t)256) + j4);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = e0 + i * kHeadThreads + tid, s = e / 64, j4 = e % 64;
+        m[4 * j4][s] = x[i].x;
+        m[4 * j4 + 1][s] = x[i].y;
+        m[4 * j4 + 2][s] = x[i].z;
+        m[4 * j4 + 3][s] = x[i].w;
+      }
+    }
+    __syncthreads();
+    dense<kTS, 64, false>(P.wfT, P.bf, 256, m, S.z, S.w);
+  }
+  // e = 0 for empty sides; debug copy
+  for (int e = tid; e < 64 * kTS; e += kHeadThreads) {
+    const int j = e / kTS, s = e % kTS;
+    if (S.nside[s] == 0) S.z[j][s] = 0.f;
+  }
+  __syncthreads();
+  if (emb)
+    for (int e = tid; e < 2 * npairs * 64; e += kHeadThreads) {
+      const int s = e / 64, j = e % 64;
+      emb[(2 * i0 + s) * (int64_t)64 + j] = S.z[j][s];
+    }
+  // S8 object MLP (shared by both sides)
+  dense<kTS, 128, true>(P.o1T, P.ob1, 71, S.z, S.u, S.w);
+  dense<kTS, 128, true>(P.o2T, P.ob2, 128, S.u, S.v, S.w);
+  dense<kTS, 128, true>(P.o3T, P.ob3, 128, S.v, S.u, S.w);
+  // S9 max across the pair -> v[o][p]
+  for (int e = tid; e < 128 * kTP; e += kHeadThreads) {
+    const int o = e / kTP, p = e % kTP;
+    S.v[o][p] = fmaxf(S.u[o][2 * p], S.u[o][2 * p + 1]);
+  }
+  __syncthreads();
+  dense<kTP, 128, true>(P.p1T, P.pb1, 128, S.v, S.u, S.w);
+  dense<kTP, 128, true>(P.p2T, P.pb2, 128, S.u, S.v, S.w);
+  dense<kTP, 128, true>(P.p3T, P.pb3, 128, S.v, S.u, S.w);
+  // output unit: 4 threads per pair, 32 features each, then combined
+  {
+    const int p = tid >> 2, part = tid & 3;
+    float acc = 0.f;
+    for (int j = 32 * part; j < 32 * part + 32; ++j) acc = fmaf(P.wout[j], S.u[j][p], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (part == 0 && p < npairs) {
+      const int64_t i = i0 + p;
+      float lg, pr;
+      if (S.nside[2 * p] + S.nside[2 * p + 1] == 0) {
+        lg = -INFINITY;
+        pr = 0.f;
+      } else {
+        lg = acc + P.bout[0];
+        pr = 1.f / (1.f + expf(-lg));
+        atomicAdd(&b.stats->evaluated_pairs, 1ull);
+      }
+      probs[i] = pr;
+      if (labels) labels[i] = pr > 0.5f ? 1 : 0;
+      if (logits) logits[i] = lg;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ generic fallback (any H, F)
 constexpr int PB = 16;      // pairs per block
 constexpr int NS = 2 * PB;  // sides per block
 constexpr int LD = 36;      // row stride (floats) of the transposed activation buffers
@@ -79,16 +294,13 @@ __global__ void __launch_bounds__(128) head_kernel(DevParams P, Batch b, float* 
   const int npairs = (int)min((int64_t)PB, b.B - i0);
   if (tid < NS) nside[tid] = tid < 2 * npairs ? b.counts[2 * i0 + tid] : 0;
   __syncthreads();
-  // pooled features, transposed (empty or padding sides -> 0)
   for (int idx = tid; idx < NS * H; idx += blockDim.x) {
     const int s = idx / H, j = idx - s * H;
     X[j * LD + s] = nside[s] > 0 ? b.pooled[(2 * i0 + s) * (int64_t)H + j] : 0.f;
   }
   __syncthreads();
-  // S7 projection e = W_F m + b_F -> Z[0:F]: thread (o, row half)
   dense_t<NS / 2>(P.wfT, P.bf, H, F, X, (tid >> 6) * (NS / 2), Z, false, tid & 63, 64);
   __syncthreads();
-  // z = [e (0 if empty); canonical q; t]
   if (tid < NS) {
     const int s = tid;
     if (nside[s] == 0)
@@ -115,14 +327,12 @@ __global__ void __launch_bounds__(128) head_kernel(DevParams P, Batch b, float* 
       const int s = idx / F, j = idx - s * F;
       emb[(2 * i0 + s) * (int64_t)F + j] = Z[j * LD + s];
     }
-  // S8 object MLP (shared by both sides)
   dense_t<NS>(P.o1T, P.ob1, F + 7, kPredW, Z, 0, Y, true, tid, 128);
   __syncthreads();
   dense_t<NS>(P.o2T, P.ob2, kPredW, kPredW, Y, 0, X, true, tid, 128);
   __syncthreads();
   dense_t<NS>(P.o3T, P.ob3, kPredW, kPredW, X, 0, Y, true, tid, 128);
   __syncthreads();
-  // S9 max across the pair -> X[o][p]
   for (int idx = tid; idx < PB * kPredW; idx += blockDim.x) {
     const int o = idx / PB, p = idx - o * PB;
     X[o * LD + p] = fmaxf(Y[o * LD + 2 * p], Y[o * LD + 2 * p + 1]);
@@ -134,7 +344,6 @@ __global__ void __launch_bounds__(128) head_kernel(DevParams P, Batch b, float* 
   __syncthreads();
   dense_t<PB>(P.p3T, P.pb3, kPredW, kPredW, X, 0, Y, true, tid, 128);
   __syncthreads();
-  // output unit + sigmoid
   if (tid < npairs) {
     const int p = tid;
     float acc = 0.f;
@@ -160,6 +369,14 @@ __global__ void __launch_bounds__(128) head_kernel(DevParams P, Batch b, float* 
 cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_t* labels, float* logits, float* emb,
                         cudaStream_t st) {
   if (b.B == 0) return cudaSuccess;
+  if (P.H == 256 && P.F == 64) {
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(head_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeadSmem));
+    if (attr != cudaSuccess) return attr;
+    head_tile_kernel<<<(unsigned)((b.B + kTP - 1) / kTP), kHeadThreads, sizeof(HeadSmem), st>>>(P, b, probs, labels,
+                                                                                                logits, emb);
+    return cudaGetLastError();
+  }
   const size_t sm = sizeof(float) * (size_t)(256 + 128 + P.F + 7) * LD;
   static const cudaError_t attr = cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        (int)(sizeof(float) * (256 + 128 + 256 + 7) * LD));
