@@ -242,10 +242,20 @@ __global__ void __launch_bounds__(256) crop_count_kernel(ShapeTable T, Batch b, 
   const uint16_t* perm = T.perm + (int64_t)own * T.K;
   uint32_t* mask = b.masks ? b.masks + g * words : nullptr;
   int n = 0, C = 0, carry = -1;
-  for (int base = 0; base < T.K; base += 32) {
+  // four 32-point steps per round: their loads are in flight together (the table lives in L2)
+  for (int base0 = 0; base0 < T.K; base0 += 128) {
+    float4 pp[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = base0 + 32 * j + lane;
+      pp[j] = k < T.K ? pts[k] : make_float4(0.f, 0.f, 0.f, __int_as_float(-2));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+    const int base = base0 + 32 * j;
+    if (base >= T.K) break;
     const int k = base + lane;
-    float4 p = make_float4(0.f, 0.f, 0.f, __int_as_float(-2));
-    if (k < T.K) p = pts[k];
+    const float4 p = pp[j];
     const bool keep = k < T.K && keep_point(X, p.x, p.y, p.z, lo, hi);
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     if (m == 0) continue;
@@ -260,6 +270,7 @@ __global__ void __launch_bounds__(256) crop_count_kernel(ShapeTable T, Batch b, 
     if (mask && keep) {
       const int ck = perm[k];
       atomicOr(mask + (ck >> 5), 1u << (ck & 31));
+    }
     }
   }
   if (lane == 0) {
@@ -294,10 +305,19 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
   bool pending = false;   // a held-back row (warp-uniform)
   float4 prow;            // held-back row payload (valid in every lane)
   int pcell = 0, pidx = 0;
-  for (int base = 0; base < T.K; base += 32) {
+  for (int base0 = 0; base0 < T.K; base0 += 128) {
+    float4 pp[4];  // four steps' loads in flight together
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = base0 + 32 * j + lane;
+      pp[j] = k < T.K ? pts[k] : make_float4(0.f, 0.f, 0.f, __int_as_float(-2));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+    const int base = base0 + 32 * j;
+    if (base >= T.K) break;
     const int k = base + lane;
-    float4 p = make_float4(0.f, 0.f, 0.f, __int_as_float(-2));
-    if (k < T.K) p = pts[k];
+    const float4 p = pp[j];
     const bool keep = k < T.K && keep_point(X, p.x, p.y, p.z, lo, hi);
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     if (m == 0) continue;
@@ -323,6 +343,7 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
     pidx = written + __popc(m) - 1;
     pending = true;
     written += __popc(m);
+    }
   }
   if (pending && lane == 0) {
     const uint32_t f = segbits | kRowFlagCellEnd | kRowFlagSegEnd;
