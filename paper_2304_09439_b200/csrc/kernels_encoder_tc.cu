@@ -56,9 +56,14 @@ constexpr int kL1Warps = LOCC_L1_WARPS;  // 8: layer 1 on warps 0-7, epi L2 on 8
                                          // 4: layer 1 on warps 0-3, epi L2 on 4-11 (one half each)
 constexpr int kL1Threads = 32 * kL1Warps;
 constexpr int kE2Warps = 12 - kL1Warps;
-constexpr int kWarpL1 = 0;            // layer 1: thread = 4 features x (8 or 16) rows per K block
-constexpr int kWarpE2 = kL1Warps;     // epi L2: thread = row
-constexpr int kWarpE3 = 12;   // warps 12..15: epi L3 (thread = output feature)
+#ifndef LOCC_WARP_ORDER
+#define LOCC_WARP_ORDER 0
+#endif
+// Role order by warp id (the scheduler favours higher ids).  0: L1 < E2 < E3 < MMA; 1: E2 < L1 < E3;
+// 2: E2 < E3 < L1.  TMEM-reading groups (E2, E3) start at multiples of 4.
+constexpr int kWarpL1 = LOCC_WARP_ORDER == 0 ? 0 : LOCC_WARP_ORDER == 1 ? kE2Warps : kE2Warps + 4;
+constexpr int kWarpE2 = LOCC_WARP_ORDER == 0 ? kL1Warps : 0;
+constexpr int kWarpE3 = LOCC_WARP_ORDER == 2 ? kE2Warps : 12;
 constexpr int kWarpMMA = 16;  // warp 16: TMEM allocation + MMA issue (leader CTA)
 constexpr int kWarps = 17;
 constexpr int kThreads = 32 * kWarps;
@@ -409,7 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         ++it;
       }
     }
-  } else if (warp < kWarpL1 + kL1Warps) {
+  } else if (warp >= kWarpL1 && warp < kWarpL1 + kL1Warps) {
     // ============ layer 1: K block kb -> thread = features 64kb + 4fq..+3, rows 8rq + {0..7, 64..71} ====
     const uint32_t lt = threadIdx.x - 32 * kWarpL1;  // 0..kL1Threads-1
     const uint32_t fq = lt & 15, rq = lt >> 4;  // 8 warps: rows 8rq..8rq+7; 4 warps: also 64 + 8rq..
@@ -487,7 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       stage(pf, buf ^ 1);
       ++it;
     }
-  } else if (warp < kWarpE3) {
+  } else if (warp >= kWarpE2 && warp < kWarpE2 + kE2Warps) {
     // ============ epi L2: thread = row; 8 warps: one half each, 4 warps: both halves in turn ============
     const uint32_t q = warp & 3;  // TMEM lane quarter (rows 32q..32q+31)
     const uint32_t row = 32 * q + lane;
@@ -504,7 +509,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         const uint32_t half = kE2Warps == 4 ? hh : (warp - kWarpE2) >> 2;
         if ((warp & 3) == 0) {  // one warp per group polls; the group waits on a named barrier
           mbar_wait(&S.bar[half ? B_D2BF : B_D2AF], it & 1);
-          if (lt == 0 && half == 0) trace_ev(a, rank, cid, it, 8);
+          if (lt == 0) trace_ev(a, rank, cid, it, half ? 11 : 8);  // D2AF / D2BF seen
           if (hh == 0) mbar_wait(&S.bar[B_H2_EMPTY], (it & 1) ^ 1);
           if (lt == 0 && half == 0) trace_ev(a, rank, cid, it, 9);
         }
@@ -572,7 +577,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         }
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 11);
       const int np = nrows > 128 ? 2 : 1;
 #pragma unroll 1
       for (int p = 0; p < np; ++p) {
