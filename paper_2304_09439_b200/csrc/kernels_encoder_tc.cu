@@ -177,9 +177,23 @@ struct TileIter {
 };
 
 // One warp of a role group polls the mbarrier; the others wait on a named barrier (no issue slots).
-template <int ID, int NTHREADS>
+#ifndef LOCC_SPIN_E2
+#define LOCC_SPIN_E2 0
+#endif
+#ifndef LOCC_SPIN_E3
+#define LOCC_SPIN_E3 0
+#endif
+#ifndef LOCC_SPIN_L1
+#define LOCC_SPIN_L1 0
+#endif
+template <int ID, int NTHREADS, bool kSpin = false>
 __device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool poller) {
-  if (poller) mbar_wait(bar, parity);
+  if (poller) {
+    if (kSpin)
+      mbar_wait_spin(bar, parity);
+    else
+      mbar_wait(bar, parity);
+  }
   __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(NTHREADS) : "memory");
 }
@@ -457,7 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           wz[k] = f2(w.z, w.z);
           wb[k] = f2(w.w, w.w);
         }
-        group_wait<2, kL1Threads>(&S.bar[B_H1E0 + kb], (it & 1) ^ 1, warp == kWarpL1);
+        group_wait<2, kL1Threads, LOCC_SPIN_L1>(&S.bar[B_H1E0 + kb], (it & 1) ^ 1, warp == kWarpL1);
         if (lt == 0 && kb == 0) trace_ev(a, rank, cid, it, 6);
 #pragma unroll
         for (uint32_t g = 0; g < 128 / (8 * (kL1Threads / 16)); ++g) {  // local rows 64g + 8rq .. +7
@@ -508,7 +522,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       for (uint32_t hh = 0; hh < (kE2Warps == 4 ? 2u : 1u); ++hh) {
         const uint32_t half = kE2Warps == 4 ? hh : (warp - kWarpE2) >> 2;
         if ((warp & 3) == 0) {  // one warp per group polls; the group waits on a named barrier
-          mbar_wait(&S.bar[half ? B_D2BF : B_D2AF], it & 1);
+          if (LOCC_SPIN_E2) mbar_wait_spin(&S.bar[half ? B_D2BF : B_D2AF], it & 1); else mbar_wait(&S.bar[half ? B_D2BF : B_D2AF], it & 1);
           if (lt == 0) trace_ev(a, rank, cid, it, half ? 11 : 8);  // D2AF / D2BF seen
           if (hh == 0) mbar_wait(&S.bar[B_H2_EMPTY], (it & 1) ^ 1);
           if (lt == 0 && half == 0) trace_ev(a, rank, cid, it, 9);
@@ -580,7 +594,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       const int np = nrows > 128 ? 2 : 1;
 #pragma unroll 1
       for (int p = 0; p < np; ++p) {
-        group_wait<1, 128>(&S.bar[p ? B_D3F1 : B_D3F0], (p ? c1 : c0) & 1, warp == kWarpE3);
+        group_wait<1, 128, LOCC_SPIN_E3>(&S.bar[p ? B_D3F1 : B_D3F0], (p ? c1 : c0) & 1, warp == kWarpE3);
         if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 12 + 2 * p);
         tc_fence_after();
         e3_part2(tmem + ((32 * q) << 16) + region_col(p ? kRegionP1 : R.P), S.masks + 8 * p, S.flags + 128 * p, w, nb3, b3,

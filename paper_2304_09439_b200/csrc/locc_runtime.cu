@@ -93,7 +93,9 @@ struct locc_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host-buffer queries: input uploads overlap the previous sub-batch
   cudaEvent_t ev[2] = {};          // whole-query timing
+  cudaEvent_t ev_in[2] = {}, ev_free[2] = {};  // input buffer k & 1: uploaded / released by the kernels
   std::vector<cudaEvent_t> enc_ev;  // per sub-batch encoder start/stop pairs
   bool timing = false;
   bool has_weights = false, has_shapes = false;
@@ -107,7 +109,7 @@ struct locc_ctx {
   // scratch for one sub-batch
   int64_t cap_B = 0;
   DevBuf trace;
-  DevBuf in_pairs, in_poses, counts, occ, offsets, scan_tmp, rows, pooled, stats;
+  DevBuf in_pairs, in_poses, in_pairs2, in_poses2, counts, occ, offsets, scan_tmp, rows, pooled, stats;
   DevBuf out_probs, out_labels, out_logits, out_kept, out_occ, out_masks, out_emb;
   locc_stats last{};
   int64_t timed_subs = 0;  // sub-batches whose encoder events await reading
@@ -210,6 +212,8 @@ locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks) {
   if (B > c->cap_B) {
     CK(c->in_pairs.ensure(sizeof(int32_t) * 2 * B));
     CK(c->in_poses.ensure(sizeof(float) * 14 * B));
+    CK(c->in_pairs2.ensure(sizeof(int32_t) * 2 * B));
+    CK(c->in_poses2.ensure(sizeof(float) * 14 * B));
     CK(c->counts.ensure(sizeof(int32_t) * G));
     CK(c->occ.ensure(sizeof(int32_t) * G));
     CK(c->offsets.ensure(sizeof(int64_t) * (G + 1)));
@@ -226,23 +230,6 @@ locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks) {
   }
   CK(c->stats.ensure(sizeof(DevStats)));
   if (need_masks) CK(c->out_masks.ensure(sizeof(uint32_t) * (size_t)G * ((K + 31) / 32)));
-  return LOCC_OK;
-}
-
-locc_status validate_host(const locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N) {
-  for (int64_t i = 0; i < N; ++i) {
-    for (int s = 0; s < 2; ++s) {
-      const int32_t id = pairs[2 * i + s];
-      if (id < 0 || id >= c->T.S)
-        return fail(LOCC_E_INVALID_ARG, "pair %lld side %d: shape id %d not in [0, %d)", (long long)i, s, id, c->T.S);
-      const float* p = poses + 14 * i + 7 * s;
-      for (int j = 0; j < 7; ++j)
-        if (!std::isfinite(p[j])) return fail(LOCC_E_INVALID_ARG, "pair %lld side %d: non-finite pose", (long long)i, s);
-      const double w = p[0], x = p[1], y = p[2], z = p[3];
-      if (!(((w * w + x * x) + y * y) + z * z >= 1e-12))
-        return fail(LOCC_E_INVALID_ARG, "pair %lld side %d: |q|^2 < 1e-12", (long long)i, s);
-    }
-  }
   return LOCC_OK;
 }
 
@@ -288,10 +275,8 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
   for (const void* p : all)
     if (p && is_device_ptr(p) != dev)
       return fail(LOCC_E_INVALID_ARG, "all buffers of one call must be host or all device memory");
-  if (!dev) {
-    locc_status s = validate_host(c, pairs, poses, N);
-    if (s != LOCC_OK) return s;
-  }
+  // Inputs are validated on the device (segment_setup in the crop kernels: ids in range, finite
+  // poses, |q|^2 >= 1e-12); an invalid segment is counted and the call returns LOCC_E_INVALID_ARG.
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   const bool sync = !dev || !stream;
   const int64_t Bcap = std::min<int64_t>(N, batch_cap(c));
@@ -319,10 +304,18 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       b.pairs = pairs + 2 * i0;
       b.poses = poses + 14 * i0;
     } else {
-      CK(cudaMemcpyAsync(c->in_pairs.p, pairs + 2 * i0, sizeof(int32_t) * 2 * B, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(c->in_poses.p, poses + 14 * i0, sizeof(float) * 14 * B, cudaMemcpyHostToDevice, st));
-      b.pairs = c->in_pairs.as<int32_t>();
-      b.poses = c->in_poses.as<float>();
+      // upload on the copy stream into buffer subs & 1 (released by sub-batch subs - 2), so it overlaps
+      // the kernels of the previous sub-batch
+      const int buf = (int)(subs & 1);
+      DevBuf& dp = buf ? c->in_pairs2 : c->in_pairs;
+      DevBuf& dq = buf ? c->in_poses2 : c->in_poses;
+      if (subs >= 2) CK(cudaStreamWaitEvent(c->copy_stream, c->ev_free[buf], 0));
+      CK(cudaMemcpyAsync(dp.p, pairs + 2 * i0, sizeof(int32_t) * 2 * B, cudaMemcpyHostToDevice, c->copy_stream));
+      CK(cudaMemcpyAsync(dq.p, poses + 14 * i0, sizeof(float) * 14 * B, cudaMemcpyHostToDevice, c->copy_stream));
+      CK(cudaEventRecord(c->ev_in[buf], c->copy_stream));
+      CK(cudaStreamWaitEvent(st, c->ev_in[buf], 0));
+      b.pairs = dp.as<int32_t>();
+      b.poses = dq.as<float>();
     }
     b.counts = (dev && kept) ? kept + 2 * i0 : c->counts.as<int32_t>();
     b.occ = (dev && occ) ? occ + 2 * i0 : c->occ.as<int32_t>();
@@ -374,6 +367,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs + 1], st));
     CK(launch_head(c->P, b, d_probs, d_labels, d_logits, d_emb, st));
     launches += 7;
+    if (!dev) CK(cudaEventRecord(c->ev_free[subs & 1], st));  // the kernels are done with the inputs
     ++subs;
     if (!dev) {
       CK(cudaMemcpyAsync(probs + i0, d_probs, sizeof(float) * B, cudaMemcpyDeviceToHost, st));
@@ -466,7 +460,10 @@ locc_status locc_create(const locc_config* cfg, locc_ctx** out) {
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) c->num_sms = prop.multiProcessorCount;
   cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming);
   if (e != cudaSuccess) {
     locc_destroy(c);
     return fail(LOCC_E_CUDA, "stream/event creation: %s", cudaGetErrorString(e));
@@ -479,8 +476,14 @@ void locc_destroy(locc_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
+    if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (auto& e : c->enc_ev) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
