@@ -40,6 +40,9 @@ def lib():
         L.oracle_rel_transform.argtypes = [vp] * 6
         L.oracle_query.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, C.c_int32, C.c_int32, vp, vp,
                                    C.c_int64] + [vp] * 7
+        L.oracle_head_grad.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, vp, vp, vp, vp, vp]
+        L.oracle_query_grad.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, C.c_int32, C.c_int32, vp, vp, C.c_int64,
+                                        vp, vp]
         L.oracle_load_weights.argtypes = [C.c_char_p, vp, C.c_size_t, vp, vp, vp]
         L.oracle_load_weights.restype = C.c_int64
         L.oracle_n_params.argtypes = [C.c_int32, C.c_int32]
@@ -101,6 +104,39 @@ def query(weights_flat, points, pairs, poses, M=6, H=256, F=64, bf16_emul=False,
     if rc:
         raise ValueError(f"oracle_query: {rc}")
     return out
+
+
+def head_grad(weights_flat, eA, eB, poseA, poseB, H=256, F=64):
+    """NEXT-2: predictor logit and d logit / d [q_A, t_A, q_B, t_B] (14) at given embeddings (fp64)."""
+    w = np.ascontiguousarray(weights_flat, np.float32)
+    a = np.ascontiguousarray(eA, np.float64)
+    b = np.ascontiguousarray(eB, np.float64)
+    pa = np.ascontiguousarray(poseA, np.float64)
+    pb = np.ascontiguousarray(poseB, np.float64)
+    lg = np.zeros(1)
+    g = np.zeros(14)
+    cfg = _Cfg(6, H, F, 0, 1)
+    rc = lib().oracle_head_grad(C.byref(cfg), _p(w), w.size, _p(a), _p(b), _p(pa), _p(pb), _p(lg), _p(g))
+    if rc:
+        raise ValueError(f"oracle_head_grad: {rc}")
+    return float(lg[0]), g
+
+
+def query_grad(weights_flat, points, pairs, poses, M=6, H=256, F=64, bf16_emul=False, n_threads=0):
+    """Whole query plus d logit / d pose per pair: returns (logits [N], grad [N][14])."""
+    w = np.ascontiguousarray(weights_flat, np.float32)
+    pts = np.ascontiguousarray(points, np.float32)
+    pr = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+    po = np.ascontiguousarray(poses, np.float32).reshape(-1, 2, 7)
+    N = pr.shape[0]
+    lg = np.zeros(N)
+    g = np.zeros((N, 14))
+    cfg = _Cfg(M, H, F, 1 if bf16_emul else 0, n_threads)
+    rc = lib().oracle_query_grad(C.byref(cfg), _p(w), w.size, _p(pts), pts.shape[0], pts.shape[1], _p(pr), _p(po), N,
+                                 _p(lg), _p(g))
+    if rc:
+        raise ValueError(f"oracle_query_grad: {rc}")
+    return lg, g
 
 
 def load_weights(manifest):

@@ -318,6 +318,101 @@ double pair_head(const Params& P, const double* uA, const double* uB) {
   return logit;
 }
 
+// ------------------------------------------------------------------ NEXT-2: pose gradient
+// d logit / d (q_A, t_A, q_B, t_B) of the predictor at fixed crops (the crop mask is
+// piecewise constant in the pose, so nothing flows through it; the encoder sees local-frame points,
+// so e does not depend on the pose).  Plain reverse-mode chain rule in fp64 over the same layers as
+// object_mlp / pair_head; ReLU'(x) = [x > 0]; the max across the pair passes the gradient to the
+// side it selected (uA > uB -> A, else B, as pair_head).  Raw quaternion q -> q^ = sgn q / |q| with
+// |q| from O1's grouping and sgn the canonical sign (Q12): dq = sgn (dq^ - q^ (q^ . dq^)) / |q|.
+// grad = [d/dq_A (4), d/dt_A (3), d/dq_B (4), d/dt_B (3)].
+struct ObjAct {
+  std::vector<double> z, a1, a2, u;
+};
+
+void object_fwd(const Params& P, const double* e, int F, const double qh[4], const double t[3], ObjAct& A) {
+  A.z.assign(F + 7, 0.0);
+  A.a1.assign(kP, 0.0);
+  A.a2.assign(kP, 0.0);
+  A.u.assign(kP, 0.0);
+  for (int j = 0; j < F; ++j) A.z[j] = e[j];
+  for (int i = 0; i < 4; ++i) A.z[F + i] = qh[i];
+  for (int i = 0; i < 3; ++i) A.z[F + 4 + i] = t[i];
+  dense(P.obj1, A.z.data(), A.a1.data(), true);
+  dense(P.obj2, A.a1.data(), A.a2.data(), true);
+  dense(P.obj3, A.a2.data(), A.u.data(), true);
+}
+
+// y = W^T g (W row-major [out][in]): the transpose product of reverse mode.
+void dense_T(const Layer& L, const double* g, double* y) {
+  for (int i = 0; i < L.in; ++i) y[i] = 0.0;
+  for (int o = 0; o < L.out; ++o)
+    for (int i = 0; i < L.in; ++i) y[i] += (double)L.W[(int64_t)o * L.in + i] * g[o];
+}
+
+// O1 + Q12 on a raw quaternion held in doubles: q^ (canonical sign), |q| and the sign.
+bool canonical(const double q[4], double qh[4], double& norm, double& sgn) {
+  const double n2 = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
+  if (!(n2 >= 1e-12)) return false;
+  norm = std::sqrt(n2);
+  double n[4];
+  for (int i = 0; i < 4; ++i) n[i] = q[i] / norm;
+  sgn = 1.0;
+  for (int i = 0; i < 4; ++i)
+    if (n[i] != 0.0) {
+      sgn = n[i] > 0.0 ? 1.0 : -1.0;
+      break;
+    }
+  for (int i = 0; i < 4; ++i) qh[i] = sgn * n[i];
+  return true;
+}
+
+double head_grad(const Params& P, const double* eA, const double* eB, int F, const double qA[4], const double tA[3],
+                 const double qB[4], const double tB[3], double grad[14]) {
+  double qhA[4], qhB[4], nA, nB, sA, sB;
+  canonical(qA, qhA, nA, sA);
+  canonical(qB, qhB, nB, sB);
+  ObjAct A, B;
+  object_fwd(P, eA, F, qhA, tA, A);
+  object_fwd(P, eB, F, qhB, tB, B);
+  std::vector<double> v(kP), c1(kP), c2(kP), c3(kP);
+  for (int j = 0; j < kP; ++j) v[j] = A.u[j] > B.u[j] ? A.u[j] : B.u[j];
+  dense(P.pair1, v.data(), c1.data(), true);
+  dense(P.pair2, c1.data(), c2.data(), true);
+  dense(P.pair3, c2.data(), c3.data(), true);
+  double logit;
+  dense(P.out, c3.data(), &logit, false);
+  // reverse mode
+  std::vector<double> g(kP), h(kP);
+  for (int j = 0; j < kP; ++j) g[j] = c3[j] > 0.0 ? (double)P.out.W[j] : 0.0;  // d/d pre3 of pair
+  dense_T(P.pair3, g.data(), h.data());                                         // d/d c2
+  for (int j = 0; j < kP; ++j) g[j] = c2[j] > 0.0 ? h[j] : 0.0;
+  dense_T(P.pair2, g.data(), h.data());  // d/d c1
+  for (int j = 0; j < kP; ++j) g[j] = c1[j] > 0.0 ? h[j] : 0.0;
+  std::vector<double> gv(kP);
+  dense_T(P.pair1, g.data(), gv.data());  // d/d v
+  auto side = [&](const ObjAct& S, bool is_a, const double qh[4], double norm, double sgn, double* out7) {
+    std::vector<double> gu(kP), x(kP), y(kP), gz(F + 7);
+    for (int j = 0; j < kP; ++j) {
+      const bool sel = is_a ? (A.u[j] > B.u[j]) : !(A.u[j] > B.u[j]);
+      gu[j] = sel ? gv[j] : 0.0;
+    }
+    for (int j = 0; j < kP; ++j) x[j] = S.u[j] > 0.0 ? gu[j] : 0.0;
+    dense_T(P.obj3, x.data(), y.data());  // d/d a2
+    for (int j = 0; j < kP; ++j) x[j] = S.a2[j] > 0.0 ? y[j] : 0.0;
+    dense_T(P.obj2, x.data(), y.data());  // d/d a1
+    for (int j = 0; j < kP; ++j) x[j] = S.a1[j] > 0.0 ? y[j] : 0.0;
+    dense_T(P.obj1, x.data(), gz.data());  // d/d z
+    const double* gq = gz.data() + F;
+    const double dot = ((qh[0] * gq[0] + qh[1] * gq[1]) + qh[2] * gq[2]) + qh[3] * gq[3];
+    for (int i = 0; i < 4; ++i) out7[i] = sgn * (gq[i] - qh[i] * dot) / norm;
+    for (int i = 0; i < 3; ++i) out7[4 + i] = gz[F + 4 + i];
+  };
+  side(A, true, qhA, nA, sA, grad);
+  side(B, false, qhB, nB, sB, grad + 7);
+  return logit;
+}
+
 bool finite_n(const float* p, int64_t n) {
   for (int64_t i = 0; i < n; ++i)
     if (!std::isfinite(p[i])) return false;
@@ -446,6 +541,45 @@ int oracle_query(const oracle_cfg* cfg, const float* weights, size_t n_weights, 
   for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
   worker();
   for (auto& th : pool) th.join();
+  return 0;
+}
+
+int oracle_head_grad(const oracle_cfg* cfg, const float* weights, size_t n_weights, const double* eA,
+                     const double* eB, const double poseA[7], const double poseB[7], double* logit, double grad[14]) {
+  if (!cfg || !weights || (int64_t)n_weights != n_params(cfg->H, cfg->F)) return -3;
+  const Params P = bind_params(weights, cfg->H, cfg->F);
+  double qh[4], nrm, sg;
+  if (!canonical(poseA, qh, nrm, sg) || !canonical(poseB, qh, nrm, sg)) return -1;
+  const double l = head_grad(P, eA, eB, cfg->F, poseA, poseA + 4, poseB, poseB + 4, grad);
+  if (logit) *logit = l;
+  return 0;
+}
+
+int oracle_query_grad(const oracle_cfg* cfg, const float* weights, size_t n_weights, const float* points,
+                      int32_t S, int32_t K, const int32_t* pairs, const float* poses, int64_t N, double* logits,
+                      double* grad) {
+  if (!cfg || N < 0) return -1;
+  const int F = cfg->F;
+  std::vector<double> emb((size_t)(2 * N > 0 ? 2 * N : 1) * F), lg((size_t)(N > 0 ? N : 1));
+  std::vector<int32_t> kept((size_t)(2 * N > 0 ? 2 * N : 1));
+  const int rc = oracle_query(cfg, weights, n_weights, points, S, K, pairs, poses, N, nullptr, nullptr, lg.data(),
+                              kept.data(), nullptr, nullptr, emb.data());
+  if (rc) return rc;
+  const Params P = bind_params(weights, cfg->H, F);
+  for (int64_t i = 0; i < N; ++i) {
+    double* g = grad + 14 * i;
+    if (logits) logits[i] = lg[i];
+    if (kept[2 * i] + kept[2 * i + 1] == 0) {  // short-circuit: constant -inf, zero gradient
+      for (int j = 0; j < 14; ++j) g[j] = 0.0;
+      continue;
+    }
+    double pa[7], pb[7];
+    for (int j = 0; j < 7; ++j) {
+      pa[j] = poses[14 * i + j];
+      pb[j] = poses[14 * i + 7 + j];
+    }
+    head_grad(P, emb.data() + (2 * i) * F, emb.data() + (2 * i + 1) * F, F, pa, pa + 4, pb, pb + 4, g);
+  }
   return 0;
 }
 

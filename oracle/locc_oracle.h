@@ -49,6 +49,19 @@ int oracle_query(const oracle_cfg* cfg, const float* weights, size_t n_weights, 
                  double* probs, uint8_t* labels, double* logits, int32_t* kept, int32_t* occ,
                  uint32_t* masks, double* emb);
 
+/* NEXT-2: predictor forward + reverse-mode gradient of the logit w.r.t. the raw pose inputs
+ * [q_A(4), t_A(3), q_B(4), t_B(3)] at given embeddings e_A, e_B (fp64, poses as doubles so finite
+ * differences can probe it).  Crops and embeddings are constant in the pose (see the .cpp). */
+int oracle_head_grad(const oracle_cfg* cfg, const float* weights, size_t n_weights, const double* eA,
+                     const double* eB, const double poseA[7], const double poseB[7], double* logit,
+                     double grad[14]);
+
+/* Whole query plus the pose gradient of each logit: grad [N][14] (zero for short-circuited pairs,
+ * whose logit is the constant -inf).  logits may be NULL. */
+int oracle_query_grad(const oracle_cfg* cfg, const float* weights, size_t n_weights, const float* points,
+                      int32_t S, int32_t K, const int32_t* pairs, const float* poses, int64_t N, double* logits,
+                      double* grad);
+
 /* Parse a weight manifest + .bin (format in include/locc.h) into `out` (canonical order).
  * Returns the float count, or a negative code; writes M, H, F. */
 int64_t oracle_load_weights(const char* manifest, float* out, size_t cap, int32_t* M, int32_t* H,
