@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--s", type=float, default=0.5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-grad", action="store_true", help="skip the NEXT-2 pose-gradient measurement")
     return ap.parse_args()
 
 
@@ -264,6 +265,36 @@ def main():
                        "l2": "L2 flushed (256 MB write) before every timed step; working set (GBs of rows) >> L2",
                        "parallelism": f"pair-batch shards, 1 process/GPU x {world}"},
             "gpu_launches": launches_per_step * a.steps, "clocks": clk, "roofline": roof}
+
+    # NEXT-2: the same step with the pose gradient (locc_query_grad), device-timed the same way
+    if not a.no_grad:
+        d_grad = torch.empty(N, 14, device="cuda")
+
+        def gstep():
+            ctx.query_grad_into(d_pairs, d_poses, d_probs, d_grad, d_labels, stream=stream.cuda_stream)
+
+        for _ in range(a.warmup):
+            gstep()
+        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(a.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                gev[i][0].record(stream)
+            gstep()
+            with torch.cuda.stream(stream):
+                gev[i][1].record(stream)
+        torch.cuda.synchronize()
+        gms = statistics.mean([s.elapsed_time(e) for s, e in gev])
+        if world > 1:
+            t = torch.tensor([gms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            gms = float(t.item())
+        line["pose_grad"] = {"metric": "collision checks with d logit / d pose per second", "value": world * N / (gms / 1e3),
+                             "unit": UNIT, "ms_per_step": gms, "overhead_vs_forward": gms / ms - 1.0,
+                             "api": "locc_query_grad (grad [N][14] fp32)"}
 
     # e2e: same metric through the public API with HOST buffers (pinned), copies in the timed region
     if not a.no_e2e:

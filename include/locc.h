@@ -125,6 +125,19 @@ locc_status locc_query_debug(locc_ctx* ctx, const int32_t* pairs, const float* p
                              float* probs, uint8_t* labels, float* logits, int32_t* kept,
                              int32_t* occ, uint32_t* masks, float* emb, void* stream);
 
+/* locc_query plus the pose gradient of each logit (the paper's use of the
+ * network inside gradient-based planning, PAPER.md §"Introduction"/§"Experiments"):
+ * grad float32 [N][14] = d logit_i / d (q_A[4], t_A[3], q_B[4], t_B[3]) of pair i, in the order of
+ * poses[14i .. 14i+13].  The crops are held fixed (the crop mask is piecewise constant in the pose,
+ * so no gradient flows through it), ReLU'(x) = [x > 0], the max across the pair routes the gradient
+ * to the side it selected (u_A > u_B -> A, ties -> B), and the raw quaternion's gradient includes
+ * the normalisation and canonical sign: dq = s (dq^ - q^ (q^ . dq^)) / |q|.  Short-circuited pairs
+ * (constant logit -inf): grad 0.  Computed in fp32 (CUDA cores) in the same fused predictor kernel
+ * as the forward.  Requires H = 256, F = 64.  Same residency, stream and error rules as locc_query.
+ * Errors: INVALID_ARG (as locc_query, null grad, H/F not 256/64), STATE, CUDA, OOM. */
+locc_status locc_query_grad(locc_ctx* ctx, const int32_t* pairs, const float* poses, int64_t N,
+                            float* probs, uint8_t* labels, float* logits, float* grad, void* stream);
+
 /* Switch the encoder precision of an existing context (LOCC_PREC_FP32 / LOCC_PREC_BF16). */
 locc_status locc_set_precision(locc_ctx* ctx, int32_t precision);
 

@@ -42,7 +42,7 @@ def lib():
                                    C.c_int64] + [vp] * 7
         L.oracle_head_grad.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, vp, vp, vp, vp, vp]
         L.oracle_query_grad.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, C.c_int32, C.c_int32, vp, vp, C.c_int64,
-                                        vp, vp]
+                                        vp, vp, vp]
         L.oracle_load_weights.argtypes = [C.c_char_p, vp, C.c_size_t, vp, vp, vp]
         L.oracle_load_weights.restype = C.c_int64
         L.oracle_n_params.argtypes = [C.c_int32, C.c_int32]
@@ -123,7 +123,8 @@ def head_grad(weights_flat, eA, eB, poseA, poseB, H=256, F=64):
 
 
 def query_grad(weights_flat, points, pairs, poses, M=6, H=256, F=64, bf16_emul=False, n_threads=0):
-    """Whole query plus d logit / d pose per pair: returns (logits [N], grad [N][14])."""
+    """Whole query plus d logit / d pose per pair: returns (logits [N], grad [N][14], margin [N]) with
+    margin the pair's smallest ReLU / max-routing distance from its threshold (inf: short-circuit)."""
     w = np.ascontiguousarray(weights_flat, np.float32)
     pts = np.ascontiguousarray(points, np.float32)
     pr = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
@@ -131,12 +132,13 @@ def query_grad(weights_flat, points, pairs, poses, M=6, H=256, F=64, bf16_emul=F
     N = pr.shape[0]
     lg = np.zeros(N)
     g = np.zeros((N, 14))
+    mg = np.zeros(N)
     cfg = _Cfg(M, H, F, 1 if bf16_emul else 0, n_threads)
     rc = lib().oracle_query_grad(C.byref(cfg), _p(w), w.size, _p(pts), pts.shape[0], pts.shape[1], _p(pr), _p(po), N,
-                                 _p(lg), _p(g))
+                                 _p(lg), _p(g), _p(mg))
     if rc:
         raise ValueError(f"oracle_query_grad: {rc}")
-    return lg, g
+    return lg, g, mg
 
 
 def load_weights(manifest):

@@ -330,7 +330,18 @@ struct ObjAct {
   std::vector<double> z, a1, a2, u;
 };
 
-void object_fwd(const Params& P, const double* e, int F, const double qh[4], const double t[3], ObjAct& A) {
+// dense + ReLU that also lowers mg to the smallest |pre-activation| seen: how far a ReLU decision is
+// from its threshold (reported so tests can set aside pairs whose fp32 decisions may legitimately flip).
+void dense_relu_mg(const Layer& L, const double* x, double* y, double& mg) {
+  dense(L, x, y, false);
+  for (int o = 0; o < L.out; ++o) {
+    mg = std::min(mg, std::fabs(y[o]));
+    y[o] = y[o] > 0.0 ? y[o] : 0.0;
+  }
+}
+
+void object_fwd(const Params& P, const double* e, int F, const double qh[4], const double t[3], ObjAct& A,
+                double& mg) {
   A.z.assign(F + 7, 0.0);
   A.a1.assign(kP, 0.0);
   A.a2.assign(kP, 0.0);
@@ -338,9 +349,9 @@ void object_fwd(const Params& P, const double* e, int F, const double qh[4], con
   for (int j = 0; j < F; ++j) A.z[j] = e[j];
   for (int i = 0; i < 4; ++i) A.z[F + i] = qh[i];
   for (int i = 0; i < 3; ++i) A.z[F + 4 + i] = t[i];
-  dense(P.obj1, A.z.data(), A.a1.data(), true);
-  dense(P.obj2, A.a1.data(), A.a2.data(), true);
-  dense(P.obj3, A.a2.data(), A.u.data(), true);
+  dense_relu_mg(P.obj1, A.z.data(), A.a1.data(), mg);
+  dense_relu_mg(P.obj2, A.a1.data(), A.a2.data(), mg);
+  dense_relu_mg(P.obj3, A.a2.data(), A.u.data(), mg);
 }
 
 // y = W^T g (W row-major [out][in]): the transpose product of reverse mode.
@@ -368,18 +379,23 @@ bool canonical(const double q[4], double qh[4], double& norm, double& sgn) {
 }
 
 double head_grad(const Params& P, const double* eA, const double* eB, int F, const double qA[4], const double tA[3],
-                 const double qB[4], const double tB[3], double grad[14]) {
+                 const double qB[4], const double tB[3], double grad[14], double* margin = nullptr) {
   double qhA[4], qhB[4], nA, nB, sA, sB;
   canonical(qA, qhA, nA, sA);
   canonical(qB, qhB, nB, sB);
   ObjAct A, B;
-  object_fwd(P, eA, F, qhA, tA, A);
-  object_fwd(P, eB, F, qhB, tB, B);
+  double mg = INFINITY;
+  object_fwd(P, eA, F, qhA, tA, A, mg);
+  object_fwd(P, eB, F, qhB, tB, B, mg);
   std::vector<double> v(kP), c1(kP), c2(kP), c3(kP);
-  for (int j = 0; j < kP; ++j) v[j] = A.u[j] > B.u[j] ? A.u[j] : B.u[j];
-  dense(P.pair1, v.data(), c1.data(), true);
-  dense(P.pair2, c1.data(), c2.data(), true);
-  dense(P.pair3, c2.data(), c3.data(), true);
+  for (int j = 0; j < kP; ++j) {
+    v[j] = A.u[j] > B.u[j] ? A.u[j] : B.u[j];
+    if (v[j] > 0.0) mg = std::min(mg, std::fabs(A.u[j] - B.u[j]));  // the max's routing decision
+  }
+  dense_relu_mg(P.pair1, v.data(), c1.data(), mg);
+  dense_relu_mg(P.pair2, c1.data(), c2.data(), mg);
+  dense_relu_mg(P.pair3, c2.data(), c3.data(), mg);
+  if (margin) *margin = mg;
   double logit;
   dense(P.out, c3.data(), &logit, false);
   // reverse mode
@@ -557,7 +573,7 @@ int oracle_head_grad(const oracle_cfg* cfg, const float* weights, size_t n_weigh
 
 int oracle_query_grad(const oracle_cfg* cfg, const float* weights, size_t n_weights, const float* points,
                       int32_t S, int32_t K, const int32_t* pairs, const float* poses, int64_t N, double* logits,
-                      double* grad) {
+                      double* grad, double* margin) {
   if (!cfg || N < 0) return -1;
   const int F = cfg->F;
   std::vector<double> emb((size_t)(2 * N > 0 ? 2 * N : 1) * F), lg((size_t)(N > 0 ? N : 1));
@@ -571,6 +587,7 @@ int oracle_query_grad(const oracle_cfg* cfg, const float* weights, size_t n_weig
     if (logits) logits[i] = lg[i];
     if (kept[2 * i] + kept[2 * i + 1] == 0) {  // short-circuit: constant -inf, zero gradient
       for (int j = 0; j < 14; ++j) g[j] = 0.0;
+      if (margin) margin[i] = INFINITY;
       continue;
     }
     double pa[7], pb[7];
@@ -578,7 +595,8 @@ int oracle_query_grad(const oracle_cfg* cfg, const float* weights, size_t n_weig
       pa[j] = poses[14 * i + j];
       pb[j] = poses[14 * i + 7 + j];
     }
-    head_grad(P, emb.data() + (2 * i) * F, emb.data() + (2 * i + 1) * F, F, pa, pa + 4, pb, pb + 4, g);
+    head_grad(P, emb.data() + (2 * i) * F, emb.data() + (2 * i + 1) * F, F, pa, pa + 4, pb, pb + 4, g,
+              margin ? margin + i : nullptr);
   }
   return 0;
 }

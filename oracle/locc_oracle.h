@@ -57,10 +57,12 @@ int oracle_head_grad(const oracle_cfg* cfg, const float* weights, size_t n_weigh
                      double grad[14]);
 
 /* Whole query plus the pose gradient of each logit: grad [N][14] (zero for short-circuited pairs,
- * whose logit is the constant -inf).  logits may be NULL. */
+ * whose logit is the constant -inf).  logits, margin may be NULL.  margin [N]: the smallest
+ * |pre-activation| over the predictor's ReLUs and |u_A - u_B| over the max's routed features (inf
+ * for a short-circuit) — how close the pair's gradient is to a discontinuity. */
 int oracle_query_grad(const oracle_cfg* cfg, const float* weights, size_t n_weights, const float* points,
                       int32_t S, int32_t K, const int32_t* pairs, const float* poses, int64_t N, double* logits,
-                      double* grad);
+                      double* grad, double* margin);
 
 /* Parse a weight manifest + .bin (format in include/locc.h) into `out` (canonical order).
  * Returns the float count, or a negative code; writes M, H, F. */

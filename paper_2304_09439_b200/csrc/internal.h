@@ -52,6 +52,13 @@ struct DevParams {
   const float* pb3;
   const float* wout; // [128]
   const float* bout; // [1]
+  // original [out][in] layouts for the reverse mode (NEXT-2): d/d in = W^T d/d out
+  const float* o1p;  // the 7 pose columns of obj.l1, [7][128]
+  const float* o2;
+  const float* o3;
+  const float* p1;
+  const float* p2;
+  const float* p3;
   const void* tc_w2; // bf16 W2/W3 pre-arranged as the encoder_tc shared-memory image
   const void* tc_w3;
 };
@@ -97,7 +104,7 @@ cudaError_t launch_encoder_f32(const DevParams& P, const Batch& b, cudaStream_t 
 cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b, int num_sms, cudaStream_t st,
                               long long* trace = nullptr);
 cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_t* labels,
-                        float* logits, float* emb, cudaStream_t st);
+                        float* logits, float* emb, float* grad, cudaStream_t st);
 size_t scan_tmp_elems(int64_t G);
 size_t encoder_tc_smem_bytes();
 

@@ -44,9 +44,12 @@ struct HeadSmem {
 
 // out[n][r] = act(sum_k W[k][n] in[k][r] + b[n]), r < ROWS, n < N; W = transposed weights [K][N]
 // (global, row-major).  in / out: [feature][kLD] shared buffers.  RT rows x 8 outputs per thread.
-template <int ROWS, int N, bool kRelu>
+// kMode 0: forward (+ bias, optional ReLU).  Reverse mode (NEXT-2): 1 = no bias; 2 = no bias and the
+// result multiplied by the ReLU mask bit of the layer below (mask [N][ROWS / 32] words, bit r of row r).
+template <int ROWS, int N, bool kRelu, int kMode = 0>
 __device__ __forceinline__ void dense(const float* __restrict__ W, const float* __restrict__ bias, int K,
-                                      const float (*in)[kLD], float (*out)[kLD], float (*ws)[kKC][128]) {
+                                      const float (*in)[kLD], float (*out)[kLD], float (*ws)[kKC][128],
+                                      const uint32_t* __restrict__ mask = nullptr) {
   constexpr int CG = N / 8;                  // column groups
   constexpr int RG = kHeadThreads / CG;      // row groups
   constexpr int RT = ROWS / RG;              // rows per thread
@@ -121,12 +124,17 @@ __device__ __forceinline__ void dense(const float* __restrict__ W, const float* 
   }
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    const float b = bias[c0 + c];
+    const float b = kMode == 0 ? bias[c0 + c] : 0.f;
 #pragma unroll
     for (int r = 0; r < RT; r += 4) {
       float v4[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) v4[q] = ((c & 1) ? f2_hi(acc[r + q][c >> 1]) : f2_lo(acc[r + q][c >> 1])) + b;
+      if (kMode == 2) {
+        const uint32_t mw = mask[(c0 + c) * (ROWS / 32) + ((r0 + r) >> 5)] >> ((r0 + r) & 31);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v4[q] = (mw >> q) & 1u ? v4[q] : 0.f;
+      }
       float4 y = make_float4(v4[0], v4[1], v4[2], v4[3]);
       if (kRelu) y = make_float4(fmaxf(y.x, 0.f), fmaxf(y.y, 0.f), fmaxf(y.z, 0.f), fmaxf(y.w, 0.f));
       *reinterpret_cast<float4*>(&out[c0 + c][r0 + r]) = y;
@@ -135,11 +143,106 @@ __device__ __forceinline__ void dense(const float* __restrict__ W, const float* 
   __syncthreads();
 }
 
+// NEXT-2 reverse mode: ReLU masks of the forward (bit r of word [feature][r / 32] = row r's activation
+// > 0) and the side the max across the pair selected (bit p = u_A > u_B, ties -> B as the forward).
+struct GradMasks {
+  uint32_t obj[3][128][kTS / 32];   // a1, a2, u per side
+  uint32_t pair[3][128][kTP / 32];  // c1, c2, c3 per pair
+  uint32_t selA[128][kTP / 32];
+};
+struct HeadGradSmem {
+  HeadSmem h;
+  GradMasks m;
+};
+
+// mask[f][w] bit l = buf[f][32w + l] > 0, f < 128, rows < ROWS (one ballot per word).
+template <int ROWS>
+__device__ __forceinline__ void record_mask(const float (*buf)[kLD], uint32_t (*mask)[ROWS / 32]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = warp; i < 128 * (ROWS / 32); i += kHeadThreads / 32) {
+    const int f = i / (ROWS / 32), w = i % (ROWS / 32);
+    const uint32_t bits = __ballot_sync(0xffffffffu, buf[f][32 * w + lane] > 0.f);
+    if (lane == 0) mask[f][w] = bits;
+  }
+}
+
+// NEXT-2: d logit / d [q_A, t_A, q_B, t_B] by reverse mode through the predictor (oracle:
+// head_grad).  On entry S.u holds c3 (pair layer 3 output) and the forward masks are recorded.
+// Each backward layer is dense<> over the original [out][in] weights (= the transpose of the
+// forward's), masked by the ReLU of the layer below; the object MLP's first layer only needs its
+// 7 pose columns (o1p [7][128]).  Quaternion: dq = s (dq^ - q^ (q^ . dq^)) / |q| (fp64 q^, |q|).
+__device__ __forceinline__ void head_tile_backward(const DevParams& P, const Batch& b, HeadSmem& S,
+                                                   const GradMasks& GM, int64_t i0, int npairs,
+                                                   float* __restrict__ grad) {
+  const int tid = threadIdx.x;
+  __syncthreads();  // the output stage read S.u
+  for (int e = tid; e < 128 * kTP; e += kHeadThreads) {  // d/d pre3 (pair) = w_out [c3 > 0]
+    const int n = e / kTP, p = e % kTP;
+    S.v[n][p] = (GM.pair[2][n][p >> 5] >> (p & 31)) & 1u ? __ldg(P.wout + n) : 0.f;
+  }
+  __syncthreads();
+  dense<kTP, 128, false, 2>(P.p3, nullptr, 128, S.v, S.u, S.w, &GM.pair[1][0][0]);  // d/d pre2 (pair)
+  dense<kTP, 128, false, 2>(P.p2, nullptr, 128, S.u, S.v, S.w, &GM.pair[0][0][0]);  // d/d pre1 (pair)
+  dense<kTP, 128, false, 1>(P.p1, nullptr, 128, S.v, S.u, S.w);                     // d/d v
+  for (int e = tid; e < 128 * kTS; e += kHeadThreads) {  // d/d pre3 (object) per side
+    const int n = e / kTS, s = e % kTS, p = s >> 1;
+    const bool selA = (GM.selA[n][p >> 5] >> (p & 31)) & 1u;
+    const bool pos = (GM.obj[2][n][s >> 5] >> (s & 31)) & 1u;
+    S.v[n][s] = (pos && (selA == ((s & 1) == 0))) ? S.u[n][p] : 0.f;
+  }
+  __syncthreads();
+  dense<kTS, 128, false, 2>(P.o3, nullptr, 128, S.v, S.u, S.w, &GM.obj[1][0][0]);  // d/d pre2 (object)
+  dense<kTS, 128, false, 2>(P.o2, nullptr, 128, S.u, S.v, S.w, &GM.obj[0][0][0]);  // d/d pre1 (object)
+  // d/d z[F + c] = sum_o O1[o][F + c] g[o]: side s = tid & 127, components c = tid >> 7, +2, ...
+  {
+    const int s = tid & (kTS - 1);
+    for (int c = tid >> 7; c < 7; c += kHeadThreads / kTS) {
+      const float* w = P.o1p + c * 128;
+      float a0 = 0.f, a1 = 0.f;
+#pragma unroll 8
+      for (int o = 0; o < 128; o += 2) {
+        a0 = fmaf(__ldg(w + o), S.v[o][s], a0);
+        a1 = fmaf(__ldg(w + o + 1), S.v[o + 1][s], a1);
+      }
+      S.z[c][s] = a0 + a1;
+    }
+  }
+  __syncthreads();
+  if (tid < 2 * npairs) {
+    const int s = tid;
+    const int64_t side = 2 * i0 + s;
+    float* g = grad + side * 7;
+    if (S.nside[s & ~1] + S.nside[s | 1] == 0) {
+      for (int c = 0; c < 7; ++c) g[c] = 0.f;  // short-circuit: constant logit
+    } else {
+      const float* pose = b.poses + side * 7;
+      const double q[4] = {pose[0], pose[1], pose[2], pose[3]};
+      const double n = sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+      double sg = 1.0;
+      for (int c = 0; c < 4; ++c)
+        if (q[c] != 0.0) {
+          sg = q[c] > 0.0 ? 1.0 : -1.0;
+          break;
+        }
+      double qh[4], dot = 0.0;
+      for (int c = 0; c < 4; ++c) {
+        qh[c] = sg * q[c] / n;
+        dot += qh[c] * (double)S.z[c][s];
+      }
+      for (int c = 0; c < 4; ++c) g[c] = (float)(sg * ((double)S.z[c][s] - qh[c] * dot) / n);
+      for (int c = 4; c < 7; ++c) g[c] = S.z[c][s];
+    }
+  }
+}
+
+template <bool kGrad>
 __global__ void __launch_bounds__(kHeadThreads, 1) head_tile_kernel(DevParams P, Batch b, float* __restrict__ probs,
                                                                     uint8_t* __restrict__ labels,
-                                                                    float* __restrict__ logits, float* __restrict__ emb) {
+                                                                    float* __restrict__ logits, float* __restrict__ emb,
+                                                                    float* __restrict__ grad) {
   extern __shared__ float4 smem4[];
   HeadSmem& S = *reinterpret_cast<HeadSmem*>(smem4);
+  GradMasks& GM = reinterpret_cast<HeadGradSmem*>(smem4)->m;  // only touched when kGrad
   const int tid = threadIdx.x;
   const int64_t i0 = (int64_t)blockIdx.x * kTP;
   const int npairs = (int)min((int64_t)kTP, b.B - i0);
@@ -203,8 +306,19 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_tile_kernel(DevParams P,
     }
   // S8 object MLP (shared by both sides)
   dense<kTS, 128, true>(P.o1T, P.ob1, 71, S.z, S.u, S.w);
+  if (kGrad) record_mask<kTS>(S.u, GM.obj[0]);
   dense<kTS, 128, true>(P.o2T, P.ob2, 128, S.u, S.v, S.w);
+  if (kGrad) record_mask<kTS>(S.v, GM.obj[1]);
   dense<kTS, 128, true>(P.o3T, P.ob3, 128, S.v, S.u, S.w);
+  if (kGrad) {
+    record_mask<kTS>(S.u, GM.obj[2]);
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int i = warp; i < 128 * (kTP / 32); i += kHeadThreads / 32) {
+      const int o = i / (kTP / 32), w = i % (kTP / 32), p = 32 * w + lane;
+      const uint32_t bits = __ballot_sync(0xffffffffu, S.u[o][2 * p] > S.u[o][2 * p + 1]);
+      if (lane == 0) GM.selA[o][w] = bits;
+    }
+  }
   // S9 max across the pair -> v[o][p]
   for (int e = tid; e < 128 * kTP; e += kHeadThreads) {
     const int o = e / kTP, p = e % kTP;
@@ -212,8 +326,11 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_tile_kernel(DevParams P,
   }
   __syncthreads();
   dense<kTP, 128, true>(P.p1T, P.pb1, 128, S.v, S.u, S.w);
+  if (kGrad) record_mask<kTP>(S.u, GM.pair[0]);
   dense<kTP, 128, true>(P.p2T, P.pb2, 128, S.u, S.v, S.w);
+  if (kGrad) record_mask<kTP>(S.v, GM.pair[1]);
   dense<kTP, 128, true>(P.p3T, P.pb3, 128, S.v, S.u, S.w);
+  if (kGrad) record_mask<kTP>(S.u, GM.pair[2]);
   // output unit: 4 threads per pair, 32 features each, then combined
   {
     const int p = tid >> 2, part = tid & 3;
@@ -237,6 +354,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_tile_kernel(DevParams P,
       if (logits) logits[i] = lg;
     }
   }
+  if constexpr (kGrad) head_tile_backward(P, b, S, GM, i0, npairs, grad);
 }
 
 // ------------------------------------------------------------------ generic fallback (any H, F)
@@ -367,16 +485,24 @@ __global__ void __launch_bounds__(128) head_kernel(DevParams P, Batch b, float* 
 }  // namespace
 
 cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_t* labels, float* logits, float* emb,
-                        cudaStream_t st) {
+                        float* grad, cudaStream_t st) {
   if (b.B == 0) return cudaSuccess;
   if (P.H == 256 && P.F == 64) {
+    const unsigned grid = (unsigned)((b.B + kTP - 1) / kTP);
+    if (grad) {
+      static const cudaError_t attr = cudaFuncSetAttribute(
+          head_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeadGradSmem));
+      if (attr != cudaSuccess) return attr;
+      head_tile_kernel<true><<<grid, kHeadThreads, sizeof(HeadGradSmem), st>>>(P, b, probs, labels, logits, emb, grad);
+      return cudaGetLastError();
+    }
     static const cudaError_t attr =
-        cudaFuncSetAttribute(head_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeadSmem));
+        cudaFuncSetAttribute(head_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeadSmem));
     if (attr != cudaSuccess) return attr;
-    head_tile_kernel<<<(unsigned)((b.B + kTP - 1) / kTP), kHeadThreads, sizeof(HeadSmem), st>>>(P, b, probs, labels,
-                                                                                                logits, emb);
+    head_tile_kernel<false><<<grid, kHeadThreads, sizeof(HeadSmem), st>>>(P, b, probs, labels, logits, emb, nullptr);
     return cudaGetLastError();
   }
+  if (grad) return cudaErrorNotSupported;  // the pose gradient is built for H = 256, F = 64
   const size_t sm = sizeof(float) * (size_t)(256 + 128 + P.F + 7) * LD;
   static const cudaError_t attr = cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        (int)(sizeof(float) * (256 + 128 + 256 + 7) * LD));

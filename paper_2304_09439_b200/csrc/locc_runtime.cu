@@ -110,7 +110,7 @@ struct locc_ctx {
   int64_t cap_B = 0;
   DevBuf trace;
   DevBuf in_pairs, in_poses, in_pairs2, in_poses2, counts, occ, offsets, scan_tmp, rows, pooled, stats;
-  DevBuf out_probs, out_labels, out_logits, out_kept, out_occ, out_masks, out_emb;
+  DevBuf out_probs, out_labels, out_logits, out_kept, out_occ, out_masks, out_emb, out_grad;
   locc_stats last{};
   int64_t timed_subs = 0;  // sub-batches whose encoder events await reading
 };
@@ -171,6 +171,17 @@ locc_status upload_params(locc_ctx* c, const float* flat) {
   push(p3.b, P);                 // 18
   push(out.W, P);                // 19
   push(out.b, 1);                // 20
+  {                              // 21: obj.l1's pose columns [7][128] (reverse mode)
+    std::vector<float> t((size_t)7 * P);
+    for (int c = 0; c < 7; ++c)
+      for (int o = 0; o < P; ++o) t[(size_t)c * P + o] = o1.W[(size_t)o * o1.i + F + c];
+    push(t.data(), t.size());
+  }
+  push(o2.W, (size_t)P * P);     // 22..26: original [out][in] layouts (reverse mode)
+  push(o3.W, (size_t)P * P);
+  push(p1.W, (size_t)P * P);
+  push(p2.W, (size_t)P * P);
+  push(p3.W, (size_t)P * P);
   const size_t bytes = img.size() * sizeof(float);
   CK(c->params.ensure(bytes));
   CK(cudaMemcpy(c->params.p, img.data(), bytes, cudaMemcpyHostToDevice));
@@ -200,13 +211,19 @@ locc_status upload_params(locc_ctx* c, const float* flat) {
   D.pb3 = d + off[18];
   D.wout = d + off[19];
   D.bout = d + off[20];
+  D.o1p = d + off[21];
+  D.o2 = d + off[22];
+  D.o3 = d + off[23];
+  D.p1 = d + off[24];
+  D.p2 = d + off[25];
+  D.p3 = d + off[26];
   D.tc_w2 = nullptr;
   D.tc_w3 = nullptr;
   c->has_weights = true;
   return LOCC_OK;
 }
 
-locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks) {
+locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks, bool need_grad) {
   const int K = c->T.K;
   const int64_t G = 2 * B;
   if (B > c->cap_B) {
@@ -230,6 +247,7 @@ locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks) {
   }
   CK(c->stats.ensure(sizeof(DevStats)));
   if (need_masks) CK(c->out_masks.ensure(sizeof(uint32_t) * (size_t)G * ((K + 31) / 32)));
+  if (need_grad) CK(c->out_grad.ensure(sizeof(float) * (size_t)14 * c->cap_B));
   return LOCC_OK;
 }
 
@@ -260,7 +278,7 @@ locc_status read_timing(locc_ctx* c) {
 
 locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
                       uint8_t* labels, float* logits, int32_t* kept, int32_t* occ, uint32_t* masks, float* emb,
-                      void* stream) {
+                      float* grad, void* stream) {
   if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
   if (N < 0) return fail(LOCC_E_INVALID_ARG, "N < 0");
   if (!c->has_weights || !c->has_shapes) return fail(LOCC_E_STATE, "weights and shapes must be set before a query");
@@ -271,7 +289,9 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
   if (!pairs || !poses || !probs) return fail(LOCC_E_INVALID_ARG, "pairs, poses and probs must be non-null");
   CK(cudaSetDevice(c->device));
   const bool dev = is_device_ptr(pairs);
-  const void* all[] = {poses, probs, labels, logits, kept, occ, masks, emb};
+  if (grad && (c->cfg.H != 256 || c->cfg.F != 64))
+    return fail(LOCC_E_INVALID_ARG, "the pose gradient is built for H = 256, F = 64");
+  const void* all[] = {poses, probs, labels, logits, kept, occ, masks, emb, grad};
   for (const void* p : all)
     if (p && is_device_ptr(p) != dev)
       return fail(LOCC_E_INVALID_ARG, "all buffers of one call must be host or all device memory");
@@ -280,7 +300,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   const bool sync = !dev || !stream;
   const int64_t Bcap = std::min<int64_t>(N, batch_cap(c));
-  locc_status s = ensure_scratch(c, Bcap, masks != nullptr);
+  locc_status s = ensure_scratch(c, Bcap, masks != nullptr, grad != nullptr);
   if (s != LOCC_OK) return s;
   const int K = c->T.K, words = (K + 31) / 32;
   DevStats* dstats = c->stats.as<DevStats>();
@@ -332,6 +352,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     uint8_t* d_labels = labels ? (dev ? labels + i0 : c->out_labels.as<uint8_t>()) : nullptr;
     float* d_logits = logits ? (dev ? logits + i0 : c->out_logits.as<float>()) : nullptr;
     float* d_emb = emb ? (dev ? emb + (size_t)2 * i0 * c->cfg.F : c->out_emb.as<float>()) : nullptr;
+    float* d_grad = grad ? (dev ? grad + 14 * i0 : c->out_grad.as<float>()) : nullptr;
 
     CK(launch_crop_count(c->T, b, words, st));
     CK(launch_scan(b.counts, b.G, b.offsets, c->scan_tmp.as<int64_t>(), st));
@@ -365,7 +386,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       CK(launch_encoder_f32(c->P, b, st));
     }
     if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs + 1], st));
-    CK(launch_head(c->P, b, d_probs, d_labels, d_logits, d_emb, st));
+    CK(launch_head(c->P, b, d_probs, d_labels, d_logits, d_emb, d_grad, st));
     launches += 7;
     if (!dev) CK(cudaEventRecord(c->ev_free[subs & 1], st));  // the kernels are done with the inputs
     ++subs;
@@ -381,6 +402,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       if (emb)
         CK(cudaMemcpyAsync(emb + (size_t)2 * i0 * c->cfg.F, d_emb, sizeof(float) * (size_t)2 * B * c->cfg.F,
                            cudaMemcpyDeviceToHost, st));
+      if (grad) CK(cudaMemcpyAsync(grad + 14 * i0, d_grad, sizeof(float) * 14 * B, cudaMemcpyDeviceToHost, st));
     } else {
       if (kept && b.counts != kept + 2 * i0)
         CK(cudaMemcpyAsync(kept + 2 * i0, b.counts, sizeof(int32_t) * 2 * B, cudaMemcpyDeviceToDevice, st));
@@ -621,13 +643,19 @@ locc_status locc_set_shapes(locc_ctx* c, const float* points, int32_t S, int32_t
 
 locc_status locc_query(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
                        uint8_t* labels, float* logits, void* stream) {
-  return run_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, stream);
+  return run_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
 }
 
 locc_status locc_query_debug(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
                              uint8_t* labels, float* logits, int32_t* kept, int32_t* occ, uint32_t* masks,
                              float* emb, void* stream) {
-  return run_query(c, pairs, poses, N, probs, labels, logits, kept, occ, masks, emb, stream);
+  return run_query(c, pairs, poses, N, probs, labels, logits, kept, occ, masks, emb, nullptr, stream);
+}
+
+locc_status locc_query_grad(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
+                            uint8_t* labels, float* logits, float* grad, void* stream) {
+  if (N > 0 && !grad) return fail(LOCC_E_INVALID_ARG, "grad must be non-null");
+  return run_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, grad, stream);
 }
 
 }  // extern "C"

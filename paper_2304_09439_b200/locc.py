@@ -18,7 +18,7 @@ LOCC_PREC_FP32 = 0
 LOCC_PREC_BF16 = 1
 
 EXPORTS = ("locc_create", "locc_load_weights", "locc_load_weights_mem", "locc_set_shapes", "locc_query",
-           "locc_query_debug", "locc_set_precision", "locc_set_timing", "locc_get_stats", "locc_destroy",
+           "locc_query_debug", "locc_query_grad", "locc_set_precision", "locc_set_timing", "locc_get_stats", "locc_destroy",
            "locc_status_string", "locc_last_error", "locc_version")
 
 
@@ -59,6 +59,7 @@ def lib():
         L.locc_set_shapes.argtypes = [vp, vp, i32, i32]
         L.locc_query.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp]
         L.locc_query_debug.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.locc_query_grad.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp]
         L.locc_set_precision.argtypes = [vp, i32]
         L.locc_set_timing.argtypes = [vp, i32]
         L.locc_get_stats.argtypes = [vp, C.POINTER(Stats)]
@@ -165,6 +166,24 @@ class Locc:
         logits = np.zeros(N, np.float32)
         self.query_into(pairs, poses, probs, labels, logits)
         return probs, labels, logits
+
+    def query_grad_into(self, pairs, poses, probs, grad, labels=None, logits=None, stream=None):
+        """locc_query_grad on caller buffers: grad [N][14] = d logit / d (q_A, t_A, q_B, t_B)."""
+        N = int(pairs.shape[0])
+        _check(lib().locc_query_grad(self._h, _ptr(pairs), _ptr(poses), N, _ptr(probs), _ptr(labels), _ptr(logits),
+                                     _ptr(grad), stream))
+
+    def query_grad(self, pairs, poses):
+        """Host form of locc_query_grad -> (probs, labels, logits, grad [N][14])."""
+        pairs = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+        poses = np.ascontiguousarray(poses, np.float32).reshape(-1, 2, 7)
+        N = pairs.shape[0]
+        probs = np.zeros(N, np.float32)
+        labels = np.zeros(N, np.uint8)
+        logits = np.zeros(N, np.float32)
+        grad = np.zeros((N, 14), np.float32)
+        self.query_grad_into(pairs, poses, probs, grad, labels, logits)
+        return probs, labels, logits, grad
 
     def query_debug(self, pairs, poses):
         """Host form of locc_query_debug -> dict of every output and intermediate."""
