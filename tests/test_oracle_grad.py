@@ -34,7 +34,7 @@ def test_head_logit_matches_query(oracle_mod):
     pairs, poses = ls.make_pairs_poses(pts, 24, s=0.5, seed=41)
     w = spread()
     r = oracle_mod.query(w, pts, pairs, poses)
-    lg, _ = oracle_mod.query_grad(w, pts, pairs, poses)
+    lg, _, _ = oracle_mod.query_grad(w, pts, pairs, poses)
     n = 0
     for i in range(len(pairs)):
         if r["kept"][i].sum() == 0:
@@ -105,10 +105,11 @@ def test_query_grad_short_circuit_and_per_pair(oracle_mod):
     pairs, poses = ls.make_pairs_poses(pts, 30, s=0.6, seed=44)
     w = spread()
     r = oracle_mod.query(w, pts, pairs, poses)
-    lg, g = oracle_mod.query_grad(w, pts, pairs, poses)
+    lg, g, mg = oracle_mod.query_grad(w, pts, pairs, poses)
     sc = r["kept"].sum(1) == 0
     assert sc.any() and (~sc).any()
-    assert np.all(g[sc] == 0) and np.all(np.isneginf(lg[sc]))
+    assert np.all(g[sc] == 0) and np.all(np.isneginf(lg[sc])) and np.all(np.isinf(mg[sc]))
+    assert np.all(mg[~sc] >= 0) and np.all(np.isfinite(mg[~sc]))
     for i in np.nonzero(~sc)[0]:
         _, gi = oracle_mod.head_grad(w, r["emb"][i, 0], r["emb"][i, 1], poses[i, 0].astype(np.float64),
                                      poses[i, 1].astype(np.float64))
