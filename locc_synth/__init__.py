@@ -232,6 +232,45 @@ def make_weights(kind: str = "spread", H: int = 256, F: int = 64, seed: int = 3,
     return w
 
 
+def unet_layout(H: int = 256, F: int = 64, C: int = 128):
+    """NEXT-1 U-Net parameter order (Q30): (name, shape).  3D kernels [out][in][27]."""
+    L = [("unet.c1", C, H), ("unet.c2", C, C), ("unet.c3", C, C), ("unet.c4", C, C),
+         ("unet.d4", C, C), ("unet.d3", C, 2 * C), ("unet.d2", C, 2 * C), ("unet.d1", C, 2 * C)]
+    out = []
+    for name, o, i in L:
+        out.append((name + ".W", (o, i, 27)))
+        out.append((name + ".b", (o,)))
+    out.append(("unet.proj.W", (F, 2 * C)))
+    out.append(("unet.proj.b", (F,)))
+    return out
+
+
+def make_unet_weights(kind: str = "spread", H: int = 256, F: int = 64, seed: int = 4):
+    """Seeded U-Net weights: He-uniform 3D kernels (fan_in = 27 Cin), Xavier-uniform projection;
+    biases 0 ('spread') or U(+-1/sqrt(fan_in)) ('he'); 'zero' = all 0."""
+    rng = np.random.default_rng(seed)
+    w = {}
+    for name, shape in unet_layout(H, F):
+        if name.endswith(".W"):
+            if name == "unet.proj.W":
+                bound = np.sqrt(6.0 / (shape[0] + shape[1]))
+            else:
+                bound = np.sqrt(6.0 / (shape[1] * 27))
+            w[name] = rng.uniform(-bound, bound, size=shape).astype(np.float32)
+        else:
+            fan_in = int(np.prod(w[name[:-2] + ".W"].shape[1:]))
+            b = rng.uniform(-1, 1, size=shape) / np.sqrt(fan_in)
+            w[name] = (b if kind == "he" else np.zeros(shape)).astype(np.float32)
+    if kind == "zero":
+        for k in w:
+            w[k] = np.zeros_like(w[k])
+    return w
+
+
+def flatten_unet(w, H: int = 256, F: int = 64):
+    return np.concatenate([np.asarray(w[name], np.float32).reshape(-1) for name, _ in unet_layout(H, F)])
+
+
 def flatten_weights(w, H: int = 256, F: int = 64):
     """Concatenate in canonical order -> 1-D float32."""
     parts = []

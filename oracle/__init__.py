@@ -43,6 +43,12 @@ def lib():
         L.oracle_head_grad.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, vp, vp, vp, vp, vp]
         L.oracle_query_grad.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, C.c_int32, C.c_int32, vp, vp, C.c_int64,
                                         vp, vp, vp]
+        L.oracle_unet_n_params.argtypes = [C.c_int32, C.c_int32]
+        L.oracle_unet_n_params.restype = C.c_int64
+        L.oracle_conv3d.argtypes = [vp, C.c_int32, C.c_int32, vp, vp, C.c_int32, C.c_int32, C.c_int32, vp]
+        L.oracle_encode_grid.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, C.c_size_t, vp, C.c_int32, vp, vp]
+        L.oracle_query_cells.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, C.c_size_t, vp, C.c_int32, C.c_int32,
+                                         vp, vp, C.c_int64] + [vp] * 7
         L.oracle_load_weights.argtypes = [C.c_char_p, vp, C.c_size_t, vp, vp, vp]
         L.oracle_load_weights.restype = C.c_int64
         L.oracle_n_params.argtypes = [C.c_int32, C.c_int32]
@@ -139,6 +145,63 @@ def query_grad(weights_flat, points, pairs, poses, M=6, H=256, F=64, bf16_emul=F
     if rc:
         raise ValueError(f"oracle_query_grad: {rc}")
     return lg, g, mg
+
+
+# ----------------------------------------------------------------------------- NEXT-1 (encode once)
+def unet_n_params(H=256, F=64):
+    return int(lib().oracle_unet_n_params(H, F))
+
+
+def conv3d(x, W, b=None, pad=0, transposed=False):
+    """One 3x3x3 layer in fp64: x [D,D,D,Cin] (z, y, x, channel), W [Cout][Cin][27] -> y grid."""
+    x = np.ascontiguousarray(x, np.float64)
+    W = np.ascontiguousarray(W, np.float64)
+    D, Cin = x.shape[0], x.shape[3]
+    Cout = W.shape[0]
+    Do = D + 2 - 2 * pad if transposed else D + 2 * pad - 2
+    y = np.zeros((Do, Do, Do, Cout))
+    bb = None if b is None else np.ascontiguousarray(b, np.float64)
+    rc = lib().oracle_conv3d(_p(x), D, Cin, _p(W), _p(bb), Cout, pad, 1 if transposed else 0, _p(y))
+    if rc:
+        raise ValueError(f"oracle_conv3d: {rc}")
+    return y
+
+
+def encode_grid(weights_flat, unet_flat, points_k3, M=6, H=256, F=64):
+    """Encode one shape -> (G [M^3][H] cell-max grid, E [M^3][F] embedding grid), fp64."""
+    w = np.ascontiguousarray(weights_flat, np.float32)
+    u = np.ascontiguousarray(unet_flat, np.float32)
+    p = np.ascontiguousarray(points_k3, np.float32)
+    G = np.zeros((M ** 3, H))
+    E = np.zeros((M ** 3, F))
+    cfg = _Cfg(M, H, F, 0, 1)
+    rc = lib().oracle_encode_grid(C.byref(cfg), _p(w), w.size, _p(u), u.size, _p(p), p.shape[0], _p(G), _p(E))
+    if rc:
+        raise ValueError(f"oracle_encode_grid: {rc}")
+    return G, E
+
+
+def query_cells(weights_flat, unet_flat, points, pairs, poses, M=6, H=256, F=64, n_threads=0):
+    """Encode-once query: dict with probs, labels, logits, nsel [N][2], cells [N][2][ceil(M^3/32)],
+    emb [N][2][F] and grids [S][M^3][F] (zeros for unreferenced shapes)."""
+    w = np.ascontiguousarray(weights_flat, np.float32)
+    u = np.ascontiguousarray(unet_flat, np.float32)
+    pts = np.ascontiguousarray(points, np.float32)
+    pr = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+    po = np.ascontiguousarray(poses, np.float32).reshape(-1, 2, 7)
+    S, K = pts.shape[0], pts.shape[1]
+    N = pr.shape[0]
+    words = (M ** 3 + 31) // 32
+    out = dict(probs=np.zeros(N), labels=np.zeros(N, np.uint8), logits=np.zeros(N),
+               nsel=np.zeros((N, 2), np.int32), cells=np.zeros((N, 2, words), np.uint32),
+               emb=np.zeros((N, 2, F)), grids=np.zeros((S, M ** 3, F)))
+    cfg = _Cfg(M, H, F, 0, n_threads)
+    rc = lib().oracle_query_cells(C.byref(cfg), _p(w), w.size, _p(u), u.size, _p(pts), S, K, _p(pr), _p(po), N,
+                                  _p(out["probs"]), _p(out["labels"]), _p(out["logits"]), _p(out["nsel"]),
+                                  _p(out["cells"]), _p(out["emb"]), _p(out["grids"]))
+    if rc:
+        raise ValueError(f"oracle_query_cells: {rc}")
+    return out
 
 
 def load_weights(manifest):

@@ -429,6 +429,188 @@ double head_grad(const Params& P, const double* eA, const double* eB, int F, con
   return logit;
 }
 
+// ------------------------------------------------------------------ NEXT-1: encode-once LOCC
+// The paper's own inference design (readings Q27-Q30): each shape
+// is encoded ONCE into an M x M x M x F embedding grid; a query only selects cells and pools them.
+//
+// Grids are channel-last, position index x + D (y + D z) (the cell-id order of O0).  3D kernels
+// W[o][i][k], k = kx + 3 (ky + 3 kz) (the same order), 3 x 3 x 3, stride 1.
+
+// conv3d ("3D convolution layers ... filter of size (3,3,3)"): cross-correlation with zero
+// padding p: y[q][o] = b[o] + sum_k sum_i W[o][i][k] x[q + k - p][i], q in [0, D + 2p - 2)^3.
+void conv3d(const double* x, int D, int Cin, const double* W, const double* b, int Cout, int p, double* y) {
+  const int Do = D + 2 * p - 2;
+  for (int qz = 0; qz < Do; ++qz)
+    for (int qy = 0; qy < Do; ++qy)
+      for (int qx = 0; qx < Do; ++qx) {
+        double* yq = y + ((int64_t)(qz * Do + qy) * Do + qx) * Cout;
+        for (int o = 0; o < Cout; ++o) {
+          double acc = b ? b[o] : 0.0;
+          for (int k = 0; k < 27; ++k) {
+            const int iz = qz + k / 9 - p, iy = qy + (k / 3) % 3 - p, ix = qx + k % 3 - p;
+            if (iz < 0 || iy < 0 || ix < 0 || iz >= D || iy >= D || ix >= D) continue;
+            const double* xi = x + ((int64_t)(iz * D + iy) * D + ix) * Cin;
+            for (int i = 0; i < Cin; ++i) acc += W[((int64_t)o * Cin + i) * 27 + k] * xi[i];
+          }
+          yq[o] = acc;
+        }
+      }
+}
+
+// deconv3d ("deconvolution layers with the same parameters in reverse order"): the transposed
+// convolution, by its definition — every input position q scatters W[o][i][k] x[q][i] to output
+// position q + k - p; output size D + 2 - 2p (p = 1: same size; p = 0: undoes a valid conv).
+void deconv3d(const double* x, int D, int Cin, const double* W, const double* b, int Cout, int p, double* y) {
+  const int Do = D + 2 - 2 * p;
+  for (int64_t q = 0; q < (int64_t)Do * Do * Do; ++q)
+    for (int o = 0; o < Cout; ++o) y[q * Cout + o] = b ? b[o] : 0.0;
+  for (int iz = 0; iz < D; ++iz)
+    for (int iy = 0; iy < D; ++iy)
+      for (int ix = 0; ix < D; ++ix) {
+        const double* xi = x + ((int64_t)(iz * D + iy) * D + ix) * Cin;
+        for (int k = 0; k < 27; ++k) {
+          const int qz = iz + k / 9 - p, qy = iy + (k / 3) % 3 - p, qx = ix + k % 3 - p;
+          if (qz < 0 || qy < 0 || qx < 0 || qz >= Do || qy >= Do || qx >= Do) continue;
+          double* yq = y + ((int64_t)(qz * Do + qy) * Do + qx) * Cout;
+          for (int o = 0; o < Cout; ++o) {
+            double acc = 0.0;
+            for (int i = 0; i < Cin; ++i) acc += W[((int64_t)o * Cin + i) * 27 + k] * xi[i];
+            yq[o] += acc;
+          }
+        }
+      }
+}
+
+void relu_inplace(std::vector<double>& v) {
+  for (double& a : v) a = a > 0.0 ? a : 0.0;
+}
+
+// [a ; b] per position ("skip connection with concatenation").
+std::vector<double> concat(const std::vector<double>& a, int Ca, const std::vector<double>& b, int Cb, int64_t npos) {
+  std::vector<double> r((size_t)npos * (Ca + Cb));
+  for (int64_t q = 0; q < npos; ++q) {
+    for (int c = 0; c < Ca; ++c) r[q * (Ca + Cb) + c] = a[q * Ca + c];
+    for (int c = 0; c < Cb; ++c) r[q * (Ca + Cb) + Ca + c] = b[q * Cb + c];
+  }
+  return r;
+}
+
+constexpr int kU = 128;  // U-Net channels ("# channels of 3D CNN ... 128")
+
+// Canonical U-Net parameter order (Q30): c1 [128][H][27], c2..c4 [128][128][27], d4 [128][128][27],
+// d3, d2, d1 [128][256][27], each W then b [128]; proj W [F][256], b [F].
+int64_t unet_n_params(int H, int F) {
+  return (int64_t)kU * 27 * (H + 3 * kU + kU + 3 * 2 * kU) + 8 * kU + (int64_t)F * 2 * kU + F;
+}
+
+struct UNetW {
+  std::vector<double> W[8], b[8], pW, pb;  // 0..3 = c1..c4, 4..7 = d4, d3, d2, d1
+};
+
+UNetW bind_unet(const float* u, int H, int F) {
+  UNetW U;
+  const int cin[8] = {H, kU, kU, kU, kU, 2 * kU, 2 * kU, 2 * kU};
+  for (int l = 0; l < 8; ++l) {
+    const int64_t n = (int64_t)kU * cin[l] * 27;
+    U.W[l].assign(u, u + n);
+    u += n;
+    U.b[l].assign(u, u + kU);
+    u += kU;
+  }
+  U.pW.assign(u, u + (int64_t)F * 2 * kU);
+  u += (int64_t)F * 2 * kU;
+  U.pb.assign(u, u + F);
+  return U;
+}
+
+// Q27: every point of the shape through the point MLP (the same 3 layers as O6), cell-
+// wise max ("cell-wise max-pooling"); an empty cell is 0.  G: [M^3][H].
+void grid_maxpool(const Params& P, const EncW& EW, const float* pts, int K, const ShapeInfo& s, int M, int H,
+                  std::vector<double>& G) {
+  const int ncell = M * M * M;
+  G.assign((size_t)ncell * H, 0.0);
+  std::vector<uint8_t> occ(ncell, 0);
+  std::vector<double> x(3), h1(H), h2(H), h3(H);
+  for (int k = 0; k < K; ++k) {
+    for (int d = 0; d < 3; ++d) x[d] = pts[3 * k + d];
+    dense(P.enc1, EW.w1.data(), x.data(), h1.data(), true, false);
+    dense(P.enc2, EW.w2.data(), h1.data(), h2.data(), true, false);
+    dense(P.enc3, EW.w3.data(), h2.data(), h3.data(), true, false);
+    double* gc = &G[(size_t)s.cell[k] * H];
+    if (!occ[s.cell[k]]) {
+      occ[s.cell[k]] = 1;
+      for (int j = 0; j < H; ++j) gc[j] = h3[j];
+    } else {
+      for (int j = 0; j < H; ++j) gc[j] = h3[j] > gc[j] ? h3[j] : gc[j];
+    }
+  }
+}
+
+// Q28: the 3D U-Net: 4 conv (128 ch, 3^3, ReLU; the first valid M^3 -> (M-2)^3,
+// the rest same), global average of the last conv's features, 4 deconv in reverse order with
+// concatenation skips (d4 <- c4; d3 <- [d4; c3]; d2 <- [d3; c2]; d1 <- [d2; c1], the last one the
+// transposed valid conv back to M^3), the global feature tiled and concatenated, one linear layer to F
+// (P:422).  E: [M^3][F].
+void unet(const UNetW& U, const std::vector<double>& G, int M, int H, int F, std::vector<double>& E) {
+  const int D = M - 2;
+  const int64_t n4 = (int64_t)D * D * D, n6 = (int64_t)M * M * M;
+  std::vector<double> c1(n4 * kU), c2(n4 * kU), c3(n4 * kU), c4(n4 * kU), d4(n4 * kU), d3(n4 * kU), d2(n4 * kU),
+      d1(n6 * kU);
+  conv3d(G.data(), M, H, U.W[0].data(), U.b[0].data(), kU, 0, c1.data());
+  relu_inplace(c1);
+  conv3d(c1.data(), D, kU, U.W[1].data(), U.b[1].data(), kU, 1, c2.data());
+  relu_inplace(c2);
+  conv3d(c2.data(), D, kU, U.W[2].data(), U.b[2].data(), kU, 1, c3.data());
+  relu_inplace(c3);
+  conv3d(c3.data(), D, kU, U.W[3].data(), U.b[3].data(), kU, 1, c4.data());
+  relu_inplace(c4);
+  std::vector<double> g(kU, 0.0);
+  for (int64_t q = 0; q < n4; ++q)
+    for (int c = 0; c < kU; ++c) g[c] += c4[q * kU + c];
+  for (int c = 0; c < kU; ++c) g[c] /= (double)n4;
+  deconv3d(c4.data(), D, kU, U.W[4].data(), U.b[4].data(), kU, 1, d4.data());
+  relu_inplace(d4);
+  std::vector<double> x = concat(d4, kU, c3, kU, n4);
+  deconv3d(x.data(), D, 2 * kU, U.W[5].data(), U.b[5].data(), kU, 1, d3.data());
+  relu_inplace(d3);
+  x = concat(d3, kU, c2, kU, n4);
+  deconv3d(x.data(), D, 2 * kU, U.W[6].data(), U.b[6].data(), kU, 1, d2.data());
+  relu_inplace(d2);
+  x = concat(d2, kU, c1, kU, n4);
+  deconv3d(x.data(), D, 2 * kU, U.W[7].data(), U.b[7].data(), kU, 0, d1.data());
+  relu_inplace(d1);
+  E.assign((size_t)n6 * F, 0.0);
+  for (int64_t c = 0; c < n6; ++c)
+    for (int f = 0; f < F; ++f) {
+      double acc = 0.0;
+      for (int j = 0; j < kU; ++j) acc += U.pW[(int64_t)f * 2 * kU + j] * d1[c * kU + j];
+      for (int j = 0; j < kU; ++j) acc += U.pW[(int64_t)f * 2 * kU + kU + j] * g[j];
+      E[c * F + f] = acc + U.pb[f];
+    }
+}
+
+// Q29: cell centre of cell (ix, iy, iz) in the shape's own frame, fp64 rounded once to fp32.
+void cell_centre(const ShapeInfo& s, int M, int c, float out[3]) {
+  const int i[3] = {c % M, (c / M) % M, c / (M * M)};
+  for (int d = 0; d < 3; ++d) {
+    const double ext = (double)s.hi[d] - (double)s.lo[d];
+    out[d] = (float)((double)s.lo[d] + (((double)i[d] + 0.5) * ext) / (double)M);
+  }
+}
+
+// Q29: cell c of this object is selected iff its centre, moved into the other object's
+// frame by (R, t), lies within this object's own cell half-diagonal (the "margin ... distance from the
+// center point to a vertex of a cell") of the other's AABB — O4's fp32 test on the cell centre.
+int select_cells(const ShapeInfo& self, int M, const float R[9], const float t[3], const ShapeInfo& other,
+                 std::vector<uint8_t>& sel) {
+  const int ncell = M * M * M;
+  std::vector<float> ctr((size_t)3 * ncell);
+  for (int c = 0; c < ncell; ++c) cell_centre(self, M, c, &ctr[3 * c]);
+  ShapeInfo o = other;  // other's AABB with this object's margin
+  o.eps2 = self.eps2;
+  return crop(ctr.data(), ncell, R, t, o, sel);
+}
+
 bool finite_n(const float* p, int64_t n) {
   for (int64_t i = 0; i < n; ++i)
     if (!std::isfinite(p[i])) return false;
@@ -598,6 +780,157 @@ int oracle_query_grad(const oracle_cfg* cfg, const float* weights, size_t n_weig
     head_grad(P, emb.data() + (2 * i) * F, emb.data() + (2 * i + 1) * F, F, pa, pa + 4, pb, pb + 4, g,
               margin ? margin + i : nullptr);
   }
+  return 0;
+}
+
+int64_t oracle_unet_n_params(int32_t H, int32_t F) { return unet_n_params(H, F); }
+
+int oracle_conv3d(const double* x, int32_t D, int32_t Cin, const double* W, const double* b, int32_t Cout,
+                  int32_t pad, int32_t transposed, double* y) {
+  if (!x || !W || !y || D < 1 || Cin < 1 || Cout < 1 || pad < 0 || pad > 2) return -1;
+  if (transposed)
+    deconv3d(x, D, Cin, W, b, Cout, pad, y);
+  else
+    conv3d(x, D, Cin, W, b, Cout, pad, y);
+  return 0;
+}
+
+int oracle_encode_grid(const oracle_cfg* cfg, const float* weights, size_t n_weights, const float* unet_w,
+                       size_t n_unet, const float* pts, int32_t K, double* G, double* E) {
+  if (!cfg || cfg->M < 3 || cfg->H < 1 || cfg->F < 1) return -1;
+  const int M = cfg->M, H = cfg->H, F = cfg->F;
+  if (!weights || (int64_t)n_weights != n_params(H, F)) return -3;
+  if (!unet_w || (int64_t)n_unet != unet_n_params(H, F)) return -3;
+  ShapeInfo s;
+  if (!pts || !shape_prep(pts, K, M, s)) return -2;
+  const Params P = bind_params(weights, H, F);
+  const EncW EW{widen(P.enc1, false), widen(P.enc2, false), widen(P.enc3, false), widen(P.proj, false)};
+  std::vector<double> g, e;
+  grid_maxpool(P, EW, pts, K, s, M, H, g);
+  if (G) std::memcpy(G, g.data(), sizeof(double) * g.size());
+  unet(bind_unet(unet_w, H, F), g, M, H, F, e);
+  if (E) std::memcpy(E, e.data(), sizeof(double) * e.size());
+  return 0;
+}
+
+int oracle_query_cells(const oracle_cfg* cfg, const float* weights, size_t n_weights, const float* unet_w,
+                       size_t n_unet, const float* points, int32_t S, int32_t K, const int32_t* pairs,
+                       const float* poses, int64_t N, double* probs, uint8_t* labels, double* logits,
+                       int32_t* nsel, uint32_t* cells, double* emb, double* grids) {
+  if (!cfg || cfg->M < 3 || cfg->H < 1 || cfg->F < 1 || N < 0) return -1;
+  const int M = cfg->M, H = cfg->H, F = cfg->F, ncell = M * M * M, words = (ncell + 31) / 32;
+  if (!weights || (int64_t)n_weights != n_params(H, F) || !finite_n(weights, (int64_t)n_weights)) return -3;
+  if (!unet_w || (int64_t)n_unet != unet_n_params(H, F) || !finite_n(unet_w, (int64_t)n_unet)) return -3;
+  if (!points || S < 1 || K < 1) return -2;
+  if (N > 0 && (!pairs || !poses)) return -1;
+  for (int64_t i = 0; i < 2 * N; ++i)
+    if (pairs[i] < 0 || pairs[i] >= S) return -1;
+  if (!finite_n(poses, 14 * N)) return -1;
+  for (int64_t i = 0; i < 2 * N; ++i) {
+    Quat q;
+    if (!normalise(poses + 7 * i, q)) return -1;
+  }
+  const Params P = bind_params(weights, H, F);
+  const EncW EW{widen(P.enc1, false), widen(P.enc2, false), widen(P.enc3, false), widen(P.proj, false)};
+  const UNetW U = bind_unet(unet_w, H, F);
+  std::vector<ShapeInfo> shapes(S);
+  for (int s = 0; s < S; ++s)
+    if (!shape_prep(points + (int64_t)s * K * 3, K, M, shapes[s])) return -2;
+  // encode once per referenced shape (the cached embedding of P:331)
+  std::vector<uint8_t> used(S, 0);
+  for (int64_t i = 0; i < 2 * N; ++i) used[pairs[i]] = 1;
+  std::vector<std::vector<double>> E(S);
+  int nt = cfg->n_threads > 0 ? cfg->n_threads : (int)std::thread::hardware_concurrency();
+  if (nt < 1) nt = 1;
+  {
+    std::atomic<int> next(0);
+    auto enc = [&]() {
+      std::vector<double> g;
+      for (;;) {
+        const int s = next.fetch_add(1);
+        if (s >= S) break;
+        if (!used[s]) continue;
+        grid_maxpool(P, EW, points + (int64_t)s * K * 3, K, shapes[s], M, H, g);
+        unet(U, g, M, H, F, E[s]);
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < std::min(nt, S); ++t) pool.emplace_back(enc);
+    enc();
+    for (auto& th : pool) th.join();
+  }
+  if (grids)
+    for (int s = 0; s < S; ++s)
+      if (used[s]) std::memcpy(grids + (int64_t)s * ncell * F, E[s].data(), sizeof(double) * ncell * F);
+  std::atomic<int64_t> next(0);
+  auto worker = [&]() {
+    std::vector<uint8_t> selA, selB;
+    std::vector<double> eA(F), eB(F), uA(kP), uB(kP);
+    for (;;) {
+      const int64_t i = next.fetch_add(1);
+      if (i >= N) break;
+      const int a = pairs[2 * i], b = pairs[2 * i + 1];
+      const float* pA = poses + 14 * i;
+      const float* pB = pA + 7;
+      Quat qA, qB;
+      normalise(pA, qA);
+      normalise(pB, qB);
+      float R_BA[9], t_BA[3], R_AB[9], t_AB[3];
+      relative(qA, pA + 4, qB, pB + 4, R_BA, t_BA);
+      relative(qB, pB + 4, qA, pA + 4, R_AB, t_AB);
+      const int nA = select_cells(shapes[a], M, R_BA, t_BA, shapes[b], selA);
+      const int nB = select_cells(shapes[b], M, R_AB, t_AB, shapes[a], selB);
+      if (nsel) {
+        nsel[2 * i] = nA;
+        nsel[2 * i + 1] = nB;
+      }
+      if (cells) {
+        uint32_t* mA = cells + (2 * i) * words;
+        uint32_t* mB = mA + words;
+        std::memset(mA, 0, sizeof(uint32_t) * 2 * words);
+        for (int c = 0; c < ncell; ++c) {
+          if (selA[c]) mA[c / 32] |= 1u << (c % 32);
+          if (selB[c]) mB[c / 32] |= 1u << (c % 32);
+        }
+      }
+      // P:337 "average pooling" of the selected cells' features (ascending cell order); 0 if none
+      auto pool_sel = [&](const std::vector<double>& Es, const std::vector<uint8_t>& sel, int n, double* e) {
+        for (int f = 0; f < F; ++f) e[f] = 0.0;
+        if (n == 0) return;
+        for (int c = 0; c < ncell; ++c)
+          if (sel[c])
+            for (int f = 0; f < F; ++f) e[f] += Es[(int64_t)c * F + f];
+        for (int f = 0; f < F; ++f) e[f] /= (double)n;
+      };
+      double logit, prob;
+      if (nA + nB == 0) {  // disjoint: short-circuit
+        for (int f = 0; f < F; ++f) eA[f] = eB[f] = 0.0;
+        logit = -INFINITY;
+        prob = 0.0;
+      } else {
+        pool_sel(E[a], selA, nA, eA.data());
+        pool_sel(E[b], selB, nB, eB.data());
+        object_mlp(P, eA.data(), F, qA, pA + 4, uA.data());
+        object_mlp(P, eB.data(), F, qB, pB + 4, uB.data());
+        logit = pair_head(P, uA.data(), uB.data());
+        prob = 1.0 / (1.0 + std::exp(-logit));
+      }
+      if (emb)
+        for (int f = 0; f < F; ++f) {
+          emb[(2 * i) * F + f] = eA[f];
+          emb[(2 * i + 1) * F + f] = eB[f];
+        }
+      if (probs) probs[i] = prob;
+      if (logits) logits[i] = logit;
+      if (labels) labels[i] = prob > 0.5 ? 1 : 0;
+    }
+  };
+  int nq = nt;
+  if (nq > N) nq = (int)(N > 0 ? N : 1);
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nq; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
   return 0;
 }
 

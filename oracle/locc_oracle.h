@@ -64,6 +64,31 @@ int oracle_query_grad(const oracle_cfg* cfg, const float* weights, size_t n_weig
                       int32_t S, int32_t K, const int32_t* pairs, const float* poses, int64_t N, double* logits,
                       double* grad, double* margin);
 
+/* ---- NEXT-1: encode-once LOCC (the paper's own inference design, Q27-Q30) ----
+ * U-Net parameters (canonical order): c1 [128][H][27], c2..c4 [128][128][27], d4 [128][128][27],
+ * d3, d2, d1 [128][256][27] (each W then b [128]); proj W [F][256], b [F].  Kernel index
+ * k = kx + 3 (ky + 3 kz); grids channel-last, position x + D (y + D z). */
+int64_t oracle_unet_n_params(int32_t H, int32_t F);
+
+/* One 3x3x3 stride-1 layer in fp64 (b nullable): transposed = 0: cross-correlation with zero padding
+ * pad, y [(D+2pad-2)^3][Cout]; transposed = 1: the transposed convolution (scatter definition),
+ * y [(D+2-2pad)^3][Cout].  W [Cout][Cin][27]. */
+int oracle_conv3d(const double* x, int32_t D, int32_t Cin, const double* W, const double* b, int32_t Cout,
+                  int32_t pad, int32_t transposed, double* y);
+
+/* Encode one shape: G [M^3][H] cell-wise max of the point MLP over all K points (nullable), E [M^3][F]
+ * the embedding grid (nullable).  M >= 3. */
+int oracle_encode_grid(const oracle_cfg* cfg, const float* weights, size_t n_weights, const float* unet_w,
+                       size_t n_unet, const float* pts, int32_t K, double* G, double* E);
+
+/* Query through the cached grids: nsel [N][2] selected cells, cells [N][2][ceil(M^3/32)] selection
+ * bits, emb [N][2][F] pooled embeddings, grids [S][M^3][F] (only referenced shapes written); all
+ * nullable.  Short-circuit when neither side selects a cell. */
+int oracle_query_cells(const oracle_cfg* cfg, const float* weights, size_t n_weights, const float* unet_w,
+                       size_t n_unet, const float* points, int32_t S, int32_t K, const int32_t* pairs,
+                       const float* poses, int64_t N, double* probs, uint8_t* labels, double* logits,
+                       int32_t* nsel, uint32_t* cells, double* emb, double* grids);
+
 /* Parse a weight manifest + .bin (format in include/locc.h) into `out` (canonical order).
  * Returns the float count, or a negative code; writes M, H, F. */
 int64_t oracle_load_weights(const char* manifest, float* out, size_t cap, int32_t* M, int32_t* H,
