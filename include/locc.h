@@ -138,6 +138,42 @@ locc_status locc_query_debug(locc_ctx* ctx, const int32_t* pairs, const float* p
 locc_status locc_query_grad(locc_ctx* ctx, const int32_t* pairs, const float* poses, int64_t N,
                             float* probs, uint8_t* labels, float* logits, float* grad, void* stream);
 
+/* ---- Encode-once mode: the paper's own inference design ----
+ * every shape is encoded ONCE into an M x M x M x F embedding grid
+ * (point MLP over all K points -> cell-wise max -> 3D U-Net -> linear), cached on the device; a query
+ * transforms the M^3 cell centres of each object into the other's frame, selects the cells within
+ * the own cell's half diagonal (the "margin ... distance from the center point to a vertex of a
+ * cell") of the other AABB, average-pools the selected embeddings and runs the same
+ * predictor.  Query cost is independent of K.  fp32 throughout (CUDA cores); readings
+ * Q27-Q30 in DESIGN.md.  Requires 3 <= M <= 8, H = 256, F = 64.
+ *
+ * U-Net parameters, canonical order (each W then b [128]; kernels [out][in][27], tap k = kx + 3 (ky
+ * + 3 kz)): c1 [128][H][27], c2, c3, c4 [128][128][27], d4 [128][128][27], d3, d2, d1 [128][256][27];
+ * then proj W [F][256], b [F].  Count: locc_unet_n_params(H, F). */
+int64_t locc_unet_n_params(int32_t H, int32_t F);
+
+/* Load the U-Net parameters (host array of n_floats fp32, canonical order above).
+ * Errors: INVALID_ARG (null), WEIGHTS (count, non-finite), CUDA, OOM. */
+locc_status locc_load_unet_weights_mem(locc_ctx* ctx, const float* flat, size_t n_floats);
+
+/* Encode every shape of the current table and cache the grids on the device (synchronous).  Must be
+ * re-run after locc_set_shapes / locc_load_weights / locc_load_unet_weights_mem.
+ * Errors: STATE (weights, U-Net weights or shapes missing), INVALID_ARG (M, H, F), CUDA, OOM. */
+locc_status locc_encode_shapes(locc_ctx* ctx);
+
+/* Copy the cached grids to out float32 [S][M^3][F] (host or device; nullable) and report the device
+ * time of the last locc_encode_shapes in *encode_ms (nullable).  Errors: STATE (nothing encoded). */
+locc_status locc_get_cell_embeddings(locc_ctx* ctx, float* out, double* encode_ms);
+
+/* Batched query through the cached grids.  Same inputs, outputs, residency, stream and error rules as
+ * locc_query, plus nullable debug outputs: nsel int32 [N][2] selected cells per side, cells uint32
+ * [N][2][ceil(M^3/32)] (bit c of word c/32 = cell c = x + M (y + M z) selected), emb float32 [N][2][F]
+ * pooled embeddings (0 for a side with no cell).  Short-circuit (prob 0, label 0, logit -inf) when
+ * neither side selects a cell.  Errors: as locc_query; STATE if the shapes are not encoded. */
+locc_status locc_query_cells(locc_ctx* ctx, const int32_t* pairs, const float* poses, int64_t N,
+                             float* probs, uint8_t* labels, float* logits, int32_t* nsel, uint32_t* cells,
+                             float* emb, void* stream);
+
 /* Switch the encoder precision of an existing context (LOCC_PREC_FP32 / LOCC_PREC_BF16). */
 locc_status locc_set_precision(locc_ctx* ctx, int32_t precision);
 

@@ -63,6 +63,22 @@ struct DevParams {
   const void* tc_w3;
 };
 
+// NEXT-1 (encode-once) U-Net parameters, rearranged for the implicit-GEMM conv kernel:
+// Wt[l] = [27][Cin][128] (tap-major; deconv layers stored as the equivalent conv: taps flipped).
+struct UNetParams {
+  const float* Wt[8];  // 0..3 = c1..c4, 4..7 = d4, d3, d2, d1
+  const float* b[8];
+  const float* pW;     // [F][256] projection of [d1 ; g]
+  const float* pb;     // [F]
+};
+
+// Per-shape cached embedding grids of the encode-once mode.
+struct CellsTable {
+  const float* E;      // [S][M^3][F] cell embeddings
+  const float4* ctr;   // [S][M^3] cell centres in the shape's frame (x, y, z, 0)
+  int M;
+};
+
 // Device counters of one query (int64 atomics), zeroed per query.
 struct DevStats {
   unsigned long long kept_rows;
@@ -82,6 +98,7 @@ struct Batch {
   int64_t* offsets;      // [G+1] exclusive scan of counts
   float4* rows;          // [sum n] kept rows (x, y, z, flags)
   float* pooled;         // [G][H] mean over occupied cells of the cell-max features
+  const float* emb_in;   // encode-once mode: [G][F] pooled cell embeddings (the predictor's e); else null
   uint32_t* masks;       // nullable [B][2][ceil(K/32)] caller-order keep bits (debug)
   DevStats* stats;
 };
@@ -105,6 +122,13 @@ cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b
                               long long* trace = nullptr);
 cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_t* labels,
                         float* logits, float* emb, float* grad, cudaStream_t st);
+// NEXT-1 encode-once mode (kernels_cells.cu)
+cudaError_t launch_grid_encode(const DevParams& P, const ShapeTable& T, int M, float* G, cudaStream_t st);
+cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, int F, const float* G, float* act,
+                        float* E, float4* ctr, cudaStream_t st);
+size_t unet_act_floats(int S, int M);
+cudaError_t launch_cells_select(const ShapeTable& T, const CellsTable& C, const Batch& b, int F, uint32_t* cells,
+                                float* emb_out, cudaStream_t st);
 size_t scan_tmp_elems(int64_t G);
 size_t encoder_tc_smem_bytes();
 

@@ -1,0 +1,394 @@
+// kernels_cells.cu — NEXT-1: the paper's own encode-once inference (DESIGN.md
+// readings Q27-Q30).  Each shape is encoded ONCE into an M x M x M x F embedding grid (PAPER.md:331-333,
+// :421-422); a query then only selects the cells near the other object and average-pools their
+// embeddings, so its cost does not depend on K.
+//
+//   grid_encode_kernel   point MLP over all K points of a shape, cell-wise max -> G [S][M^3][H]
+//   conv3d_kernel        one 3x3x3 layer of the U-Net as an implicit GEMM (fp32 FFMA2): rows = output
+//                        positions of one shape, columns = 128 output channels, K = 27 taps x C_in
+//                        (two inputs = the concatenation skip); deconv layers run as the equivalent
+//                        conv (flipped taps, padding 2 - p) — the same sums, in another order
+//   unet_tail_kernel     global average of the last conv, [d1 ; g] -> linear F, and the
+//                        cell centres used by the selection
+//   cells_select_kernel  per (pair, side): the O4 distance test on the M^3 cell centres with the own
+//                        cell's half diagonal as margin, selection bits, mean of the selected rows of E
+// The predictor is head_tile_kernel reading e from the selection (Batch::emb_in).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "geom.cuh"
+#include "internal.h"
+#include "point_mlp.cuh"
+#include "tc_ptx.cuh"
+
+namespace locc {
+namespace {
+
+using tc::f2;
+using tc::f2_hi;
+using tc::f2_lo;
+using tc::ffma2;
+
+// ---------------------------------------------------------------- Q27: cell-max grid of every shape
+// One block per shape, thread f = feature f.  The shape's points are cell-sorted (S0), so the cell-wise
+// max is a running max closed at each cell change; ReLU(max + b3) = max of ReLU(acc + b3).  Empty cells
+// stay 0 (the buffer is cleared first).
+__global__ void __launch_bounds__(256) grid_encode_kernel(DevParams P, ShapeTable T, int M, float* __restrict__ G) {
+  extern __shared__ float4 smem4[];
+  float4* rows_s = smem4;                                // [64]
+  float* hT = reinterpret_cast<float*>(smem4 + kMlpTR);  // [H][kMlpLDH]
+  __shared__ int next_cell;
+  const int H = P.H, f = threadIdx.x, s = blockIdx.x;
+  const bool act = f < H;
+  float4 w1 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float b2 = 0.f, b3 = 0.f;
+  if (act) {
+    w1 = P.w1b[f];
+    b2 = P.b2[f];
+    b3 = P.b3[f];
+  }
+  const float4* pts = T.pts + (int64_t)s * T.K;
+  float* Gs = G + (int64_t)s * M * M * M * H;
+  float run_max = -INFINITY;
+  for (int t0 = 0; t0 < T.K; t0 += kMlpTR) {
+    const int nr = min(kMlpTR, T.K - t0);
+    if (f < kMlpTR) rows_s[f] = f < nr ? pts[t0 + f] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+    if (f == 0) next_cell = t0 + kMlpTR < T.K ? __float_as_int(pts[t0 + kMlpTR].w) : -1;
+    __syncthreads();
+    float acc[kMlpTR];
+    point_mlp_tile(P, rows_s, hT, acc, w1, b2, f, act);
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < kMlpTR; ++r) {
+        if (r < nr) {
+          run_max = fmaxf(run_max, acc[r]);
+          const int cell = __float_as_int(rows_s[r].w);
+          const int nxt = r + 1 < nr ? __float_as_int(rows_s[r + 1].w) : next_cell;
+          if (nxt != cell) {
+            Gs[(int64_t)cell * H + f] = fmaxf(run_max + b3, 0.f);
+            run_max = -INFINITY;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- Q28: U-Net layers (implicit GEMM)
+constexpr int kCvBM = 64;   // output positions per block
+constexpr int kCvBK = 32;   // input channels per staged chunk
+constexpr int kCvLDA = kCvBM + 4;
+constexpr size_t kCvSmem = sizeof(float) * 2 * kCvBK * (kCvLDA + 128);
+
+struct ConvArgs {
+  const float* x1;  // [S][Di^3][C1]
+  const float* x2;  // [S][Di^3][C2] or null (channels C1.. of the concatenation)
+  int C1, C2;
+  int Di, Do, pad;  // y[q] = sum_k x[q + k - pad] (taps k = kx + 3 (ky + 3 kz))
+  const float* Wt;  // [27][C1 + C2][128]
+  const float* bias;
+  float* y;         // [S][Do^3][128], ReLU applied
+};
+
+__global__ void __launch_bounds__(256) conv3d_kernel(ConvArgs a) {
+  extern __shared__ float4 cv_smem[];
+  float (*As)[kCvBK][kCvLDA] = reinterpret_cast<float (*)[kCvBK][kCvLDA]>(cv_smem);  // [2][ci][position]
+  float (*Bs)[kCvBK][128] = reinterpret_cast<float (*)[kCvBK][128]>(
+      reinterpret_cast<float*>(cv_smem) + 2 * kCvBK * kCvLDA);                       // [2][ci][out channel]
+  const int tid = threadIdx.x, s = blockIdx.y, q0 = blockIdx.x * kCvBM;
+  const int Cin = a.C1 + a.C2, Di3 = a.Di * a.Di * a.Di, nq = a.Do * a.Do * a.Do;
+  const int c0 = (tid & 15) * 8, r0 = (tid >> 4) * 4;  // 4 positions x 8 channels per thread
+  unsigned long long acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0ull;
+  // the two positions this thread gathers (one float4 of 4 channels each) per chunk
+  int gq[2], gc4[2], gz[2], gy[2], gx[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int e = tid + 256 * i;
+    gq[i] = e >> 3;
+    gc4[i] = e & 7;
+    const int q = q0 + gq[i];
+    gx[i] = q % a.Do;
+    gy[i] = (q / a.Do) % a.Do;
+    gz[i] = q < nq ? q / (a.Do * a.Do) : -1000;
+  }
+  const int nci = Cin / kCvBK, nchunks = 27 * nci;
+  float4 pa[2], pb[4];
+  auto fetch = [&](int ch) {
+    const int k = ch / nci, ci0 = (ch - k * nci) * kCvBK;
+    const int kx = k % 3 - a.pad, ky = (k / 3) % 3 - a.pad, kz = k / 9 - a.pad;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int ix = gx[i] + kx, iy = gy[i] + ky, iz = gz[i] + kz;
+      pa[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ix >= 0 && iy >= 0 && iz >= 0 && ix < a.Di && iy < a.Di && iz < a.Di) {
+        const int64_t pos = (int64_t)s * Di3 + (iz * a.Di + iy) * a.Di + ix;
+        const int ci = ci0 + 4 * gc4[i];
+        pa[i] = ci < a.C1 ? __ldg(reinterpret_cast<const float4*>(a.x1 + pos * a.C1 + ci))
+                          : __ldg(reinterpret_cast<const float4*>(a.x2 + pos * a.C2 + (ci - a.C1)));
+      }
+    }
+    const float* w = a.Wt + ((int64_t)k * Cin + ci0) * 128;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) pb[i] = __ldg(reinterpret_cast<const float4*>(w) + tid + 256 * i);
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int c = 4 * gc4[i];
+      As[buf][c][gq[i]] = pa[i].x;
+      As[buf][c + 1][gq[i]] = pa[i].y;
+      As[buf][c + 2][gq[i]] = pa[i].z;
+      As[buf][c + 3][gq[i]] = pa[i].w;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = tid + 256 * i;
+      *reinterpret_cast<float4*>(&Bs[buf][e >> 5][4 * (e & 31)]) = pb[i];
+    }
+  };
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nchunks) fetch(ch + 1);
+#pragma unroll 4
+    for (int kk = 0; kk < kCvBK; ++kk) {
+      const float4 xa = *reinterpret_cast<const float4*>(&As[buf][kk][r0]);
+      const float4 wa = *reinterpret_cast<const float4*>(&Bs[buf][kk][c0]);
+      const float4 wb = *reinterpret_cast<const float4*>(&Bs[buf][kk][c0 + 4]);
+      const unsigned long long w2[4] = {f2(wa.x, wa.y), f2(wa.z, wa.w), f2(wb.x, wb.y), f2(wb.z, wb.w)};
+      const float xr[4] = {xa.x, xa.y, xa.z, xa.w};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const unsigned long long x2 = f2(xr[r], xr[r]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = ffma2(x2, w2[c], acc[r][c]);
+      }
+    }
+    if (ch + 1 < nchunks) stash(buf ^ 1);
+    __syncthreads();
+  }
+  float bias[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) bias[c] = __ldg(a.bias + c0 + c);
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int q = q0 + r0 + r;
+    if (q >= nq) continue;
+    float v[8];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      v[2 * c] = fmaxf(f2_lo(acc[r][c]) + bias[2 * c], 0.f);
+      v[2 * c + 1] = fmaxf(f2_hi(acc[r][c]) + bias[2 * c + 1], 0.f);
+    }
+    float4* yo = reinterpret_cast<float4*>(a.y + ((int64_t)s * nq + q) * 128 + c0);
+    yo[0] = make_float4(v[0], v[1], v[2], v[3]);
+    yo[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
+// ---------------------------------------------------------------- Q28 tail + Q29 cell centres
+// g = mean over the (M-2)^3 positions of c4 ("average pooling ... global feature");
+// E[c] = W_P [d1[c] ; g] + b_P; cell centres lo + (i + 1/2) ext / M in fp64, rounded once.
+__global__ void __launch_bounds__(256) unet_tail_kernel(UNetParams U, ShapeTable T, int M, int F,
+                                                        const float* __restrict__ c4, const float* __restrict__ d1,
+                                                        float* __restrict__ E, float4* __restrict__ ctr) {
+  extern __shared__ float sm[];
+  float* pW = sm;                  // [F][257] (padded: thread f reads row f)
+  float* g = pW + (size_t)F * 257;  // [128]
+  float* gb = g + 128;             // [F]
+  const int s = blockIdx.x, tid = threadIdx.x, nc = M * M * M, D = M - 2, n4 = D * D * D;
+  for (int e = tid; e < F * 256; e += 256) pW[(e >> 8) * 257 + (e & 255)] = U.pW[e];
+  if (tid < 128) {
+    float acc = 0.f;
+    const float* x = c4 + (int64_t)s * n4 * 128 + tid;
+    for (int q = 0; q < n4; ++q) acc += x[(int64_t)q * 128];
+    g[tid] = __fdiv_rn(acc, (float)n4);
+  }
+  __syncthreads();
+  if (tid < F) {
+    float acc = U.pb[tid];
+    for (int j = 0; j < 128; ++j) acc = fmaf(pW[tid * 257 + 128 + j], g[j], acc);
+    gb[tid] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < nc * F; e += 256) {  // F consecutive threads share one d1 row (L1 broadcast)
+    const int c = e / F, f = e - c * F;
+    const float4* x = reinterpret_cast<const float4*>(d1 + ((int64_t)s * nc + c) * 128);
+    const float* w = pW + f * 257;
+    float a0 = 0.f, a1 = 0.f;
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+      const float4 v = __ldg(x + j);
+      a0 = fmaf(w[4 * j], v.x, a0);
+      a1 = fmaf(w[4 * j + 1], v.y, a1);
+      a0 = fmaf(w[4 * j + 2], v.z, a0);
+      a1 = fmaf(w[4 * j + 3], v.w, a1);
+    }
+    E[((int64_t)s * nc + c) * F + f] = (a0 + a1) + gb[f];
+  }
+  const float4 lo = T.lo[s], hi = T.hi[s];
+  for (int c = tid; c < nc; c += 256) {
+    const int i[3] = {c % M, (c / M) % M, c / (M * M)};
+    const float l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
+    float o[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double ext = __dsub_rn((double)h[d], (double)l[d]);
+      o[d] = __double2float_rn(__dadd_rn((double)l[d], __ddiv_rn(__dmul_rn(__dadd_rn((double)i[d], 0.5), ext), (double)M)));
+    }
+    ctr[(int64_t)s * nc + c] = make_float4(o[0], o[1], o[2], 0.f);
+  }
+}
+
+// ---------------------------------------------------------------- Q29: selection + pooled embedding
+// One warp per (pair, side) segment.  Cell c of the own shape is selected iff its centre, moved into the
+// other object's frame with the crop's fp32 transform, is within the OWN cell half-diagonal of the other
+// AABB (keep_point with eps^2 = own lo.w).  e = mean over the selected cells (ascending c, fp32) of E.
+__global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTable C, Batch b, int F,
+                                                           uint32_t* __restrict__ cells, float* __restrict__ emb) {
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= b.G) return;
+  const int nc = C.M * C.M * C.M, nw = (nc + 31) >> 5;
+  int own = 0, other = 0;
+  Xf X;
+  float* e = emb + g * F;
+  if (!segment_setup(T, b, g, own, other, X)) {
+    if (lane == 0) {
+      b.counts[g] = 0;
+      atomicAdd(&b.stats->bad_input, 1ull);
+    }
+    for (int f = lane; f < F; f += 32) e[f] = 0.f;
+    return;
+  }
+  float4 lo = T.lo[other];
+  lo.w = T.lo[own].w;  // the own cell's half-diagonal squared as the margin
+  const float4 hi = T.hi[other];
+  const float4* ctr = C.ctr + (int64_t)own * nc;
+  uint32_t words[16];
+  int n = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    words[j] = 0u;
+    if (j < nw) {
+      const int c = 32 * j + lane;
+      bool keep = false;
+      if (c < nc) {
+        const float4 p = ctr[c];
+        keep = keep_point(X, p.x, p.y, p.z, lo, hi);
+      }
+      words[j] = __ballot_sync(0xffffffffu, keep);
+      n += __popc(words[j]);
+    }
+  }
+  // mean of the selected rows: lane owns features lane, lane + 32 (F <= 64)
+  const float* Es = C.E + (int64_t)own * nc * F;
+  float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    uint32_t m = words[j];
+    while (m) {
+      const int c0 = 32 * j + __ffs(m) - 1;
+      m &= m - 1;
+      const int c1 = m ? 32 * j + __ffs(m) - 1 : -1;
+      if (m) m &= m - 1;
+      const float* r0 = Es + (int64_t)c0 * F;
+      const float v0 = lane < F ? r0[lane] : 0.f, w0 = lane + 32 < F ? r0[lane + 32] : 0.f;
+      float v1 = 0.f, w1 = 0.f;
+      if (c1 >= 0) {
+        const float* r1 = Es + (int64_t)c1 * F;
+        v1 = lane < F ? r1[lane] : 0.f;
+        w1 = lane + 32 < F ? r1[lane + 32] : 0.f;
+      }
+      a0 = __fadd_rn(a0, v0);
+      a1 = __fadd_rn(a1, w0);
+      if (c1 >= 0) {
+        a0 = __fadd_rn(a0, v1);
+        a1 = __fadd_rn(a1, w1);
+      }
+    }
+  }
+  if (lane < F) e[lane] = n ? __fdiv_rn(a0, (float)n) : 0.f;
+  if (lane + 32 < F) e[lane + 32] = n ? __fdiv_rn(a1, (float)n) : 0.f;
+  if (cells) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < nw && lane == j) cells[g * nw + j] = words[j];
+  }
+  if (lane == 0) {
+    b.counts[g] = n;
+    if (n) atomicAdd(&b.stats->nonempty_sides, 1ull);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_grid_encode(const DevParams& P, const ShapeTable& T, int M, float* G, cudaStream_t st) {
+  const size_t sm = sizeof(float4) * kMlpTR + sizeof(float) * 256 * kMlpLDH;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(grid_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (attr != cudaSuccess) return attr;
+  cudaError_t e = cudaMemsetAsync(G, 0, sizeof(float) * (size_t)T.S * M * M * M * P.H, st);
+  if (e != cudaSuccess) return e;
+  grid_encode_kernel<<<T.S, 256, sm, st>>>(P, T, M, G);
+  return cudaGetLastError();
+}
+
+// Activation scratch of the U-Net: c1..c4, d4, d3, d2 [S][(M-2)^3][128] and d1 [S][M^3][128].
+size_t unet_act_floats(int S, int M) {
+  const size_t n4 = (size_t)(M - 2) * (M - 2) * (M - 2), n6 = (size_t)M * M * M;
+  return (size_t)S * 128 * (7 * n4 + n6);
+}
+
+cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, int F, const float* G, float* act,
+                        float* E, float4* ctr, cudaStream_t st) {
+  const int D = M - 2, S = T.S;
+  const size_t n4 = (size_t)S * D * D * D * 128;
+  float* c[4];
+  for (int i = 0; i < 4; ++i) c[i] = act + i * n4;
+  float* d4 = act + 4 * n4;
+  float* d3 = act + 5 * n4;
+  float* d2 = act + 6 * n4;
+  float* d1 = act + 7 * n4;
+  auto conv = [&](const float* x1, int C1, const float* x2, int C2, int Di, int Do, int pad, int l, float* y) {
+    ConvArgs a{x1, x2, C1, C2, Di, Do, pad, U.Wt[l], U.b[l], y};
+    dim3 grid((unsigned)((Do * Do * Do + kCvBM - 1) / kCvBM), (unsigned)S);
+    conv3d_kernel<<<grid, 256, kCvSmem, st>>>(a);
+    return cudaGetLastError();
+  };
+  static const cudaError_t attr0 =
+      cudaFuncSetAttribute(conv3d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCvSmem);
+  if (attr0 != cudaSuccess) return attr0;
+  cudaError_t e;
+  if ((e = conv(G, H, nullptr, 0, M, D, 0, 0, c[0])) != cudaSuccess) return e;        // valid
+  for (int i = 1; i < 4; ++i)
+    if ((e = conv(c[i - 1], 128, nullptr, 0, D, D, 1, i, c[i])) != cudaSuccess) return e;  // same
+  // deconv (transposed, stride 1) with padding p == conv with flipped taps and padding 2 - p
+  if ((e = conv(c[3], 128, nullptr, 0, D, D, 1, 4, d4)) != cudaSuccess) return e;
+  if ((e = conv(d4, 128, c[2], 128, D, D, 1, 5, d3)) != cudaSuccess) return e;
+  if ((e = conv(d3, 128, c[1], 128, D, D, 1, 6, d2)) != cudaSuccess) return e;
+  if ((e = conv(d2, 128, c[0], 128, D, M, 2, 7, d1)) != cudaSuccess) return e;      // transposed valid
+  const size_t sm = sizeof(float) * ((size_t)F * 257 + 128 + F);
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(unet_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float) * (64 * 257 + 128 + 64)));
+  if (attr != cudaSuccess) return attr;
+  unet_tail_kernel<<<S, 256, sm, st>>>(U, T, M, F, c[3], d1, E, ctr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cells_select(const ShapeTable& T, const CellsTable& C, const Batch& b, int F, uint32_t* cells,
+                                float* emb_out, cudaStream_t st) {
+  if (b.G == 0) return cudaSuccess;
+  cells_select_kernel<<<(unsigned)((b.G * 32 + 255) / 256), 256, 0, st>>>(T, C, b, F, cells, emb_out);
+  return cudaGetLastError();
+}
+
+}  // namespace locc

@@ -14,12 +14,13 @@
 #include <stdint.h>
 
 #include "internal.h"
+#include "point_mlp.cuh"
 
 namespace locc {
 namespace {
 
-constexpr int TR = 64;        // rows per tile
-constexpr int LDH = TR + 4;   // padded row stride of the transposed activation tile
+constexpr int TR = kMlpTR;
+constexpr int LDH = kMlpLDH;
 
 __global__ void __launch_bounds__(256) encoder_f32_kernel(DevParams P, Batch b) {
   extern __shared__ float4 smem4[];
@@ -47,53 +48,8 @@ __global__ void __launch_bounds__(256) encoder_f32_kernel(DevParams P, Batch b) 
     const int nr = (int)min((int64_t)TR, r1 - t0);
     if (f < TR) rows_s[f] = f < nr ? b.rows[t0 + f] : make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
-    // layer 1 (fp32 FFMA)
-    if (act) {
-#pragma unroll
-      for (int r = 0; r < TR; r += 4) {
-        float v[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float4 p = rows_s[r + j];
-          const float h = fmaf(w1.x, p.x, fmaf(w1.y, p.y, fmaf(w1.z, p.z, w1.w)));
-          v[j] = fmaxf(h, 0.f);
-        }
-        *reinterpret_cast<float4*>(&hT[f * LDH + r]) = make_float4(v[0], v[1], v[2], v[3]);
-      }
-    }
-    __syncthreads();
     float acc[TR];
-    for (int layer = 0; layer < 2; ++layer) {
-      const float* WT = layer == 0 ? P.w2T : P.w3T;
-#pragma unroll
-      for (int r = 0; r < TR; ++r) acc[r] = 0.f;
-      if (act) {
-#pragma unroll 2
-        for (int k = 0; k < H; ++k) {
-          const float w = __ldg(WT + (int64_t)k * H + f);
-          const float4* hk = reinterpret_cast<const float4*>(&hT[k * LDH]);
-#pragma unroll
-          for (int r = 0; r < TR / 4; ++r) {
-            const float4 h = hk[r];
-            acc[4 * r + 0] = fmaf(w, h.x, acc[4 * r + 0]);
-            acc[4 * r + 1] = fmaf(w, h.y, acc[4 * r + 1]);
-            acc[4 * r + 2] = fmaf(w, h.z, acc[4 * r + 2]);
-            acc[4 * r + 3] = fmaf(w, h.w, acc[4 * r + 3]);
-          }
-        }
-      }
-      __syncthreads();
-      if (layer == 0) {
-        if (act) {
-#pragma unroll
-          for (int r = 0; r < TR; r += 4)
-            *reinterpret_cast<float4*>(&hT[f * LDH + r]) =
-                make_float4(fmaxf(acc[r] + b2, 0.f), fmaxf(acc[r + 1] + b2, 0.f), fmaxf(acc[r + 2] + b2, 0.f),
-                            fmaxf(acc[r + 3] + b2, 0.f));
-        }
-        __syncthreads();
-      }
-    }
+    point_mlp_tile(P, rows_s, hT, acc, w1, b2, f, act);
     // S6-S7: segmented cell max + occupied-cell sum over the tile's rows (row flags are uniform)
     if (act) {
 #pragma unroll

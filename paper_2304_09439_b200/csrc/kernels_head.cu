@@ -235,7 +235,7 @@ __device__ __forceinline__ void head_tile_backward(const DevParams& P, const Bat
   }
 }
 
-template <bool kGrad>
+template <bool kGrad, bool kEmbIn>
 __global__ void __launch_bounds__(kHeadThreads, 1) head_tile_kernel(DevParams P, Batch b, float* __restrict__ probs,
                                                                     uint8_t* __restrict__ labels,
                                                                     float* __restrict__ logits, float* __restrict__ emb,
@@ -267,9 +267,21 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_tile_kernel(DevParams P,
     for (int c = 0; c < 7; ++c) S.z[64 + c][s] = zq[c];
     S.z[71][s] = 0.f;
   }
+  if constexpr (kEmbIn) {
+    // encode-once mode (NEXT-1): e is the selection's pooled cell embedding, [G][64]
+    __syncthreads();  // nside
+    for (int e = tid; e < kTS * 16; e += kHeadThreads) {
+      const int s = e >> 4, j4 = e & 15;
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (S.nside[s] > 0) x = __ldg(reinterpret_cast<const float4*>(b.emb_in + (2 * i0 + s) * (int64_t)64) + j4);
+      S.z[4 * j4][s] = x.x;
+      S.z[4 * j4 + 1][s] = x.y;
+      S.z[4 * j4 + 2][s] = x.z;
+      S.z[4 * j4 + 3][s] = x.w;
+    }
+  } else {
   // S7 projection e = W_F m + b_F: the pooled rows (256 features) are staged transposed into u..v
   // (contiguous: one [256][kLD] buffer); empty and padding sides read as 0
-  {
     float (*m)[kLD] = reinterpret_cast<float (*)[kLD]>(&S.u[0][0]);  // u and v are contiguous
     __syncthreads();  // nside
 #pragma unroll 1
@@ -489,20 +501,20 @@ cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_
   if (b.B == 0) return cudaSuccess;
   if (P.H == 256 && P.F == 64) {
     const unsigned grid = (unsigned)((b.B + kTP - 1) / kTP);
-    if (grad) {
-      static const cudaError_t attr = cudaFuncSetAttribute(
-          head_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeadGradSmem));
+    auto run = [&](auto kern, size_t sm, float* g) {
+      const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (attr != cudaSuccess) return attr;
-      head_tile_kernel<true><<<grid, kHeadThreads, sizeof(HeadGradSmem), st>>>(P, b, probs, labels, logits, emb, grad);
+      kern<<<grid, kHeadThreads, sm, st>>>(P, b, probs, labels, logits, emb, g);
       return cudaGetLastError();
+    };
+    if (grad) {
+      if (b.emb_in) return cudaErrorNotSupported;
+      return run(head_tile_kernel<true, false>, sizeof(HeadGradSmem), grad);
     }
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(head_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HeadSmem));
-    if (attr != cudaSuccess) return attr;
-    head_tile_kernel<false><<<grid, kHeadThreads, sizeof(HeadSmem), st>>>(P, b, probs, labels, logits, emb, nullptr);
-    return cudaGetLastError();
+    if (b.emb_in) return run(head_tile_kernel<false, true>, sizeof(HeadSmem), nullptr);
+    return run(head_tile_kernel<false, false>, sizeof(HeadSmem), nullptr);
   }
-  if (grad) return cudaErrorNotSupported;  // the pose gradient is built for H = 256, F = 64
+  if (grad || b.emb_in) return cudaErrorNotSupported;  // the pose gradient and encode-once mode: H = 256, F = 64
   const size_t sm = sizeof(float) * (size_t)(256 + 128 + P.F + 7) * LD;
   static const cudaError_t attr = cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        (int)(sizeof(float) * (256 + 128 + 256 + 7) * LD));

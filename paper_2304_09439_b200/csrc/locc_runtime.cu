@@ -113,6 +113,12 @@ struct locc_ctx {
   DevBuf out_probs, out_labels, out_logits, out_kept, out_occ, out_masks, out_emb, out_grad;
   locc_stats last{};
   int64_t timed_subs = 0;  // sub-batches whose encoder events await reading
+  // NEXT-1 encode-once mode
+  bool has_unet = false, has_cells = false;
+  DevBuf unet_params, cells_E, cells_ctr, cells_emb;
+  UNetParams U{};
+  CellsTable cells{};
+  double encode_ms = 0.0;  // device time of the last locc_encode_shapes
 };
 
 namespace {
@@ -278,10 +284,12 @@ locc_status read_timing(locc_ctx* c) {
 
 locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
                       uint8_t* labels, float* logits, int32_t* kept, int32_t* occ, uint32_t* masks, float* emb,
-                      float* grad, void* stream) {
+                      float* grad, void* stream, bool cells = false) {
   if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
   if (N < 0) return fail(LOCC_E_INVALID_ARG, "N < 0");
   if (!c->has_weights || !c->has_shapes) return fail(LOCC_E_STATE, "weights and shapes must be set before a query");
+  if (cells && !c->has_cells)
+    return fail(LOCC_E_STATE, "locc_encode_shapes must run (after weights, U-Net weights and shapes) first");
   if (N == 0) {
     c->last = locc_stats{};
     return LOCC_OK;
@@ -300,9 +308,14 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   const bool sync = !dev || !stream;
   const int64_t Bcap = std::min<int64_t>(N, batch_cap(c));
-  locc_status s = ensure_scratch(c, Bcap, masks != nullptr, grad != nullptr);
+  const int K = c->T.K, ncell = c->cfg.M * c->cfg.M * c->cfg.M;
+  const int words = cells ? (ncell + 31) / 32 : (K + 31) / 32;
+  locc_status s = ensure_scratch(c, Bcap, masks != nullptr && !cells, grad != nullptr);
   if (s != LOCC_OK) return s;
-  const int K = c->T.K, words = (K + 31) / 32;
+  if (cells) {
+    CK(c->cells_emb.ensure(sizeof(float) * (size_t)2 * Bcap * c->cfg.F));
+    if (masks) CK(c->out_masks.ensure(sizeof(uint32_t) * (size_t)2 * Bcap * words));
+  }
   DevStats* dstats = c->stats.as<DevStats>();
   CK(cudaMemsetAsync(dstats, 0, sizeof(DevStats), st));
   const int64_t n_sub = (N + Bcap - 1) / Bcap;
@@ -354,6 +367,18 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     float* d_emb = emb ? (dev ? emb + (size_t)2 * i0 * c->cfg.F : c->out_emb.as<float>()) : nullptr;
     float* d_grad = grad ? (dev ? grad + 14 * i0 : c->out_grad.as<float>()) : nullptr;
 
+    if (cells) {
+      // encode-once mode: select cells, pool the cached embeddings, then the predictor
+      if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs], st));
+      float* e_in = (emb && dev) ? emb + (size_t)2 * i0 * c->cfg.F : c->cells_emb.as<float>();
+      CK(launch_cells_select(c->T, c->cells, b, c->cfg.F, b.masks, e_in, st));
+      if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs + 1], st));
+      b.emb_in = e_in;
+      if (occ) CK(cudaMemsetAsync(b.occ, 0, sizeof(int32_t) * 2 * B, st));
+      CK(launch_head(c->P, b, d_probs, d_labels, d_logits, nullptr, d_grad, st));
+      if (emb) d_emb = e_in;  // the selection wrote e (0 for an empty side) in place
+      launches += 2;
+    } else {
     CK(launch_crop_count(c->T, b, words, st));
     CK(launch_scan(b.counts, b.G, b.offsets, c->scan_tmp.as<int64_t>(), st));
     CK(launch_crop_emit(c->T, b, st));
@@ -388,6 +413,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs + 1], st));
     CK(launch_head(c->P, b, d_probs, d_labels, d_logits, d_emb, d_grad, st));
     launches += 7;
+    }
     if (!dev) CK(cudaEventRecord(c->ev_free[subs & 1], st));  // the kernels are done with the inputs
     ++subs;
     if (!dev) {
@@ -553,6 +579,7 @@ locc_status locc_load_weights_mem(locc_ctx* c, const float* flat, size_t n) {
   for (size_t i = 0; i < n; ++i)
     if (!std::isfinite(flat[i])) return fail(LOCC_E_WEIGHTS, "non-finite parameter at %zu", i);
   CK(cudaSetDevice(c->device));
+  c->has_cells = false;  // the cached grids depend on the encoder weights
   locc_status s = upload_params(c, flat);
   if (s != LOCC_OK) return s;
   if (c->cfg.H == 256) s = locc_upload_tc_weights(c, flat);
@@ -635,6 +662,7 @@ locc_status locc_set_shapes(locc_ctx* c, const float* points, int32_t S, int32_t
   c->T.lo = c->sh_lo.as<float4>();
   c->T.hi = c->sh_hi.as<float4>();
   c->T.S = S;
+  c->has_cells = false;  // the cached grids belong to the previous shape table
   if (c->T.K != K) c->cap_B = 0;  // row buffer depends on K
   c->T.K = K;
   c->has_shapes = true;
@@ -656,6 +684,113 @@ locc_status locc_query_grad(locc_ctx* c, const int32_t* pairs, const float* pose
                             uint8_t* labels, float* logits, float* grad, void* stream) {
   if (N > 0 && !grad) return fail(LOCC_E_INVALID_ARG, "grad must be non-null");
   return run_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, grad, stream);
+}
+
+// ---------------------------------------------------------------- NEXT-1: encode-once mode
+int64_t locc_unet_n_params(int32_t H, int32_t F) {
+  const int64_t C = 128;
+  return C * 27 * (H + 3 * C + C + 3 * 2 * C) + 8 * C + (int64_t)F * 2 * C + F;
+}
+
+locc_status locc_load_unet_weights_mem(locc_ctx* c, const float* flat, size_t n) {
+  if (!c || !flat) return fail(LOCC_E_INVALID_ARG, "null argument");
+  const int H = c->cfg.H, F = c->cfg.F, C = 128;
+  const int64_t want = locc_unet_n_params(H, F);
+  if ((int64_t)n != want)
+    return fail(LOCC_E_WEIGHTS, "expected %lld U-Net floats for H=%d F=%d, got %zu", (long long)want, H, F, n);
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(flat[i])) return fail(LOCC_E_WEIGHTS, "non-finite U-Net parameter at %zu", i);
+  CK(cudaSetDevice(c->device));
+  // Wt[l][k][i][o] = W[o][i][k] for the convs; the deconvs as the equivalent conv: taps flipped (26 - k)
+  const int cin[8] = {H, C, C, C, C, 2 * C, 2 * C, 2 * C};
+  std::vector<float> img;
+  size_t offW[8], offb[8];
+  const float* q = flat;
+  for (int l = 0; l < 8; ++l) {
+    offW[l] = img.size();
+    img.resize(img.size() + (size_t)27 * cin[l] * C);
+    float* wt = img.data() + offW[l];
+    for (int o = 0; o < C; ++o)
+      for (int i = 0; i < cin[l]; ++i)
+        for (int k = 0; k < 27; ++k) {
+          const int kk = l < 4 ? k : 26 - k;
+          wt[((size_t)kk * cin[l] + i) * C + o] = q[((size_t)o * cin[l] + i) * 27 + k];
+        }
+    q += (size_t)C * cin[l] * 27;
+    offb[l] = img.size();
+    img.insert(img.end(), q, q + C);
+    q += C;
+  }
+  const size_t offP = img.size();
+  img.insert(img.end(), q, q + (size_t)F * 2 * C);
+  q += (size_t)F * 2 * C;
+  const size_t offPb = img.size();
+  img.insert(img.end(), q, q + F);
+  CK(c->unet_params.ensure(sizeof(float) * img.size()));
+  CK(cudaMemcpy(c->unet_params.p, img.data(), sizeof(float) * img.size(), cudaMemcpyHostToDevice));
+  const float* d = c->unet_params.as<float>();
+  for (int l = 0; l < 8; ++l) {
+    c->U.Wt[l] = d + offW[l];
+    c->U.b[l] = d + offb[l];
+  }
+  c->U.pW = d + offP;
+  c->U.pb = d + offPb;
+  c->has_unet = true;
+  c->has_cells = false;
+  return LOCC_OK;
+}
+
+locc_status locc_encode_shapes(locc_ctx* c) {
+  if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
+  if (!c->has_weights || !c->has_shapes || !c->has_unet)
+    return fail(LOCC_E_STATE, "weights, U-Net weights and shapes must be set before locc_encode_shapes");
+  const int M = c->cfg.M, H = c->cfg.H, F = c->cfg.F, S = c->T.S;
+  if (M < 3 || M > 8 || H != 256 || F != 64)
+    return fail(LOCC_E_INVALID_ARG, "encode-once mode is built for 3 <= M <= 8, H = 256, F = 64");
+  CK(cudaSetDevice(c->device));
+  const int nc = M * M * M;
+  DevBuf G, act;
+  CK(G.ensure(sizeof(float) * (size_t)S * nc * H));
+  CK(act.ensure(sizeof(float) * unet_act_floats(S, M)));
+  CK(c->cells_E.ensure(sizeof(float) * (size_t)S * nc * F));
+  CK(c->cells_ctr.ensure(sizeof(float4) * (size_t)S * nc));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, c->stream));
+  CK(launch_grid_encode(c->P, c->T, M, G.as<float>(), c->stream));
+  CK(launch_unet(c->U, c->T, M, H, F, G.as<float>(), act.as<float>(), c->cells_E.as<float>(),
+                 c->cells_ctr.as<float4>(), c->stream));
+  CK(cudaEventRecord(e1, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  c->encode_ms = ms;
+  c->cells.E = c->cells_E.as<float>();
+  c->cells.ctr = c->cells_ctr.as<float4>();
+  c->cells.M = M;
+  c->has_cells = true;
+  return LOCC_OK;
+}
+
+locc_status locc_get_cell_embeddings(locc_ctx* c, float* out, double* encode_ms) {
+  if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
+  if (!c->has_cells) return fail(LOCC_E_STATE, "no encoded shapes");
+  CK(cudaSetDevice(c->device));
+  if (out) {
+    const size_t bytes = sizeof(float) * (size_t)c->T.S * c->cfg.M * c->cfg.M * c->cfg.M * c->cfg.F;
+    CK(cudaMemcpy(out, c->cells_E.p, bytes, is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+  }
+  if (encode_ms) *encode_ms = c->encode_ms;
+  return LOCC_OK;
+}
+
+locc_status locc_query_cells(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
+                             uint8_t* labels, float* logits, int32_t* nsel, uint32_t* cells, float* emb,
+                             void* stream) {
+  return run_query(c, pairs, poses, N, probs, labels, logits, nsel, nullptr, cells, emb, nullptr, stream, true);
 }
 
 }  // extern "C"

@@ -18,7 +18,8 @@ LOCC_PREC_FP32 = 0
 LOCC_PREC_BF16 = 1
 
 EXPORTS = ("locc_create", "locc_load_weights", "locc_load_weights_mem", "locc_set_shapes", "locc_query",
-           "locc_query_debug", "locc_query_grad", "locc_set_precision", "locc_set_timing", "locc_get_stats", "locc_destroy",
+           "locc_query_debug", "locc_query_grad", "locc_unet_n_params", "locc_load_unet_weights_mem",
+           "locc_encode_shapes", "locc_get_cell_embeddings", "locc_query_cells", "locc_set_precision", "locc_set_timing", "locc_get_stats", "locc_destroy",
            "locc_status_string", "locc_last_error", "locc_version")
 
 
@@ -60,6 +61,12 @@ def lib():
         L.locc_query.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp]
         L.locc_query_debug.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp]
         L.locc_query_grad.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp]
+        L.locc_unet_n_params.argtypes = [i32, i32]
+        L.locc_unet_n_params.restype = i64
+        L.locc_load_unet_weights_mem.argtypes = [vp, vp, C.c_size_t]
+        L.locc_encode_shapes.argtypes = [vp]
+        L.locc_get_cell_embeddings.argtypes = [vp, vp, vp]
+        L.locc_query_cells.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]
         L.locc_set_precision.argtypes = [vp, i32]
         L.locc_set_timing.argtypes = [vp, i32]
         L.locc_get_stats.argtypes = [vp, C.POINTER(Stats)]
@@ -138,6 +145,7 @@ class Locc:
             points = np.ascontiguousarray(points, np.float32)
         _check(lib().locc_set_shapes(self._h, _ptr(points, np.float32), S, K))
         self.K = K
+        self.S = S
 
     def set_precision(self, precision):
         _check(lib().locc_set_precision(self._h, precision))
@@ -184,6 +192,40 @@ class Locc:
         grad = np.zeros((N, 14), np.float32)
         self.query_grad_into(pairs, poses, probs, grad, labels, logits)
         return probs, labels, logits, grad
+
+    # ------------------------------------------------------------- encode-once mode (NEXT-1)
+    def load_unet_weights_mem(self, flat):
+        flat = np.ascontiguousarray(flat, np.float32)
+        _check(lib().locc_load_unet_weights_mem(self._h, _ptr(flat), flat.size))
+
+    def encode_shapes(self):
+        _check(lib().locc_encode_shapes(self._h))
+
+    def cell_embeddings(self):
+        """(E float32 [S][M^3][F] of the cached grids, device ms of the last encode)."""
+        ms = C.c_double(0.0)
+        out = np.zeros((self.S, self.M ** 3, self.F), np.float32)
+        _check(lib().locc_get_cell_embeddings(self._h, _ptr(out), C.byref(ms)))
+        return out, ms.value
+
+    def query_cells_into(self, pairs, poses, probs, labels=None, logits=None, nsel=None, cells=None, emb=None,
+                         stream=None):
+        N = int(pairs.shape[0])
+        _check(lib().locc_query_cells(self._h, _ptr(pairs), _ptr(poses), N, _ptr(probs), _ptr(labels),
+                                      _ptr(logits), _ptr(nsel), _ptr(cells), _ptr(emb), stream))
+
+    def query_cells(self, pairs, poses, debug=False):
+        """Host form of locc_query_cells -> dict (probs, labels, logits [, nsel, cells, emb])."""
+        pairs = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+        poses = np.ascontiguousarray(poses, np.float32).reshape(-1, 2, 7)
+        N = pairs.shape[0]
+        o = dict(probs=np.zeros(N, np.float32), labels=np.zeros(N, np.uint8), logits=np.zeros(N, np.float32))
+        if debug:
+            o.update(nsel=np.zeros((N, 2), np.int32), cells=np.zeros((N, 2, (self.M ** 3 + 31) // 32), np.uint32),
+                     emb=np.zeros((N, 2, self.F), np.float32))
+        self.query_cells_into(pairs, poses, o["probs"], o["labels"], o["logits"], o.get("nsel"), o.get("cells"),
+                              o.get("emb"))
+        return o
 
     def query_debug(self, pairs, poses):
         """Host form of locc_query_debug -> dict of every output and intermediate."""

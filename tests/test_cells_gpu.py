@@ -1,0 +1,133 @@
+"""GPU parity of the encode-once mode (NEXT-1: locc_load_unet_weights_mem, locc_encode_shapes,
+locc_query_cells) against the oracle (oracle_query_cells / oracle_encode_grid).
+
+Bars (Q27-Q30): selected-cell bits and counts bit-exact (both sides take the decision with
+the same fp32 arithmetic on the same fp32 cell centres); embedding grids within 2e-5 of max|E| (fp32
+sums of up to 6912 terms against fp64); pooled e within 2e-5; |p - p_oracle| <= 1e-5 and labels
+identical outside |p_oracle - 0.5| <= 1e-3; short-circuit exactly where neither side selects a cell.
+"""
+import numpy as np
+import pytest
+
+import locc_synth as ls
+from test_oracle_cells import identity_encoder, unet_probe
+
+pytestmark = pytest.mark.gpu
+E_TOL = 2e-5
+
+
+@pytest.fixture(scope="module")
+def locc_mod():
+    from paper_2304_09439_b200 import build as b
+    b.build()
+    from paper_2304_09439_b200 import locc
+    return locc
+
+
+@pytest.fixture(scope="module")
+def weights():
+    w = ls.flatten_weights(ls.make_weights("spread", calib=ls.load_calibration()))
+    u = ls.flatten_unet(ls.make_unet_weights())
+    return w, u
+
+
+@pytest.fixture(scope="module")
+def wl():
+    """300 pairs over 12 shapes (K = 1500, s = 0.5): ragged against max_batch 128."""
+    w = ls.make_workload("C1", N=300, S=12)
+    return w.points, w.pairs, w.poses
+
+
+@pytest.fixture(scope="module")
+def wl_oracle(oracle_mod, wl, weights):
+    pts, pairs, poses = wl
+    return oracle_mod.query_cells(weights[0], weights[1], pts, pairs, poses)
+
+
+def make_ctx(locc_mod, w, u, points, max_batch=0, M=6):
+    ctx = locc_mod.Locc(M=M, H=256, F=64, precision=0, device=0, max_batch=max_batch)
+    ctx.load_weights_mem(w)
+    ctx.load_unet_weights_mem(u)
+    ctx.set_shapes(points)
+    ctx.encode_shapes()
+    return ctx
+
+
+def assert_cells_parity(got, ref, E_gpu=None, pairs=None):
+    assert np.array_equal(got["nsel"], ref["nsel"]), "selected-cell counts differ"
+    assert np.array_equal(got["cells"], ref["cells"]), "selected-cell bits differ"
+    if E_gpu is not None:
+        used = np.unique(pairs)
+        scale = np.abs(ref["grids"][used]).max()
+        err = np.abs(E_gpu[used].astype(np.float64) - ref["grids"][used]).max()
+        assert err <= E_TOL * scale, f"grid max err {err:.3g} (scale {scale:.3g})"
+    assert np.abs(got["emb"].astype(np.float64) - ref["emb"]).max() <= E_TOL * max(1.0, np.abs(ref["emb"]).max())
+    short = ref["nsel"].sum(1) == 0
+    assert np.all(got["probs"][short] == 0) and np.all(np.isneginf(got["logits"][short]))
+    dp = np.abs(got["probs"].astype(np.float64) - ref["probs"]).max()
+    assert dp <= 1e-5, f"max |dp| = {dp:.3g}"
+    band = np.abs(ref["probs"] - 0.5) <= 1e-3
+    assert np.array_equal(got["labels"][~band], ref["labels"][~band])
+    return dp
+
+
+def test_cells_parity(locc_mod, wl, wl_oracle, weights):
+    pts, pairs, poses = wl
+    with make_ctx(locc_mod, *weights, pts, max_batch=128) as ctx:
+        E, ms = ctx.cell_embeddings()
+        got = ctx.query_cells(pairs, poses, debug=True)
+    assert ms > 0
+    assert (wl_oracle["nsel"].sum(1) == 0).any() and (wl_oracle["nsel"].sum(1) > 0).mean() > 0.8
+    assert_cells_parity(got, wl_oracle, E, pairs)
+
+
+def test_cells_probe_weights_gpu(locc_mod, oracle_mod, wl):
+    """The identity-encoder / delta-kernel U-Net probe (closed form pinned in test_oracle_cells):
+    the device grids reproduce the oracle's exactly up to fp32 rounding of the copied values."""
+    pts, pairs, poses = wl
+    w, u = identity_encoder(), unet_probe()
+    ref = oracle_mod.query_cells(w, u, pts, pairs[:40], poses[:40])
+    with make_ctx(locc_mod, w, u, pts) as ctx:
+        E, _ = ctx.cell_embeddings()
+        got = ctx.query_cells(pairs[:40], poses[:40], debug=True)
+    used = np.unique(pairs[:40])
+    np.testing.assert_allclose(E[used], ref["grids"][used], rtol=1e-6, atol=1e-7)
+    assert np.array_equal(got["cells"], ref["cells"])
+
+
+def test_cells_device_buffers_and_symmetries(locc_mod, wl, weights):
+    import torch
+    pts, pairs, poses = wl
+    with make_ctx(locc_mod, *weights, pts) as ctx:
+        h = ctx.query_cells(pairs, poses)
+        N = len(pairs)
+        dp, dq = torch.from_numpy(pairs).cuda(), torch.from_numpy(poses).cuda()
+        probs = torch.empty(N, device="cuda")
+        labels = torch.empty(N, dtype=torch.uint8, device="cuda")
+        s = torch.cuda.Stream()
+        ctx.query_cells_into(dp, dq, probs, labels, stream=s.cuda_stream)
+        s.synchronize()
+        assert np.array_equal(probs.cpu().numpy(), h["probs"]) and np.array_equal(labels.cpu().numpy(), h["labels"])
+        sw = ctx.query_cells(pairs[:, ::-1].copy(), poses[:, ::-1].copy())
+        neg = poses.copy()
+        neg[:, :, :4] *= -1
+        ng = ctx.query_cells(pairs, neg)
+    assert np.array_equal(sw["probs"], h["probs"]) and np.array_equal(ng["probs"], h["probs"])
+
+
+def test_cells_state_errors(locc_mod, wl, weights):
+    pts, pairs, poses = wl
+    ctx = locc_mod.Locc(M=6, H=256, F=64, precision=0, device=0)
+    ctx.load_weights_mem(weights[0])
+    ctx.set_shapes(pts)
+    with pytest.raises(locc_mod.LoccError):
+        ctx.encode_shapes()          # no U-Net weights
+    ctx.load_unet_weights_mem(weights[1])
+    with pytest.raises(locc_mod.LoccError):
+        ctx.query_cells(pairs, poses)  # not encoded
+    ctx.encode_shapes()
+    ctx.query_cells(pairs[:4], poses[:4])
+    ctx.set_shapes(pts[:4])           # new shape table invalidates the grids
+    with pytest.raises(locc_mod.LoccError):
+        ctx.query_cells(pairs[:1] % 4, poses[:1])
+    ctx.close()
