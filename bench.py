@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-grad", action="store_true", help="skip the NEXT-2 pose-gradient measurement")
+    ap.add_argument("--no-cells", action="store_true", help="skip the NEXT-1 encode-once measurement")
     return ap.parse_args()
 
 
@@ -295,6 +296,40 @@ def main():
         line["pose_grad"] = {"metric": "collision checks with d logit / d pose per second", "value": world * N / (gms / 1e3),
                              "unit": UNIT, "ms_per_step": gms, "overhead_vs_forward": gms / ms - 1.0,
                              "api": "locc_query_grad (grad [N][14] fp32)"}
+
+    # NEXT-1: the paper's encode-once inference on the same pairs (grids cached once per shape table)
+    if not a.no_cells:
+        import locc_synth as ls
+        ctx.load_unet_weights_mem(ls.flatten_unet(ls.make_unet_weights()))
+        ctx.encode_shapes()
+        enc_ms = ctx.encode_ms()
+
+        def cstep():
+            ctx.query_cells_into(d_pairs, d_poses, d_probs, d_labels, stream=stream.cuda_stream)
+
+        for _ in range(a.warmup):
+            cstep()
+        cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(a.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                cev[i][0].record(stream)
+            cstep()
+            with torch.cuda.stream(stream):
+                cev[i][1].record(stream)
+        torch.cuda.synchronize()
+        cms = statistics.mean([s.elapsed_time(e) for s, e in cev])
+        if world > 1:
+            t = torch.tensor([cms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            cms = float(t.item())
+        line["encode_once"] = {"metric": "collision checks/sec, encode-once mode (locc_query_cells)",
+                               "value": world * N / (cms / 1e3), "unit": UNIT, "ms_per_step": cms,
+                               "encode_ms_per_shape_table": enc_ms, "shapes": int(len(pts)),
+                               "note": "grids encoded once per shape table (not in the timed step); fp32"}
 
     # e2e: same metric through the public API with HOST buffers (pinned), copies in the timed region
     if not a.no_e2e:

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(256) unet_tail_kernel(UNetParams U, ShapeTable
 // ---------------------------------------------------------------- Q29: selection + pooled embedding
 // One warp per (pair, side) segment.  Cell c of the own shape is selected iff its centre, moved into the
 // other object's frame with the crop's fp32 transform, is within the OWN cell half-diagonal of the other
-// AABB (keep_point with eps^2 = own lo.w).  e = mean over the selected cells (ascending c, fp32) of E.
+// AABB (keep_point with eps^2 = own lo.w).  e = mean over the selected cells of E (fp32 sums).
 __global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTable C, Batch b, int F,
                                                            uint32_t* __restrict__ cells, float* __restrict__ emb) {
   const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -289,35 +289,47 @@ __global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTa
       n += __popc(words[j]);
     }
   }
-  // mean of the selected rows: lane owns features lane, lane + 32 (F <= 64)
-  const float* Es = C.E + (int64_t)own * nc * F;
-  float a0 = 0.f, a1 = 0.f;
+  // mean of the selected rows (F = 64): the selected cell ids are listed in shared memory, then each
+  // half-warp reads one row as 16 float4 (lane l: features 4 (l & 15) ..), 8 rows in flight per warp
+  __shared__ uint16_t sel_list[8][512];
+  uint16_t* list = sel_list[threadIdx.x >> 5];
+  int at = 0;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    uint32_t m = words[j];
-    while (m) {
-      const int c0 = 32 * j + __ffs(m) - 1;
-      m &= m - 1;
-      const int c1 = m ? 32 * j + __ffs(m) - 1 : -1;
-      if (m) m &= m - 1;
-      const float* r0 = Es + (int64_t)c0 * F;
-      const float v0 = lane < F ? r0[lane] : 0.f, w0 = lane + 32 < F ? r0[lane + 32] : 0.f;
-      float v1 = 0.f, w1 = 0.f;
-      if (c1 >= 0) {
-        const float* r1 = Es + (int64_t)c1 * F;
-        v1 = lane < F ? r1[lane] : 0.f;
-        w1 = lane + 32 < F ? r1[lane + 32] : 0.f;
-      }
-      a0 = __fadd_rn(a0, v0);
-      a1 = __fadd_rn(a1, w0);
-      if (c1 >= 0) {
-        a0 = __fadd_rn(a0, v1);
-        a1 = __fadd_rn(a1, w1);
-      }
+    if (j < nw) {
+      if ((words[j] >> lane) & 1u) list[at + __popc(words[j] & ((1u << lane) - 1u))] = (uint16_t)(32 * j + lane);
+      at += __popc(words[j]);
     }
   }
-  if (lane < F) e[lane] = n ? __fdiv_rn(a0, (float)n) : 0.f;
-  if (lane + 32 < F) e[lane + 32] = n ? __fdiv_rn(a1, (float)n) : 0.f;
+  __syncwarp();
+  const float4* Es4 = reinterpret_cast<const float4*>(C.E + (int64_t)own * nc * 64);
+  const int half = lane >> 4, f4 = lane & 15;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i0 = 0; i0 < n; i0 += 8) {
+    float4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + 2 * j + half;
+      v[j] = i < n ? __ldg(Es4 + (int)list[i] * 16 + f4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      acc.x = __fadd_rn(acc.x, v[j].x);
+      acc.y = __fadd_rn(acc.y, v[j].y);
+      acc.z = __fadd_rn(acc.z, v[j].z);
+      acc.w = __fadd_rn(acc.w, v[j].w);
+    }
+  }
+  acc.x = __fadd_rn(acc.x, __shfl_xor_sync(0xffffffffu, acc.x, 16));
+  acc.y = __fadd_rn(acc.y, __shfl_xor_sync(0xffffffffu, acc.y, 16));
+  acc.z = __fadd_rn(acc.z, __shfl_xor_sync(0xffffffffu, acc.z, 16));
+  acc.w = __fadd_rn(acc.w, __shfl_xor_sync(0xffffffffu, acc.w, 16));
+  if (half == 0) {
+    const float fn = (float)n;
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (n) r = make_float4(__fdiv_rn(acc.x, fn), __fdiv_rn(acc.y, fn), __fdiv_rn(acc.z, fn), __fdiv_rn(acc.w, fn));
+    reinterpret_cast<float4*>(e)[f4] = r;
+  }
   if (cells) {
 #pragma unroll
     for (int j = 0; j < 16; ++j)

@@ -208,6 +208,12 @@ class Locc:
         _check(lib().locc_get_cell_embeddings(self._h, _ptr(out), C.byref(ms)))
         return out, ms.value
 
+    def encode_ms(self):
+        """Device time (ms) of the last encode_shapes."""
+        ms = C.c_double(0.0)
+        _check(lib().locc_get_cell_embeddings(self._h, None, C.byref(ms)))
+        return ms.value
+
     def query_cells_into(self, pairs, poses, probs, labels=None, logits=None, nsel=None, cells=None, emb=None,
                          stream=None):
         N = int(pairs.shape[0])
