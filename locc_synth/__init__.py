@@ -324,6 +324,43 @@ def load_calibration(path=None):
         return json.load(f)
 
 
+# --------------------------------------------------------------------------- closed-loop scenes
+SIM_DEFAULTS = dict(h=0.01 / 4 / 4, substeps=4, detector="crop", gravity=(0.0, 0.0, -9.81), ks=2.0, kd=0.02,
+                    amp=(0.01, 0.01, 0.0), freq=2.0, slack=0.01)
+
+
+def make_sim_scene(points, E: int, seed: int = 5, bowl: int = 4, drop: float = 0.03):
+    """E environments of PAPER.md:91's scene: body 0 = the bowl (shape `bowl`, the synthetic bowl family),
+    bodies 1, 2 = two random shapes dropped just above its rim.  Returns ids int32 [E][3], body float32
+    [E][3][4] (m, Ixx, Iyy, Izz: 0.1 kg boxes of the shape's AABB) and state float32 [E][3][13]
+    (q, t, v, w).  SIM_DEFAULTS holds the step constants (dt = 0.01/4 s, 4 substeps)."""
+    rng = np.random.default_rng(seed)
+    S = points.shape[0]
+    ids = np.empty((E, 3), np.int32)
+    ids[:, 0] = bowl
+    ids[:, 1:] = rng.integers(0, S, size=(E, 2))
+    ext = (points.max(1) - points.min(1)).astype(np.float64)
+    m = 0.1
+    body = np.empty((E, 3, 4), np.float32)
+    for b in range(3):
+        e = ext[ids[:, b]]
+        body[:, b, 0] = m
+        body[:, b, 1] = m / 12 * (e[:, 1] ** 2 + e[:, 2] ** 2)
+        body[:, b, 2] = m / 12 * (e[:, 0] ** 2 + e[:, 2] ** 2)
+        body[:, b, 3] = m / 12 * (e[:, 0] ** 2 + e[:, 1] ** 2)
+    state = np.zeros((E, 3, 13), np.float32)
+    state[:, 0, 0] = 1.0
+    q = rng.standard_normal((E, 2, 4))
+    q /= np.linalg.norm(q, axis=-1, keepdims=True)
+    state[:, 1:, :4] = q
+    rb = 0.5 * ext[bowl][2]
+    state[:, 1, 4:7] = np.stack([rng.uniform(-0.02, 0.02, E), rng.uniform(-0.02, 0.02, E),
+                                 rb + rng.uniform(0.0, drop, E)], 1)
+    state[:, 2, 4:7] = np.stack([rng.uniform(-0.02, 0.02, E), rng.uniform(-0.02, 0.02, E),
+                                 rb + drop + rng.uniform(0.0, drop, E)], 1)
+    return ids, body, state
+
+
 # --------------------------------------------------------------------------- workloads
 @dataclass
 class Workload:

@@ -49,6 +49,8 @@ def lib():
         L.oracle_encode_grid.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, C.c_size_t, vp, C.c_int32, vp, vp]
         L.oracle_query_cells.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, C.c_size_t, vp, C.c_int32, C.c_int32,
                                          vp, vp, C.c_int64] + [vp] * 7
+        L.oracle_sim_run.argtypes = [C.POINTER(_Cfg), vp, C.c_size_t, vp, C.c_size_t, vp, C.c_int32, C.c_int32, vp,
+                                     C.c_int32, vp, vp, vp, C.c_double, vp, vp]
         L.oracle_load_weights.argtypes = [C.c_char_p, vp, C.c_size_t, vp, vp, vp]
         L.oracle_load_weights.restype = C.c_int64
         L.oracle_n_params.argtypes = [C.c_int32, C.c_int32]
@@ -202,6 +204,30 @@ def query_cells(weights_flat, unet_flat, points, pairs, poses, M=6, H=256, F=64,
     if rc:
         raise ValueError(f"oracle_query_cells: {rc}")
     return out
+
+
+# ----------------------------------------------------------------------------- NEXT-3 (closed loop)
+def sim_run(weights_flat, points, sim, ids, body, state, t0=0.0, unet_flat=None, M=6, H=256, F=64, n_threads=0):
+    """Advance `state` [E][3][13] (float64, copied) by sim['substeps'] substeps.  sim: dict with h,
+    substeps, detector ('crop' | 'cells'), gravity, ks, kd, amp, freq, slack.  Returns (state,
+    contacts [E][3], margins [E][4])."""
+    w = np.ascontiguousarray(weights_flat, np.float32)
+    u = None if unet_flat is None else np.ascontiguousarray(unet_flat, np.float32)
+    pts = np.ascontiguousarray(points, np.float32)
+    ids = np.ascontiguousarray(ids, np.int32).reshape(-1, 3)
+    E = ids.shape[0]
+    body = np.ascontiguousarray(body, np.float64).reshape(E, 3, 4)
+    st = np.array(state, np.float64).reshape(E, 3, 13).copy()
+    sv = np.array([sim["h"], sim["substeps"], 1 if sim.get("detector", "crop") == "cells" else 0, *sim["gravity"],
+                   sim["ks"], sim["kd"], *sim["amp"], sim["freq"], sim["slack"]], np.float64)
+    contacts = np.zeros((E, 3), np.int32)
+    margins = np.zeros((E, 4))
+    cfg = _Cfg(M, H, F, 0, n_threads)
+    rc = lib().oracle_sim_run(C.byref(cfg), _p(w), w.size, _p(u), 0 if u is None else u.size, _p(pts), pts.shape[0],
+                              pts.shape[1], _p(sv), E, _p(ids), _p(body), _p(st), t0, _p(contacts), _p(margins))
+    if rc:
+        raise ValueError(f"oracle_sim_run: {rc}")
+    return st, contacts, margins
 
 
 def load_weights(manifest):

@@ -611,6 +611,37 @@ int select_cells(const ShapeInfo& self, int M, const float R[9], const float t[3
   return crop(ctr.data(), ncell, R, t, o, sel);
 }
 
+// ------------------------------------------------------------------ NEXT-3: closed-loop step
+// A Brax-style rigid-body substep with LOCC as the contact detector (SPEC.md
+// S:638-665; reading Q31).  Per environment: body 0 = the kinematic bowl (shaken), bodies 1, 2
+// dynamic; pairs (0,1), (0,2), (1,2).  State per body: q (4), t (3), v (3), w (3), world frame.
+// Per substep of length h at time tau:
+//   1. bowl: q kept, t = A sin(2 pi f tau), v = 2 pi f A cos(2 pi f tau), w = 0
+//   2. broad phase per pair: world AABBs (centre R c + t, half-extent |R| e) overlap within `slack`
+//   3. detector: logit s and d s / d(q_A, t_A, q_B, t_B) (the query + NEXT-2 gradient, crop or cells)
+//   4. contact iff not culled and s > 0 (p > 1/2)
+//   5. penalty along the descent of s: per side X the translational gradient g_t and the
+//      rotational one G_w[k] = g_q . (1/2 (0, e_k) (x) q); n = |(all g_t, G_w)|; ds/dt = sum g_t.v + G_w.w;
+//      lambda = max(0, ks s + kd ds/dt); F_X = -lambda g_t / n, tau_X = -lambda G_w / n (dynamic bodies)
+//   6. semi-implicit Euler: v += h (F / m + gravity); w += h R diag(1/I) R^T tau; t += h v;
+//      q = normalise(q + h/2 (0, w) (x) q)
+// Margins reported per environment (min over the call): |s| and the predictor's ReLU margin over the
+// unculled pairs, the broad-phase decision distance, |ks s + kd ds/dt| over contacts.
+struct SimCfg {
+  double h;
+  int32_t substeps, detector;
+  double gravity[3], ks, kd, amp[3], freq, slack;
+};
+
+void quat_left_e(const double q[4], int k, double out[4]) {  // (0, e_k) (x) q
+  const Quat e{0.0, k == 0 ? 1.0 : 0.0, k == 1 ? 1.0 : 0.0, k == 2 ? 1.0 : 0.0};
+  const Quat r = hamilton(e, Quat{q[0], q[1], q[2], q[3]});
+  out[0] = r.w;
+  out[1] = r.x;
+  out[2] = r.y;
+  out[3] = r.z;
+}
+
 bool finite_n(const float* p, int64_t n) {
   for (int64_t i = 0; i < n; ++i)
     if (!std::isfinite(p[i])) return false;
@@ -931,6 +962,209 @@ int oracle_query_cells(const oracle_cfg* cfg, const float* weights, size_t n_wei
   for (int t = 1; t < nq; ++t) pool.emplace_back(worker);
   worker();
   for (auto& th : pool) th.join();
+  return 0;
+}
+
+int oracle_sim_run(const oracle_cfg* cfg, const float* weights, size_t n_weights, const float* unet_w,
+                   size_t n_unet, const float* points, int32_t S, int32_t K, const double* sim, int32_t E,
+                   const int32_t* ids, const double* body, double* state, double t0, int32_t* contacts,
+                   double* margins) {
+  if (!cfg || !sim || E < 0 || !ids || !body || !state) return -1;
+  SimCfg c;
+  c.h = sim[0];
+  c.substeps = (int32_t)sim[1];
+  c.detector = (int32_t)sim[2];
+  for (int i = 0; i < 3; ++i) c.gravity[i] = sim[3 + i];
+  c.ks = sim[6];
+  c.kd = sim[7];
+  for (int i = 0; i < 3; ++i) c.amp[i] = sim[8 + i];
+  c.freq = sim[11];
+  c.slack = sim[12];
+  if (!(c.h > 0.0) || c.substeps < 1) return -1;
+  if (c.detector == 1 && (!unet_w || (int64_t)n_unet != unet_n_params(cfg->H, cfg->F))) return -3;
+  const int M = cfg->M, H = cfg->H, F = cfg->F, ncell = M * M * M;
+  if (!weights || (int64_t)n_weights != n_params(H, F)) return -3;
+  std::vector<ShapeInfo> shapes(S);
+  for (int s = 0; s < S; ++s)
+    if (!shape_prep(points + (int64_t)s * K * 3, K, M, shapes[s])) return -2;
+  const Params P = bind_params(weights, H, F);
+  // encode-once detector: the referenced grids, once per call
+  std::vector<std::vector<double>> grids(S);
+  if (c.detector == 1) {
+    const EncW EW{widen(P.enc1, false), widen(P.enc2, false), widen(P.enc3, false), widen(P.proj, false)};
+    const UNetW U = bind_unet(unet_w, H, F);
+    std::vector<uint8_t> used(S, 0);
+    for (int64_t i = 0; i < 3 * (int64_t)E; ++i) used[ids[i]] = 1;
+    std::vector<double> g;
+    for (int s = 0; s < S; ++s)
+      if (used[s]) {
+        grid_maxpool(P, EW, points + (int64_t)s * K * 3, K, shapes[s], M, H, g);
+        unet(U, g, M, H, F, grids[s]);
+      }
+  }
+  const int pa_[3] = {0, 0, 1}, pb_[3] = {1, 2, 2};
+  const int64_t NP = 3 * (int64_t)E;
+  std::vector<int32_t> pairs(2 * NP);
+  std::vector<float> poses(14 * NP);
+  std::vector<double> lg(NP), gr(14 * NP), mg(NP);
+  std::vector<uint8_t> culled(NP);
+  if (contacts)
+    for (int64_t i = 0; i < NP; ++i) contacts[i] = 0;
+  if (margins)
+    for (int64_t i = 0; i < 4 * (int64_t)E; ++i) margins[i] = INFINITY;
+  for (int n = 0; n < c.substeps; ++n) {
+    const double tau = t0 + n * c.h, w2 = 2.0 * M_PI * c.freq;
+    for (int e = 0; e < E; ++e) {  // 1. the kinematic bowl
+      double* b = state + (int64_t)e * 39;
+      for (int i = 0; i < 3; ++i) {
+        b[4 + i] = c.amp[i] * std::sin(w2 * tau);
+        b[7 + i] = c.amp[i] * w2 * std::cos(w2 * tau);
+        b[10 + i] = 0.0;
+      }
+    }
+    for (int e = 0; e < E; ++e)  // 2. broad phase + the detector's inputs
+      for (int p = 0; p < 3; ++p) {
+        const int64_t i = 3 * (int64_t)e + p;
+        const double* X[2] = {state + (int64_t)e * 39 + 13 * pa_[p], state + (int64_t)e * 39 + 13 * pb_[p]};
+        double cw[2][3], hw[2][3];
+        for (int side = 0; side < 2; ++side) {
+          const int sid = ids[3 * e + (side ? pb_[p] : pa_[p])];
+          pairs[2 * i + side] = sid;
+          for (int j = 0; j < 7; ++j) poses[14 * i + 7 * side + j] = (float)X[side][j];
+          const ShapeInfo& sh = shapes[sid];
+          double q[4] = {X[side][0], X[side][1], X[side][2], X[side][3]}, R[3][3];
+          const double nq = std::sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+          rotmat(Quat{q[0] / nq, q[1] / nq, q[2] / nq, q[3] / nq}, R);
+          for (int r = 0; r < 3; ++r) {
+            cw[side][r] = X[side][4 + r];
+            hw[side][r] = 0.0;
+            for (int k = 0; k < 3; ++k) {
+              const double cl = 0.5 * ((double)sh.lo[k] + (double)sh.hi[k]), hl = 0.5 * ((double)sh.hi[k] - (double)sh.lo[k]);
+              cw[side][r] += R[r][k] * cl;
+              hw[side][r] += std::fabs(R[r][k]) * hl;
+            }
+          }
+        }
+        double gmax = -INFINITY;  // culled iff some axis separates: max gap > 0
+        for (int r = 0; r < 3; ++r)
+          gmax = std::max(gmax, std::fabs(cw[0][r] - cw[1][r]) - (hw[0][r] + hw[1][r] + c.slack));
+        culled[i] = gmax > 0.0;
+        if (margins) margins[4 * e + 2] = std::min(margins[4 * e + 2], std::fabs(gmax));
+      }
+    // 3. detector
+    if (c.detector == 0) {
+      const int rc = oracle_query_grad(cfg, weights, n_weights, points, S, K, pairs.data(), poses.data(), NP,
+                                       lg.data(), gr.data(), mg.data());
+      if (rc) return rc;
+    } else {
+      for (int64_t i = 0; i < NP; ++i) {
+        const int a = pairs[2 * i], b = pairs[2 * i + 1];
+        const float* pA = &poses[14 * i];
+        const float* pB = pA + 7;
+        Quat qA, qB;
+        if (!normalise(pA, qA) || !normalise(pB, qB)) return -1;
+        float R_BA[9], t_BA[3], R_AB[9], t_AB[3];
+        relative(qA, pA + 4, qB, pB + 4, R_BA, t_BA);
+        relative(qB, pB + 4, qA, pA + 4, R_AB, t_AB);
+        std::vector<uint8_t> sA, sB;
+        const int nA = select_cells(shapes[a], M, R_BA, t_BA, shapes[b], sA);
+        const int nB = select_cells(shapes[b], M, R_AB, t_AB, shapes[a], sB);
+        double* g = &gr[14 * i];
+        if (nA + nB == 0) {
+          lg[i] = -INFINITY;
+          for (int j = 0; j < 14; ++j) g[j] = 0.0;
+          mg[i] = INFINITY;
+          continue;
+        }
+        std::vector<double> eA(F, 0.0), eB(F, 0.0);
+        for (int cc = 0; cc < ncell; ++cc) {
+          if (sA[cc])
+            for (int f = 0; f < F; ++f) eA[f] += grids[a][(int64_t)cc * F + f];
+          if (sB[cc])
+            for (int f = 0; f < F; ++f) eB[f] += grids[b][(int64_t)cc * F + f];
+        }
+        for (int f = 0; f < F; ++f) {
+          if (nA) eA[f] /= (double)nA;
+          if (nB) eB[f] /= (double)nB;
+        }
+        double da[7], db[7];
+        for (int j = 0; j < 7; ++j) {
+          da[j] = pA[j];
+          db[j] = pB[j];
+        }
+        lg[i] = head_grad(P, eA.data(), eB.data(), F, da, da + 4, db, db + 4, g, &mg[i]);
+      }
+    }
+    // 4.-6. contacts, penalty, integration
+    for (int e = 0; e < E; ++e) {
+      double Fo[3][3] = {}, To[3][3] = {};
+      double* st = state + (int64_t)e * 39;
+      for (int p = 0; p < 3; ++p) {
+        const int64_t i = 3 * (int64_t)e + p;
+        if (culled[i]) continue;
+        if (margins) {
+          margins[4 * e] = std::min(margins[4 * e], std::fabs(lg[i]));
+          margins[4 * e + 1] = std::min(margins[4 * e + 1], mg[i]);
+        }
+        if (!(lg[i] > 0.0)) continue;
+        if (contacts) ++contacts[i];
+        const int bx[2] = {pa_[p], pb_[p]};
+        double gt[2][3], gw[2][3], nrm2 = 0.0, sdot = 0.0;
+        for (int side = 0; side < 2; ++side) {
+          const double* g = &gr[14 * i + 7 * side];
+          const double* X = st + 13 * bx[side];
+          for (int k = 0; k < 3; ++k) {
+            double d[4];
+            quat_left_e(X, k, d);
+            gw[side][k] = 0.5 * (((g[0] * d[0] + g[1] * d[1]) + g[2] * d[2]) + g[3] * d[3]);
+            gt[side][k] = g[4 + k];
+            nrm2 += gt[side][k] * gt[side][k] + gw[side][k] * gw[side][k];
+            sdot += gt[side][k] * X[7 + k] + gw[side][k] * X[10 + k];
+          }
+        }
+        const double nrm = std::sqrt(nrm2);
+        if (!(nrm > 1e-12)) continue;
+        const double raw = c.ks * lg[i] + c.kd * sdot;
+        if (margins) margins[4 * e + 3] = std::min(margins[4 * e + 3], std::fabs(raw));
+        const double lam = raw > 0.0 ? raw : 0.0;
+        for (int side = 0; side < 2; ++side)
+          for (int k = 0; k < 3; ++k) {
+            Fo[bx[side]][k] -= lam * gt[side][k] / nrm;
+            To[bx[side]][k] -= lam * gw[side][k] / nrm;
+          }
+      }
+      for (int bi = 1; bi < 3; ++bi) {
+        double* X = st + 13 * bi;
+        const double* bd = body + ((int64_t)e * 3 + bi) * 4;  // m, Ixx, Iyy, Izz
+        double q[4] = {X[0], X[1], X[2], X[3]}, R[3][3];
+        const double nq = std::sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+        rotmat(Quat{q[0] / nq, q[1] / nq, q[2] / nq, q[3] / nq}, R);
+        double tb[3], dw[3];
+        for (int k = 0; k < 3; ++k) tb[k] = (R[0][k] * To[bi][0] + R[1][k] * To[bi][1]) + R[2][k] * To[bi][2];
+        for (int k = 0; k < 3; ++k) tb[k] /= bd[1 + k];
+        for (int r = 0; r < 3; ++r) dw[r] = (R[r][0] * tb[0] + R[r][1] * tb[1]) + R[r][2] * tb[2];
+        for (int k = 0; k < 3; ++k) {
+          X[7 + k] += c.h * (Fo[bi][k] / bd[0] + c.gravity[k]);
+          X[10 + k] += c.h * dw[k];
+        }
+        for (int k = 0; k < 3; ++k) X[4 + k] += c.h * X[7 + k];
+        const Quat wq = hamilton(Quat{0.0, X[10], X[11], X[12]}, Quat{q[0], q[1], q[2], q[3]});
+        double qn[4] = {q[0] + 0.5 * c.h * wq.w, q[1] + 0.5 * c.h * wq.x, q[2] + 0.5 * c.h * wq.y,
+                        q[3] + 0.5 * c.h * wq.z};
+        const double nn = std::sqrt(((qn[0] * qn[0] + qn[1] * qn[1]) + qn[2] * qn[2]) + qn[3] * qn[3]);
+        for (int k = 0; k < 4; ++k) X[k] = qn[k] / nn;
+      }
+    }
+  }
+  const double tau = t0 + c.substeps * c.h, w2 = 2.0 * M_PI * c.freq;  // the bowl at the end time
+  for (int e = 0; e < E; ++e) {
+    double* b = state + (int64_t)e * 39;
+    for (int i = 0; i < 3; ++i) {
+      b[4 + i] = c.amp[i] * std::sin(w2 * tau);
+      b[7 + i] = c.amp[i] * w2 * std::cos(w2 * tau);
+      b[10 + i] = 0.0;
+    }
+  }
   return 0;
 }
 

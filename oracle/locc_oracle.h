@@ -89,6 +89,17 @@ int oracle_query_cells(const oracle_cfg* cfg, const float* weights, size_t n_wei
                        const float* poses, int64_t N, double* probs, uint8_t* labels, double* logits,
                        int32_t* nsel, uint32_t* cells, double* emb, double* grids);
 
+/* ---- NEXT-3: closed-loop rigid-body substeps with LOCC as the contact detector (Q31) ----
+ * sim (13 doubles): h, substeps, detector (0 crop / 1 encode-once cells), gravity[3], ks, kd,
+ * amp[3], freq, slack.  ids int32 [E][3] (body 0 = kinematic bowl); body [E][3][4] = m, Ixx, Iyy, Izz
+ * (body frame); state [E][3][13] = q, t, v, w (world) in/out; contacts int32 [E][3] = contact substeps
+ * per pair (nullable); margins [E][4] = min |logit|, min ReLU margin, min broad-phase gap, min
+ * |ks s + kd ds/dt| (nullable).  unet_w needed for detector 1. */
+int oracle_sim_run(const oracle_cfg* cfg, const float* weights, size_t n_weights, const float* unet_w,
+                   size_t n_unet, const float* points, int32_t S, int32_t K, const double* sim, int32_t E,
+                   const int32_t* ids, const double* body, double* state, double t0, int32_t* contacts,
+                   double* margins);
+
 /* Parse a weight manifest + .bin (format in include/locc.h) into `out` (canonical order).
  * Returns the float count, or a negative code; writes M, H, F. */
 int64_t oracle_load_weights(const char* manifest, float* out, size_t cap, int32_t* M, int32_t* H,
