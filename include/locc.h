@@ -174,6 +174,36 @@ locc_status locc_query_cells(locc_ctx* ctx, const int32_t* pairs, const float* p
                              float* probs, uint8_t* labels, float* logits, int32_t* nsel, uint32_t* cells,
                              float* emb, void* stream);
 
+/* ---- Closed-loop simulation step (reading Q31) ----
+ * PAPER.md:18-24, :91, :187-192 (BRAX-LOCC: objects dropped into a shaken bowl; the OCN's pose gradient
+ * gives the contact direction), SPEC.md S:638-665 (penalty resolution).  E independent environments, 3
+ * bodies each: body 0 the kinematic bowl, shaken as t = amp sin(2 pi freq tau), bodies 1, 2 dynamic;
+ * pairs (0,1), (0,2), (1,2).  One substep of length h at time tau: bowl pose; world-AABB broad phase with
+ * `slack`; the LOCC query with the pose gradient (detector 0: the crop path in the context's precision;
+ * 1: the encode-once path); contact iff unculled and logit > 0; per contact, with g_t the translational
+ * and G_w[k] = g_q . (1/2 (0, e_k) (x) q) the rotational gradient of the logit s of each body,
+ * n = |(g_t, G_w) of both bodies|, ds/dt = sum g_t . v + G_w . w, lambda = max(0, ks s + kd ds/dt):
+ * force -lambda g_t / n, torque -lambda G_w / n on the dynamic bodies; semi-implicit Euler
+ * (v += h (F/m + gravity), w += h R diag(1/I) R^T tau, t += h v, q = normalise(q + h/2 (0,w) (x) q)). */
+typedef struct {
+  double h;           /* substep length, s (dt = 0.01/4 s split into 4 substeps) */
+  int32_t substeps;   /* substeps per call */
+  int32_t detector;   /* 0 = crop path, 1 = encode-once path (needs locc_encode_shapes) */
+  float gravity[3];   /* m/s^2 */
+  float ks, kd;       /* penalty stiffness (N per logit unit) and damping (N s per logit unit) */
+  float amp[3];       /* bowl shake amplitude, m */
+  float freq;         /* bowl shake frequency, Hz */
+  float slack;        /* broad-phase AABB slack, m */
+} locc_sim_config;
+
+/* Advance E environments by cfg->substeps substeps starting at time t0.  DEVICE buffers: ids int32
+ * [E][3] shape ids; body float32 [E][3][4] = mass, body-frame principal inertia (Ixx, Iyy, Izz); state
+ * float32 [E][3][13] = q (4), t (3), v (3), w (3), world frame, updated in place; contacts int32 [E][3]
+ * (nullable) = substeps in contact per pair.  stream NULL: synchronous; else asynchronous on it.
+ * Errors: INVALID_ARG (sizes, host buffers, H/F not 256/64), STATE (weights/shapes/encoding), CUDA, OOM. */
+locc_status locc_sim_run(locc_ctx* ctx, const locc_sim_config* cfg, int32_t E, const int32_t* ids,
+                         const float* body, float* state, double t0, int32_t* contacts, void* stream);
+
 /* Switch the encoder precision of an existing context (LOCC_PREC_FP32 / LOCC_PREC_BF16). */
 locc_status locc_set_precision(locc_ctx* ctx, int32_t precision);
 

@@ -79,6 +79,16 @@ struct CellsTable {
   int M;
 };
 
+// NEXT-3 closed-loop step constants (see include/locc.h locc_sim_config).
+struct SimParams {
+  float h;
+  float g[3];
+  float ks, kd;
+  float amp[3];
+  float freq;
+  float slack;
+};
+
 // Device counters of one query (int64 atomics), zeroed per query.
 struct DevStats {
   unsigned long long kept_rows;
@@ -129,6 +139,12 @@ cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, 
 size_t unet_act_floats(int S, int M);
 cudaError_t launch_cells_select(const ShapeTable& T, const CellsTable& C, const Batch& b, int F, uint32_t* cells,
                                 float* emb_out, cudaStream_t st);
+// NEXT-3 closed loop (kernels_sim.cu)
+cudaError_t launch_sim_prepare(const ShapeTable& T, const SimParams& sp, int E, const int32_t* ids, float* state,
+                               double tau, int32_t* pairs, float* poses, uint8_t* culled, cudaStream_t st);
+cudaError_t launch_sim_integrate(const SimParams& sp, int E, const float* body, float* state, const float* logits,
+                                 const float* grad, const uint8_t* culled, int32_t* contacts, double tau_next,
+                                 cudaStream_t st);
 size_t scan_tmp_elems(int64_t G);
 size_t encoder_tc_smem_bytes();
 

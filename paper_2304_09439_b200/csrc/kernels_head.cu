@@ -507,10 +507,9 @@ cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_
       kern<<<grid, kHeadThreads, sm, st>>>(P, b, probs, labels, logits, emb, g);
       return cudaGetLastError();
     };
-    if (grad) {
-      if (b.emb_in) return cudaErrorNotSupported;
-      return run(head_tile_kernel<true, false>, sizeof(HeadGradSmem), grad);
-    }
+    if (grad)
+      return b.emb_in ? run(head_tile_kernel<true, true>, sizeof(HeadGradSmem), grad)
+                      : run(head_tile_kernel<true, false>, sizeof(HeadGradSmem), grad);
     if (b.emb_in) return run(head_tile_kernel<false, true>, sizeof(HeadSmem), nullptr);
     return run(head_tile_kernel<false, false>, sizeof(HeadSmem), nullptr);
   }

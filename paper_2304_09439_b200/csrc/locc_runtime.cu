@@ -119,6 +119,9 @@ struct locc_ctx {
   UNetParams U{};
   CellsTable cells{};
   double encode_ms = 0.0;  // device time of the last locc_encode_shapes
+  // NEXT-3 closed-loop scratch
+  int64_t sim_cap = 0;
+  DevBuf sim_pairs, sim_poses, sim_probs, sim_logits, sim_grad, sim_culled;
 };
 
 namespace {
@@ -791,6 +794,60 @@ locc_status locc_query_cells(locc_ctx* c, const int32_t* pairs, const float* pos
                              uint8_t* labels, float* logits, int32_t* nsel, uint32_t* cells, float* emb,
                              void* stream) {
   return run_query(c, pairs, poses, N, probs, labels, logits, nsel, nullptr, cells, emb, nullptr, stream, true);
+}
+
+// ---------------------------------------------------------------- NEXT-3: closed-loop substeps
+locc_status locc_sim_run(locc_ctx* c, const locc_sim_config* cfg, int32_t E, const int32_t* ids, const float* body,
+                         float* state, double t0, int32_t* contacts, void* stream) {
+  if (!c || !cfg) return fail(LOCC_E_INVALID_ARG, "null argument");
+  if (E < 0 || cfg->substeps < 1 || !(cfg->h > 0.0)) return fail(LOCC_E_INVALID_ARG, "need E >= 0, substeps >= 1, h > 0");
+  if (cfg->detector != 0 && cfg->detector != 1) return fail(LOCC_E_INVALID_ARG, "detector must be 0 or 1");
+  if (!c->has_weights || !c->has_shapes) return fail(LOCC_E_STATE, "weights and shapes must be set");
+  if (cfg->detector == 1 && !c->has_cells) return fail(LOCC_E_STATE, "detector 1 needs locc_encode_shapes");
+  if (c->cfg.H != 256 || c->cfg.F != 64) return fail(LOCC_E_INVALID_ARG, "the pose gradient is built for H = 256, F = 64");
+  if (E == 0) return LOCC_OK;
+  if (!ids || !body || !state) return fail(LOCC_E_INVALID_ARG, "ids, body and state must be non-null");
+  if (!is_device_ptr(ids) || !is_device_ptr(body) || !is_device_ptr(state) || (contacts && !is_device_ptr(contacts)))
+    return fail(LOCC_E_INVALID_ARG, "locc_sim_run takes device buffers");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  const int64_t NP = 3 * (int64_t)E;
+  if (NP > c->sim_cap) {
+    CK(c->sim_pairs.ensure(sizeof(int32_t) * 2 * NP));
+    CK(c->sim_poses.ensure(sizeof(float) * 14 * NP));
+    CK(c->sim_probs.ensure(sizeof(float) * NP));
+    CK(c->sim_logits.ensure(sizeof(float) * NP));
+    CK(c->sim_grad.ensure(sizeof(float) * 14 * NP));
+    CK(c->sim_culled.ensure(NP));
+    c->sim_cap = NP;
+  }
+  SimParams sp{};
+  sp.h = (float)cfg->h;
+  for (int i = 0; i < 3; ++i) {
+    sp.g[i] = cfg->gravity[i];
+    sp.amp[i] = cfg->amp[i];
+  }
+  sp.ks = cfg->ks;
+  sp.kd = cfg->kd;
+  sp.freq = cfg->freq;
+  sp.slack = cfg->slack;
+  if (contacts) CK(cudaMemsetAsync(contacts, 0, sizeof(int32_t) * NP, st));
+  int64_t launches = 0;
+  for (int n = 0; n < cfg->substeps; ++n) {
+    const double tau = t0 + n * cfg->h;
+    CK(launch_sim_prepare(c->T, sp, E, ids, state, tau, c->sim_pairs.as<int32_t>(), c->sim_poses.as<float>(),
+                          c->sim_culled.as<uint8_t>(), st));
+    locc_status s = run_query(c, c->sim_pairs.as<int32_t>(), c->sim_poses.as<float>(), NP, c->sim_probs.as<float>(),
+                              nullptr, c->sim_logits.as<float>(), nullptr, nullptr, nullptr, nullptr,
+                              c->sim_grad.as<float>(), st, cfg->detector == 1);
+    if (s != LOCC_OK) return s;
+    launches += c->last.kernel_launches + 2;
+    CK(launch_sim_integrate(sp, E, body, state, c->sim_logits.as<float>(), c->sim_grad.as<float>(),
+                            c->sim_culled.as<uint8_t>(), contacts, tau + cfg->h, st));
+  }
+  c->last.kernel_launches = launches;
+  if (!stream) CK(cudaStreamSynchronize(st));
+  return LOCC_OK;
 }
 
 }  // extern "C"

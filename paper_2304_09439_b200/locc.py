@@ -19,7 +19,7 @@ LOCC_PREC_BF16 = 1
 
 EXPORTS = ("locc_create", "locc_load_weights", "locc_load_weights_mem", "locc_set_shapes", "locc_query",
            "locc_query_debug", "locc_query_grad", "locc_unet_n_params", "locc_load_unet_weights_mem",
-           "locc_encode_shapes", "locc_get_cell_embeddings", "locc_query_cells", "locc_set_precision", "locc_set_timing", "locc_get_stats", "locc_destroy",
+           "locc_encode_shapes", "locc_get_cell_embeddings", "locc_query_cells", "locc_sim_run", "locc_set_precision", "locc_set_timing", "locc_get_stats", "locc_destroy",
            "locc_status_string", "locc_last_error", "locc_version")
 
 
@@ -32,6 +32,18 @@ class LoccError(RuntimeError):
 class Config(C.Structure):
     _fields_ = [("M", C.c_int32), ("H", C.c_int32), ("F", C.c_int32), ("precision", C.c_int32),
                 ("device", C.c_int32), ("reserved", C.c_int32), ("max_batch", C.c_int64)]
+
+
+class SimConfig(C.Structure):
+    _fields_ = [("h", C.c_double), ("substeps", C.c_int32), ("detector", C.c_int32), ("gravity", C.c_float * 3),
+                ("ks", C.c_float), ("kd", C.c_float), ("amp", C.c_float * 3), ("freq", C.c_float),
+                ("slack", C.c_float)]
+
+    @classmethod
+    def from_dict(cls, d):
+        return cls(d["h"], int(d["substeps"]), 1 if d.get("detector", "crop") == "cells" else 0,
+                   (C.c_float * 3)(*d["gravity"]), d["ks"], d["kd"], (C.c_float * 3)(*d["amp"]), d["freq"],
+                   d["slack"])
 
 
 class Stats(C.Structure):
@@ -67,6 +79,7 @@ def lib():
         L.locc_encode_shapes.argtypes = [vp]
         L.locc_get_cell_embeddings.argtypes = [vp, vp, vp]
         L.locc_query_cells.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]
+        L.locc_sim_run.argtypes = [vp, C.POINTER(SimConfig), i32, vp, vp, vp, C.c_double, vp, vp]
         L.locc_set_precision.argtypes = [vp, i32]
         L.locc_set_timing.argtypes = [vp, i32]
         L.locc_get_stats.argtypes = [vp, C.POINTER(Stats)]
@@ -232,6 +245,14 @@ class Locc:
         self.query_cells_into(pairs, poses, o["probs"], o["labels"], o["logits"], o.get("nsel"), o.get("cells"),
                               o.get("emb"))
         return o
+
+    # ------------------------------------------------------------- closed loop (NEXT-3)
+    def sim_run(self, sim, ids, body, state, t0=0.0, contacts=None, stream=None):
+        """locc_sim_run on device tensors: ids int32 [E][3], body [E][3][4], state [E][3][13] (in place)."""
+        cfg = SimConfig.from_dict(sim)
+        E = int(ids.shape[0])
+        _check(lib().locc_sim_run(self._h, C.byref(cfg), E, _ptr(ids), _ptr(body), _ptr(state), float(t0),
+                                  _ptr(contacts), stream))
 
     def query_debug(self, pairs, poses):
         """Host form of locc_query_debug -> dict of every output and intermediate."""

@@ -1,0 +1,87 @@
+"""GPU parity of the closed-loop substeps (NEXT-3, locc_sim_run) against oracle_sim_run.
+
+Bar (Q31): the step is piecewise smooth — contact (logit > 0), ReLU routing, the broad phase
+and the penalty clamp are decisions — so environments are compared where the oracle's decision margins
+exceed the fp32 forward error (|logit| > 1e-3, ReLU margin > 1e-5, broad-phase gap > 1e-5, |ks s + kd
+ds/dt| > 1e-4; >= 60 % of environments).  There the state agrees within 1e-3 of the largest state change
+of the step plus 1e-6 absolute (the query's fp32 logits/gradients carry ~1e-5 relative error into
+forces); contact counts are identical.
+"""
+import numpy as np
+import pytest
+
+import locc_synth as ls
+from test_oracle_network import spread
+
+pytestmark = pytest.mark.gpu
+SIM = dict(ls.SIM_DEFAULTS)
+
+
+@pytest.fixture(scope="module")
+def locc_mod():
+    from paper_2304_09439_b200 import build as b
+    b.build()
+    from paper_2304_09439_b200 import locc
+    return locc
+
+
+@pytest.fixture(scope="module")
+def world():
+    pts, _ = ls.make_shapes(10, 1500, seed=80)
+    ids, body, st = ls.make_sim_scene(pts, 64, seed=81)
+    return pts, ids, body, st
+
+
+def run_gpu(locc_mod, pts, ids, body, st, sim, unet=None, t0=0.0):
+    import torch
+    ctx = locc_mod.Locc(M=6, H=256, F=64, precision=0, device=0)
+    ctx.load_weights_mem(spread())
+    ctx.set_shapes(pts)
+    if unet is not None:
+        ctx.load_unet_weights_mem(unet)
+        ctx.encode_shapes()
+    d_ids = torch.from_numpy(ids).cuda()
+    d_body = torch.from_numpy(body).cuda()
+    d_st = torch.from_numpy(st.copy()).cuda()
+    d_con = torch.zeros(len(ids), 3, dtype=torch.int32, device="cuda")
+    ctx.sim_run(sim, d_ids, d_body, d_st, t0=t0, contacts=d_con)
+    out = d_st.cpu().numpy()
+    con = d_con.cpu().numpy()
+    ctx.close()
+    return out, con
+
+
+def compare(out, con, ref, st):
+    rst, rcon, mg = ref
+    ok = (mg[:, 0] > 1e-3) & (mg[:, 1] > 1e-5) & (mg[:, 2] > 1e-5) & (mg[:, 3] > 1e-4)
+    assert ok.mean() >= 0.6, f"only {ok.mean():.2f} of the environments away from every decision"
+    assert np.array_equal(con[ok], rcon[ok])
+    d = np.abs(rst[ok] - st[ok].astype(np.float64)).max(axis=(1, 2), keepdims=True)
+    err = np.abs(out[ok].astype(np.float64) - rst[ok])
+    assert np.all(err <= 1e-3 * d + 1e-6), f"max err {err.max():.3g}, step change {d.max():.3g}"
+    assert rcon[ok].sum() > 0
+    return ok
+
+
+@pytest.mark.parametrize("detector", ["crop", "cells"])
+def test_sim_parity(locc_mod, oracle_mod, world, detector):
+    pts, ids, body, st = world
+    sim = dict(SIM, substeps=2, detector=detector, ks=2.0)
+    unet = ls.flatten_unet(ls.make_unet_weights()) if detector == "cells" else None
+    out, con = run_gpu(locc_mod, pts, ids, body, st, sim, unet, t0=0.1)
+    ref = oracle_mod.sim_run(spread(), pts, sim, ids, body, st.astype(np.float64), t0=0.1, unet_flat=unet)
+    compare(out, con, ref, st)
+
+
+def test_sim_free_fall_gpu(locc_mod, world):
+    pts, ids, body, st = world
+    st = st.copy()
+    st[:, 1, 4] += 5.0
+    st[:, 2, 4] -= 5.0
+    sim = dict(SIM, substeps=8)
+    out, con = run_gpu(locc_mod, pts, ids, body, st, sim)
+    assert con.sum() == 0
+    h, n, g = sim["h"], 8, np.array(sim["gravity"])
+    np.testing.assert_allclose(out[:, 1:, 7:10], st[:, 1:, 7:10] + n * h * g, rtol=0, atol=1e-6)
+    np.testing.assert_allclose(out[:, 1:, 4:7], st[:, 1:, 4:7] + h * h * g * n * (n + 1) / 2, rtol=0, atol=1e-6)
+    np.testing.assert_allclose(np.linalg.norm(out[:, :, :4], axis=-1), 1.0, atol=1e-6)
