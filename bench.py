@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-grad", action="store_true", help="skip the NEXT-2 pose-gradient measurement")
     ap.add_argument("--no-cells", action="store_true", help="skip the NEXT-1 encode-once measurement")
+    ap.add_argument("--no-sim", action="store_true", help="skip the NEXT-3 closed-loop measurement")
+    ap.add_argument("--sim-envs", type=int, default=30000)
     return ap.parse_args()
 
 
@@ -330,6 +332,47 @@ def main():
                                "value": world * N / (cms / 1e3), "unit": UNIT, "ms_per_step": cms,
                                "encode_ms_per_shape_table": enc_ms, "shapes": int(len(pts)),
                                "note": "grids encoded once per shape table (not in the timed step); fp32"}
+
+    # NEXT-3: closed-loop substeps (30,000 environments, dt = 0.01/4 s in 4 substeps)
+    if not a.no_sim and not a.no_cells:
+        import locc_synth as ls
+        E = a.sim_envs
+        ids, body, st0 = ls.make_sim_scene(pts, E, seed=5 + rank)
+        d_ids = torch.from_numpy(ids).cuda()
+        d_body = torch.from_numpy(body).cuda()
+        d_con = torch.zeros(E, 3, dtype=torch.int32, device="cuda")
+        res = {}
+        for det in ("cells", "crop"):
+            sim = dict(ls.SIM_DEFAULTS, detector=det)
+            d_st = torch.from_numpy(st0).cuda()
+            t = 0.0
+            for _ in range(a.warmup):
+                ctx.sim_run(sim, d_ids, d_body, d_st, t0=t, contacts=d_con, stream=stream.cuda_stream)
+                t += sim["h"] * sim["substeps"]
+            sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+            torch.cuda.synchronize()
+            ncon = 0
+            for i in range(a.steps):
+                with torch.cuda.stream(stream):
+                    sev[i][0].record(stream)
+                ctx.sim_run(sim, d_ids, d_body, d_st, t0=t, contacts=d_con, stream=stream.cuda_stream)
+                with torch.cuda.stream(stream):
+                    sev[i][1].record(stream)
+                t += sim["h"] * sim["substeps"]
+            torch.cuda.synchronize()
+            ncon = int(d_con.sum().item())
+            sms = statistics.mean([s_.elapsed_time(e_) for s_, e_ in sev])
+            if world > 1:
+                tt = torch.tensor([sms], device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                sms = float(tt.item())
+            res[det] = {"ms_per_dt": sms, "contact_pair_substeps_last_dt": ncon,
+                        "finite_state": bool(torch.isfinite(d_st).all().item())}
+        line["closed_loop"] = {"metric": "device time per simulated dt (4 substeps), locc_sim_run",
+                               "envs_per_gpu": E, "pairs_per_substep": 3 * E, "unit": "ms",
+                               "detector_encode_once": res["cells"], "detector_crop_" + a.precision: res["crop"],
+                               "note": "PAPER.md:91/:100 scene: bowl shaken + 2 dropped objects per env; "
+                                       "query + pose gradient + penalty + semi-implicit Euler on the GPU"}
 
     # e2e: same metric through the public API with HOST buffers (pinned), copies in the timed region
     if not a.no_e2e:
