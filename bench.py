@@ -26,6 +26,13 @@ import numpy as np  # noqa: E402
 METRIC = "collision checks/sec (LOCC inference)"
 UNIT = "checks/s"
 FLOP_PER_ROW = 2 * (3 * 256 + 2 * 256 * 256)  # encoder layers 1-3 per kept row
+HEAD_FLOP = 2 * (2 * (71 * 128 + 2 * 128 * 128) + 3 * 128 * 128 + 128)  # predictor per evaluated pair
+PROJ_FLOP = 2 * 2 * 256 * 64  # the two projections to F per evaluated pair (crop path)
+
+
+def fp32_peak_tflops(mhz):
+    """FP32 FFMA peak: 148 SMs x 128 lanes x 2 flop x clock (B200_PROFILING.md unit counts)."""
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12
 
 
 def parse():
@@ -258,6 +265,14 @@ def main():
                  "traffic": traffic, "kernel": "encoder_tc_kernel" if prec else "encoder_f32_kernel",
                  "launches_per_step": subs, "flop_per_launch": FLOP_PER_ROW * kept / subs,
                  "avg_launch_ms": 1e3 * enc_s / subs, "encoder_share_of_step": (1e3 * enc_s) / ms})
+    mhz_load = clk.get("sm_mhz") or 1965.0
+    if st.get("head_ms"):
+        hf = (HEAD_FLOP + PROJ_FLOP) * st["evaluated_pairs"]
+        roof["head_tile_kernel"] = {"bound": "alu", "ms_per_step": st["head_ms"],
+                                    "achieved": hf / (st["head_ms"] / 1e3) / 1e12, "unit": "TFLOP/s",
+                                    "peak": fp32_peak_tflops(mhz_load),
+                                    "frac": hf / (st["head_ms"] / 1e3) / 1e12 / fp32_peak_tflops(mhz_load),
+                                    "flop_per_evaluated_pair": HEAD_FLOP + PROJ_FLOP}
 
     line = {"metric": METRIC, "value": world * N / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -328,7 +343,20 @@ def main():
             t = torch.tensor([cms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             cms = float(t.item())
+        ctx.set_timing(True)
+        cstep()
+        stream.synchronize()
+        cst = ctx.stats()
+        ctx.set_timing(False)
+        hf = HEAD_FLOP * cst["evaluated_pairs"]
+        mhz_load = clk.get("sm_mhz") or 1965.0
         line["encode_once"] = {"metric": "collision checks/sec, encode-once mode (locc_query_cells)",
+                               "kernels": {"cells_select_ms": cst["encoder_ms"], "head_ms": cst["head_ms"],
+                                           "head_roofline": {"bound": "alu", "unit": "TFLOP/s",
+                                                             "achieved": hf / (cst["head_ms"] / 1e3) / 1e12,
+                                                             "peak": fp32_peak_tflops(mhz_load),
+                                                             "frac": hf / (cst["head_ms"] / 1e3) / 1e12
+                                                             / fp32_peak_tflops(mhz_load)}},
                                "value": world * N / (cms / 1e3), "unit": UNIT, "ms_per_step": cms,
                                "encode_ms_per_shape_table": enc_ms, "shapes": int(len(pts)),
                                "note": "grids encoded once per shape table (not in the timed step); fp32"}

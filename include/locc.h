@@ -77,6 +77,8 @@ typedef struct {
   int64_t kernel_launches;  /* kernels the library launched for the query */
   double  encoder_ms;       /* device time of the encoder launches (CUDA events; 0 if timing off) */
   double  total_ms;         /* device time of the whole query on its stream (0 if timing off) */
+  double  head_ms;          /* device time of the predictor launches (0 if timing off); in the
+                               encode-once mode encoder_ms is the cell selection's time */
 } locc_stats;
 
 /* Create a context on cfg->device.  Out: *out (free with locc_destroy).

@@ -97,6 +97,7 @@ struct locc_ctx {
   cudaEvent_t ev[2] = {};          // whole-query timing
   cudaEvent_t ev_in[2] = {}, ev_free[2] = {};  // input buffer k & 1: uploaded / released by the kernels
   std::vector<cudaEvent_t> enc_ev;  // per sub-batch encoder start/stop pairs
+  std::vector<cudaEvent_t> head_ev;  // per sub-batch predictor stop (its start = the encoder stop)
   bool timing = false;
   bool has_weights = false, has_shapes = false;
   // parameters
@@ -275,12 +276,15 @@ locc_status read_timing(locc_ctx* c) {
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
   c->last.total_ms = ms;
-  double enc = 0.0;
+  double enc = 0.0, head = 0.0;
   for (int64_t s = 0; s < c->timed_subs; ++s) {
     CK(cudaEventElapsedTime(&ms, c->enc_ev[2 * s], c->enc_ev[2 * s + 1]));
     enc += ms;
+    CK(cudaEventElapsedTime(&ms, c->enc_ev[2 * s + 1], c->head_ev[s]));
+    head += ms;
   }
   c->last.encoder_ms = enc;
+  c->last.head_ms = head;
   c->timed_subs = 0;
   return LOCC_OK;
 }
@@ -327,6 +331,11 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
       c->enc_ev.push_back(e);
+    }
+    while ((int64_t)c->head_ev.size() < n_sub) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->head_ev.push_back(e);
     }
     CK(cudaEventRecord(c->ev[0], st));
   }
@@ -379,6 +388,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       b.emb_in = e_in;
       if (occ) CK(cudaMemsetAsync(b.occ, 0, sizeof(int32_t) * 2 * B, st));
       CK(launch_head(c->P, b, d_probs, d_labels, d_logits, nullptr, d_grad, st));
+      if (c->timing) CK(cudaEventRecord(c->head_ev[subs], st));
       if (emb) d_emb = e_in;  // the selection wrote e (0 for an empty side) in place
       launches += 2;
     } else {
@@ -415,6 +425,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     }
     if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs + 1], st));
     CK(launch_head(c->P, b, d_probs, d_labels, d_logits, d_emb, d_grad, st));
+    if (c->timing) CK(cudaEventRecord(c->head_ev[subs], st));
     launches += 7;
     }
     if (!dev) CK(cudaEventRecord(c->ev_free[subs & 1], st));  // the kernels are done with the inputs
@@ -536,6 +547,7 @@ void locc_destroy(locc_ctx* c) {
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (auto& e : c->enc_ev) cudaEventDestroy(e);
+  for (auto& e : c->head_ev) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
