@@ -1,0 +1,22 @@
+#!/bin/bash
+# ncu captures of the NEXT-mode kernels (run under gpurun, 1 GPU).  Usage: tools/profile_next.sh <tag>
+# tools/next_modes.py launches, in order: grid encode + U-Net, query_cells (select, head<0,1>),
+# query_grad (crop path, head<1,0>), closed loop (sim_prepare, select, head<1,1>, sim_integrate, ...).
+TAG=${1:-r1next}
+mkdir -p gpurun_out
+python tools/next_modes.py > gpurun_out/next_plain_$TAG.log 2>&1 || exit 1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/next_launches_$TAG.csv \
+    python tools/next_modes.py > /dev/null 2>&1
+cap() {  # name regex skip
+  ncu --set full --clock-control none --import-source on -k regex:$2 -s $3 -c 1 -o gpurun_out/next_${TAG}_$1 \
+      python tools/next_modes.py > gpurun_out/ncu_next_${TAG}_$1.log 2>&1 || true
+  ncu -i gpurun_out/next_${TAG}_$1.ncu-rep --page details > gpurun_out/next_details_${TAG}_$1.txt 2>/dev/null || true
+  ncu -i gpurun_out/next_${TAG}_$1.ncu-rep --page raw --csv > gpurun_out/next_raw_${TAG}_$1.csv 2>/dev/null || true
+}
+cap grid_encode grid_encode 0
+cap conv3d_c1 conv3d 0
+cap conv3d_d1 conv3d 7
+cap cells_select cells_select 0
+cap head_cells head_tile 0
+cap head_grad head_tile 1
+cap sim_integrate sim_integrate 0
