@@ -1,0 +1,279 @@
+// kernels_head_tc.cu — S8-S9 collision predictor on the 5th-generation tensor cores, fp32-accurate.
+//
+// Same function as head_tile_kernel ([e ; q ; t] -> 3 x 128 ReLU shared by both
+// objects -> max across the pair -> 3 x 128 ReLU -> linear -> sigmoid), for the encode-once mode where
+// e arrives pooled (Batch::emb_in).  Each layer is a [rows x K] x [K x 128] GEMM on tcgen05.mma
+// kind::tf32 with the "3xTF32" split: every fp32 operand x = hi + lo, hi = x with the low 13 mantissa
+// bits cleared (exactly representable in tf32), lo = x - hi (<= 13 significant bits, ~2 lost to tf32),
+// and A B ~= A_hi B_hi + A_hi B_lo + A_lo B_hi — relative error ~2^-21 per product, the same order as
+// fp32 FFMA summation, so the 1e-5 probability bar of the fp32 path holds (tested against the fp64
+// oracle).  Accumulators in TMEM (128 columns), operands K-major SW128 in shared memory.
+//
+// Persistent CTAs (one per SM), 64 pairs (128 sides) per tile, 6 warps:
+//   warp 0     weight producer: streams the 23 pre-split, pre-swizzled 32-K chunks of the six layers'
+//              weights (32 KB each: hi then lo) through a 2-stage ring with cp.async.bulk
+//   warp 1     MMA issuer (one elected lane): 12 MMAs (4 K-steps x 3 products) per chunk
+//   warps 2-5  epilogue (TMEM lane quadrant = warp % 4, thread = row): stage z for layer 1, then per
+//              layer tcgen05.ld the accumulator row, bias + ReLU, split, write the next layer's A
+//              operand (the max across the pair = a lane shuffle: sides 2p, 2p+1 are adjacent lanes)
+// Pair layers run M = 128 with rows 64..127 zero (64 pairs per tile).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "internal.h"
+#include "quat.cuh"
+#include "tc_ptx.cuh"
+
+namespace locc {
+namespace {
+
+using namespace tc;
+
+constexpr int kHP = 64;             // pairs per tile
+constexpr int kChunkBytes = 32768;  // one 32-K chunk of one layer: hi [128 x 32] then lo, SW128
+constexpr int kHalfChunk = 16384;
+constexpr int kLayers = 6;
+constexpr int kChunks = 23;         // obj1 3 (K = 71 padded to 96), obj2, obj3, pair1..3 4 each
+constexpr int kThreadsTC = 192;
+__constant__ int kLayerChunks[kLayers] = {3, 4, 4, 4, 4, 4};
+
+struct __align__(1024) HeadTcSmem {
+  uint8_t a_hi[4 * kHalfChunk];     // A operand, 4 K-blocks of [128 rows x 32 fp32] SW128
+  uint8_t a_lo[4 * kHalfChunk];
+  uint8_t w[2][kChunkBytes];        // weight ring
+  float bias[kLayers][128];
+  float wout[128];
+  float bout;
+  int nside[128];
+  uint64_t w_full[2], w_empty[2], a_full, d_full;
+  uint32_t tmem_base;
+};
+
+// Clear the low 13 mantissa bits: the tf32 value the tensor core reads exactly.
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+// Write 4 consecutive K values (k0 .. k0+3, k0 % 4 == 0) of row r into the split A operand.
+__device__ __forceinline__ void put4(HeadTcSmem& S, int r, int k0, float x0, float x1, float x2, float x3) {
+  const float h0 = tf32_hi(x0), h1 = tf32_hi(x1), h2 = tf32_hi(x2), h3 = tf32_hi(x3);
+  const uint32_t off = (uint32_t)(k0 >> 5) * kHalfChunk + sw128_off((uint32_t)r, (uint32_t)((k0 & 31) >> 2));
+  st_shared_v4(smem_u32(S.a_hi) + off, __float_as_uint(h0), __float_as_uint(h1), __float_as_uint(h2),
+               __float_as_uint(h3));
+  st_shared_v4(smem_u32(S.a_lo) + off, __float_as_uint(x0 - h0), __float_as_uint(x1 - h1), __float_as_uint(x2 - h2),
+               __float_as_uint(x3 - h3));
+}
+
+__global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Batch b, float* __restrict__ probs,
+                                                                uint8_t* __restrict__ labels,
+                                                                float* __restrict__ logits) {
+  extern __shared__ uint8_t smem_raw[];
+  HeadTcSmem& S = *reinterpret_cast<HeadTcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (b.B + kHP - 1) / kHP;
+  const float* bias_src = P.head_tc_bias;  // [6][128] biases, wout [128], bout
+  for (int i = threadIdx.x; i < kLayers * 128; i += kThreadsTC) S.bias[i / 128][i % 128] = bias_src[i];
+  for (int i = threadIdx.x; i < 128; i += kThreadsTC) S.wout[i] = bias_src[kLayers * 128 + i];
+  if (threadIdx.x == 0) {
+    S.bout = bias_src[kLayers * 128 + 128];
+    mbar_init(&S.w_full[0], 1);
+    mbar_init(&S.w_full[1], 1);
+    mbar_init(&S.w_empty[0], 1);
+    mbar_init(&S.w_empty[1], 1);
+    mbar_init(&S.a_full, 128);
+    mbar_init(&S.d_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_1cta(&S.tmem_base, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- weight producer
+    const uint8_t* img = static_cast<const uint8_t*>(P.head_tc_img);
+    uint32_t n = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int c = 0; c < kChunks; ++c, ++n) {
+        const int st = n & 1;
+        if (lane == 0) {
+          if (n >= 2) mbar_wait_spin(&S.w_empty[st], ((n >> 1) - 1) & 1);
+          mbar_arrive_expect_tx(&S.w_full[st], kChunkBytes);
+          bulk_g2s(S.w[st], img + (size_t)c * kChunkBytes, kChunkBytes, &S.w_full[st]);
+        }
+        __syncwarp();
+      }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = idesc_tf32_f32(128, 128);
+    const uint32_t ahi = smem_u32(S.a_hi), alo = smem_u32(S.a_lo);
+    uint32_t n = 0, aph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int l = 0; l < kLayers; ++l) {
+        mbar_wait_spin(&S.a_full, aph);
+        aph ^= 1;
+        tc_fence_after();
+        for (int j = 0; j < kLayerChunks[l]; ++j, ++n) {
+          const int st = n & 1;
+          mbar_wait_spin(&S.w_full[st], (n >> 1) & 1);
+          tc_fence_after();
+          const uint32_t bhi = smem_u32(S.w[st]), blo = bhi + kHalfChunk;
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t ao = (uint32_t)j * kHalfChunk + 32u * k, bo = 32u * k;
+              mma_tf32_ss(tmem, smem_desc_sw128(ahi + ao, 1024), smem_desc_sw128(bhi + bo, 1024), idesc,
+                          (j | k) != 0);
+              mma_tf32_ss(tmem, smem_desc_sw128(ahi + ao, 1024), smem_desc_sw128(blo + bo, 1024), idesc, 1);
+              mma_tf32_ss(tmem, smem_desc_sw128(alo + ao, 1024), smem_desc_sw128(bhi + bo, 1024), idesc, 1);
+            }
+            mma_commit_1cta(&S.w_empty[st]);
+            if (j == kLayerChunks[l] - 1) mma_commit_1cta(&S.d_full);
+          }
+          __syncwarp();
+        }
+      }
+  } else {
+    // ---------------------------------------------------------------- epilogue (warps 2..5)
+    const int q = warp & 3, r = 32 * q + lane;  // TMEM lane quadrant, row
+    const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
+    uint32_t dph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int64_t i0 = t * kHP;
+      const int npairs = (int)min((int64_t)kHP, b.B - i0);
+      // z = [e ; canonical q ; t ; 0...] (K = 96) for side r (e = 0 for an empty side)
+      {
+        float z[8];
+        const bool live = r < 2 * npairs;
+        const int64_t g = 2 * i0 + r;
+        const int ns = live ? b.counts[g] : 0;
+        S.nside[r] = ns;
+        const float4* e4 = reinterpret_cast<const float4*>(b.emb_in + g * 64);
+        for (int k0 = 0; k0 < 64; k0 += 4) {
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (ns > 0) v = __ldg(e4 + (k0 >> 2));
+          put4(S, r, k0, v.x, v.y, v.z, v.w);
+        }
+        for (int c = 0; c < 8; ++c) z[c] = 0.f;
+        if (live) {
+          const float* pose = b.poses + g * 7;
+          double qd[4] = {1.0, 0.0, 0.0, 0.0};
+          quat_unit(pose, qd);
+          double sg = 1.0;
+          for (int c = 0; c < 4; ++c)
+            if (qd[c] != 0.0) {
+              sg = qd[c] > 0.0 ? 1.0 : -1.0;
+              break;
+            }
+          for (int c = 0; c < 4; ++c) z[c] = __double2float_rn(sg * qd[c]);
+          for (int c = 0; c < 3; ++c) z[4 + c] = pose[4 + c];
+        }
+        put4(S, r, 64, z[0], z[1], z[2], z[3]);
+        put4(S, r, 68, z[4], z[5], z[6], 0.f);
+        for (int k0 = 72; k0 < 96; k0 += 4) put4(S, r, k0, 0.f, 0.f, 0.f, 0.f);
+      }
+      fence_proxy_async_smem();
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // nside of every side visible to the output rows
+      tc_fence_before();
+      mbar_arrive(&S.a_full);
+      for (int l = 0; l < kLayers; ++l) {
+        mbar_wait(&S.d_full, dph);
+        dph ^= 1;
+        tc_fence_after();
+        const float* bl = S.bias[l];
+        if (l < 2 || (l >= 3 && l < 5)) {
+          // hidden layer: ReLU(D + b) -> next A (pair layers: rows >= 64 are padding -> 0)
+          const bool pad = l >= 3 && r >= 64;
+#pragma unroll 1
+          for (int c0 = 0; c0 < 128; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(trow + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 32; k += 4) {
+              float x[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) x[u] = pad ? 0.f : fmaxf(__uint_as_float(v[k + u]) + bl[c0 + k + u], 0.f);
+              put4(S, r, c0 + k, x[0], x[1], x[2], x[3]);
+            }
+          }
+        } else if (l == 2) {
+          // object layer 3, then the max across the pair: pair p = r / 2 (even lanes) -> row p,
+          // odd lanes write the padding rows 64 + (r - 1) / 2 as 0
+          const int prow = (r & 1) ? 64 + (r >> 1) : (r >> 1);
+#pragma unroll 1
+          for (int c0 = 0; c0 < 128; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(trow + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 32; k += 4) {
+              float x[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float mine = fmaxf(__uint_as_float(v[k + u]) + bl[c0 + k + u], 0.f);
+                const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
+                x[u] = (r & 1) ? 0.f : fmaxf(mine, other);
+              }
+              put4(S, prow, c0 + k, x[0], x[1], x[2], x[3]);
+            }
+          }
+        } else {
+          // pair layer 3 + output unit: row p < 64 = pair p
+          float acc = 0.f;
+#pragma unroll 1
+          for (int c0 = 0; c0 < 128; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(trow + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              acc = fmaf(S.wout[c0 + k], fmaxf(__uint_as_float(v[k]) + bl[c0 + k], 0.f), acc);
+          }
+          if (r < npairs) {
+            const int64_t i = i0 + r;
+            float lg, pr;
+            if (S.nside[2 * r] + S.nside[2 * r + 1] == 0) {
+              lg = -INFINITY;
+              pr = 0.f;
+            } else {
+              lg = acc + S.bout;
+              pr = 1.f / (1.f + expf(-lg));
+              atomicAdd(&b.stats->evaluated_pairs, 1ull);
+            }
+            probs[i] = pr;
+            if (labels) labels[i] = pr > 0.5f ? 1 : 0;
+            if (logits) logits[i] = lg;
+          }
+        }
+        if (l < kLayers - 1) {
+          fence_proxy_async_smem();
+          tc_fence_before();
+          mbar_arrive(&S.a_full);
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // this tile's nside reads precede the next tile's writes
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc_1cta(tmem, 128);
+}
+
+}  // namespace
+
+size_t head_tc_smem_bytes() { return sizeof(HeadTcSmem) + 1024; }
+
+cudaError_t launch_head_tc(const DevParams& P, const Batch& b, float* probs, uint8_t* labels, float* logits,
+                           int num_sms, cudaStream_t st) {
+  if (b.B == 0) return cudaSuccess;
+  static const cudaError_t attr = cudaFuncSetAttribute(head_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)head_tc_smem_bytes());
+  if (attr != cudaSuccess) return attr;
+  const int64_t ntiles = (b.B + kHP - 1) / kHP;
+  const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
+  head_tc_kernel<<<grid, kThreadsTC, head_tc_smem_bytes(), st>>>(P, b, probs, labels, logits);
+  return cudaGetLastError();
+}
+
+}  // namespace locc

@@ -101,7 +101,7 @@ struct locc_ctx {
   bool timing = false;
   bool has_weights = false, has_shapes = false;
   // parameters
-  DevBuf params, tc_img;
+  DevBuf params, tc_img, head_tc_img;
   DevParams P{};
   TcL1 tc_l1{};
   // shapes
@@ -192,6 +192,12 @@ locc_status upload_params(locc_ctx* c, const float* flat) {
   push(p1.W, (size_t)P * P);
   push(p2.W, (size_t)P * P);
   push(p3.W, (size_t)P * P);
+  // 27: tensor-core predictor bias block [6][128] + wout [128] + bout
+  std::vector<float> hb;
+  for (const L* l : {&o1, &o2, &o3, &p1, &p2, &p3}) hb.insert(hb.end(), l->b, l->b + P);
+  hb.insert(hb.end(), out.W, out.W + P);
+  hb.push_back(out.b[0]);
+  push(hb.data(), hb.size());
   const size_t bytes = img.size() * sizeof(float);
   CK(c->params.ensure(bytes));
   CK(cudaMemcpy(c->params.p, img.data(), bytes, cudaMemcpyHostToDevice));
@@ -227,6 +233,37 @@ locc_status upload_params(locc_ctx* c, const float* flat) {
   D.p1 = d + off[24];
   D.p2 = d + off[25];
   D.p3 = d + off[26];
+  D.head_tc_bias = d + off[27];
+  // tensor-core predictor weights: per layer, 32-K chunks of [128 out x 32 in] K-major SW128 images,
+  // tf32 hi (low 13 mantissa bits cleared) then lo = w - hi (see kernels_head_tc.cu)
+  D.head_tc_img = nullptr;
+  if (F + 7 <= 96) {
+    std::vector<uint8_t> himg;
+    for (const L* l : {&o1, &o2, &o3, &p1, &p2, &p3}) {
+      const int nch = (l->i + 31) / 32;
+      for (int j = 0; j < nch; ++j) {
+        const size_t base = himg.size();
+        himg.resize(base + 32768, 0);
+        for (int n = 0; n < P; ++n)
+          for (int k = 0; k < 32; ++k) {
+            const int kk = 32 * j + k;
+            const float w = kk < l->i ? l->W[(size_t)n * l->i + kk] : 0.f;
+            uint32_t u;
+            std::memcpy(&u, &w, 4);
+            u &= 0xFFFFE000u;
+            float hi;
+            std::memcpy(&hi, &u, 4);
+            const float lo = w - hi;
+            const size_t off = tc::sw128_off((uint32_t)n, (uint32_t)(k >> 2)) + (size_t)(k & 3) * 4;
+            std::memcpy(&himg[base + off], &hi, 4);
+            std::memcpy(&himg[base + 16384 + off], &lo, 4);
+          }
+      }
+    }
+    CK(c->head_tc_img.ensure(himg.size()));
+    CK(cudaMemcpy(c->head_tc_img.p, himg.data(), himg.size(), cudaMemcpyHostToDevice));
+    D.head_tc_img = c->head_tc_img.p;
+  }
   D.tc_w2 = nullptr;
   D.tc_w3 = nullptr;
   c->has_weights = true;
@@ -387,7 +424,10 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs + 1], st));
       b.emb_in = e_in;
       if (occ) CK(cudaMemsetAsync(b.occ, 0, sizeof(int32_t) * 2 * B, st));
-      CK(launch_head(c->P, b, d_probs, d_labels, d_logits, nullptr, d_grad, st));
+      if (!d_grad && c->P.head_tc_img && c->cfg.F == 64 && !getenv("LOCC_HEAD_FFMA"))
+        CK(launch_head_tc(c->P, b, d_probs, d_labels, d_logits, c->num_sms, st));
+      else
+        CK(launch_head(c->P, b, d_probs, d_labels, d_logits, nullptr, d_grad, st));
       if (c->timing) CK(cudaEventRecord(c->head_ev[subs], st));
       if (emb) d_emb = e_in;  // the selection wrote e (0 for an empty side) in place
       launches += 2;
