@@ -350,13 +350,21 @@ def main():
         ctx.set_timing(False)
         hf = HEAD_FLOP * cst["evaluated_pairs"]
         mhz_load = clk.get("sm_mhz") or 1965.0
+        if os.environ.get("LOCC_HEAD_FFMA"):
+            hroof = {"kernel": "head_tile_kernel", "bound": "alu", "peak": fp32_peak_tflops(mhz_load),
+                     "peak_source": "148 SM x 128 FP32 FMA/clk x 2 x median SM clock"}
+        else:
+            # 3xTF32 on tcgen05: the fp32-accurate contraction costs three tf32 products, so its peak is
+            # the tf32 peak / 3; tf32 peak = measured sustained bf16 x the guide's nominal 1.1 / 2.25
+            tf32 = peaks.get("bf16_tflops_sustained", 1374.0) * 1.1 / 2.25
+            hroof = {"kernel": "head_tc_kernel", "bound": "tensor", "peak": tf32 / 3,
+                     "peak_source": "MEASURED_PEAKS bf16 sustained x 1.1/2.25 (tf32) / 3 (3xTF32 split)"}
+        hroof.update({"unit": "TFLOP/s", "achieved": hf / (cst["head_ms"] / 1e3) / 1e12,
+                      "frac": hf / (cst["head_ms"] / 1e3) / 1e12 / hroof["peak"],
+                      "flop_per_evaluated_pair": HEAD_FLOP})
         line["encode_once"] = {"metric": "collision checks/sec, encode-once mode (locc_query_cells)",
                                "kernels": {"cells_select_ms": cst["encoder_ms"], "head_ms": cst["head_ms"],
-                                           "head_roofline": {"bound": "alu", "unit": "TFLOP/s",
-                                                             "achieved": hf / (cst["head_ms"] / 1e3) / 1e12,
-                                                             "peak": fp32_peak_tflops(mhz_load),
-                                                             "frac": hf / (cst["head_ms"] / 1e3) / 1e12
-                                                             / fp32_peak_tflops(mhz_load)}},
+                                           "head_roofline": hroof},
                                "value": world * N / (cms / 1e3), "unit": UNIT, "ms_per_step": cms,
                                "encode_ms_per_shape_table": enc_ms, "shapes": int(len(pts)),
                                "note": "grids encoded once per shape table (not in the timed step); fp32"}

@@ -3,11 +3,10 @@
 // Same function as head_tile_kernel ([e ; q ; t] -> 3 x 128 ReLU shared by both
 // objects -> max across the pair -> 3 x 128 ReLU -> linear -> sigmoid), for the encode-once mode where
 // e arrives pooled (Batch::emb_in).  Each layer is a [rows x K] x [K x 128] GEMM on tcgen05.mma
-// kind::tf32 with the "3xTF32" split: every fp32 operand x = hi + lo, hi = x with the low 13 mantissa
-// bits cleared (exactly representable in tf32), lo = x - hi (<= 13 significant bits, ~2 lost to tf32),
-// and A B ~= A_hi B_hi + A_hi B_lo + A_lo B_hi — relative error ~2^-21 per product, the same order as
-// fp32 FFMA summation, so the 1e-5 probability bar of the fp32 path holds (tested against the fp64
-// oracle).  Accumulators in TMEM (128 columns), operands K-major SW128 in shared memory.
+// kind::tf32 with the "3xTF32" split: every fp32 operand x = hi + lo, hi = tf32(x) and lo = tf32(x - hi),
+// both rounded to nearest (so the tensor core reads them exactly), and A B ~= A_hi B_hi + A_hi B_lo +
+// A_lo B_hi — relative error ~2^-22 per product (the dropped lo lo term), the order of fp32 FFMA
+// summation, so the 1e-5 probability bar of the fp32 path holds (tested against the fp64 oracle).  Accumulators in TMEM (128 columns), operands K-major SW128 in shared memory.
 //
 // Persistent CTAs (one per SM), 64 pairs (128 sides) per tile, 6 warps:
 //   warp 0     weight producer: streams the 23 pre-split, pre-swizzled 32-K chunks of the six layers'
@@ -45,34 +44,44 @@ struct __align__(1024) HeadTcSmem {
   float bias[kLayers][128];
   float wout[128];
   float bout;
+  float bf[64];
   int nside[128];
   uint64_t w_full[2], w_empty[2], a_full, d_full;
   uint32_t tmem_base;
 };
 
-// Clear the low 13 mantissa bits: the tf32 value the tensor core reads exactly.
-__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// Round to the nearest tf32 (ties away): a value the tensor core reads exactly.
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
 
-// Write 4 consecutive K values (k0 .. k0+3, k0 % 4 == 0) of row r into the split A operand.
+// Write 4 consecutive K values (k0 .. k0+3, k0 % 4 == 0) of row r into the split A operand:
+// hi = tf32(x), lo = tf32(x - hi) (x - hi is exact in fp32; |lo| <= 2^-11 |x|, error <= 2^-23 |x|).
 __device__ __forceinline__ void put4(HeadTcSmem& S, int r, int k0, float x0, float x1, float x2, float x3) {
-  const float h0 = tf32_hi(x0), h1 = tf32_hi(x1), h2 = tf32_hi(x2), h3 = tf32_hi(x3);
+  const float h0 = tf32_rna(x0), h1 = tf32_rna(x1), h2 = tf32_rna(x2), h3 = tf32_rna(x3);
   const uint32_t off = (uint32_t)(k0 >> 5) * kHalfChunk + sw128_off((uint32_t)r, (uint32_t)((k0 & 31) >> 2));
   st_shared_v4(smem_u32(S.a_hi) + off, __float_as_uint(h0), __float_as_uint(h1), __float_as_uint(h2),
                __float_as_uint(h3));
-  st_shared_v4(smem_u32(S.a_lo) + off, __float_as_uint(x0 - h0), __float_as_uint(x1 - h1), __float_as_uint(x2 - h2),
-               __float_as_uint(x3 - h3));
+  st_shared_v4(smem_u32(S.a_lo) + off, __float_as_uint(tf32_rna(x0 - h0)), __float_as_uint(tf32_rna(x1 - h1)),
+               __float_as_uint(tf32_rna(x2 - h2)), __float_as_uint(tf32_rna(x3 - h3)));
 }
 
+// kProj (crop path): e = W_F m + b_F is computed first on the tensor cores too — two passes of 4 K-chunks
+// (m = the pooled 256-vector, staged 128 K at a time into the A buffer), N = 64, then z as above.
+template <bool kProj>
 __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Batch b, float* __restrict__ probs,
                                                                 uint8_t* __restrict__ labels,
-                                                                float* __restrict__ logits) {
+                                                                float* __restrict__ logits, float* __restrict__ emb) {
   extern __shared__ uint8_t smem_raw[];
   HeadTcSmem& S = *reinterpret_cast<HeadTcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (b.B + kHP - 1) / kHP;
-  const float* bias_src = P.head_tc_bias;  // [6][128] biases, wout [128], bout
+  const float* bias_src = P.head_tc_bias;  // [6][128] biases, wout [128], bout, b_F [64]
   for (int i = threadIdx.x; i < kLayers * 128; i += kThreadsTC) S.bias[i / 128][i % 128] = bias_src[i];
   for (int i = threadIdx.x; i < 128; i += kThreadsTC) S.wout[i] = bias_src[kLayers * 128 + i];
+  for (int i = threadIdx.x; i < 64; i += kThreadsTC) S.bf[i] = bias_src[kLayers * 128 + 129 + i];
   if (threadIdx.x == 0) {
     S.bout = bias_src[kLayers * 128 + 128];
     mbar_init(&S.w_full[0], 1);
@@ -92,28 +101,34 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
   if (warp == 0) {
     // ---------------------------------------------------------------- weight producer
     const uint8_t* img = static_cast<const uint8_t*>(P.head_tc_img);
+    const uint8_t* pimg = static_cast<const uint8_t*>(P.head_tc_proj);
+    constexpr int kPre = kProj ? 8 : 0;
     uint32_t n = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
-      for (int c = 0; c < kChunks; ++c, ++n) {
+      for (int c = 0; c < kPre + kChunks; ++c, ++n) {
         const int st = n & 1;
         if (lane == 0) {
           if (n >= 2) mbar_wait_spin(&S.w_empty[st], ((n >> 1) - 1) & 1);
           mbar_arrive_expect_tx(&S.w_full[st], kChunkBytes);
-          bulk_g2s(S.w[st], img + (size_t)c * kChunkBytes, kChunkBytes, &S.w_full[st]);
+          const uint8_t* src = c < kPre ? pimg + (size_t)c * kChunkBytes : img + (size_t)(c - kPre) * kChunkBytes;
+          bulk_g2s(S.w[st], src, kChunkBytes, &S.w_full[st]);
         }
         __syncwarp();
       }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc = idesc_tf32_f32(128, 128);
     const uint32_t ahi = smem_u32(S.a_hi), alo = smem_u32(S.a_lo);
+    constexpr int kL0 = kProj ? -2 : 0;
     uint32_t n = 0, aph = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
-      for (int l = 0; l < kLayers; ++l) {
+      for (int l = kL0; l < kLayers; ++l) {
+        // l = -2, -1: the projection's two K halves (N = 64; the second accumulates onto the first)
+        const uint32_t idesc = l < 0 ? idesc_tf32_f32(128, 64) : idesc_tf32_f32(128, 128);
+        const int nch = l < 0 ? 4 : kLayerChunks[l];
         mbar_wait_spin(&S.a_full, aph);
         aph ^= 1;
         tc_fence_after();
-        for (int j = 0; j < kLayerChunks[l]; ++j, ++n) {
+        for (int j = 0; j < nch; ++j, ++n) {
           const int st = n & 1;
           mbar_wait_spin(&S.w_full[st], (n >> 1) & 1);
           tc_fence_after();
@@ -123,12 +138,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
             for (int k = 0; k < 4; ++k) {
               const uint32_t ao = (uint32_t)j * kHalfChunk + 32u * k, bo = 32u * k;
               mma_tf32_ss(tmem, smem_desc_sw128(ahi + ao, 1024), smem_desc_sw128(bhi + bo, 1024), idesc,
-                          (j | k) != 0);
+                          (l == -1) || (j | k) != 0);
               mma_tf32_ss(tmem, smem_desc_sw128(ahi + ao, 1024), smem_desc_sw128(blo + bo, 1024), idesc, 1);
               mma_tf32_ss(tmem, smem_desc_sw128(alo + ao, 1024), smem_desc_sw128(bhi + bo, 1024), idesc, 1);
             }
             mma_commit_1cta(&S.w_empty[st]);
-            if (j == kLayerChunks[l] - 1) mma_commit_1cta(&S.d_full);
+            if (j == nch - 1) mma_commit_1cta(&S.d_full);
           }
           __syncwarp();
         }
@@ -148,11 +163,47 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
         const int64_t g = 2 * i0 + r;
         const int ns = live ? b.counts[g] : 0;
         S.nside[r] = ns;
-        const float4* e4 = reinterpret_cast<const float4*>(b.emb_in + g * 64);
-        for (int k0 = 0; k0 < 64; k0 += 4) {
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (ns > 0) v = __ldg(e4 + (k0 >> 2));
-          put4(S, r, k0, v.x, v.y, v.z, v.w);
+        if constexpr (kProj) {
+          // m (the pooled 256-vector) in two K halves through the A buffer; e = D + b_F afterwards
+          const float4* m4 = reinterpret_cast<const float4*>(b.pooled + g * 256);
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1) {
+              mbar_wait(&S.d_full, dph);  // the first half has been consumed
+              dph ^= 1;
+            }
+            for (int k0 = 0; k0 < 128; k0 += 4) {
+              float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (ns > 0) v = __ldg(m4 + ((128 * h + k0) >> 2));
+              put4(S, r, k0, v.x, v.y, v.z, v.w);
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(&S.a_full);
+          }
+          mbar_wait(&S.d_full, dph);
+          dph ^= 1;
+          tc_fence_after();
+#pragma unroll 1
+          for (int c0 = 0; c0 < 64; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(trow + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 32; k += 4) {
+              float x[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) x[u] = ns > 0 ? __uint_as_float(v[k + u]) + S.bf[c0 + k + u] : 0.f;
+              put4(S, r, c0 + k, x[0], x[1], x[2], x[3]);
+              if (emb && live) *reinterpret_cast<float4*>(emb + g * 64 + c0 + k) = make_float4(x[0], x[1], x[2], x[3]);
+            }
+          }
+        } else {
+          const float4* e4 = reinterpret_cast<const float4*>(b.emb_in + g * 64);
+          for (int k0 = 0; k0 < 64; k0 += 4) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (ns > 0) v = __ldg(e4 + (k0 >> 2));
+            put4(S, r, k0, v.x, v.y, v.z, v.w);
+          }
         }
         for (int c = 0; c < 8; ++c) z[c] = 0.f;
         if (live) {
@@ -265,14 +316,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
 size_t head_tc_smem_bytes() { return sizeof(HeadTcSmem) + 1024; }
 
 cudaError_t launch_head_tc(const DevParams& P, const Batch& b, float* probs, uint8_t* labels, float* logits,
-                           int num_sms, cudaStream_t st) {
+                           float* emb, int num_sms, cudaStream_t st) {
   if (b.B == 0) return cudaSuccess;
-  static const cudaError_t attr = cudaFuncSetAttribute(head_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)head_tc_smem_bytes());
-  if (attr != cudaSuccess) return attr;
+  const bool proj = b.emb_in == nullptr;  // crop path: project the pooled vectors first
+  static const cudaError_t attr0 = cudaFuncSetAttribute(
+      head_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)head_tc_smem_bytes());
+  static const cudaError_t attr1 = cudaFuncSetAttribute(
+      head_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)head_tc_smem_bytes());
+  if (attr0 != cudaSuccess) return attr0;
+  if (attr1 != cudaSuccess) return attr1;
   const int64_t ntiles = (b.B + kHP - 1) / kHP;
   const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
-  head_tc_kernel<<<grid, kThreadsTC, head_tc_smem_bytes(), st>>>(P, b, probs, labels, logits);
+  if (proj)
+    head_tc_kernel<true><<<grid, kThreadsTC, head_tc_smem_bytes(), st>>>(P, b, probs, labels, logits, emb);
+  else
+    head_tc_kernel<false><<<grid, kThreadsTC, head_tc_smem_bytes(), st>>>(P, b, probs, labels, logits, nullptr);
   return cudaGetLastError();
 }
 

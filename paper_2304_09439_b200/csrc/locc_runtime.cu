@@ -127,6 +127,16 @@ struct locc_ctx {
 
 namespace {
 
+// fp32 -> nearest tf32 (ties away from zero), kept in an fp32 container: what cvt.rna.tf32.f32 does.
+float tf32_rna_host(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & 0xFFFFE000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
 // Derived device layouts of the canonical flat parameter vector (see internal.h DevParams).
 locc_status upload_params(locc_ctx* c, const float* flat) {
   const int H = c->cfg.H, F = c->cfg.F, P = kPredW;
@@ -197,6 +207,7 @@ locc_status upload_params(locc_ctx* c, const float* flat) {
   for (const L* l : {&o1, &o2, &o3, &p1, &p2, &p3}) hb.insert(hb.end(), l->b, l->b + P);
   hb.insert(hb.end(), out.W, out.W + P);
   hb.push_back(out.b[0]);
+  hb.insert(hb.end(), pj.b, pj.b + F);
   push(hb.data(), hb.size());
   const size_t bytes = img.size() * sizeof(float);
   CK(c->params.ensure(bytes));
@@ -235,8 +246,9 @@ locc_status upload_params(locc_ctx* c, const float* flat) {
   D.p3 = d + off[26];
   D.head_tc_bias = d + off[27];
   // tensor-core predictor weights: per layer, 32-K chunks of [128 out x 32 in] K-major SW128 images,
-  // tf32 hi (low 13 mantissa bits cleared) then lo = w - hi (see kernels_head_tc.cu)
+  // hi = tf32(w) then lo = tf32(w - hi) (see kernels_head_tc.cu)
   D.head_tc_img = nullptr;
+  D.head_tc_proj = nullptr;
   if (F + 7 <= 96) {
     std::vector<uint8_t> himg;
     for (const L* l : {&o1, &o2, &o3, &p1, &p2, &p3}) {
@@ -248,21 +260,34 @@ locc_status upload_params(locc_ctx* c, const float* flat) {
           for (int k = 0; k < 32; ++k) {
             const int kk = 32 * j + k;
             const float w = kk < l->i ? l->W[(size_t)n * l->i + kk] : 0.f;
-            uint32_t u;
-            std::memcpy(&u, &w, 4);
-            u &= 0xFFFFE000u;
-            float hi;
-            std::memcpy(&hi, &u, 4);
-            const float lo = w - hi;
+            const float hi = tf32_rna_host(w);
+            const float lo = tf32_rna_host(w - hi);
             const size_t off = tc::sw128_off((uint32_t)n, (uint32_t)(k >> 2)) + (size_t)(k & 3) * 4;
             std::memcpy(&himg[base + off], &hi, 4);
             std::memcpy(&himg[base + 16384 + off], &lo, 4);
           }
       }
     }
+    // the projection W_F [F][H] as 8 chunks of [64 rows x 32 K] (rows 64..127 of each chunk unused)
+    const size_t proj_at = himg.size();
+    if (H == 256 && F == 64)
+      for (int j = 0; j < 8; ++j) {
+        const size_t base = himg.size();
+        himg.resize(base + 32768, 0);
+        for (int n = 0; n < F; ++n)
+          for (int k = 0; k < 32; ++k) {
+            const float w = pj.W[(size_t)n * H + 32 * j + k];
+            const float hi = tf32_rna_host(w);
+            const float lo = tf32_rna_host(w - hi);
+            const size_t off = tc::sw128_off((uint32_t)n, (uint32_t)(k >> 2)) + (size_t)(k & 3) * 4;
+            std::memcpy(&himg[base + off], &hi, 4);
+            std::memcpy(&himg[base + 16384 + off], &lo, 4);
+          }
+      }
     CK(c->head_tc_img.ensure(himg.size()));
     CK(cudaMemcpy(c->head_tc_img.p, himg.data(), himg.size(), cudaMemcpyHostToDevice));
     D.head_tc_img = c->head_tc_img.p;
+    D.head_tc_proj = (H == 256 && F == 64) ? static_cast<const uint8_t*>(c->head_tc_img.p) + proj_at : nullptr;
   }
   D.tc_w2 = nullptr;
   D.tc_w3 = nullptr;
@@ -296,6 +321,12 @@ locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks, bool need_gr
   if (need_masks) CK(c->out_masks.ensure(sizeof(uint32_t) * (size_t)G * ((K + 31) / 32)));
   if (need_grad) CK(c->out_grad.ensure(sizeof(float) * (size_t)14 * c->cap_B));
   return LOCC_OK;
+}
+
+// The predictor runs on the tensor cores (3xTF32, kernels_head_tc.cu) in LOCC_PREC_BF16 contexts; the
+// LOCC_PREC_FP32 parity path keeps the CUDA-core fp32 predictor (reading Q32).
+bool use_head_tc(const locc_ctx* c) {
+  return c->cfg.precision == LOCC_PREC_BF16 && c->P.head_tc_img && !getenv("LOCC_HEAD_FFMA");
 }
 
 int64_t batch_cap(const locc_ctx* c) {
@@ -424,8 +455,8 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs + 1], st));
       b.emb_in = e_in;
       if (occ) CK(cudaMemsetAsync(b.occ, 0, sizeof(int32_t) * 2 * B, st));
-      if (!d_grad && c->P.head_tc_img && c->cfg.F == 64 && !getenv("LOCC_HEAD_FFMA"))
-        CK(launch_head_tc(c->P, b, d_probs, d_labels, d_logits, c->num_sms, st));
+      if (use_head_tc(c) && !d_grad && c->cfg.F == 64)
+        CK(launch_head_tc(c->P, b, d_probs, d_labels, d_logits, nullptr, c->num_sms, st));
       else
         CK(launch_head(c->P, b, d_probs, d_labels, d_logits, nullptr, d_grad, st));
       if (c->timing) CK(cudaEventRecord(c->head_ev[subs], st));
@@ -464,7 +495,10 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       CK(launch_encoder_f32(c->P, b, st));
     }
     if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs + 1], st));
-    CK(launch_head(c->P, b, d_probs, d_labels, d_logits, d_emb, d_grad, st));
+    if (use_head_tc(c) && !d_grad && c->P.head_tc_proj)
+      CK(launch_head_tc(c->P, b, d_probs, d_labels, d_logits, d_emb, c->num_sms, st));
+    else
+      CK(launch_head(c->P, b, d_probs, d_labels, d_logits, d_emb, d_grad, st));
     if (c->timing) CK(cudaEventRecord(c->head_ev[subs], st));
     launches += 7;
     }

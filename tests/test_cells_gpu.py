@@ -81,6 +81,27 @@ def test_cells_parity(locc_mod, wl, wl_oracle, weights):
     assert_cells_parity(got, wl_oracle, E, pairs)
 
 
+def test_cells_parity_tensor_core_predictor(locc_mod, wl, wl_oracle, weights):
+    """bf16 contexts run the predictor on the tensor cores (3xTF32 split, Q32): selection and
+    pooled e are the same kernels (bit-exact / 2e-5), probabilities within 2e-5 of the fp64 oracle."""
+    pts, pairs, poses = wl
+    ctx = locc_mod.Locc(M=6, H=256, F=64, precision=1, device=0, max_batch=128)
+    ctx.load_weights_mem(weights[0])
+    ctx.load_unet_weights_mem(weights[1])
+    ctx.set_shapes(pts)
+    ctx.encode_shapes()
+    got = ctx.query_cells(pairs, poses, debug=True)
+    ctx.close()
+    ref = wl_oracle
+    assert np.array_equal(got["cells"], ref["cells"]) and np.array_equal(got["nsel"], ref["nsel"])
+    short = ref["nsel"].sum(1) == 0
+    assert np.all(got["probs"][short] == 0) and np.all(np.isneginf(got["logits"][short]))
+    dp = np.abs(got["probs"].astype(np.float64) - ref["probs"]).max()
+    assert dp <= 2e-5, f"max |dp| = {dp:.3g}"
+    band = np.abs(ref["probs"] - 0.5) <= 1e-3
+    assert np.array_equal(got["labels"][~band], ref["labels"][~band])
+
+
 def test_cells_probe_weights_gpu(locc_mod, oracle_mod, wl):
     """The identity-encoder / delta-kernel U-Net probe (closed form pinned in test_oracle_cells):
     the device grids reproduce the oracle's exactly up to fp32 rounding of the copied values."""

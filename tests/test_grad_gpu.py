@@ -7,7 +7,8 @@ forward's error (>= 90% of the pairs on this workload).  There both paths agree 
 pair's gradient scale max(1, max|g|) — the fp32 path against the fp64 oracle, the bf16 path against
 the bf16-emulating oracle (measured: <= 1.7e-6).  Against the fp64 oracle the bf16 path's gradient
 is NOT close (bf16 embeddings move many ReLU decisions): a property of the bf16 encoder, not of the
-gradient kernel.  The forward outputs of locc_query_grad are the same bits as locc_query's;
+gradient kernel.  The forward outputs of locc_query_grad are locc_query's bits in fp32 contexts and
+within 2e-5 in bf16 contexts (whose locc_query predictor is the 3xTF32 tensor-core kernel);
 short-circuited pairs have a zero gradient.
 """
 import numpy as np
@@ -76,7 +77,12 @@ def test_grad_parity_host(locc_mod, wl, wl_oracle, spread_flat, precision):
     with make_ctx(locc_mod, spread_flat, pts, precision, max_batch=256) as ctx:
         pr, lb, lg, g = ctx.query_grad(pairs, poses)
         pr0, lb0, lg0 = ctx.query(pairs, poses)
-    assert np.array_equal(pr, pr0) and np.array_equal(lb, lb0) and np.array_equal(lg, lg0)
+    if precision == 0:  # same fp32 predictor kernel family: the same bits
+        assert np.array_equal(pr, pr0) and np.array_equal(lb, lb0) and np.array_equal(lg, lg0)
+    else:  # bf16 contexts run locc_query's predictor on the tensor cores (3xTF32, Q32)
+        assert np.abs(pr - pr0).max() <= 2e-5 and np.array_equal(np.isneginf(lg), np.isneginf(lg0))
+        band = np.abs(pr0 - 0.5) <= 1e-4
+        assert np.array_equal(lb[~band], lb0[~band])
     check_grad(g, wl_oracle[precision == 1], precision)
 
 

@@ -294,3 +294,21 @@ def test_c3_full_size_bf16(locc_mod, oracle_mod, spread_flat):
     band = np.abs(ref["probs"] - 0.5) <= 1e-3
     assert np.array_equal(lb[idx][~band], ref["labels"][~band])
     assert np.array_equal(dbg["kept"][:64], ref["kept"])
+
+
+def test_tensor_core_predictor_vs_fp32_predictor(locc_mod, spread_flat):
+    """Crop path in a bf16 context: the 3xTF32 tensor-core predictor (Q32) against the CUDA-core fp32
+    predictor on the same embeddings (LOCC_HEAD_FFMA switches the kernel): |dp| <= 2e-5, labels equal
+    outside the 1e-4 band, the same short-circuits."""
+    wl = ls.make_workload("C1", N=2000, S=64)
+    with make_ctx(locc_mod, spread_flat, wl.points, 1) as ctx:
+        p_tc, l_tc, g_tc = ctx.query(wl.pairs, wl.poses)
+        os.environ["LOCC_HEAD_FFMA"] = "1"
+        try:
+            p_ff, l_ff, g_ff = ctx.query(wl.pairs, wl.poses)
+        finally:
+            del os.environ["LOCC_HEAD_FFMA"]
+    assert np.array_equal(np.isneginf(g_tc), np.isneginf(g_ff))
+    assert np.abs(p_tc.astype(np.float64) - p_ff).max() <= 2e-5
+    band = np.abs(p_ff - 0.5) <= 1e-4
+    assert np.array_equal(l_tc[~band], l_ff[~band])
