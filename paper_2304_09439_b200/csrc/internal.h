@@ -78,7 +78,7 @@ struct UNetParams {
 // Per-shape cached embedding grids of the encode-once mode.
 struct CellsTable {
   const float* E;      // [S][M^3][F] cell embeddings
-  const float4* ctr;   // [S][M^3] cell centres in the shape's frame (x, y, z, 0)
+  const float* ctr;    // [S][3][8] cell-centre coordinates per axis in the shape's frame (i < M)
   int M;
 };
 
@@ -138,7 +138,7 @@ cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_
 // NEXT-1 encode-once mode (kernels_cells.cu)
 cudaError_t launch_grid_encode(const DevParams& P, const ShapeTable& T, int M, float* G, cudaStream_t st);
 cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, int F, const float* G, float* act,
-                        float* E, float4* ctr, cudaStream_t st);
+                        float* E, float* ctr, cudaStream_t st);
 size_t unet_act_floats(int S, int M);
 cudaError_t launch_cells_select(const ShapeTable& T, const CellsTable& C, const Batch& b, int F, uint32_t* cells,
                                 float* emb_out, cudaStream_t st);

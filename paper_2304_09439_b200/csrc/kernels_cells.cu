@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(256) conv3d_kernel(ConvArgs a) {
 // E[c] = W_P [d1[c] ; g] + b_P; cell centres lo + (i + 1/2) ext / M in fp64, rounded once.
 __global__ void __launch_bounds__(256) unet_tail_kernel(UNetParams U, ShapeTable T, int M, int F,
                                                         const float* __restrict__ c4, const float* __restrict__ d1,
-                                                        float* __restrict__ E, float4* __restrict__ ctr) {
+                                                        float* __restrict__ E, float* __restrict__ ctr) {
   extern __shared__ float sm[];
   float* pW = sm;                  // [F][257] (padded: thread f reads row f)
   float* g = pW + (size_t)F * 257;  // [128]
@@ -234,17 +234,15 @@ __global__ void __launch_bounds__(256) unet_tail_kernel(UNetParams U, ShapeTable
     }
     E[((int64_t)s * nc + c) * F + f] = (a0 + a1) + gb[f];
   }
+  // the centres are separable: per axis d the M values lo_d + (i + 1/2) ext_d / M -> ctr[s][8 d + i]
   const float4 lo = T.lo[s], hi = T.hi[s];
-  for (int c = tid; c < nc; c += 256) {
-    const int i[3] = {c % M, (c / M) % M, c / (M * M)};
-    const float l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
-    float o[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const double ext = __dsub_rn((double)h[d], (double)l[d]);
-      o[d] = __double2float_rn(__dadd_rn((double)l[d], __ddiv_rn(__dmul_rn(__dadd_rn((double)i[d], 0.5), ext), (double)M)));
-    }
-    ctr[(int64_t)s * nc + c] = make_float4(o[0], o[1], o[2], 0.f);
+  if (tid < 24) {
+    const int d = tid >> 3, i = tid & 7;
+    const float l = d == 0 ? lo.x : d == 1 ? lo.y : lo.z, h = d == 0 ? hi.x : d == 1 ? hi.y : hi.z;
+    const double ext = __dsub_rn((double)h, (double)l);
+    ctr[(int64_t)s * 24 + tid] =
+        i < M ? __double2float_rn(__dadd_rn((double)l, __ddiv_rn(__dmul_rn(__dadd_rn((double)i, 0.5), ext), (double)M)))
+              : 0.f;
   }
 }
 
@@ -272,7 +270,8 @@ __global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTa
   float4 lo = T.lo[other];
   lo.w = T.lo[own].w;  // the own cell's half-diagonal squared as the margin
   const float4 hi = T.hi[other];
-  const float4* ctr = C.ctr + (int64_t)own * nc;
+  const float axv = lane < 24 ? __ldg(C.ctr + (int64_t)own * 24 + lane) : 0.f;  // centre value per axis, index
+  const int M = C.M;
   uint32_t words[16];
   int n = 0;
 #pragma unroll
@@ -280,11 +279,10 @@ __global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTa
     words[j] = 0u;
     if (j < nw) {
       const int c = 32 * j + lane;
-      bool keep = false;
-      if (c < nc) {
-        const float4 p = ctr[c];
-        keep = keep_point(X, p.x, p.y, p.z, lo, hi);
-      }
+      const int ix = c % M, iy = (c / M) % M, iz = c / (M * M);
+      const float px = __shfl_sync(0xffffffffu, axv, ix & 7), py = __shfl_sync(0xffffffffu, axv, 8 + (iy & 7));
+      const float pz = __shfl_sync(0xffffffffu, axv, 16 + (iz & 7));
+      const bool keep = c < nc && keep_point(X, px, py, pz, lo, hi);
       words[j] = __ballot_sync(0xffffffffu, keep);
       n += __popc(words[j]);
     }
@@ -361,7 +359,7 @@ size_t unet_act_floats(int S, int M) {
 }
 
 cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, int F, const float* G, float* act,
-                        float* E, float4* ctr, cudaStream_t st) {
+                        float* E, float* ctr, cudaStream_t st) {
   const int D = M - 2, S = T.S;
   const size_t n4 = (size_t)S * D * D * D * 128;
   float* c[4];

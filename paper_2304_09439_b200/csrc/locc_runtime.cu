@@ -842,14 +842,14 @@ locc_status locc_encode_shapes(locc_ctx* c) {
   CK(G.ensure(sizeof(float) * (size_t)S * nc * H));
   CK(act.ensure(sizeof(float) * unet_act_floats(S, M)));
   CK(c->cells_E.ensure(sizeof(float) * (size_t)S * nc * F));
-  CK(c->cells_ctr.ensure(sizeof(float4) * (size_t)S * nc));
+  CK(c->cells_ctr.ensure(sizeof(float) * (size_t)S * 24));
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, c->stream));
   CK(launch_grid_encode(c->P, c->T, M, G.as<float>(), c->stream));
   CK(launch_unet(c->U, c->T, M, H, F, G.as<float>(), act.as<float>(), c->cells_E.as<float>(),
-                 c->cells_ctr.as<float4>(), c->stream));
+                 c->cells_ctr.as<float>(), c->stream));
   CK(cudaEventRecord(e1, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   float ms = 0.f;
@@ -858,7 +858,7 @@ locc_status locc_encode_shapes(locc_ctx* c) {
   cudaEventDestroy(e1);
   c->encode_ms = ms;
   c->cells.E = c->cells_E.as<float>();
-  c->cells.ctr = c->cells_ctr.as<float4>();
+  c->cells.ctr = c->cells_ctr.as<float>();
   c->cells.M = M;
   c->has_cells = true;
   return LOCC_OK;
