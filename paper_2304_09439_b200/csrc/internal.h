@@ -61,6 +61,7 @@ struct DevParams {
   const float* p3;
   const void* head_tc_img;    // tensor-core predictor: 23 pre-split (tf32 hi/lo), SW128 weight chunks
   const void* head_tc_proj;   // the projection W_F as 8 such chunks (rows 0..63)
+  const void* head_tc_bwd;    // reverse mode: pair3^T, pair2^T, pair1^T, obj3^T, obj2^T as 20 such chunks
   const float* head_tc_bias;  // [6][128] layer biases, wout [128], bout, b_F [64]
   const void* tc_w2; // bf16 W2/W3 pre-arranged as the encoder_tc shared-memory image
   const void* tc_w3;
@@ -149,7 +150,7 @@ cudaError_t launch_sim_integrate(const SimParams& sp, int E, const float* body, 
                                  const float* grad, const uint8_t* culled, int32_t* contacts, double tau_next,
                                  cudaStream_t st);
 cudaError_t launch_head_tc(const DevParams& P, const Batch& b, float* probs, uint8_t* labels, float* logits,
-                           float* emb, int num_sms, cudaStream_t st);
+                           float* emb, float* grad, int num_sms, cudaStream_t st);
 size_t scan_tmp_elems(int64_t G);
 size_t encoder_tc_smem_bytes();
 

@@ -35,7 +35,8 @@ constexpr int kHalfChunk = 16384;
 constexpr int kLayers = 6;
 constexpr int kChunks = 23;         // obj1 3 (K = 71 padded to 96), obj2, obj3, pair1..3 4 each
 constexpr int kThreadsTC = 192;
-__constant__ int kLayerChunks[kLayers] = {3, 4, 4, 4, 4, 4};
+constexpr int kBwd = 5;             // reverse-mode GEMMs: pair3^T, pair2^T, pair1^T, obj3^T, obj2^T (4 chunks each)
+__constant__ int kLayerChunks[kLayers + kBwd] = {3, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4};
 
 struct __align__(1024) HeadTcSmem {
   uint8_t a_hi[4 * kHalfChunk];     // A operand, 4 K-blocks of [128 rows x 32 fp32] SW128
@@ -46,6 +47,12 @@ struct __align__(1024) HeadTcSmem {
   float bout;
   float bf[64];
   int nside[128];
+  // reverse mode (kGrad): ReLU masks of the forward (bit c of word [l][row][c / 32] = activation > 0;
+  // l = obj1, obj2, obj3 (side rows), pair1, pair2, pair3 (pair rows)), the max's routing (bit = u_A > u_B)
+  // and obj.l1's 7 pose columns
+  uint32_t mask[kLayers][128][4];
+  uint32_t selA[64][4];
+  float o1p[7][128];
   uint64_t w_full[2], w_empty[2], a_full, d_full;
   uint32_t tmem_base;
 };
@@ -70,10 +77,13 @@ __device__ __forceinline__ void put4(HeadTcSmem& S, int r, int k0, float x0, flo
 
 // kProj (crop path): e = W_F m + b_F is computed first on the tensor cores too — two passes of 4 K-chunks
 // (m = the pooled 256-vector, staged 128 K at a time into the A buffer), N = 64, then z as above.
-template <bool kProj>
+// kGrad: after the forward, the reverse pass d logit / d pose (NEXT-2; oracle head_grad) runs as five
+// more GEMMs on the transposed weights (pre-split images), masked by the recorded ReLU decisions.
+template <bool kProj, bool kGrad>
 __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Batch b, float* __restrict__ probs,
                                                                 uint8_t* __restrict__ labels,
-                                                                float* __restrict__ logits, float* __restrict__ emb) {
+                                                                float* __restrict__ logits, float* __restrict__ emb,
+                                                                float* __restrict__ grad) {
   extern __shared__ uint8_t smem_raw[];
   HeadTcSmem& S = *reinterpret_cast<HeadTcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -82,6 +92,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
   for (int i = threadIdx.x; i < kLayers * 128; i += kThreadsTC) S.bias[i / 128][i % 128] = bias_src[i];
   for (int i = threadIdx.x; i < 128; i += kThreadsTC) S.wout[i] = bias_src[kLayers * 128 + i];
   for (int i = threadIdx.x; i < 64; i += kThreadsTC) S.bf[i] = bias_src[kLayers * 128 + 129 + i];
+  if constexpr (kGrad)
+    for (int i = threadIdx.x; i < 7 * 128; i += kThreadsTC) S.o1p[i / 128][i % 128] = P.o1p[i];
   if (threadIdx.x == 0) {
     S.bout = bias_src[kLayers * 128 + 128];
     mbar_init(&S.w_full[0], 1);
@@ -102,15 +114,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
     // ---------------------------------------------------------------- weight producer
     const uint8_t* img = static_cast<const uint8_t*>(P.head_tc_img);
     const uint8_t* pimg = static_cast<const uint8_t*>(P.head_tc_proj);
-    constexpr int kPre = kProj ? 8 : 0;
+    const uint8_t* bimg = static_cast<const uint8_t*>(P.head_tc_bwd);
+    constexpr int kPre = kProj ? 8 : 0, kPost = kGrad ? 4 * kBwd : 0;
     uint32_t n = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
-      for (int c = 0; c < kPre + kChunks; ++c, ++n) {
+      for (int c = 0; c < kPre + kChunks + kPost; ++c, ++n) {
         const int st = n & 1;
         if (lane == 0) {
           if (n >= 2) mbar_wait_spin(&S.w_empty[st], ((n >> 1) - 1) & 1);
           mbar_arrive_expect_tx(&S.w_full[st], kChunkBytes);
-          const uint8_t* src = c < kPre ? pimg + (size_t)c * kChunkBytes : img + (size_t)(c - kPre) * kChunkBytes;
+          const uint8_t* src = c < kPre ? pimg + (size_t)c * kChunkBytes
+                               : c < kPre + kChunks ? img + (size_t)(c - kPre) * kChunkBytes
+                                                    : bimg + (size_t)(c - kPre - kChunks) * kChunkBytes;
           bulk_g2s(S.w[st], src, kChunkBytes, &S.w_full[st]);
         }
         __syncwarp();
@@ -120,8 +135,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
     const uint32_t ahi = smem_u32(S.a_hi), alo = smem_u32(S.a_lo);
     constexpr int kL0 = kProj ? -2 : 0;
     uint32_t n = 0, aph = 0;
+    constexpr int kLEnd = kGrad ? kLayers + kBwd : kLayers;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
-      for (int l = kL0; l < kLayers; ++l) {
+      for (int l = kL0; l < kLEnd; ++l) {
         // l = -2, -1: the projection's two K halves (N = 64; the second accumulates onto the first)
         const uint32_t idesc = l < 0 ? idesc_tf32_f32(128, 64) : idesc_tf32_f32(128, 128);
         const int nch = l < 0 ? 4 : kLayerChunks[l];
@@ -237,6 +253,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
           const bool pad = l >= 3 && r >= 64;
 #pragma unroll 1
           for (int c0 = 0; c0 < 128; c0 += 32) {
+            uint32_t bits = 0;
             uint32_t v[32];
             tmem_ld32(trow + c0, v);
             tmem_ld_wait();
@@ -246,7 +263,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
 #pragma unroll
               for (int u = 0; u < 4; ++u) x[u] = pad ? 0.f : fmaxf(__uint_as_float(v[k + u]) + bl[c0 + k + u], 0.f);
               put4(S, r, c0 + k, x[0], x[1], x[2], x[3]);
+              if (kGrad)
+                bits |= (uint32_t)(x[0] > 0.f) << k | (uint32_t)(x[1] > 0.f) << (k + 1) |
+                        (uint32_t)(x[2] > 0.f) << (k + 2) | (uint32_t)(x[3] > 0.f) << (k + 3);
             }
+            if (kGrad) S.mask[l][r][c0 >> 5] = bits;
           }
         } else if (l == 2) {
           // object layer 3, then the max across the pair: pair p = r / 2 (even lanes) -> row p,
@@ -254,7 +275,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
           const int prow = (r & 1) ? 64 + (r >> 1) : (r >> 1);
 #pragma unroll 1
           for (int c0 = 0; c0 < 128; c0 += 32) {
-            uint32_t v[32];
+            uint32_t v[32], mb = 0, sb = 0;
             tmem_ld32(trow + c0, v);
             tmem_ld_wait();
 #pragma unroll
@@ -265,8 +286,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
                 const float mine = fmaxf(__uint_as_float(v[k + u]) + bl[c0 + k + u], 0.f);
                 const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
                 x[u] = (r & 1) ? 0.f : fmaxf(mine, other);
+                if (kGrad) {
+                  mb |= (uint32_t)(mine > 0.f) << (k + u);
+                  sb |= (uint32_t)(mine > other) << (k + u);  // even lane: u_A > u_B (ties -> B)
+                }
               }
               put4(S, prow, c0 + k, x[0], x[1], x[2], x[3]);
+            }
+            if (kGrad) {
+              S.mask[2][r][c0 >> 5] = mb;
+              if (!(r & 1)) S.selA[r >> 1][c0 >> 5] = sb;
             }
           }
         } else {
@@ -280,6 +309,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
 #pragma unroll
             for (int k = 0; k < 32; ++k)
               acc = fmaf(S.wout[c0 + k], fmaxf(__uint_as_float(v[k]) + bl[c0 + k], 0.f), acc);
+            if (kGrad) {  // reverse mode starts here: d logit / d pre3 = w_out [c3 > 0] (pair rows)
+#pragma unroll
+              for (int k = 0; k < 32; k += 4) {
+                float x[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  x[u] = (r < 64 && __uint_as_float(v[k + u]) + bl[c0 + k + u] > 0.f) ? S.wout[c0 + k + u] : 0.f;
+                put4(S, r, c0 + k, x[0], x[1], x[2], x[3]);
+              }
+            }
           }
           if (r < npairs) {
             const int64_t i = i0 + r;
@@ -297,10 +336,131 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
             if (logits) logits[i] = lg;
           }
         }
-        if (l < kLayers - 1) {
+        if (kGrad || l < kLayers - 1) {
+          if (kGrad && l == 2) asm volatile("bar.sync 1, 128;" ::: "memory");  // masks/selA visible to pair rows
           fence_proxy_async_smem();
           tc_fence_before();
           mbar_arrive(&S.a_full);
+        }
+      }
+      if constexpr (kGrad) {
+        // reverse GEMMs: B1 (pair3^T) -> d/d c2, B2 -> d/d c1, B3 (pair1^T) -> d/d v, B4 (obj3^T) -> d/d a2,
+        // B5 (obj2^T) -> d/d a1
+        for (int l = 0; l < kBwd; ++l) {
+          mbar_wait(&S.d_full, dph);
+          dph ^= 1;
+          tc_fence_after();
+          if (l == 0 || l == 1) {
+            // mask by c2 / c1 (pair rows), next A; rows >= 64 stay 0
+            const int ml = 4 - l;
+#pragma unroll 1
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+              uint32_t v[32];
+              tmem_ld32(trow + c0, v);
+              tmem_ld_wait();
+              const uint32_t m = r < 64 ? S.mask[ml][r][c0 >> 5] : 0u;
+#pragma unroll
+              for (int k = 0; k < 32; k += 4) {
+                float x[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) x[u] = (m >> (k + u)) & 1u ? __uint_as_float(v[k + u]) : 0.f;
+                put4(S, r, c0 + k, x[0], x[1], x[2], x[3]);
+              }
+            }
+          } else if (l == 2) {
+            // d/d v (pair row p) routed to the side the max selected, masked by u > 0: rows 2p, 2p+1
+            if (r < 64) {  // pair row p = r writes side rows 2p, 2p+1 (the MMA has consumed A)
+#pragma unroll 1
+              for (int c0 = 0; c0 < 128; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(trow + c0, v);
+                tmem_ld_wait();
+                const uint32_t sa = S.selA[r][c0 >> 5], ma = S.mask[2][2 * r][c0 >> 5] & sa,
+                               mbb = S.mask[2][2 * r + 1][c0 >> 5] & ~sa;
+#pragma unroll
+                for (int k = 0; k < 32; k += 4) {
+                  float xa[4], xb[4];
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) {
+                    const float gv = __uint_as_float(v[k + u]);
+                    xa[u] = (ma >> (k + u)) & 1u ? gv : 0.f;
+                    xb[u] = (mbb >> (k + u)) & 1u ? gv : 0.f;
+                  }
+                  put4(S, 2 * r, c0 + k, xa[0], xa[1], xa[2], xa[3]);
+                  put4(S, 2 * r + 1, c0 + k, xb[0], xb[1], xb[2], xb[3]);
+                }
+              }
+            } else {
+              // quadrants 2, 3 read their (padding) accumulator rows too: tcgen05.ld is warp-collective
+#pragma unroll 1
+              for (int c0 = 0; c0 < 128; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(trow + c0, v);
+                tmem_ld_wait();
+              }
+            }
+          } else if (l == 3) {
+            // d/d a2 (side rows) masked by a2 > 0
+#pragma unroll 1
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+              uint32_t v[32];
+              tmem_ld32(trow + c0, v);
+              tmem_ld_wait();
+              const uint32_t m = S.mask[1][r][c0 >> 5];
+#pragma unroll
+              for (int k = 0; k < 32; k += 4) {
+                float x[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) x[u] = (m >> (k + u)) & 1u ? __uint_as_float(v[k + u]) : 0.f;
+                put4(S, r, c0 + k, x[0], x[1], x[2], x[3]);
+              }
+            }
+          } else {
+            // d/d a1 masked by a1 > 0 = d/d pre1; d/d z[F + c] = sum_o O1[o][F + c] d/d pre1[o]
+            float gz[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+              uint32_t v[32];
+              tmem_ld32(trow + c0, v);
+              tmem_ld_wait();
+              const uint32_t m = S.mask[0][r][c0 >> 5];
+#pragma unroll
+              for (int k = 0; k < 32; ++k) {
+                const float x = (m >> k) & 1u ? __uint_as_float(v[k]) : 0.f;
+#pragma unroll
+                for (int c = 0; c < 7; ++c) gz[c] = fmaf(S.o1p[c][c0 + k], x, gz[c]);
+              }
+            }
+            const int64_t side = 2 * i0 + r;
+            if (r < 2 * npairs) {
+              float* gout = grad + side * 7;
+              if (S.nside[r & ~1] + S.nside[r | 1] == 0) {
+                for (int c = 0; c < 7; ++c) gout[c] = 0.f;
+              } else {
+                const float* pose = b.poses + side * 7;
+                const double qv[4] = {pose[0], pose[1], pose[2], pose[3]};
+                const double nq = sqrt(((qv[0] * qv[0] + qv[1] * qv[1]) + qv[2] * qv[2]) + qv[3] * qv[3]);
+                double sg = 1.0;
+                for (int c = 0; c < 4; ++c)
+                  if (qv[c] != 0.0) {
+                    sg = qv[c] > 0.0 ? 1.0 : -1.0;
+                    break;
+                  }
+                double qh[4], dot = 0.0;
+                for (int c = 0; c < 4; ++c) {
+                  qh[c] = sg * qv[c] / nq;
+                  dot += qh[c] * (double)gz[c];
+                }
+                for (int c = 0; c < 4; ++c) gout[c] = (float)(sg * ((double)gz[c] - qh[c] * dot) / nq);
+                for (int c = 4; c < 7; ++c) gout[c] = gz[c];
+              }
+            }
+          }
+          if (l < kBwd - 1) {
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(&S.a_full);
+          }
         }
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");  // this tile's nside reads precede the next tile's writes
@@ -316,22 +476,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
 size_t head_tc_smem_bytes() { return sizeof(HeadTcSmem) + 1024; }
 
 cudaError_t launch_head_tc(const DevParams& P, const Batch& b, float* probs, uint8_t* labels, float* logits,
-                           float* emb, int num_sms, cudaStream_t st) {
+                           float* emb, float* grad, int num_sms, cudaStream_t st) {
   if (b.B == 0) return cudaSuccess;
   const bool proj = b.emb_in == nullptr;  // crop path: project the pooled vectors first
-  static const cudaError_t attr0 = cudaFuncSetAttribute(
-      head_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)head_tc_smem_bytes());
-  static const cudaError_t attr1 = cudaFuncSetAttribute(
-      head_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)head_tc_smem_bytes());
-  if (attr0 != cudaSuccess) return attr0;
-  if (attr1 != cudaSuccess) return attr1;
+  if (grad && !P.head_tc_bwd) return cudaErrorNotSupported;
   const int64_t ntiles = (b.B + kHP - 1) / kHP;
   const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
-  if (proj)
-    head_tc_kernel<true><<<grid, kThreadsTC, head_tc_smem_bytes(), st>>>(P, b, probs, labels, logits, emb);
-  else
-    head_tc_kernel<false><<<grid, kThreadsTC, head_tc_smem_bytes(), st>>>(P, b, probs, labels, logits, nullptr);
-  return cudaGetLastError();
+  auto run = [&](auto kern) {
+    const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)head_tc_smem_bytes());
+    if (attr != cudaSuccess) return attr;
+    kern<<<grid, kThreadsTC, head_tc_smem_bytes(), st>>>(P, b, probs, labels, logits, emb, grad);
+    return cudaGetLastError();
+  };
+  if (proj) return grad ? run(head_tc_kernel<true, true>) : run(head_tc_kernel<true, false>);
+  return grad ? run(head_tc_kernel<false, true>) : run(head_tc_kernel<false, false>);
 }
 
 }  // namespace locc

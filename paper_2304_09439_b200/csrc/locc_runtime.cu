@@ -249,6 +249,7 @@ locc_status upload_params(locc_ctx* c, const float* flat) {
   // hi = tf32(w) then lo = tf32(w - hi) (see kernels_head_tc.cu)
   D.head_tc_img = nullptr;
   D.head_tc_proj = nullptr;
+  D.head_tc_bwd = nullptr;
   if (F + 7 <= 96) {
     std::vector<uint8_t> himg;
     for (const L* l : {&o1, &o2, &o3, &p1, &p2, &p3}) {
@@ -284,10 +285,27 @@ locc_status upload_params(locc_ctx* c, const float* flat) {
             std::memcpy(&himg[base + 16384 + off], &lo, 4);
           }
       }
+    // reverse mode: the transposed weights B[n = in][k = out] = W[out][in] of pair3, pair2, pair1, obj3, obj2
+    const size_t bwd_at = himg.size();
+    for (const L* l : {&p3, &p2, &p1, &o3, &o2})
+      for (int j = 0; j < 4; ++j) {
+        const size_t base = himg.size();
+        himg.resize(base + 32768, 0);
+        for (int n = 0; n < P; ++n)
+          for (int k = 0; k < 32; ++k) {
+            const float w = l->W[(size_t)(32 * j + k) * l->i + n];
+            const float hi = tf32_rna_host(w);
+            const float lo = tf32_rna_host(w - hi);
+            const size_t off = tc::sw128_off((uint32_t)n, (uint32_t)(k >> 2)) + (size_t)(k & 3) * 4;
+            std::memcpy(&himg[base + off], &hi, 4);
+            std::memcpy(&himg[base + 16384 + off], &lo, 4);
+          }
+      }
     CK(c->head_tc_img.ensure(himg.size()));
     CK(cudaMemcpy(c->head_tc_img.p, himg.data(), himg.size(), cudaMemcpyHostToDevice));
     D.head_tc_img = c->head_tc_img.p;
     D.head_tc_proj = (H == 256 && F == 64) ? static_cast<const uint8_t*>(c->head_tc_img.p) + proj_at : nullptr;
+    D.head_tc_bwd = static_cast<const uint8_t*>(c->head_tc_img.p) + bwd_at;
   }
   D.tc_w2 = nullptr;
   D.tc_w3 = nullptr;
@@ -455,8 +473,8 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs + 1], st));
       b.emb_in = e_in;
       if (occ) CK(cudaMemsetAsync(b.occ, 0, sizeof(int32_t) * 2 * B, st));
-      if (use_head_tc(c) && !d_grad && c->cfg.F == 64)
-        CK(launch_head_tc(c->P, b, d_probs, d_labels, d_logits, nullptr, c->num_sms, st));
+      if (use_head_tc(c) && c->cfg.F == 64)
+        CK(launch_head_tc(c->P, b, d_probs, d_labels, d_logits, nullptr, d_grad, c->num_sms, st));
       else
         CK(launch_head(c->P, b, d_probs, d_labels, d_logits, nullptr, d_grad, st));
       if (c->timing) CK(cudaEventRecord(c->head_ev[subs], st));
@@ -495,8 +513,8 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       CK(launch_encoder_f32(c->P, b, st));
     }
     if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs + 1], st));
-    if (use_head_tc(c) && !d_grad && c->P.head_tc_proj)
-      CK(launch_head_tc(c->P, b, d_probs, d_labels, d_logits, d_emb, c->num_sms, st));
+    if (use_head_tc(c) && c->P.head_tc_proj)
+      CK(launch_head_tc(c->P, b, d_probs, d_labels, d_logits, d_emb, d_grad, c->num_sms, st));
     else
       CK(launch_head(c->P, b, d_probs, d_labels, d_logits, d_emb, d_grad, st));
     if (c->timing) CK(cudaEventRecord(c->head_ev[subs], st));
