@@ -268,11 +268,17 @@ def main():
     mhz_load = clk.get("sm_mhz") or 1965.0
     if st.get("head_ms"):
         hf = (HEAD_FLOP + PROJ_FLOP) * st["evaluated_pairs"]
-        roof["head_tile_kernel"] = {"bound": "alu", "ms_per_step": st["head_ms"],
-                                    "achieved": hf / (st["head_ms"] / 1e3) / 1e12, "unit": "TFLOP/s",
-                                    "peak": fp32_peak_tflops(mhz_load),
-                                    "frac": hf / (st["head_ms"] / 1e3) / 1e12 / fp32_peak_tflops(mhz_load),
-                                    "flop_per_evaluated_pair": HEAD_FLOP + PROJ_FLOP}
+        if prec == locc.LOCC_PREC_BF16 and not os.environ.get("LOCC_HEAD_FFMA"):
+            hk = {"kernel": "head_tc_kernel", "bound": "tensor",
+                  "peak": peaks.get("bf16_tflops_sustained", 1374.0) * 1.1 / 2.25 / 3,
+                  "peak_source": "MEASURED_PEAKS bf16 sustained x 1.1/2.25 (tf32) / 3 (3xTF32 split)"}
+        else:
+            hk = {"kernel": "head_tile_kernel", "bound": "alu", "peak": fp32_peak_tflops(mhz_load),
+                  "peak_source": "148 SM x 128 FP32 FMA/clk x 2 x median SM clock"}
+        hk.update({"ms_per_step": st["head_ms"], "achieved": hf / (st["head_ms"] / 1e3) / 1e12, "unit": "TFLOP/s",
+                   "flop_per_evaluated_pair": HEAD_FLOP + PROJ_FLOP})
+        hk["frac"] = hk["achieved"] / hk["peak"]
+        roof["predictor"] = hk
 
     line = {"metric": METRIC, "value": world * N / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

@@ -1,7 +1,8 @@
 #!/bin/bash
 # ncu captures of the NEXT-mode kernels (run under gpurun, 1 GPU).  Usage: tools/profile_next.sh <tag>
 # tools/next_modes.py launches, in order: grid encode + U-Net, query_cells (select, head<0,1>),
-# query_grad (crop path, head<1,0>), closed loop (sim_prepare, select, head<1,1>, sim_integrate, ...).
+# query_grad (crop path, head_tc<1,1>), closed loop (sim_prepare, select, head_tc<0,1>, sim_integrate, ...).
+# The context is bf16, so the predictor is the tensor-core kernel (head_tc_kernel<kProj, kGrad>).
 TAG=${1:-r1next}
 mkdir -p gpurun_out
 python tools/next_modes.py > gpurun_out/next_plain_$TAG.log 2>&1 || exit 1
@@ -17,6 +18,6 @@ cap grid_encode grid_encode 0
 cap conv3d_c1 conv3d 0
 cap conv3d_d1 conv3d 7
 cap cells_select cells_select 0
-cap head_cells head_tile 0
-cap head_grad head_tile 1
+cap head_cells head_tc 0
+cap head_grad head_tc 1
 cap sim_integrate sim_integrate 0

@@ -24,8 +24,8 @@ CAPS = [("grid_encode", "point MLP over all K points, cell max (once per shape t
         ("conv3d_c1", "U-Net c1: valid 3^3 conv 256 -> 128 (once per shape table)"),
         ("conv3d_d1", "U-Net d1: transposed valid conv [d2; c1] -> 128 (once per shape table)"),
         ("cells_select", "encode-once query: cell selection + pooled embedding"),
-        ("head_cells", "head_tile_kernel<0,1>: predictor on pooled cell embeddings"),
-        ("head_grad", "head_tile_kernel<1,0>: predictor + pose gradient (crop path)"),
+        ("head_cells", "head_tc_kernel<0,0>: tensor-core predictor on pooled cell embeddings"),
+        ("head_grad", "head_tc_kernel<1,1>: tensor-core predictor + pose gradient (crop path)"),
         ("sim_integrate", "closed loop: penalty + semi-implicit Euler")]
 
 

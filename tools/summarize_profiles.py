@@ -60,7 +60,7 @@ def main(tag="r1"):
         step[name] = step.get(name, 0.0) + t
     tot = sum(step.values())
     kern = {}
-    for k in ("encoder_tc", "crop_count", "crop_emit", "head_tile"):
+    for k in ("encoder_tc", "crop_count", "crop_emit", "head_tc", "head_tile"):
         p = os.path.join(OUT, f"raw_{tag}_{k}.csv")
         if os.path.exists(p):
             kern[k] = raw(p)
