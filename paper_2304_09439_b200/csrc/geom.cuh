@@ -97,5 +97,18 @@ __device__ __forceinline__ bool segment_setup(const ShapeTable& T, const Batch& 
   return true;
 }
 
+// The segment's transform as written by segment_xf_kernel (one thread per segment, so the fp64
+// quaternion work is not repeated by every lane of every kernel that needs it).  False = invalid.
+__device__ __forceinline__ bool segment_load(const Batch& b, int64_t g, int& own, int& other, Xf& X) {
+  const float4* x = b.xf + 4 * g;
+  const float4 r0 = x[0], r1 = x[1], r2 = x[2], id = x[3];
+  own = __float_as_int(id.x);
+  other = __float_as_int(id.y);
+  X.R[0] = r0.x, X.R[1] = r0.y, X.R[2] = r0.z, X.t[0] = r0.w;
+  X.R[3] = r1.x, X.R[4] = r1.y, X.R[5] = r1.z, X.t[1] = r1.w;
+  X.R[6] = r2.x, X.R[7] = r2.y, X.R[8] = r2.z, X.t[2] = r2.w;
+  return own >= 0;
+}
+
 }  // namespace
 }  // namespace locc

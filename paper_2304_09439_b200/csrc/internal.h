@@ -113,6 +113,9 @@ struct Batch {
   float4* rows;          // [sum n] kept rows (x, y, z, flags)
   float* pooled;         // [G][H] mean over occupied cells of the cell-max features
   const float* emb_in;   // encode-once mode: [G][F] pooled cell embeddings (the predictor's e); else null
+  float4* xf;            // [G][4] per-segment transform into the other object's frame (segment_xf_kernel):
+                         // rows (R00 R01 R02 t0), (R10 R11 R12 t1), (R20 R21 R22 t2), (own, other, -, -) as ints;
+                         // own = -1 for an invalid segment (id out of range, non-finite pose, |q|^2 < 1e-12)
   uint32_t* masks;       // nullable [B][2][ceil(K/32)] caller-order keep bits (debug)
   DevStats* stats;
 };
@@ -127,6 +130,7 @@ struct TcL1 {
 // Launchers (kernels_*.cu).  All asynchronous on `st`.
 cudaError_t launch_shape_prep(const float* pts_in, int S, int K, int M, float4* pts, uint16_t* perm,
                               float4* lo, float4* hi, uint16_t* cell_tmp, int* bad, cudaStream_t st);
+cudaError_t launch_segment_xf(const ShapeTable& T, const Batch& b, cudaStream_t st);
 cudaError_t launch_crop_count(const ShapeTable& T, const Batch& b, int words, cudaStream_t st);
 cudaError_t launch_scan(const int32_t* counts, int64_t G, int64_t* offsets, int64_t* block_tmp,
                         cudaStream_t st);

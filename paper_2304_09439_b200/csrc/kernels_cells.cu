@@ -259,11 +259,8 @@ __global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTa
   int own = 0, other = 0;
   Xf X;
   float* e = emb + g * F;
-  if (!segment_setup(T, b, g, own, other, X)) {
-    if (lane == 0) {
-      b.counts[g] = 0;
-      atomicAdd(&b.stats->bad_input, 1ull);
-    }
+  if (!segment_load(b, g, own, other, X)) {
+    if (lane == 0) b.counts[g] = 0;
     for (int f = lane; f < F; f += 32) e[f] = 0.f;
     return;
   }

@@ -135,6 +135,25 @@ __global__ void shape_sort_kernel(const float* __restrict__ in, int K, int M, co
   }
 }
 
+// ---------------------------------------------------------------- S1 per segment
+// One thread per (pair, side) segment: validate the inputs and write the transform (segment_setup's
+// prescribed fp64 arithmetic, rounded once to fp32) for the crop and cell-selection kernels.
+__global__ void __launch_bounds__(256) segment_xf_kernel(ShapeTable T, Batch b) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= b.G) return;
+  int own = -1, other = -1;
+  Xf X{};
+  if (!segment_setup(T, b, g, own, other, X)) {
+    own = other = -1;
+    atomicAdd(&b.stats->bad_input, 1ull);
+  }
+  float4* x = b.xf + 4 * g;
+  x[0] = make_float4(X.R[0], X.R[1], X.R[2], X.t[0]);
+  x[1] = make_float4(X.R[3], X.R[4], X.R[5], X.t[1]);
+  x[2] = make_float4(X.R[6], X.R[7], X.R[8], X.t[2]);
+  x[3] = make_float4(__int_as_float(own), __int_as_float(other), 0.f, 0.f);
+}
+
 // ---------------------------------------------------------------- S2-S3 pass 1: counts
 // One warp per segment: float4 point loads (coalesced, 512 B per warp step), fp32 transform +
 // eps test, warp ballot.  Writes n_s and C_s (occupied cells among the kept points: cell runs,
@@ -145,11 +164,10 @@ __global__ void __launch_bounds__(256) crop_count_kernel(ShapeTable T, Batch b, 
   if (g >= b.G) return;
   int own = 0, other = 0;
   Xf X;
-  if (!segment_setup(T, b, g, own, other, X)) {
+  if (!segment_load(b, g, own, other, X)) {
     if (lane == 0) {
       b.counts[g] = 0;
       b.occ[g] = 0;
-      atomicAdd(&b.stats->bad_input, 1ull);
     }
     return;
   }
@@ -212,7 +230,7 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
   if (n == 0) return;
   int own = 0, other = 0;
   Xf X;
-  if (!segment_setup(T, b, g, own, other, X)) return;
+  if (!segment_load(b, g, own, other, X)) return;
   const float4 lo = T.lo[other], hi = T.hi[other];
   const float4* pts = T.pts + (int64_t)own * T.K;
   float4* out = b.rows + b.offsets[g];
@@ -343,6 +361,12 @@ cudaError_t launch_shape_prep(const float* pts_in, int S, int K, int M, float4* 
   shape_bounds_kernel<<<S, 256, 0, st>>>(pts_in, K, M, lo, hi, cell_tmp, bad);
   const size_t sm = sizeof(int) * (size_t)M * M * M;
   shape_sort_kernel<<<S, 256, sm, st>>>(pts_in, K, M, cell_tmp, pts, perm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_segment_xf(const ShapeTable& T, const Batch& b, cudaStream_t st) {
+  if (b.G == 0) return cudaSuccess;
+  segment_xf_kernel<<<(unsigned)((b.G + 255) / 256), 256, 0, st>>>(T, b);
   return cudaGetLastError();
 }
 

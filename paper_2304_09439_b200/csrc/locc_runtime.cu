@@ -110,7 +110,7 @@ struct locc_ctx {
   // scratch for one sub-batch
   int64_t cap_B = 0;
   DevBuf trace;
-  DevBuf in_pairs, in_poses, in_pairs2, in_poses2, counts, occ, offsets, scan_tmp, rows, pooled, stats;
+  DevBuf in_pairs, in_poses, in_pairs2, in_poses2, counts, occ, offsets, scan_tmp, rows, pooled, stats, xf;
   DevBuf out_probs, out_labels, out_logits, out_kept, out_occ, out_masks, out_emb, out_grad;
   locc_stats last{};
   int64_t timed_subs = 0;  // sub-batches whose encoder events await reading
@@ -322,6 +322,7 @@ locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks, bool need_gr
     CK(c->in_pairs2.ensure(sizeof(int32_t) * 2 * B));
     CK(c->in_poses2.ensure(sizeof(float) * 14 * B));
     CK(c->counts.ensure(sizeof(int32_t) * G));
+    CK(c->xf.ensure(sizeof(float4) * 4 * G));
     CK(c->occ.ensure(sizeof(int32_t) * G));
     CK(c->offsets.ensure(sizeof(int64_t) * (G + 1)));
     CK(c->scan_tmp.ensure(sizeof(int64_t) * scan_tmp_elems(G)));
@@ -396,7 +397,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
   for (const void* p : all)
     if (p && is_device_ptr(p) != dev)
       return fail(LOCC_E_INVALID_ARG, "all buffers of one call must be host or all device memory");
-  // Inputs are validated on the device (segment_setup in the crop kernels: ids in range, finite
+  // Inputs are validated on the device (segment_xf_kernel: ids in range, finite
   // poses, |q|^2 >= 1e-12); an invalid segment is counted and the call returns LOCC_E_INVALID_ARG.
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   const bool sync = !dev || !stream;
@@ -454,6 +455,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     b.rows = c->rows.as<float4>();
     b.pooled = c->pooled.as<float>();
     b.stats = dstats;
+    b.xf = c->xf.as<float4>();
     b.masks = nullptr;
     if (masks) {
       b.masks = dev ? masks + (size_t)2 * i0 * words : c->out_masks.as<uint32_t>();
@@ -469,6 +471,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       // encode-once mode: select cells, pool the cached embeddings, then the predictor
       if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs], st));
       float* e_in = (emb && dev) ? emb + (size_t)2 * i0 * c->cfg.F : c->cells_emb.as<float>();
+      CK(launch_segment_xf(c->T, b, st));
       CK(launch_cells_select(c->T, c->cells, b, c->cfg.F, b.masks, e_in, st));
       if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs + 1], st));
       b.emb_in = e_in;
@@ -479,8 +482,9 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
         CK(launch_head(c->P, b, d_probs, d_labels, d_logits, nullptr, d_grad, st));
       if (c->timing) CK(cudaEventRecord(c->head_ev[subs], st));
       if (emb) d_emb = e_in;  // the selection wrote e (0 for an empty side) in place
-      launches += 2;
+      launches += 3;
     } else {
+    CK(launch_segment_xf(c->T, b, st));
     CK(launch_crop_count(c->T, b, words, st));
     CK(launch_scan(b.counts, b.G, b.offsets, c->scan_tmp.as<int64_t>(), st));
     CK(launch_crop_emit(c->T, b, st));
@@ -518,7 +522,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     else
       CK(launch_head(c->P, b, d_probs, d_labels, d_logits, d_emb, d_grad, st));
     if (c->timing) CK(cudaEventRecord(c->head_ev[subs], st));
-    launches += 7;
+    launches += 8;
     }
     if (!dev) CK(cudaEventRecord(c->ev_free[subs & 1], st));  // the kernels are done with the inputs
     ++subs;
