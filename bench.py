@@ -410,7 +410,25 @@ def main():
                 sms = float(tt.item())
             res[det] = {"ms_per_dt": sms, "contact_pair_substeps_last_dt": ncon,
                         "finite_state": bool(torch.isfinite(d_st).all().item())}
+        # Fig. 3c's axis: time per dt against the number of environments (encode-once detector)
+        sweep = {}
+        for Es in (4096, 16384, 65536):
+            ids_s, body_s, st_s = ls.make_sim_scene(pts, Es, seed=6 + rank)
+            di, db, ds = (torch.from_numpy(x).cuda() for x in (ids_s, body_s, st_s))
+            sim = dict(ls.SIM_DEFAULTS, detector="cells")
+            for _ in range(2):
+                ctx.sim_run(sim, di, db, ds, stream=stream.cuda_stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+            for k in range(5):
+                ctx.sim_run(sim, di, db, ds, t0=k * sim["h"] * sim["substeps"], stream=stream.cuda_stream)
+            with torch.cuda.stream(stream):
+                e1.record(stream)
+            torch.cuda.synchronize()
+            sweep[str(Es)] = e0.elapsed_time(e1) / 5
         line["closed_loop"] = {"metric": "device time per simulated dt (4 substeps), locc_sim_run",
+                               "ms_per_dt_vs_envs_encode_once": sweep,
                                "envs_per_gpu": E, "pairs_per_substep": 3 * E, "unit": "ms",
                                "detector_encode_once": res["cells"], "detector_crop_" + a.precision: res["crop"],
                                "note": "PAPER.md:91/:100 scene: bowl shaken + 2 dropped objects per env; "

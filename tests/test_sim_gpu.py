@@ -85,3 +85,21 @@ def test_sim_free_fall_gpu(locc_mod, world):
     np.testing.assert_allclose(out[:, 1:, 7:10], st[:, 1:, 7:10] + n * h * g, rtol=0, atol=1e-6)
     np.testing.assert_allclose(out[:, 1:, 4:7], st[:, 1:, 4:7] + h * h * g * n * (n + 1) / 2, rtol=0, atol=1e-6)
     np.testing.assert_allclose(np.linalg.norm(out[:, :, :4], axis=-1), 1.0, atol=1e-6)
+
+
+def test_sim_argument_and_state_errors(locc_mod, world):
+    import torch
+    pts, ids, body, st = world
+    ctx = locc_mod.Locc(M=6, H=256, F=64, precision=0, device=0)
+    ctx.load_weights_mem(spread())
+    ctx.set_shapes(pts)
+    d_ids, d_body, d_st = torch.from_numpy(ids).cuda(), torch.from_numpy(body).cuda(), torch.from_numpy(st).cuda()
+    with pytest.raises(locc_mod.LoccError):  # the encode-once detector before locc_encode_shapes
+        ctx.sim_run(dict(SIM, detector="cells"), d_ids, d_body, d_st)
+    with pytest.raises(locc_mod.LoccError):  # host buffers are rejected
+        ctx.sim_run(SIM, ids, body, st.copy())
+    with pytest.raises(locc_mod.LoccError):
+        ctx.sim_run(dict(SIM, substeps=0), d_ids, d_body, d_st)
+    ctx.sim_run(dict(SIM, substeps=1), d_ids, d_body, d_st)  # still usable
+    assert torch.isfinite(d_st).all()
+    ctx.close()
