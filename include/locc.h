@@ -52,7 +52,9 @@ typedef enum {
 typedef enum {
   LOCC_PREC_FP32 = 0, /* encoder layers 2-3 as fp32 FFMA on CUDA cores */
   LOCC_PREC_BF16 = 1  /* encoder layers 2-3 on tcgen05 tensor cores: bf16 h1, W2, h2, W3,
-                         fp32 accumulate; layer 1, pooling and head stay fp32 */
+                         fp32 accumulate; layer 1 and pooling stay fp32; the predictor (projection,
+                         object and pair MLPs, and its pose gradient) runs on the tensor cores with
+                         fp32-accurate 3xTF32 products (reading Q32) */
 } locc_precision;
 
 typedef struct {
