@@ -32,9 +32,9 @@ def world():
     return pts, ids, body, st
 
 
-def run_gpu(locc_mod, pts, ids, body, st, sim, unet=None, t0=0.0):
+def run_gpu(locc_mod, pts, ids, body, st, sim, unet=None, t0=0.0, precision=0):
     import torch
-    ctx = locc_mod.Locc(M=6, H=256, F=64, precision=0, device=0)
+    ctx = locc_mod.Locc(M=6, H=256, F=64, precision=precision, device=0)
     ctx.load_weights_mem(spread())
     ctx.set_shapes(pts)
     if unet is not None:
@@ -63,12 +63,14 @@ def compare(out, con, ref, st):
     return ok
 
 
-@pytest.mark.parametrize("detector", ["crop", "cells"])
-def test_sim_parity(locc_mod, oracle_mod, world, detector):
+@pytest.mark.parametrize("detector,precision", [("crop", 0), ("cells", 0), ("cells", 1)])
+def test_sim_parity(locc_mod, oracle_mod, world, detector, precision):
+    """(cells, 1): a bf16 context, whose encode-once detector runs the tensor-core (3xTF32) predictor and
+    gradient (reading Q32); the encode-once embeddings are fp32 in both precisions."""
     pts, ids, body, st = world
     sim = dict(SIM, substeps=2, detector=detector, ks=2.0)
     unet = ls.flatten_unet(ls.make_unet_weights()) if detector == "cells" else None
-    out, con = run_gpu(locc_mod, pts, ids, body, st, sim, unet, t0=0.1)
+    out, con = run_gpu(locc_mod, pts, ids, body, st, sim, unet, t0=0.1, precision=precision)
     ref = oracle_mod.sim_run(spread(), pts, sim, ids, body, st.astype(np.float64), t0=0.1, unet_flat=unet)
     compare(out, con, ref, st)
 
