@@ -279,6 +279,16 @@ def main():
                    "flop_per_evaluated_pair": HEAD_FLOP + PROJ_FLOP})
         hk["frac"] = hk["achieved"] / hk["peak"]
         roof["predictor"] = hk
+    if st.get("crop_ms"):
+        # north_star's crop evidence: the algorithmic point bytes 2 K 12 B + 69 B of pair I/O per pair
+        # against HBM (the shape table itself is L2-resident, so this is an algorithmic rate)
+        hbm = peaks.get("hbm_gbs", 6546.6)
+        cb = (2 * a.K * 12 + 69) * N
+        roof["crop"] = {"bound": "hbm", "kernels": "segment_xf + crop_count + scan + crop_emit",
+                        "ms_per_step": st["crop_ms"], "unit": "GB/s",
+                        "achieved": cb / (st["crop_ms"] / 1e3) / 1e9, "peak": hbm,
+                        "frac": cb / (st["crop_ms"] / 1e3) / 1e9 / hbm,
+                        "algorithmic_bytes_per_pair": 2 * a.K * 12 + 69}
 
     line = {"metric": METRIC, "value": world * N / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

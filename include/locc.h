@@ -81,6 +81,7 @@ typedef struct {
   double  total_ms;         /* device time of the whole query on its stream (0 if timing off) */
   double  head_ms;          /* device time of the predictor launches (0 if timing off); in the
                                encode-once mode encoder_ms is the cell selection's time */
+  double  crop_ms;          /* device time of the transform + crop + compaction launches (0 if timing off) */
 } locc_stats;
 
 /* Create a context on cfg->device.  Out: *out (free with locc_destroy).

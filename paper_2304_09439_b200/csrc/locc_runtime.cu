@@ -98,6 +98,7 @@ struct locc_ctx {
   cudaEvent_t ev_in[2] = {}, ev_free[2] = {};  // input buffer k & 1: uploaded / released by the kernels
   std::vector<cudaEvent_t> enc_ev;  // per sub-batch encoder start/stop pairs
   std::vector<cudaEvent_t> head_ev;  // per sub-batch predictor stop (its start = the encoder stop)
+  std::vector<cudaEvent_t> crop_ev;  // per sub-batch crop start (its stop = the encoder start)
   bool timing = false;
   bool has_weights = false, has_shapes = false;
   // parameters
@@ -363,15 +364,18 @@ locc_status read_timing(locc_ctx* c) {
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
   c->last.total_ms = ms;
-  double enc = 0.0, head = 0.0;
+  double enc = 0.0, head = 0.0, crop = 0.0;
   for (int64_t s = 0; s < c->timed_subs; ++s) {
     CK(cudaEventElapsedTime(&ms, c->enc_ev[2 * s], c->enc_ev[2 * s + 1]));
     enc += ms;
     CK(cudaEventElapsedTime(&ms, c->enc_ev[2 * s + 1], c->head_ev[s]));
     head += ms;
+    CK(cudaEventElapsedTime(&ms, c->crop_ev[s], c->enc_ev[2 * s]));
+    crop += ms;
   }
   c->last.encoder_ms = enc;
   c->last.head_ms = head;
+  c->last.crop_ms = crop;
   c->timed_subs = 0;
   return LOCC_OK;
 }
@@ -424,6 +428,11 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       CK(cudaEventCreate(&e));
       c->head_ev.push_back(e);
     }
+    while ((int64_t)c->crop_ev.size() < n_sub) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->crop_ev.push_back(e);
+    }
     CK(cudaEventRecord(c->ev[0], st));
   }
   int64_t launches = 0, subs = 0;
@@ -469,6 +478,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
 
     if (cells) {
       // encode-once mode: select cells, pool the cached embeddings, then the predictor
+      if (c->timing) CK(cudaEventRecord(c->crop_ev[subs], st));
       if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs], st));
       float* e_in = (emb && dev) ? emb + (size_t)2 * i0 * c->cfg.F : c->cells_emb.as<float>();
       CK(launch_segment_xf(c->T, b, st));
@@ -484,6 +494,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       if (emb) d_emb = e_in;  // the selection wrote e (0 for an empty side) in place
       launches += 3;
     } else {
+    if (c->timing) CK(cudaEventRecord(c->crop_ev[subs], st));
     CK(launch_segment_xf(c->T, b, st));
     CK(launch_crop_count(c->T, b, words, st));
     CK(launch_scan(b.counts, b.G, b.offsets, c->scan_tmp.as<int64_t>(), st));
@@ -644,6 +655,7 @@ void locc_destroy(locc_ctx* c) {
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (auto& e : c->enc_ev) cudaEventDestroy(e);
   for (auto& e : c->head_ev) cudaEventDestroy(e);
+  for (auto& e : c->crop_ev) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }

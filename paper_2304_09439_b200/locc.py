@@ -49,7 +49,8 @@ class SimConfig(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("pairs", C.c_int64), ("evaluated_pairs", C.c_int64), ("kept_rows", C.c_int64),
                 ("nonempty_sides", C.c_int64), ("sub_batches", C.c_int64), ("kernel_launches", C.c_int64),
-                ("encoder_ms", C.c_double), ("total_ms", C.c_double), ("head_ms", C.c_double)]
+                ("encoder_ms", C.c_double), ("total_ms", C.c_double), ("head_ms", C.c_double),
+                ("crop_ms", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -312,3 +312,16 @@ def test_tensor_core_predictor_vs_fp32_predictor(locc_mod, spread_flat):
     assert np.abs(p_tc.astype(np.float64) - p_ff).max() <= 2e-5
     band = np.abs(p_ff - 0.5) <= 1e-4
     assert np.array_equal(l_tc[~band], l_ff[~band])
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+@pytest.mark.parametrize("K", [512, 4096])
+def test_k_sweep_parity(locc_mod, oracle_mod, spread_flat, precision, K):
+    """BASELINE.json config 5's K values (512 / 4096 points per object): C1-sized batches against the
+    oracle at the same bars as C1 (the full-size sweep is a bench setting, `bench.py --K`)."""
+    wl = ls.make_workload("C1", N=48, K=K, S=12)
+    ref = oracle_mod.query(spread_flat, wl.points, wl.pairs, wl.poses, bf16_emul=precision == 1)
+    with make_ctx(locc_mod, spread_flat, wl.points, precision) as ctx:
+        got = ctx.query_debug(wl.pairs, wl.poses)
+    assert_parity(got, ref, precision)
+    assert (ref["kept"].sum(1) > 0).mean() > 0.8
