@@ -117,6 +117,7 @@ struct Batch {
                          // rows (R00 R01 R02 t0), (R10 R11 R12 t1), (R20 R21 R22 t2), (own, other, -, -) as ints;
                          // own = -1 for an invalid segment (id out of range, non-finite pose, |q|^2 < 1e-12)
   uint32_t* masks;       // nullable [B][2][ceil(K/32)] caller-order keep bits (debug)
+  uint32_t* kbits;       // [G][ceil(K/32)] keep ballots in sorted order (crop_count -> crop_emit)
   DevStats* stats;
 };
 

@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(256) crop_count_kernel(ShapeTable T, Batch b, 
   const float4* pts = T.pts + (int64_t)own * T.K;
   const uint16_t* perm = T.perm + (int64_t)own * T.K;
   uint32_t* mask = b.masks ? b.masks + g * words : nullptr;
+  uint32_t* kb = b.kbits + g * ((T.K + 31) >> 5);
   int n = 0, C = 0, carry = -1;
   // four 32-point steps per round: their loads are in flight together (the table lives in L2)
   for (int base0 = 0; base0 < T.K; base0 += 128) {
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(256) crop_count_kernel(ShapeTable T, Batch b, 
     const float4 p = pp[j];
     const bool keep = k < T.K && keep_point(X, p.x, p.y, p.z, lo, hi);
     const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) kb[base >> 5] = m;  // the emit pass replays these decisions
     if (m == 0) continue;
     const int cell = __float_as_int(p.w);
     const unsigned before = m & lanemask_lt();
@@ -231,8 +233,9 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
   int own = 0, other = 0;
   Xf X;
   if (!segment_load(b, g, own, other, X)) return;
-  const float4 lo = T.lo[other], hi = T.hi[other];
   const float4* pts = T.pts + (int64_t)own * T.K;
+  const int nsteps = (T.K + 31) >> 5;
+  const uint32_t* kb = b.kbits + g * nsteps;
   float4* out = b.rows + b.offsets[g];
   const uint32_t segbits = (uint32_t)g << kRowSegShift;
   int written = 0;        // kept rows before this step
@@ -240,20 +243,23 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
   float4 prow;            // held-back row payload (valid in every lane)
   int pcell = 0, pidx = 0;
   for (int base0 = 0; base0 < T.K; base0 += 128) {
-    float4 pp[4];  // four steps' loads in flight together
+    // four steps in flight together: the count pass's ballots, then only the kept points' loads
+    float4 pp[4];
+    unsigned mm[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      const int step = (base0 >> 5) + j;
+      mm[j] = step < nsteps ? kb[step] : 0u;
       const int k = base0 + 32 * j + lane;
-      pp[j] = k < T.K ? pts[k] : make_float4(0.f, 0.f, 0.f, __int_as_float(-2));
+      pp[j] = (mm[j] >> lane) & 1u ? pts[k] : make_float4(0.f, 0.f, 0.f, __int_as_float(-2));
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
     const int base = base0 + 32 * j;
     if (base >= T.K) break;
-    const int k = base + lane;
     const float4 p = pp[j];
-    const bool keep = k < T.K && keep_point(X, p.x, p.y, p.z, lo, hi);
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const unsigned m = mm[j];
+    const bool keep = (m >> lane) & 1u;
     if (m == 0) continue;
     const int cell = __float_as_int(p.w);
     const int first = __ffs(m) - 1, last = 31 - __clz(m);

@@ -111,7 +111,7 @@ struct locc_ctx {
   // scratch for one sub-batch
   int64_t cap_B = 0;
   DevBuf trace;
-  DevBuf in_pairs, in_poses, in_pairs2, in_poses2, counts, occ, offsets, scan_tmp, rows, pooled, stats, xf;
+  DevBuf in_pairs, in_poses, in_pairs2, in_poses2, counts, occ, offsets, scan_tmp, rows, pooled, stats, xf, kbits;
   DevBuf out_probs, out_labels, out_logits, out_kept, out_occ, out_masks, out_emb, out_grad;
   locc_stats last{};
   int64_t timed_subs = 0;  // sub-batches whose encoder events await reading
@@ -324,6 +324,7 @@ locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks, bool need_gr
     CK(c->in_poses2.ensure(sizeof(float) * 14 * B));
     CK(c->counts.ensure(sizeof(int32_t) * G));
     CK(c->xf.ensure(sizeof(float4) * 4 * G));
+    CK(c->kbits.ensure(sizeof(uint32_t) * G * ((K + 31) / 32)));
     CK(c->occ.ensure(sizeof(int32_t) * G));
     CK(c->offsets.ensure(sizeof(int64_t) * (G + 1)));
     CK(c->scan_tmp.ensure(sizeof(int64_t) * scan_tmp_elems(G)));
@@ -465,6 +466,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     b.pooled = c->pooled.as<float>();
     b.stats = dstats;
     b.xf = c->xf.as<float4>();
+    b.kbits = c->kbits.as<uint32_t>();
     b.masks = nullptr;
     if (masks) {
       b.masks = dev ? masks + (size_t)2 * i0 * words : c->out_masks.as<uint32_t>();
