@@ -108,7 +108,8 @@ struct Batch {
   int64_t B;             // pairs in this sub-batch
   int64_t G;             // segments = 2B
   int32_t* counts;       // [G] n_s
-  int32_t* occ;          // [G] C_s (from the crop)
+  int32_t* occ;          // [G] C_s (from the crop; written only when want_occ)
+  int want_occ;          // the caller asked for C_s (locc_query_debug)
   int64_t* offsets;      // [G+1] exclusive scan of counts
   float4* rows;          // [sum n] kept rows (x, y, z, flags)
   float* pooled;         // [G][H] mean over occupied cells of the cell-max features

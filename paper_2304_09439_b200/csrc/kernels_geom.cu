@@ -158,6 +158,8 @@ __global__ void __launch_bounds__(256) segment_xf_kernel(ShapeTable T, Batch b) 
 // One warp per segment: float4 point loads (coalesced, 512 B per warp step), fp32 transform +
 // eps test, warp ballot.  Writes n_s and C_s (occupied cells among the kept points: cell runs,
 // the points being cell-sorted) and, in debug mode, the caller-order keep mask.
+// kOcc: also count the occupied cells C_s (only when the caller asked for them: a debug output).
+template <bool kOcc>
 __global__ void __launch_bounds__(256) crop_count_kernel(ShapeTable T, Batch b, int words) {
   const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -195,13 +197,15 @@ __global__ void __launch_bounds__(256) crop_count_kernel(ShapeTable T, Batch b, 
     const unsigned m = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) kb[base >> 5] = m;  // the emit pass replays these decisions
     if (m == 0) continue;
-    const int cell = __float_as_int(p.w);
-    const unsigned before = m & lanemask_lt();
-    const int src = before ? 31 - __clz(before) : lane;
-    int prev = __shfl_sync(0xffffffffu, cell, src);
-    if (!before) prev = carry;
-    C += __popc(__ballot_sync(0xffffffffu, keep && prev != cell));
-    carry = __shfl_sync(0xffffffffu, cell, 31 - __clz(m));
+    if (kOcc) {
+      const int cell = __float_as_int(p.w);
+      const unsigned before = m & lanemask_lt();
+      const int src = before ? 31 - __clz(before) : lane;
+      int prev = __shfl_sync(0xffffffffu, cell, src);
+      if (!before) prev = carry;
+      C += __popc(__ballot_sync(0xffffffffu, keep && prev != cell));
+      carry = __shfl_sync(0xffffffffu, cell, 31 - __clz(m));
+    }
     n += __popc(m);
     if (mask && keep) {
       const int ck = perm[k];
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(256) crop_count_kernel(ShapeTable T, Batch b, 
   }
   if (lane == 0) {
     b.counts[g] = n;
-    b.occ[g] = C;
+    if (kOcc) b.occ[g] = C;
     if (n) {
       atomicAdd(&b.stats->kept_rows, (unsigned long long)n);
       atomicAdd(&b.stats->nonempty_sides, 1ull);
@@ -379,7 +383,10 @@ cudaError_t launch_segment_xf(const ShapeTable& T, const Batch& b, cudaStream_t 
 cudaError_t launch_crop_count(const ShapeTable& T, const Batch& b, int words, cudaStream_t st) {
   if (b.G == 0) return cudaSuccess;
   const int64_t blocks = (b.G * 32 + 255) / 256;
-  crop_count_kernel<<<(unsigned)blocks, 256, 0, st>>>(T, b, words);
+  if (b.want_occ)
+    crop_count_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(T, b, words);
+  else
+    crop_count_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(T, b, words);
   return cudaGetLastError();
 }
 

@@ -461,6 +461,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     }
     b.counts = (dev && kept) ? kept + 2 * i0 : c->counts.as<int32_t>();
     b.occ = (dev && occ) ? occ + 2 * i0 : c->occ.as<int32_t>();
+    b.want_occ = occ != nullptr;
     b.offsets = c->offsets.as<int64_t>();
     b.rows = c->rows.as<float4>();
     b.pooled = c->pooled.as<float>();
