@@ -56,7 +56,7 @@ def main(tag="r1"):
     L = launches(os.path.join(OUT, f"launches_{tag}.csv"))
     # one step = launches from the first crop_count to the head before the next crop_count
     step, per = {}, {}
-    for name, t in L[:7]:
+    for name, t in L[:8]:
         step[name] = step.get(name, 0.0) + t
     tot = sum(step.values())
     kern = {}
@@ -69,7 +69,7 @@ def main(tag="r1"):
              "the 1,048,576-pair step is four of these).  ncu 2025, `--clock-control none`, 1 x B200.", "",
              "## Launch list of one sub-batch (gpu__time_duration, serialised, cold cache)", "",
              "| kernel | ms | share |", "|---|---|---|"]
-    for name, t in L[:7]:
+    for name, t in L[:8]:
         lines.append(f"| {name} | {t * 1e3:.3f} | {100 * t / tot:.1f}% |")
     lines += ["", f"Total {tot * 1e3:.2f} ms.", "", "## `--set full` per kernel (one launch)", "",
               "| kernel | ms | DRAM read GB | DRAM write GB | tensor pipe active | SM throughput | regs | SM clock GHz |",
@@ -81,7 +81,7 @@ def main(tag="r1"):
     md = "\n".join(lines) + "\n"
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     open(os.path.join(ROOT, "profiles", f"{tag}_summary.md"), "w").write(md)
-    js = {"tag": tag, "launches_one_subbatch": [{"kernel": n, "ms": t * 1e3} for n, t in L[:7]], "kernels": kern}
+    js = {"tag": tag, "launches_one_subbatch": [{"kernel": n, "ms": t * 1e3} for n, t in L[:8]], "kernels": kern}
     json.dump(js, open(os.path.join(ROOT, "profiles", f"{tag}_summary.json"), "w"), indent=1)
     if "encoder_tc" in kern:
         e = kern["encoder_tc"]
