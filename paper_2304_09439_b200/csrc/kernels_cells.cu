@@ -250,12 +250,16 @@ __global__ void __launch_bounds__(256) unet_tail_kernel(UNetParams U, ShapeTable
 // One warp per (pair, side) segment.  Cell c of the own shape is selected iff its centre, moved into the
 // other object's frame with the crop's fp32 transform, is within the OWN cell half-diagonal of the other
 // AABB (keep_point with eps^2 = own lo.w).  e = mean over the selected cells of E (fp32 sums).
+// kM > 0: the grid edge as a compile-time constant (the index arithmetic of the M^3 centre tests
+// becomes multiply-shifts); 0 = any M.
+template <int kM>
 __global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTable C, Batch b, int F,
                                                            uint32_t* __restrict__ cells, float* __restrict__ emb) {
   const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (g >= b.G) return;
-  const int nc = C.M * C.M * C.M, nw = (nc + 31) >> 5;
+  const int M = kM > 0 ? kM : C.M;
+  const int nc = M * M * M, nw = (nc + 31) >> 5;
   int own = 0, other = 0;
   Xf X;
   float* e = emb + g * F;
@@ -268,7 +272,6 @@ __global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTa
   lo.w = T.lo[own].w;  // the own cell's half-diagonal squared as the margin
   const float4 hi = T.hi[other];
   const float axv = lane < 24 ? __ldg(C.ctr + (int64_t)own * 24 + lane) : 0.f;  // centre value per axis, index
-  const int M = C.M;
   uint32_t words[16];
   int n = 0;
 #pragma unroll
@@ -394,7 +397,11 @@ cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, 
 cudaError_t launch_cells_select(const ShapeTable& T, const CellsTable& C, const Batch& b, int F, uint32_t* cells,
                                 float* emb_out, cudaStream_t st) {
   if (b.G == 0) return cudaSuccess;
-  cells_select_kernel<<<(unsigned)((b.G * 32 + 255) / 256), 256, 0, st>>>(T, C, b, F, cells, emb_out);
+  const unsigned grid = (unsigned)((b.G * 32 + 255) / 256);
+  if (C.M == 6)
+    cells_select_kernel<6><<<grid, 256, 0, st>>>(T, C, b, F, cells, emb_out);
+  else
+    cells_select_kernel<0><<<grid, 256, 0, st>>>(T, C, b, F, cells, emb_out);
   return cudaGetLastError();
 }
 
