@@ -7,12 +7,13 @@
 // and A B ~= A_hi B_hi + A_hi B_lo + A_lo B_hi — relative error ~2^-22 per product (the dropped lo lo
 // term); reading Q32 gives the measured bar.
 //
-// Persistent CTAs (one per SM), 64 pairs (128 sides) per tile, 6 warps:
+// Persistent CTAs (one per SM), 64 pairs (128 sides) per tile:
 //   warp 0     weight producer: streams pre-split, pre-swizzled 32-K weight chunks (32 KB: [128 x 32]
 //              hi then lo, K-major SW128, built at weight load) through a 5-stage ring (cp.async.bulk)
 //   warp 1     MMA issuer (one elected lane): 12 MMAs (4 K-steps x 3 products) per chunk, A from TMEM
-//   warps 2-5  epilogue (TMEM lane quadrant = warp % 4, thread = row r): per layer tcgen05.ld the
-//              accumulator row, bias + ReLU, split, and tcgen05.st the next layer's A row (hi, lo)
+//   warps 2+   epilogue (TMEM lane quadrant = warp % 4, thread = row r): per layer tcgen05.ld the
+//              accumulator row, bias + ReLU, split, and tcgen05.st the next layer's A row (hi, lo);
+//              8 warps (two column halves per row) in the forward variants, 4 with the gradient
 // TMEM (512 columns): D = 0..127, A_hi = 128..255, A_lo = 256..383 (A: row = lane, K = column), so the
 // operands never touch shared memory and 160 KB of it holds the weight ring.
 // Rows: side s of the tile in row s (pair p = sides 2p, 2p+1); the pair layers keep pair p in row 2p
@@ -42,7 +43,6 @@ constexpr int kStages = 5;          // weight ring
 constexpr int kLayers = 6;
 constexpr int kChunks = 23;         // obj1 3 (K = 71 padded to 96), obj2, obj3, pair1..3 4 each
 constexpr int kBwd = 5;             // reverse GEMMs: pair3^T, pair2^T, pair1^T, obj3^T, obj2^T (4 chunks each)
-constexpr int kThreadsTC = 192;
 constexpr uint32_t kColD = 0, kColAH = 128, kColAL = 256;
 __constant__ int kLayerChunks[kLayers + kBwd] = {3, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4};
 
@@ -53,6 +53,7 @@ struct __align__(1024) HeadTcSmem {
   float bout;
   float bf[64];
   int nside[128];
+  float part[2][128];  // the output unit's partial sums of the two column groups
   // reverse mode (kGrad): ReLU masks of the forward (bit c of word [l][row][c / 32] = activation > 0;
   // l = obj1, obj2, obj3 (side rows), pair1, pair2 (pair rows 2p)), the max's routing per pair (bit =
   // u_A > u_B, ties -> B) and obj.l1's 7 pose columns
@@ -89,28 +90,34 @@ __device__ __forceinline__ void a_ready(HeadTcSmem& S) {
   mbar_arrive(&S.a_full);
 }
 
+// kGrad variants keep 4 epilogue warps (their register footprint); the forward variants run 8, two per
+// TMEM lane quadrant, each taking half of the columns.
 template <bool kProj, bool kGrad>
-__global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Batch b, float* __restrict__ probs,
+__global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams P, Batch b, float* __restrict__ probs,
                                                                 uint8_t* __restrict__ labels,
                                                                 float* __restrict__ logits, float* __restrict__ emb,
                                                                 float* __restrict__ grad) {
+  constexpr int kEW = kGrad ? 4 : 8;         // epilogue warps
+  constexpr int kNT = 64 + 32 * kEW;         // threads
+  constexpr int kHalves = kEW / 4;           // column groups per row
+  constexpr int kCols = 128 / kHalves;       // accumulator columns per epilogue thread
   extern __shared__ uint8_t smem_raw[];
   HeadTcSmem& S = *reinterpret_cast<HeadTcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (b.B + kHP - 1) / kHP;
   const float* bias_src = P.head_tc_bias;  // [6][128] biases, wout [128], bout, b_F [64]
-  for (int i = threadIdx.x; i < kLayers * 128; i += kThreadsTC) S.bias[i / 128][i % 128] = bias_src[i];
-  for (int i = threadIdx.x; i < 128; i += kThreadsTC) S.wout[i] = bias_src[kLayers * 128 + i];
-  for (int i = threadIdx.x; i < 64; i += kThreadsTC) S.bf[i] = bias_src[kLayers * 128 + 129 + i];
+  for (int i = threadIdx.x; i < kLayers * 128; i += kNT) S.bias[i / 128][i % 128] = bias_src[i];
+  for (int i = threadIdx.x; i < 128; i += kNT) S.wout[i] = bias_src[kLayers * 128 + i];
+  for (int i = threadIdx.x; i < 64; i += kNT) S.bf[i] = bias_src[kLayers * 128 + 129 + i];
   if constexpr (kGrad)
-    for (int i = threadIdx.x; i < 7 * 128; i += kThreadsTC) S.o1p[i / 128][i % 128] = P.o1p[i];
+    for (int i = threadIdx.x; i < 7 * 128; i += kNT) S.o1p[i / 128][i % 128] = P.o1p[i];
   if (threadIdx.x == 0) {
     S.bout = bias_src[kLayers * 128 + 128];
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&S.w_full[i], 1);
       mbar_init(&S.w_empty[i], 1);
     }
-    mbar_init(&S.a_full, 128);
+    mbar_init(&S.a_full, 32 * kEW);
     mbar_init(&S.d_full, 1);
     fence_mbar_init();
   }
@@ -176,6 +183,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
   } else {
     // ---------------------------------------------------------------- epilogue (warps 2..5)
     const int q = warp & 3, r = 32 * q + lane;  // TMEM lane quadrant, row
+    const int half = (warp - 2) >> 2;          // column group (0 when kHalves == 1)
+    const int cb = half * kCols, eb = half * (kCols / 2);  // first column of 128-wide / 64-wide rows
     const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
     const bool odd = r & 1;
     uint32_t dph = 0;
@@ -197,7 +206,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
             tc_fence_after();
           }
 #pragma unroll 1
-          for (int c0 = 0; c0 < 128; c0 += 32) {
+          for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
             float x[32];
 #pragma unroll
             for (int k = 0; k < 32; k += 4) {
@@ -213,7 +222,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
         dph ^= 1;
         tc_fence_after();
 #pragma unroll 1
-        for (int c0 = 0; c0 < 64; c0 += 32) {
+        for (int c0 = eb; c0 < eb + kCols / 2; c0 += 32) {
           uint32_t v[32];
           tmem_ld32(trow + kColD + c0, v);
           tmem_ld_wait();
@@ -229,7 +238,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
       } else {
         const float4* e4 = reinterpret_cast<const float4*>(b.emb_in + g * 64);
 #pragma unroll 1
-        for (int c0 = 0; c0 < 64; c0 += 32) {
+        for (int c0 = eb; c0 < eb + kCols / 2; c0 += 32) {
           float x[32];
 #pragma unroll
           for (int k = 0; k < 32; k += 4) {
@@ -259,9 +268,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
 #pragma unroll
           for (int c = 0; c < 3; ++c) x[4 + c] = pose[4 + c];
         }
-        put32(trow, 64, x);
+        if (half == kHalves - 1) put32(trow, 64, x);
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // nside of every side visible to the pair rows
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEW) : "memory");  // nside of every side visible to the pair rows
       a_ready(S);
       // ---- forward layers
       for (int l = 0; l < kLayers; ++l) {
@@ -272,7 +281,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
         if (l < 2) {
           // object layers 1, 2 (side rows): ReLU(D + b) -> next A
 #pragma unroll 1
-          for (int c0 = 0; c0 < 128; c0 += 32) {
+          for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
             uint32_t v[32];
             tmem_ld32(trow + kColD + c0, v);
             tmem_ld_wait();
@@ -289,7 +298,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
         } else if (l == 2) {
           // object layer 3, then the max across the pair into row 2p (odd rows -> 0)
 #pragma unroll 1
-          for (int c0 = 0; c0 < 128; c0 += 32) {
+          for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
             uint32_t v[32];
             tmem_ld32(trow + kColD + c0, v);
             tmem_ld_wait();
@@ -309,11 +318,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
               if (!odd) S.selA[r >> 1][c0 >> 5] = sb;
             }
           }
-          if (kGrad) asm volatile("bar.sync 1, 128;" ::: "memory");  // selA visible to the odd rows
+          if (kGrad) asm volatile("bar.sync 1, %0;" ::"n"(32 * kEW) : "memory");  // selA visible to the odd rows
         } else if (l < 5) {
           // pair layers 1, 2 (pair p in row 2p): ReLU(D + b) -> next A, odd rows 0
 #pragma unroll 1
-          for (int c0 = 0; c0 < 128; c0 += 32) {
+          for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
             uint32_t v[32];
             tmem_ld32(trow + kColD + c0, v);
             tmem_ld_wait();
@@ -331,7 +340,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
           // pair layer 3 + output unit (even row 2p = pair p); kGrad: d logit / d pre3 = w_out [c3 > 0]
           float acc = 0.f;
 #pragma unroll 1
-          for (int c0 = 0; c0 < 128; c0 += 32) {
+          for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
             uint32_t v[32];
             tmem_ld32(trow + kColD + c0, v);
             tmem_ld_wait();
@@ -344,8 +353,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
             }
             if (kGrad) put32(trow, c0, x);
           }
+          if constexpr (kHalves == 2) {
+            S.part[half][r] = acc;
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kEW) : "memory");
+            acc = S.part[0][r] + S.part[1][r];
+          }
           const int p = r >> 1;
-          if (!odd && p < npairs) {
+          if (half == 0 && !odd && p < npairs) {
             const int64_t i = i0 + p;
             float lg, pr;
             if (S.nside[r] + S.nside[r + 1] == 0) {
@@ -374,7 +388,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
             // mask by c2 / c1 (pair rows; odd rows stay 0) or by a2 (side rows)
             const int ml = l == 3 ? 1 : 4 - l;
 #pragma unroll 1
-            for (int c0 = 0; c0 < 128; c0 += 32) {
+            for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
               uint32_t v[32];
               tmem_ld32(trow + kColD + c0, v);
               tmem_ld_wait();
@@ -387,7 +401,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
           } else if (l == 2) {
             // d/d v of pair p (row 2p) routed to the side the max selected, masked by u > 0
 #pragma unroll 1
-            for (int c0 = 0; c0 < 128; c0 += 32) {
+            for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
               uint32_t v[32];
               tmem_ld32(trow + kColD + c0, v);
               tmem_ld_wait();
@@ -405,7 +419,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
             // d/d a1 masked by a1 > 0 = d/d pre1; d/d z[F + c] = sum_o O1[o][F + c] d/d pre1[o]
             float gz[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
-            for (int c0 = 0; c0 < 128; c0 += 32) {
+            for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
               uint32_t v[32];
               tmem_ld32(trow + kColD + c0, v);
               tmem_ld_wait();
@@ -444,7 +458,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) head_tc_kernel(DevParams P, Bat
           if (l < kBwd - 1) a_ready(S);
         }
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // this tile's nside reads precede the next tile's writes
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEW) : "memory");  // this tile's nside reads precede the next tile's writes
     }
   }
   tc_fence_before();
@@ -463,11 +477,12 @@ cudaError_t launch_head_tc(const DevParams& P, const Batch& b, float* probs, uin
   if (grad && !P.head_tc_bwd) return cudaErrorNotSupported;
   const int64_t ntiles = (b.B + kHP - 1) / kHP;
   const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
+  const int threads = grad ? 192 : 320;
   auto run = [&](auto kern) {
     const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)head_tc_smem_bytes());
     if (attr != cudaSuccess) return attr;
-    kern<<<grid, kThreadsTC, head_tc_smem_bytes(), st>>>(P, b, probs, labels, logits, emb, grad);
+    kern<<<grid, threads, head_tc_smem_bytes(), st>>>(P, b, probs, labels, logits, emb, grad);
     return cudaGetLastError();
   };
   if (proj) return grad ? run(head_tc_kernel<true, true>) : run(head_tc_kernel<true, false>);
