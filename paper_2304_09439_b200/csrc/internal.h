@@ -85,6 +85,7 @@ struct CellsTable {
 
 // NEXT-3 closed-loop step constants (see include/locc.h locc_sim_config).
 struct SimParams {
+  double hd;  // substep length (s), for the substep times
   float h;
   float g[3];
   float ks, kd;
@@ -150,11 +151,13 @@ size_t unet_act_floats(int S, int M);
 cudaError_t launch_cells_select(const ShapeTable& T, const CellsTable& C, const Batch& b, int F, uint32_t* cells,
                                 float* emb_out, cudaStream_t st);
 // NEXT-3 closed loop (kernels_sim.cu)
+cudaError_t launch_sim_set_t0(double* t0_dev, double t0, cudaStream_t st);
 cudaError_t launch_sim_prepare(const ShapeTable& T, const SimParams& sp, int E, const int32_t* ids, float* state,
-                               double tau, int32_t* pairs, float* poses, uint8_t* culled, cudaStream_t st);
+                               const double* t0_dev, int n, int32_t* pairs, float* poses, uint8_t* culled,
+                               cudaStream_t st);
 cudaError_t launch_sim_integrate(const SimParams& sp, int E, const float* body, float* state, const float* logits,
-                                 const float* grad, const uint8_t* culled, int32_t* contacts, double tau_next,
-                                 cudaStream_t st);
+                                 const float* grad, const uint8_t* culled, int32_t* contacts, const double* t0_dev,
+                                 int n, cudaStream_t st);
 cudaError_t launch_head_tc(const DevParams& P, const Batch& b, float* probs, uint8_t* labels, float* logits,
                            float* emb, float* grad, int num_sms, cudaStream_t st);
 size_t scan_tmp_elems(int64_t G);

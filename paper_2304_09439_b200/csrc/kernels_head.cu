@@ -501,9 +501,19 @@ cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_
   if (b.B == 0) return cudaSuccess;
   if (P.H == 256 && P.F == 64) {
     const unsigned grid = (unsigned)((b.B + kTP - 1) / kTP);
+    static const cudaError_t attr = [] {  // once per process
+      const int g = (int)sizeof(HeadGradSmem), f = (int)sizeof(HeadSmem);
+      cudaError_t e = cudaFuncSetAttribute(head_tile_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, g);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(head_tile_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, g);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(head_tile_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, f);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(head_tile_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, f);
+      return e;
+    }();
+    if (attr != cudaSuccess) return attr;
     auto run = [&](auto kern, size_t sm, float* g) {
-      const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (attr != cudaSuccess) return attr;
       kern<<<grid, kHeadThreads, sm, st>>>(P, b, probs, labels, logits, emb, g);
       return cudaGetLastError();
     };
@@ -515,9 +525,9 @@ cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_
   }
   if (grad || b.emb_in) return cudaErrorNotSupported;  // the pose gradient and encode-once mode: H = 256, F = 64
   const size_t sm = sizeof(float) * (size_t)(256 + 128 + P.F + 7) * LD;
-  static const cudaError_t attr = cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)(sizeof(float) * (256 + 128 + 256 + 7) * LD));
-  if (attr != cudaSuccess) return attr;
+  static const cudaError_t attr2 = cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                        (int)(sizeof(float) * (256 + 128 + 256 + 7) * LD));
+  if (attr2 != cudaSuccess) return attr2;
   head_kernel<<<(unsigned)((b.B + PB - 1) / PB), 128, sm, st>>>(P, b, probs, labels, logits, emb);
   return cudaGetLastError();
 }

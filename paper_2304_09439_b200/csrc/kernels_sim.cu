@@ -49,12 +49,18 @@ __device__ __forceinline__ void set_bowl(const SimParams& sp, float* b, double t
 __constant__ int kPairA[3] = {0, 0, 1};
 __constant__ int kPairB[3] = {1, 2, 2};
 
+// The substep's time is read from the device (t0 + n h), so a captured CUDA graph of the substeps can
+// be replayed for any start time t0 (set by sim_set_t0_kernel before the replay).
+__global__ void sim_set_t0_kernel(double* t0_dev, double t0) { *t0_dev = t0; }
+
 __global__ void __launch_bounds__(128) sim_prepare_kernel(ShapeTable T, SimParams sp, int E,
                                                           const int32_t* __restrict__ ids, float* __restrict__ state,
-                                                          double tau, int32_t* __restrict__ pairs,
+                                                          const double* __restrict__ t0_dev, int n,
+                                                          int32_t* __restrict__ pairs,
                                                           float* __restrict__ poses, uint8_t* __restrict__ culled) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
+  const double tau = *t0_dev + n * sp.hd;
   float* st = state + (int64_t)e * 39;
   set_bowl(sp, st, tau);
   float cw[3][3], hw[3][3];
@@ -89,7 +95,8 @@ __global__ void __launch_bounds__(128) sim_integrate_kernel(SimParams sp, int E,
                                                             float* __restrict__ state, const float* __restrict__ logits,
                                                             const float* __restrict__ grad,
                                                             const uint8_t* __restrict__ culled,
-                                                            int32_t* __restrict__ contacts, double tau_next) {
+                                                            int32_t* __restrict__ contacts,
+                                                            const double* __restrict__ t0_dev, int n) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   float* st = state + (int64_t)e * 39;
@@ -145,23 +152,30 @@ __global__ void __launch_bounds__(128) sim_integrate_kernel(SimParams sp, int E,
     const float nn = sqrtf(((qn[0] * qn[0] + qn[1] * qn[1]) + qn[2] * qn[2]) + qn[3] * qn[3]);
     for (int k = 0; k < 4; ++k) X[k] = qn[k] / nn;
   }
-  set_bowl(sp, st, tau_next);
+  set_bowl(sp, st, *t0_dev + (n + 1) * sp.hd);
 }
 
 }  // namespace
 
+cudaError_t launch_sim_set_t0(double* t0_dev, double t0, cudaStream_t st) {
+  sim_set_t0_kernel<<<1, 1, 0, st>>>(t0_dev, t0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sim_prepare(const ShapeTable& T, const SimParams& sp, int E, const int32_t* ids, float* state,
-                               double tau, int32_t* pairs, float* poses, uint8_t* culled, cudaStream_t st) {
+                               const double* t0_dev, int n, int32_t* pairs, float* poses, uint8_t* culled,
+                               cudaStream_t st) {
   if (E == 0) return cudaSuccess;
-  sim_prepare_kernel<<<(E + 127) / 128, 128, 0, st>>>(T, sp, E, ids, state, tau, pairs, poses, culled);
+  sim_prepare_kernel<<<(E + 127) / 128, 128, 0, st>>>(T, sp, E, ids, state, t0_dev, n, pairs, poses, culled);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sim_integrate(const SimParams& sp, int E, const float* body, float* state, const float* logits,
-                                 const float* grad, const uint8_t* culled, int32_t* contacts, double tau_next,
-                                 cudaStream_t st) {
+                                 const float* grad, const uint8_t* culled, int32_t* contacts, const double* t0_dev,
+                                 int n, cudaStream_t st) {
   if (E == 0) return cudaSuccess;
-  sim_integrate_kernel<<<(E + 127) / 128, 128, 0, st>>>(sp, E, body, state, logits, grad, culled, contacts, tau_next);
+  sim_integrate_kernel<<<(E + 127) / 128, 128, 0, st>>>(sp, E, body, state, logits, grad, culled, contacts, t0_dev,
+                                                          n);
   return cudaGetLastError();
 }
 

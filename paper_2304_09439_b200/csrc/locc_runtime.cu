@@ -123,7 +123,18 @@ struct locc_ctx {
   double encode_ms = 0.0;  // device time of the last locc_encode_shapes
   // NEXT-3 closed-loop scratch
   int64_t sim_cap = 0;
-  DevBuf sim_pairs, sim_poses, sim_probs, sim_logits, sim_grad, sim_culled;
+  DevBuf sim_pairs, sim_poses, sim_probs, sim_logits, sim_grad, sim_culled, sim_t0;
+  // CUDA graph of one locc_sim_run's substeps, replayed while its inputs are unchanged
+  uint64_t generation = 1;  // bumped by every call that changes weights, shapes, grids or precision
+  struct SimKey {
+    locc_sim_config cfg;
+    int32_t E;
+    const void *ids, *body, *state, *contacts, *stream;
+    uint64_t gen;
+  } sim_key{};
+  int sim_seen = 0;  // calls with sim_key so far (capture on the second)
+  int64_t sim_launches = 0;  // kernels inside the captured graph
+  cudaGraphExec_t sim_exec = nullptr;
 };
 
 namespace {
@@ -656,6 +667,7 @@ void locc_destroy(locc_ctx* c) {
     if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->sim_exec) cudaGraphExecDestroy(c->sim_exec);
   for (auto& e : c->enc_ev) cudaEventDestroy(e);
   for (auto& e : c->head_ev) cudaEventDestroy(e);
   for (auto& e : c->crop_ev) cudaEventDestroy(e);
@@ -670,6 +682,7 @@ locc_status locc_set_precision(locc_ctx* c, int32_t precision) {
   if (precision == LOCC_PREC_BF16 && c->cfg.H != 256)
     return fail(LOCC_E_INVALID_ARG, "the tensor-core encoder is built for H = 256");
   c->cfg.precision = precision;
+  ++c->generation;
   return LOCC_OK;
 }
 
@@ -706,6 +719,7 @@ locc_status locc_load_weights_mem(locc_ctx* c, const float* flat, size_t n) {
     if (!std::isfinite(flat[i])) return fail(LOCC_E_WEIGHTS, "non-finite parameter at %zu", i);
   CK(cudaSetDevice(c->device));
   c->has_cells = false;  // the cached grids depend on the encoder weights
+  ++c->generation;
   locc_status s = upload_params(c, flat);
   if (s != LOCC_OK) return s;
   if (c->cfg.H == 256) s = locc_upload_tc_weights(c, flat);
@@ -789,6 +803,7 @@ locc_status locc_set_shapes(locc_ctx* c, const float* points, int32_t S, int32_t
   c->T.hi = c->sh_hi.as<float4>();
   c->T.S = S;
   c->has_cells = false;  // the cached grids belong to the previous shape table
+  ++c->generation;
   if (c->T.K != K) c->cap_B = 0;  // row buffer depends on K
   c->T.K = K;
   c->has_shapes = true;
@@ -863,6 +878,7 @@ locc_status locc_load_unet_weights_mem(locc_ctx* c, const float* flat, size_t n)
   c->U.pb = d + offPb;
   c->has_unet = true;
   c->has_cells = false;
+  ++c->generation;
   return LOCC_OK;
 }
 
@@ -894,6 +910,7 @@ locc_status locc_encode_shapes(locc_ctx* c) {
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   c->encode_ms = ms;
+  ++c->generation;
   c->cells.E = c->cells_E.as<float>();
   c->cells.ctr = c->cells_ctr.as<float>();
   c->cells.M = M;
@@ -954,20 +971,74 @@ locc_status locc_sim_run(locc_ctx* c, const locc_sim_config* cfg, int32_t E, con
   sp.kd = cfg->kd;
   sp.freq = cfg->freq;
   sp.slack = cfg->slack;
-  if (contacts) CK(cudaMemsetAsync(contacts, 0, sizeof(int32_t) * NP, st));
-  int64_t launches = 0;
-  for (int n = 0; n < cfg->substeps; ++n) {
-    const double tau = t0 + n * cfg->h;
-    CK(launch_sim_prepare(c->T, sp, E, ids, state, tau, c->sim_pairs.as<int32_t>(), c->sim_poses.as<float>(),
-                          c->sim_culled.as<uint8_t>(), st));
-    locc_status s = run_query(c, c->sim_pairs.as<int32_t>(), c->sim_poses.as<float>(), NP, c->sim_probs.as<float>(),
-                              nullptr, c->sim_logits.as<float>(), nullptr, nullptr, nullptr, nullptr,
-                              c->sim_grad.as<float>(), st, cfg->detector == 1);
-    if (s != LOCC_OK) return s;
-    launches += c->last.kernel_launches + 2;
-    CK(launch_sim_integrate(sp, E, body, state, c->sim_logits.as<float>(), c->sim_grad.as<float>(),
-                            c->sim_culled.as<uint8_t>(), contacts, tau + cfg->h, st));
+  sp.hd = cfg->h;
+  CK(c->sim_t0.ensure(sizeof(double)));
+  double* t0_dev = c->sim_t0.as<double>();
+  CK(launch_sim_set_t0(t0_dev, t0, st));
+  // the substeps: enqueued directly, or captured once into a CUDA graph and replayed while the call's
+  // inputs (sizes, constants, buffers, stream) and the context's state are unchanged — one launch
+  // instead of ~10 per substep (LOCC_NO_GRAPH=1 disables it)
+  auto enqueue = [&](int64_t& launches) -> locc_status {
+    if (contacts) CK(cudaMemsetAsync(contacts, 0, sizeof(int32_t) * NP, st));
+    for (int n = 0; n < cfg->substeps; ++n) {
+      CK(launch_sim_prepare(c->T, sp, E, ids, state, t0_dev, n, c->sim_pairs.as<int32_t>(), c->sim_poses.as<float>(),
+                            c->sim_culled.as<uint8_t>(), st));
+      locc_status s = run_query(c, c->sim_pairs.as<int32_t>(), c->sim_poses.as<float>(), NP,
+                                c->sim_probs.as<float>(), nullptr, c->sim_logits.as<float>(), nullptr, nullptr,
+                                nullptr, nullptr, c->sim_grad.as<float>(), st, cfg->detector == 1);
+      if (s != LOCC_OK) return s;
+      launches += c->last.kernel_launches + 2;
+      CK(launch_sim_integrate(sp, E, body, state, c->sim_logits.as<float>(), c->sim_grad.as<float>(),
+                              c->sim_culled.as<uint8_t>(), contacts, t0_dev, n, st));
+    }
+    return LOCC_OK;
+  };
+  locc_ctx::SimKey key{};
+  key.cfg = *cfg;
+  key.E = E;
+  key.ids = ids;
+  key.body = body;
+  key.state = state;
+  key.contacts = contacts;
+  key.stream = st;
+  key.gen = c->generation;
+  const bool same = std::memcmp(&key, &c->sim_key, sizeof key) == 0;
+  if (!same) {
+    if (c->sim_exec) cudaGraphExecDestroy(c->sim_exec);
+    c->sim_exec = nullptr;
+    c->sim_key = key;
+    c->sim_seen = 0;
   }
+  int64_t launches = 0;
+  const bool graphs = !getenv("LOCC_NO_GRAPH") && !c->timing;
+  if (graphs && !c->sim_exec && c->sim_seen >= 1) {
+    // capture (the first call with this key has already run directly: all scratch is allocated)
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    locc_status s = enqueue(launches);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(st, &graph);
+    if (s == LOCC_OK && ec == cudaSuccess && graph) {
+      if (cudaGraphInstantiate(&c->sim_exec, graph, 0) != cudaSuccess) c->sim_exec = nullptr;
+    }
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    if (!c->sim_exec) {  // capture not possible: stay on the direct path for this key
+      c->sim_seen = -1 << 30;
+      launches = 0;
+      locc_status s2 = enqueue(launches);
+      if (s2 != LOCC_OK) return s2;
+    } else {
+      CK(cudaGraphLaunch(c->sim_exec, st));
+      c->sim_launches = launches;
+    }
+  } else if (graphs && c->sim_exec) {
+    CK(cudaGraphLaunch(c->sim_exec, st));
+    launches = c->sim_launches;
+  } else {
+    locc_status s = enqueue(launches);
+    if (s != LOCC_OK) return s;
+  }
+  ++c->sim_seen;
   c->last.kernel_launches = launches;
   if (!stream) CK(cudaStreamSynchronize(st));
   return LOCC_OK;

@@ -105,3 +105,38 @@ def test_sim_argument_and_state_errors(locc_mod, world):
     ctx.sim_run(dict(SIM, substeps=1), d_ids, d_body, d_st)  # still usable
     assert torch.isfinite(d_st).all()
     ctx.close()
+
+
+@pytest.mark.parametrize("detector", ["crop", "cells"])
+def test_sim_graph_replay_same_bits(locc_mod, world, detector):
+    """locc_sim_run captures its substeps into a CUDA graph on the second call with unchanged inputs and
+    replays it afterwards; the trajectory must be bitwise the one of the direct path (LOCC_NO_GRAPH)."""
+    import os
+    import torch
+    pts, ids, body, st = world
+    unet = ls.flatten_unet(ls.make_unet_weights()) if detector == "cells" else None
+    sim = dict(SIM, detector=detector)
+    outs = []
+    for no_graph in (False, True):
+        if no_graph:
+            os.environ["LOCC_NO_GRAPH"] = "1"
+        try:
+            ctx = locc_mod.Locc(M=6, H=256, F=64, precision=1, device=0)
+            ctx.load_weights_mem(spread())
+            ctx.set_shapes(pts)
+            if unet is not None:
+                ctx.load_unet_weights_mem(unet)
+                ctx.encode_shapes()
+            d_ids, d_body = torch.from_numpy(ids).cuda(), torch.from_numpy(body).cuda()
+            d_st = torch.from_numpy(st.copy()).cuda()
+            d_con = torch.zeros(len(ids), 3, dtype=torch.int32, device="cuda")
+            s = torch.cuda.Stream()
+            for k in range(4):
+                ctx.sim_run(sim, d_ids, d_body, d_st, t0=k * sim["h"] * sim["substeps"], contacts=d_con,
+                            stream=s.cuda_stream)
+            s.synchronize()
+            outs.append((d_st.cpu().numpy(), d_con.cpu().numpy()))
+            ctx.close()
+        finally:
+            os.environ.pop("LOCC_NO_GRAPH", None)
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
