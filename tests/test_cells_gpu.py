@@ -152,3 +152,15 @@ def test_cells_state_errors(locc_mod, wl, weights):
     with pytest.raises(locc_mod.LoccError):
         ctx.query_cells(pairs[:1] % 4, poses[:1])
     ctx.close()
+
+
+@pytest.mark.parametrize("M", [3, 5, 8])
+def test_cells_parity_other_grid_sizes(locc_mod, oracle_mod, weights, M):
+    """The selection kernel's generic-M path (M = 6 is specialised) and the U-Net at other grid edges
+    (M = 3: a single 1^3 interior after the valid conv; M = 8: 512 cells, 16 selection words)."""
+    w = ls.make_workload("C1", N=40, S=6)
+    ref = oracle_mod.query_cells(weights[0], weights[1], w.points, w.pairs, w.poses, M=M)
+    with make_ctx(locc_mod, weights[0], weights[1], w.points, M=M) as ctx:
+        E, _ = ctx.cell_embeddings()
+        got = ctx.query_cells(w.pairs, w.poses, debug=True)
+    assert_cells_parity(got, ref, E, w.pairs)
