@@ -164,3 +164,15 @@ def test_cells_parity_other_grid_sizes(locc_mod, oracle_mod, weights, M):
         E, _ = ctx.cell_embeddings()
         got = ctx.query_cells(w.pairs, w.poses, debug=True)
     assert_cells_parity(got, ref, E, w.pairs)
+
+
+def test_cells_empty_and_disjoint_batches(locc_mod, weights, wl):
+    pts, pairs, poses = wl
+    with make_ctx(locc_mod, *weights, pts) as ctx:
+        out = ctx.query_cells(pairs[:0], poses[:0], debug=True)
+        assert out["probs"].shape == (0,)
+        far = poses[:16].copy()
+        far[:, 1, 4] += 10.0  # B far from A: no cell on either side, short-circuit
+        got = ctx.query_cells(pairs[:16], far, debug=True)
+    assert np.all(got["nsel"] == 0) and np.all(got["probs"] == 0) and np.all(got["labels"] == 0)
+    assert np.all(np.isneginf(got["logits"])) and np.all(got["emb"] == 0) and np.all(got["cells"] == 0)

@@ -130,3 +130,14 @@ def test_grad_unsupported_width_fails_loudly(locc_mod, spread_flat):
     with pytest.raises(locc_mod.LoccError):
         ctx.query_grad(pairs, poses)
     ctx.close()
+
+
+def test_grad_empty_batch_and_short_circuit(locc_mod, wl, spread_flat):
+    pts, pairs, poses = wl
+    with make_ctx(locc_mod, spread_flat, pts, 1) as ctx:
+        pr, lb, lg, g = ctx.query_grad(pairs[:0], poses[:0])
+        assert g.shape == (0, 14)
+        far = poses[:8].copy()
+        far[:, 1, 4] += 10.0
+        pr, lb, lg, g = ctx.query_grad(pairs[:8], far)
+    assert np.all(g == 0) and np.all(pr == 0) and np.all(np.isneginf(lg))
