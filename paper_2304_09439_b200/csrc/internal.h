@@ -112,7 +112,9 @@ struct Batch {
   int32_t* occ;          // [G] C_s (from the crop; written only when want_occ)
   int want_occ;          // the caller asked for C_s (locc_query_debug)
   int64_t* offsets;      // [G+1] exclusive scan of counts
-  float4* rows;          // [sum n] kept rows (x, y, z, flags)
+  uint2* rows;           // [sum pad16(n)] kept rows: (flags, point index k in the own shape's sorted table)
+  const float4* pts;     // the shape table's sorted points [S][K] (the rows' coordinates: pts[own K + k])
+  int K;
   float* pooled;         // [G][H] mean over occupied cells of the cell-max features
   const float* emb_in;   // encode-once mode: [G][F] pooled cell embeddings (the predictor's e); else null
   float4* xf;            // [G][4] per-segment transform into the other object's frame (segment_xf_kernel):

@@ -46,7 +46,16 @@ __global__ void __launch_bounds__(256) encoder_f32_kernel(DevParams P, Batch b) 
 
   for (int64_t t0 = r0; t0 < r1; t0 += TR) {
     const int nr = (int)min((int64_t)TR, r1 - t0);
-    if (f < TR) rows_s[f] = f < nr ? b.rows[t0 + f] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (f < TR) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (f < nr) {  // the row's coordinates from the shape table (own shape of the row's segment)
+        const uint2 rw = b.rows[t0 + f];
+        const int own = __float_as_int(b.xf[4 * (int64_t)(rw.x >> kRowSegShift) + 3].x);
+        const float4 p = b.pts[(int64_t)own * b.K + rw.y];
+        v = make_float4(p.x, p.y, p.z, __uint_as_float(rw.x));
+      }
+      rows_s[f] = v;
+    }
     __syncthreads();
     float acc[TR];
     point_mlp_tile(P, rows_s, hT, acc, w1, b2, f, act);

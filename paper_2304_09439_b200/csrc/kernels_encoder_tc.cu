@@ -118,7 +118,10 @@ struct TcArgs {
   const float* b3;
   const uint8_t* w2img;   // [2 ranks][5 x 16384 B] pre-swizzled (W2 + bias block)
   const uint32_t* w3img;  // [256 rows][128] bf16x2
-  const float4* rows;
+  const uint2* rows;      // (flags, point index) per row; coordinates in pts[own K + k]
+  const float4* pts;
+  const float4* xf;       // per-segment transforms (own shape id in [4 seg + 3].x)
+  int K;
   const int64_t* offsets;
   float* pooled;
   int64_t G;
@@ -448,7 +451,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
       if (ok && lt < 128) {
         const uint32_t trow = tile_row_of_local(rank, lt);
-        if ((int)trow < nr) p = a.rows[r0 + trow];
+        if ((int)trow < nr) {
+          const uint2 rw = a.rows[r0 + trow];
+          const int own = __float_as_int(a.xf[4 * (int64_t)(rw.x >> kRowSegShift) + 3].x);
+          p = a.pts[(int64_t)own * a.K + rw.y];
+        }
       }
       return p;
     };
@@ -580,9 +587,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = 128 * h + 32 * eg + lane;
-        S.flags[r] = r < nrows ? __float_as_uint(a.rows[row0 + r].w) : 0u;
+        S.flags[r] = r < nrows ? a.rows[row0 + r].x : 0u;
         const int r2 = interleaved_row(h, eg, lane);  // interleaved masks of step eg of part h
-        const uint32_t fl = r2 < nrows ? __float_as_uint(a.rows[row0 + r2].w) : 0u;
+        const uint32_t fl = r2 < nrows ? a.rows[row0 + r2].x : 0u;
         const uint32_t ce = __ballot_sync(0xffffffffu, fl & kRowFlagCellEnd);
         const uint32_t se = __ballot_sync(0xffffffffu, fl & kRowFlagSegEnd);
         if (lane == 0) {
@@ -634,6 +641,9 @@ cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b
   args.w2img = static_cast<const uint8_t*>(P.tc_w2);
   args.w3img = static_cast<const uint32_t*>(P.tc_w3);
   args.rows = b.rows;
+  args.pts = b.pts;
+  args.xf = b.xf;
+  args.K = b.K;
   args.offsets = b.offsets;
   args.pooled = b.pooled;
   args.G = b.G;

@@ -240,11 +240,11 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
   const float4* pts = T.pts + (int64_t)own * T.K;
   const int nsteps = (T.K + 31) >> 5;
   const uint32_t* kb = b.kbits + g * nsteps;
-  float4* out = b.rows + b.offsets[g];
+  uint2* out = b.rows + b.offsets[g];
   const uint32_t segbits = (uint32_t)g << kRowSegShift;
   int written = 0;        // kept rows before this step
   bool pending = false;   // a held-back row (warp-uniform)
-  float4 prow;            // held-back row payload (valid in every lane)
+  int pk = 0;             // held-back row's point index (valid in every lane)
   int pcell = 0, pidx = 0;
   for (int base0 = 0; base0 < T.K; base0 += 128) {
     // four steps in flight together: the count pass's ballots, then only the kept points' loads
@@ -273,16 +273,15 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
     const int first_cell = __shfl_sync(0xffffffffu, cell, first);
     if (pending && lane == 0) {
       const uint32_t f = segbits | (pcell != first_cell ? kRowFlagCellEnd : 0);
-      out[pidx] = make_float4(prow.x, prow.y, prow.z, __uint_as_float(f));
+      out[pidx] = make_uint2(f, (uint32_t)pk);
     }
     const int idx = written + __popc(m & lanemask_lt());
+    const int k = base + lane;
     if (keep && lane != last) {
       const uint32_t f = segbits | (cell != next_cell ? kRowFlagCellEnd : 0);
-      out[idx] = make_float4(p.x, p.y, p.z, __uint_as_float(f));
+      out[idx] = make_uint2(f, (uint32_t)k);
     }
-    prow.x = __shfl_sync(0xffffffffu, p.x, last);
-    prow.y = __shfl_sync(0xffffffffu, p.y, last);
-    prow.z = __shfl_sync(0xffffffffu, p.z, last);
+    pk = __shfl_sync(0xffffffffu, k, last);
     pcell = __shfl_sync(0xffffffffu, cell, last);
     pidx = written + __popc(m) - 1;
     pending = true;
@@ -291,11 +290,11 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
   }
   if (pending && lane == 0) {
     const uint32_t f = segbits | kRowFlagCellEnd | kRowFlagSegEnd;
-    out[pidx] = make_float4(prow.x, prow.y, prow.z, __uint_as_float(f));
+    out[pidx] = make_uint2(f, (uint32_t)pk);
   }
   // padding up to the next multiple of kSegAlign rows
   const int pad_end = (int)seg_rows(n);
-  if (n + lane < pad_end) out[n + lane] = make_float4(0.f, 0.f, 0.f, __uint_as_float(segbits | kRowFlagPad));
+  if (n + lane < pad_end) out[n + lane] = make_uint2(segbits | kRowFlagPad, 0u);
 }
 
 // ---------------------------------------------------------------- exclusive scan of segment footprints

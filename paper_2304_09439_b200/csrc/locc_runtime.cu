@@ -339,7 +339,7 @@ locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks, bool need_gr
     CK(c->occ.ensure(sizeof(int32_t) * G));
     CK(c->offsets.ensure(sizeof(int64_t) * (G + 1)));
     CK(c->scan_tmp.ensure(sizeof(int64_t) * scan_tmp_elems(G)));
-    CK(c->rows.ensure(sizeof(float4) * (size_t)G * seg_rows(K)));
+    CK(c->rows.ensure(sizeof(uint2) * (size_t)G * seg_rows(K)));
     CK(c->pooled.ensure(sizeof(float) * (size_t)G * c->cfg.H));
     CK(c->out_probs.ensure(sizeof(float) * B));
     CK(c->out_labels.ensure(B));
@@ -365,7 +365,7 @@ int64_t batch_cap(const locc_ctx* c) {
   int64_t B = c->cfg.max_batch > 0 ? c->cfg.max_batch : 262144;
   // bound the compacted-row buffer (worst case every point kept) to ~12 GiB
   const int64_t rows_budget = (int64_t)12 << 30;
-  const int64_t per_pair = 2LL * seg_rows(c->T.K) * (int64_t)sizeof(float4);
+  const int64_t per_pair = 2LL * seg_rows(c->T.K) * (int64_t)sizeof(uint2);
   B = std::min<int64_t>(B, std::max<int64_t>(1, rows_budget / per_pair));
   return std::min<int64_t>(B, (int64_t)1 << 29);
 }
@@ -474,7 +474,9 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     b.occ = (dev && occ) ? occ + 2 * i0 : c->occ.as<int32_t>();
     b.want_occ = occ != nullptr;
     b.offsets = c->offsets.as<int64_t>();
-    b.rows = c->rows.as<float4>();
+    b.rows = c->rows.as<uint2>();
+    b.pts = c->T.pts;
+    b.K = c->T.K;
     b.pooled = c->pooled.as<float>();
     b.stats = dstats;
     b.xf = c->xf.as<float4>();
