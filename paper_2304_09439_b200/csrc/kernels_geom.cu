@@ -138,7 +138,7 @@ __global__ void shape_sort_kernel(const float* __restrict__ in, int K, int M, co
 // ---------------------------------------------------------------- S1 per segment
 // One thread per (pair, side) segment: validate the inputs and write the transform (segment_setup's
 // prescribed fp64 arithmetic, rounded once to fp32) for the crop and cell-selection kernels.
-__global__ void __launch_bounds__(256) segment_xf_kernel(ShapeTable T, Batch b) {
+__global__ void __launch_bounds__(128) segment_xf_kernel(ShapeTable T, Batch b) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= b.G) return;
   int own = -1, other = -1;
@@ -298,10 +298,14 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
 }
 
 // ---------------------------------------------------------------- exclusive scan of segment footprints
-__global__ void __launch_bounds__(1024) scan_blocks_kernel(const int32_t* __restrict__ in, int64_t G,
-                                                           int64_t* __restrict__ out, int64_t* __restrict__ sums) {
-  __shared__ int64_t ws[32];
-  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+// Block size of the scan kernels: 256 threads, so that a scan block fits next to a persistent encoder
+// CTA (the overlapped crop pipeline).
+constexpr int kScanBS = 256;
+
+__global__ void __launch_bounds__(kScanBS) scan_blocks_kernel(const int32_t* __restrict__ in, int64_t G,
+                                                              int64_t* __restrict__ out, int64_t* __restrict__ sums) {
+  __shared__ int64_t ws[kScanBS / 32];
+  const int64_t i = (int64_t)blockIdx.x * kScanBS + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int64_t v = i < G ? seg_rows(in[i]) : 0, x = v;  // segment footprint: kept rows + padding
   for (int o = 1; o < 32; o <<= 1) {
@@ -311,26 +315,26 @@ __global__ void __launch_bounds__(1024) scan_blocks_kernel(const int32_t* __rest
   if (lane == 31) ws[w] = x;
   __syncthreads();
   if (w == 0) {
-    int64_t s = ws[lane], t = s;
+    int64_t s = lane < kScanBS / 32 ? ws[lane] : 0, t = s;
     for (int o = 1; o < 32; o <<= 1) {
       int64_t y = __shfl_up_sync(0xffffffffu, t, o);
       if (lane >= o) t += y;
     }
-    ws[lane] = t - s;
-    if (lane == 31) sums[blockIdx.x] = t;
+    if (lane < kScanBS / 32) ws[lane] = t - s;
+    if (lane == kScanBS / 32 - 1) sums[blockIdx.x] = t;
   }
   __syncthreads();
   if (i < G) out[i] = x - v + ws[w];
 }
 
-__global__ void __launch_bounds__(1024) scan_top_kernel(int64_t* __restrict__ sums, int64_t nb,
-                                                        int64_t* __restrict__ total) {
-  __shared__ int64_t ws[32];
+__global__ void __launch_bounds__(kScanBS) scan_top_kernel(int64_t* __restrict__ sums, int64_t nb,
+                                                           int64_t* __restrict__ total) {
+  __shared__ int64_t ws[kScanBS / 32];
   __shared__ int64_t carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t base = 0; base < nb; base += 1024) {
+  for (int64_t base = 0; base < nb; base += kScanBS) {
     const int64_t i = base + threadIdx.x;
     int64_t v = i < nb ? sums[i] : 0, x = v;
     for (int o = 1; o < 32; o <<= 1) {
@@ -340,26 +344,26 @@ __global__ void __launch_bounds__(1024) scan_top_kernel(int64_t* __restrict__ su
     if (lane == 31) ws[w] = x;
     __syncthreads();
     if (w == 0) {
-      int64_t s = ws[lane], t = s;
+      int64_t s = lane < kScanBS / 32 ? ws[lane] : 0, t = s;
       for (int o = 1; o < 32; o <<= 1) {
         int64_t y = __shfl_up_sync(0xffffffffu, t, o);
         if (lane >= o) t += y;
       }
-      ws[lane] = t - s;
+      if (lane < kScanBS / 32) ws[lane] = t - s;
     }
     __syncthreads();
     const int64_t c = carry;
     if (i < nb) sums[i] = c + x - v + ws[w];
     __syncthreads();
-    if (threadIdx.x == 1023) carry = c + x + ws[w];
+    if (threadIdx.x == kScanBS - 1) carry = c + x + ws[w];
     __syncthreads();
   }
   if (threadIdx.x == 0) *total = carry;
 }
 
-__global__ void __launch_bounds__(1024) scan_add_kernel(int64_t* __restrict__ out, int64_t G,
-                                                        const int64_t* __restrict__ sums) {
-  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+__global__ void __launch_bounds__(kScanBS) scan_add_kernel(int64_t* __restrict__ out, int64_t G,
+                                                           const int64_t* __restrict__ sums) {
+  const int64_t i = (int64_t)blockIdx.x * kScanBS + threadIdx.x;
   if (i < G) out[i] += sums[blockIdx.x];
 }
 
@@ -375,35 +379,36 @@ cudaError_t launch_shape_prep(const float* pts_in, int S, int K, int M, float4* 
 
 cudaError_t launch_segment_xf(const ShapeTable& T, const Batch& b, cudaStream_t st) {
   if (b.G == 0) return cudaSuccess;
-  segment_xf_kernel<<<(unsigned)((b.G + 255) / 256), 256, 0, st>>>(T, b);
+  segment_xf_kernel<<<(unsigned)((b.G + 127) / 128), 128, 0, st>>>(T, b);
   return cudaGetLastError();
 }
 
 cudaError_t launch_crop_count(const ShapeTable& T, const Batch& b, int words, cudaStream_t st) {
   if (b.G == 0) return cudaSuccess;
-  const int64_t blocks = (b.G * 32 + 255) / 256;
+  // 128-thread blocks: small enough to be co-resident with a persistent encoder CTA (overlapped crop)
+  const int64_t blocks = (b.G * 32 + 127) / 128;
   if (b.want_occ)
-    crop_count_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(T, b, words);
+    crop_count_kernel<true><<<(unsigned)blocks, 128, 0, st>>>(T, b, words);
   else
-    crop_count_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(T, b, words);
+    crop_count_kernel<false><<<(unsigned)blocks, 128, 0, st>>>(T, b, words);
   return cudaGetLastError();
 }
 
-size_t scan_tmp_elems(int64_t G) { return (size_t)((G + 1023) / 1024) + 1; }
+size_t scan_tmp_elems(int64_t G) { return (size_t)((G + kScanBS - 1) / kScanBS) + 1; }
 
 cudaError_t launch_scan(const int32_t* counts, int64_t G, int64_t* offsets, int64_t* block_tmp, cudaStream_t st) {
-  const int64_t nb = (G + 1023) / 1024;
+  const int64_t nb = (G + kScanBS - 1) / kScanBS;
   if (nb == 0) return cudaMemsetAsync(offsets, 0, sizeof(int64_t), st);
-  scan_blocks_kernel<<<(unsigned)nb, 1024, 0, st>>>(counts, G, offsets, block_tmp);
-  scan_top_kernel<<<1, 1024, 0, st>>>(block_tmp, nb, offsets + G);
-  scan_add_kernel<<<(unsigned)nb, 1024, 0, st>>>(offsets, G, block_tmp);
+  scan_blocks_kernel<<<(unsigned)nb, kScanBS, 0, st>>>(counts, G, offsets, block_tmp);
+  scan_top_kernel<<<1, kScanBS, 0, st>>>(block_tmp, nb, offsets + G);
+  scan_add_kernel<<<(unsigned)nb, kScanBS, 0, st>>>(offsets, G, block_tmp);
   return cudaGetLastError();
 }
 
 cudaError_t launch_crop_emit(const ShapeTable& T, const Batch& b, cudaStream_t st) {
   if (b.G == 0) return cudaSuccess;
-  const int64_t blocks = (b.G * 32 + 255) / 256;
-  crop_emit_kernel<<<(unsigned)blocks, 256, 0, st>>>(T, b);
+  const int64_t blocks = (b.G * 32 + 127) / 128;
+  crop_emit_kernel<<<(unsigned)blocks, 128, 0, st>>>(T, b);
   return cudaGetLastError();
 }
 

@@ -94,6 +94,8 @@ struct locc_ctx {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // host-buffer queries: input uploads overlap the previous sub-batch
+  cudaStream_t crop_stream = nullptr;  // crop of sub-batch s + 1 overlaps the encoder of sub-batch s
+  cudaEvent_t ev_q0 = nullptr, ev_crop[2] = {}, ev_done[2] = {}, ev_cs[64] = {}, ev_ce[64] = {};
   cudaEvent_t ev[2] = {};          // whole-query timing
   cudaEvent_t ev_in[2] = {}, ev_free[2] = {};  // input buffer k & 1: uploaded / released by the kernels
   std::vector<cudaEvent_t> enc_ev;  // per sub-batch encoder start/stop pairs
@@ -112,9 +114,13 @@ struct locc_ctx {
   int64_t cap_B = 0;
   DevBuf trace;
   DevBuf in_pairs, in_poses, in_pairs2, in_poses2, counts, occ, offsets, scan_tmp, rows, pooled, stats, xf, kbits;
+  // second buffer set of the overlapped crop pipeline (sub-batches alternate between the two)
+  DevBuf counts2, offsets2, scan_tmp2, rows2, pooled2, xf2, kbits2;
+  int64_t cap_B2 = 0;
   DevBuf out_probs, out_labels, out_logits, out_kept, out_occ, out_masks, out_emb, out_grad;
   locc_stats last{};
   int64_t timed_subs = 0;  // sub-batches whose encoder events await reading
+  bool timed_overlap = false;  // the last timed query ran the overlapped crop pipeline
   // NEXT-1 encode-once mode
   bool has_unet = false, has_cells = false;
   DevBuf unet_params, cells_E, cells_ctr, cells_emb;
@@ -325,6 +331,23 @@ locc_status upload_params(locc_ctx* c, const float* flat) {
   return LOCC_OK;
 }
 
+// The second buffer set of the overlapped crop pipeline.
+locc_status ensure_scratch2(locc_ctx* c, int64_t B) {
+  const int K = c->T.K;
+  const int64_t G = 2 * B;
+  if (B > c->cap_B2) {
+    CK(c->counts2.ensure(sizeof(int32_t) * G));
+    CK(c->offsets2.ensure(sizeof(int64_t) * (G + 1)));
+    CK(c->scan_tmp2.ensure(sizeof(int64_t) * scan_tmp_elems(G)));
+    CK(c->rows2.ensure(sizeof(uint2) * (size_t)G * seg_rows(K)));
+    CK(c->pooled2.ensure(sizeof(float) * (size_t)G * c->cfg.H));
+    CK(c->xf2.ensure(sizeof(float4) * 4 * G));
+    CK(c->kbits2.ensure(sizeof(uint32_t) * G * ((K + 31) / 32)));
+    c->cap_B2 = B;
+  }
+  return LOCC_OK;
+}
+
 locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks, bool need_grad) {
   const int K = c->T.K;
   const int64_t G = 2 * B;
@@ -382,8 +405,15 @@ locc_status read_timing(locc_ctx* c) {
     enc += ms;
     CK(cudaEventElapsedTime(&ms, c->enc_ev[2 * s + 1], c->head_ev[s]));
     head += ms;
-    CK(cudaEventElapsedTime(&ms, c->crop_ev[s], c->enc_ev[2 * s]));
-    crop += ms;
+    if (c->timed_overlap) {
+      if (s < 64) {
+        CK(cudaEventElapsedTime(&ms, c->ev_cs[s], c->ev_ce[s]));
+        crop += ms;
+      }
+    } else {
+      CK(cudaEventElapsedTime(&ms, c->crop_ev[s], c->enc_ev[2 * s]));
+      crop += ms;
+    }
   }
   c->last.encoder_ms = enc;
   c->last.head_ms = head;
@@ -428,6 +458,19 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
   }
   DevStats* dstats = c->stats.as<DevStats>();
   CK(cudaMemsetAsync(dstats, 0, sizeof(DevStats), st));
+  // Overlapped crop pipeline (device buffers, crop path, no debug outputs, >= 2 sub-batches): the crop of
+  // sub-batch s + 1 runs on a low-priority stream into the other buffer set while the encoder runs
+  // sub-batch s — the crop warps fill issue slots the latency-bound encoder leaves idle.
+  const int64_t n_sub_all = (N + Bcap - 1) / Bcap;
+  const bool overlap = !cells && dev && !kept && !occ && !masks && !emb && n_sub_all >= 2 &&
+                       c->cfg.precision == LOCC_PREC_BF16 && !getenv("LOCC_NO_OVERLAP");
+  if (overlap) {
+    s = ensure_scratch2(c, Bcap);
+    if (s != LOCC_OK) return s;
+    CK(cudaEventRecord(c->ev_q0, st));
+    CK(cudaStreamWaitEvent(c->crop_stream, c->ev_q0, 0));
+  }
+  c->timed_overlap = overlap;
   const int64_t n_sub = (N + Bcap - 1) / Bcap;
   if (c->timing) {
     while ((int64_t)c->enc_ev.size() < 2 * n_sub) {
@@ -470,17 +513,18 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       b.pairs = dp.as<int32_t>();
       b.poses = dq.as<float>();
     }
-    b.counts = (dev && kept) ? kept + 2 * i0 : c->counts.as<int32_t>();
+    const bool set2 = overlap && (subs & 1);
+    b.counts = (dev && kept) ? kept + 2 * i0 : (set2 ? c->counts2 : c->counts).as<int32_t>();
     b.occ = (dev && occ) ? occ + 2 * i0 : c->occ.as<int32_t>();
     b.want_occ = occ != nullptr;
-    b.offsets = c->offsets.as<int64_t>();
-    b.rows = c->rows.as<uint2>();
+    b.offsets = (set2 ? c->offsets2 : c->offsets).as<int64_t>();
+    b.rows = (set2 ? c->rows2 : c->rows).as<uint2>();
     b.pts = c->T.pts;
     b.K = c->T.K;
-    b.pooled = c->pooled.as<float>();
+    b.pooled = (set2 ? c->pooled2 : c->pooled).as<float>();
     b.stats = dstats;
-    b.xf = c->xf.as<float4>();
-    b.kbits = c->kbits.as<uint32_t>();
+    b.xf = (set2 ? c->xf2 : c->xf).as<float4>();
+    b.kbits = (set2 ? c->kbits2 : c->kbits).as<uint32_t>();
     b.masks = nullptr;
     if (masks) {
       b.masks = dev ? masks + (size_t)2 * i0 * words : c->out_masks.as<uint32_t>();
@@ -510,11 +554,25 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       if (emb) d_emb = e_in;  // the selection wrote e (0 for an empty side) in place
       launches += 3;
     } else {
-    if (c->timing) CK(cudaEventRecord(c->crop_ev[subs], st));
-    CK(launch_segment_xf(c->T, b, st));
-    CK(launch_crop_count(c->T, b, words, st));
-    CK(launch_scan(b.counts, b.G, b.offsets, c->scan_tmp.as<int64_t>(), st));
-    CK(launch_crop_emit(c->T, b, st));
+    if (overlap) {
+      const int j = (int)(subs & 1);
+      cudaStream_t cs = c->crop_stream;
+      if (subs >= 2) CK(cudaStreamWaitEvent(cs, c->ev_done[j], 0));  // sub-batch s - 2 done with set j
+      if (c->timing && subs < 64) CK(cudaEventRecord(c->ev_cs[subs], cs));
+      CK(launch_segment_xf(c->T, b, cs));
+      CK(launch_crop_count(c->T, b, words, cs));
+      CK(launch_scan(b.counts, b.G, b.offsets, (set2 ? c->scan_tmp2 : c->scan_tmp).as<int64_t>(), cs));
+      CK(launch_crop_emit(c->T, b, cs));
+      if (c->timing && subs < 64) CK(cudaEventRecord(c->ev_ce[subs], cs));
+      CK(cudaEventRecord(c->ev_crop[j], cs));
+      CK(cudaStreamWaitEvent(st, c->ev_crop[j], 0));
+    } else {
+      if (c->timing) CK(cudaEventRecord(c->crop_ev[subs], st));
+      CK(launch_segment_xf(c->T, b, st));
+      CK(launch_crop_count(c->T, b, words, st));
+      CK(launch_scan(b.counts, b.G, b.offsets, c->scan_tmp.as<int64_t>(), st));
+      CK(launch_crop_emit(c->T, b, st));
+    }
     if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs], st));
     if (c->cfg.precision == LOCC_PREC_BF16) {
       long long* trace = nullptr;
@@ -549,6 +607,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     else
       CK(launch_head(c->P, b, d_probs, d_labels, d_logits, d_emb, d_grad, st));
     if (c->timing) CK(cudaEventRecord(c->head_ev[subs], st));
+    if (overlap) CK(cudaEventRecord(c->ev_done[subs & 1], st));
     launches += 8;
     }
     if (!dev) CK(cudaEventRecord(c->ev_free[subs & 1], st));  // the kernels are done with the inputs
@@ -646,6 +705,16 @@ locc_status locc_create(const locc_config* cfg, locc_ctx** out) {
   if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) c->num_sms = prop.multiProcessorCount;
   cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);  // lo = least urgent: the encoder's CTAs go first
+    e = cudaStreamCreateWithPriority(&c->crop_stream, cudaStreamNonBlocking, lo);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_q0, cudaEventDisableTiming);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&c->ev_crop[i], cudaEventDisableTiming);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming);
+  for (int i = 0; i < 64 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev_cs[i]);
+  for (int i = 0; i < 64 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev_ce[i]);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreate(&c->ev[i]);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming);
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming);
@@ -669,6 +738,19 @@ void locc_destroy(locc_ctx* c) {
     if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->crop_stream) {
+    cudaStreamSynchronize(c->crop_stream);
+    cudaStreamDestroy(c->crop_stream);
+  }
+  if (c->ev_q0) cudaEventDestroy(c->ev_q0);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_crop[i]) cudaEventDestroy(c->ev_crop[i]);
+    if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
+  }
+  for (int i = 0; i < 64; ++i) {
+    if (c->ev_cs[i]) cudaEventDestroy(c->ev_cs[i]);
+    if (c->ev_ce[i]) cudaEventDestroy(c->ev_ce[i]);
+  }
   if (c->sim_exec) cudaGraphExecDestroy(c->sim_exec);
   for (auto& e : c->enc_ev) cudaEventDestroy(e);
   for (auto& e : c->head_ev) cudaEventDestroy(e);
@@ -806,7 +888,7 @@ locc_status locc_set_shapes(locc_ctx* c, const float* points, int32_t S, int32_t
   c->T.S = S;
   c->has_cells = false;  // the cached grids belong to the previous shape table
   ++c->generation;
-  if (c->T.K != K) c->cap_B = 0;  // row buffer depends on K
+  if (c->T.K != K) c->cap_B = c->cap_B2 = 0;  // row buffers depend on K
   c->T.K = K;
   c->has_shapes = true;
   return LOCC_OK;
