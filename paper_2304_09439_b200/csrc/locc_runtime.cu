@@ -458,11 +458,11 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
   }
   DevStats* dstats = c->stats.as<DevStats>();
   CK(cudaMemsetAsync(dstats, 0, sizeof(DevStats), st));
-  // Overlapped crop pipeline (device buffers, crop path, no debug outputs, >= 2 sub-batches): the crop of
+  // Overlapped crop pipeline (crop path, no debug outputs, >= 2 sub-batches): the crop of
   // sub-batch s + 1 runs on a low-priority stream into the other buffer set while the encoder runs
   // sub-batch s — the crop warps fill issue slots the latency-bound encoder leaves idle.
   const int64_t n_sub_all = (N + Bcap - 1) / Bcap;
-  const bool overlap = !cells && dev && !kept && !occ && !masks && !emb && n_sub_all >= 2 &&
+  const bool overlap = !cells && !kept && !occ && !masks && !emb && n_sub_all >= 2 &&
                        c->cfg.precision == LOCC_PREC_BF16 && !getenv("LOCC_NO_OVERLAP");
   if (overlap) {
     s = ensure_scratch2(c, Bcap);
@@ -510,6 +510,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       CK(cudaMemcpyAsync(dq.p, poses + 14 * i0, sizeof(float) * 14 * B, cudaMemcpyHostToDevice, c->copy_stream));
       CK(cudaEventRecord(c->ev_in[buf], c->copy_stream));
       CK(cudaStreamWaitEvent(st, c->ev_in[buf], 0));
+      if (overlap) CK(cudaStreamWaitEvent(c->crop_stream, c->ev_in[buf], 0));
       b.pairs = dp.as<int32_t>();
       b.poses = dq.as<float>();
     }
