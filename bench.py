@@ -228,7 +228,8 @@ def main():
         with torch.cuda.stream(stream):
             ev[i][1].record(stream)
         stream.synchronize()
-        enc_ms.append(ctx.stats()["encoder_ms"])
+        tst = ctx.stats()  # the timed step's own launch counts
+        enc_ms.append(tst["encoder_ms"])
         ctx.set_timing(False)
     torch.cuda.synchronize()
     if world > 1:
@@ -248,8 +249,8 @@ def main():
     except Exception:
         pass
     kept = st["kept_rows"]
-    launches_per_step = st["kernel_launches"]
-    subs = max(1, st["sub_batches"])
+    launches_per_step = tst["kernel_launches"]
+    subs = max(1, tst["sub_batches"])
     enc_s = statistics.mean(enc_ms) / 1e3
     achieved = FLOP_PER_ROW * kept / enc_s / 1e12 if enc_s > 0 else None
     if prec == locc.LOCC_PREC_BF16:

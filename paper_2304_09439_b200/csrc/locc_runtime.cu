@@ -491,7 +491,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     CK(cudaEventRecord(c->ev[0], st));
   }
   int64_t launches = 0, subs = 0;
-  for (int64_t i0 = 0; i0 < N; i0 += Bcap) {
+  for (int64_t i0 = 0; i0 < N;) {
     const int64_t B = std::min(Bcap, N - i0);
     Batch b{};
     b.B = B;
@@ -630,6 +630,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       if (kept && b.counts != kept + 2 * i0)
         CK(cudaMemcpyAsync(kept + 2 * i0, b.counts, sizeof(int32_t) * 2 * B, cudaMemcpyDeviceToDevice, st));
     }
+    i0 += B;
   }
   if (c->timing) CK(cudaEventRecord(c->ev[1], st));
   c->last = locc_stats{};
