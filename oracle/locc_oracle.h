@@ -13,8 +13,16 @@
  * h1, W2, h2, W3 to bf16 (round-to-nearest-even) before their products — the
  * arithmetic the bf16 tensor-core path is defined to perform.
  *
- * Parity pins: tests/test_oracle_*.py.  "parity unpinned": absolute
- * probabilities of any trained LOCC (no trained weights exist).
+ * Beyond the headline path: the pose gradient (NEXT-2, oracle_head_grad /
+ * oracle_query_grad, fp64 reverse mode), the encode-once mode with the 3D U-Net (NEXT-1,
+ * oracle_conv3d / oracle_encode_grid / oracle_query_cells) and the closed-loop substep (NEXT-3,
+ * oracle_sim_run); readings Q26-Q31.
+ *
+ * Parity pins: tests/test_oracle_*.py (network, geometry, grad: finite differences, a closed-form
+ * head, symmetries; cells: scipy correlate/convolve, the adjoint identity, a delta-kernel U-Net probe,
+ * a box-intersection superset property, a worked example; sim: discrete closed forms, score descent,
+ * body-swap symmetry).  "parity unpinned": absolute probabilities of any trained LOCC (no trained
+ * weights exist).
  *
  * Return codes: 0 ok; -1 invalid argument; -2 bad shape table; -3 bad weights.
  */
