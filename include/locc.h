@@ -161,6 +161,11 @@ int64_t locc_unet_n_params(int32_t H, int32_t F);
  * Errors: INVALID_ARG (null), WEIGHTS (count, non-finite), CUDA, OOM. */
 locc_status locc_load_unet_weights_mem(locc_ctx* ctx, const float* flat, size_t n_floats);
 
+/* The U-Net's global feature ("average pooling ... just before the deconvolution" vs
+ * :421 "max pooling to get global features"): 0 = average (default, reading Q28), 1 = max.  Takes
+ * effect at the next locc_encode_shapes (the cached grids are invalidated).  Errors: INVALID_ARG. */
+locc_status locc_set_unet_global_pool(locc_ctx* ctx, int32_t mode);
+
 /* Encode every shape of the current table and cache the grids on the device (synchronous).  Must be
  * re-run after locc_set_shapes / locc_load_weights / locc_load_unet_weights_mem.
  * Errors: STATE (weights, U-Net weights or shapes missing), INVALID_ARG (M, H, F), CUDA, OOM. */

@@ -27,7 +27,7 @@ def build(force: bool = False) -> str:
 
 class _Cfg(C.Structure):
     _fields_ = [("M", C.c_int32), ("H", C.c_int32), ("F", C.c_int32), ("bf16_emul", C.c_int32),
-                ("n_threads", C.c_int32)]
+                ("n_threads", C.c_int32), ("global_max", C.c_int32)]
 
 
 def lib():
@@ -169,21 +169,21 @@ def conv3d(x, W, b=None, pad=0, transposed=False):
     return y
 
 
-def encode_grid(weights_flat, unet_flat, points_k3, M=6, H=256, F=64):
+def encode_grid(weights_flat, unet_flat, points_k3, M=6, H=256, F=64, global_max=False):
     """Encode one shape -> (G [M^3][H] cell-max grid, E [M^3][F] embedding grid), fp64."""
     w = np.ascontiguousarray(weights_flat, np.float32)
     u = np.ascontiguousarray(unet_flat, np.float32)
     p = np.ascontiguousarray(points_k3, np.float32)
     G = np.zeros((M ** 3, H))
     E = np.zeros((M ** 3, F))
-    cfg = _Cfg(M, H, F, 0, 1)
+    cfg = _Cfg(M, H, F, 0, 1, 1 if global_max else 0)
     rc = lib().oracle_encode_grid(C.byref(cfg), _p(w), w.size, _p(u), u.size, _p(p), p.shape[0], _p(G), _p(E))
     if rc:
         raise ValueError(f"oracle_encode_grid: {rc}")
     return G, E
 
 
-def query_cells(weights_flat, unet_flat, points, pairs, poses, M=6, H=256, F=64, n_threads=0):
+def query_cells(weights_flat, unet_flat, points, pairs, poses, M=6, H=256, F=64, n_threads=0, global_max=False):
     """Encode-once query: dict with probs, labels, logits, nsel [N][2], cells [N][2][ceil(M^3/32)],
     emb [N][2][F] and grids [S][M^3][F] (zeros for unreferenced shapes)."""
     w = np.ascontiguousarray(weights_flat, np.float32)
@@ -197,7 +197,7 @@ def query_cells(weights_flat, unet_flat, points, pairs, poses, M=6, H=256, F=64,
     out = dict(probs=np.zeros(N), labels=np.zeros(N, np.uint8), logits=np.zeros(N),
                nsel=np.zeros((N, 2), np.int32), cells=np.zeros((N, 2, words), np.uint32),
                emb=np.zeros((N, 2, F)), grids=np.zeros((S, M ** 3, F)))
-    cfg = _Cfg(M, H, F, 0, n_threads)
+    cfg = _Cfg(M, H, F, 0, n_threads, 1 if global_max else 0)
     rc = lib().oracle_query_cells(C.byref(cfg), _p(w), w.size, _p(u), u.size, _p(pts), S, K, _p(pr), _p(po), N,
                                   _p(out["probs"]), _p(out["labels"]), _p(out["logits"]), _p(out["nsel"]),
                                   _p(out["cells"]), _p(out["emb"]), _p(out["grids"]))

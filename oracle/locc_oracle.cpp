@@ -8,6 +8,7 @@
 // and "O<k>" = the step of SURVEY.md §8(c) that fixes the reading used by this build.
 #include "locc_oracle.h"
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -551,7 +552,8 @@ void grid_maxpool(const Params& P, const EncW& EW, const float* pts, int K, cons
 // concatenation skips (d4 <- c4; d3 <- [d4; c3]; d2 <- [d3; c2]; d1 <- [d2; c1], the last one the
 // transposed valid conv back to M^3), the global feature tiled and concatenated, one linear layer to F
 // (P:422).  E: [M^3][F].
-void unet(const UNetW& U, const std::vector<double>& G, int M, int H, int F, std::vector<double>& E) {
+void unet(const UNetW& U, const std::vector<double>& G, int M, int H, int F, std::vector<double>& E,
+          bool global_max = false) {
   const int D = M - 2;
   const int64_t n4 = (int64_t)D * D * D, n6 = (int64_t)M * M * M;
   std::vector<double> c1(n4 * kU), c2(n4 * kU), c3(n4 * kU), c4(n4 * kU), d4(n4 * kU), d3(n4 * kU), d2(n4 * kU),
@@ -565,9 +567,14 @@ void unet(const UNetW& U, const std::vector<double>& G, int M, int H, int F, std
   conv3d(c3.data(), D, kU, U.W[3].data(), U.b[3].data(), kU, 1, c4.data());
   relu_inplace(c4);
   std::vector<double> g(kU, 0.0);
-  for (int64_t q = 0; q < n4; ++q)
-    for (int c = 0; c < kU; ++c) g[c] += c4[q * kU + c];
-  for (int c = 0; c < kU; ++c) g[c] /= (double)n4;
+  if (global_max) {  // the appendix's reading ("we apply max pooling to get global features")
+    for (int64_t q = 0; q < n4; ++q)
+      for (int c = 0; c < kU; ++c) g[c] = std::max(g[c], c4[q * kU + c]);  // c4 >= 0 (ReLU)
+  } else {
+    for (int64_t q = 0; q < n4; ++q)
+      for (int c = 0; c < kU; ++c) g[c] += c4[q * kU + c];
+    for (int c = 0; c < kU; ++c) g[c] /= (double)n4;
+  }
   deconv3d(c4.data(), D, kU, U.W[4].data(), U.b[4].data(), kU, 1, d4.data());
   relu_inplace(d4);
   std::vector<double> x = concat(d4, kU, c3, kU, n4);
@@ -839,7 +846,7 @@ int oracle_encode_grid(const oracle_cfg* cfg, const float* weights, size_t n_wei
   std::vector<double> g, e;
   grid_maxpool(P, EW, pts, K, s, M, H, g);
   if (G) std::memcpy(G, g.data(), sizeof(double) * g.size());
-  unet(bind_unet(unet_w, H, F), g, M, H, F, e);
+  unet(bind_unet(unet_w, H, F), g, M, H, F, e, cfg->global_max != 0);
   if (E) std::memcpy(E, e.data(), sizeof(double) * e.size());
   return 0;
 }
@@ -882,7 +889,7 @@ int oracle_query_cells(const oracle_cfg* cfg, const float* weights, size_t n_wei
         if (s >= S) break;
         if (!used[s]) continue;
         grid_maxpool(P, EW, points + (int64_t)s * K * 3, K, shapes[s], M, H, g);
-        unet(U, g, M, H, F, E[s]);
+        unet(U, g, M, H, F, E[s], cfg->global_max != 0);
       }
     };
     std::vector<std::thread> pool;
@@ -999,7 +1006,7 @@ int oracle_sim_run(const oracle_cfg* cfg, const float* weights, size_t n_weights
     for (int s = 0; s < S; ++s)
       if (used[s]) {
         grid_maxpool(P, EW, points + (int64_t)s * K * 3, K, shapes[s], M, H, g);
-        unet(U, g, M, H, F, grids[s]);
+        unet(U, g, M, H, F, grids[s], cfg->global_max != 0);
       }
   }
   const int pa_[3] = {0, 0, 1}, pb_[3] = {1, 2, 2};

@@ -38,6 +38,7 @@ typedef struct {
   int32_t M, H, F;    /* voxel grid edge, point-feature width, cell-feature width */
   int32_t bf16_emul;  /* 0: fp64 network; 1: bf16-operand emulation of layers 2-3 */
   int32_t n_threads;  /* 0 = hardware_concurrency */
+  int32_t global_max; /* encode-once U-Net global feature: 0 = average (default), 1 = max */
 } oracle_cfg;
 
 /* O0 for one shape: lo/hi (float3), eps2, per-point cell ids [K]. */

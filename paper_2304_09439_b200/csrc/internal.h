@@ -147,8 +147,8 @@ cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_
                         float* logits, float* emb, float* grad, cudaStream_t st);
 // NEXT-1 encode-once mode (kernels_cells.cu)
 cudaError_t launch_grid_encode(const DevParams& P, const ShapeTable& T, int M, float* G, cudaStream_t st);
-cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, int F, const float* G, float* act,
-                        float* E, float* ctr, cudaStream_t st);
+cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, int F, int global_max, const float* G,
+                        float* act, float* E, float* ctr, cudaStream_t st);
 size_t unet_act_floats(int S, int M);
 cudaError_t launch_cells_select(const ShapeTable& T, const CellsTable& C, const Batch& b, int F, uint32_t* cells,
                                 float* emb_out, cudaStream_t st);

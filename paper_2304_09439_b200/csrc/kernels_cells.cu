@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256) conv3d_kernel(ConvArgs a) {
 // ---------------------------------------------------------------- Q28 tail + Q29 cell centres
 // g = mean over the (M-2)^3 positions of c4 ("average pooling ... global feature");
 // E[c] = W_P [d1[c] ; g] + b_P; cell centres lo + (i + 1/2) ext / M in fp64, rounded once.
-__global__ void __launch_bounds__(256) unet_tail_kernel(UNetParams U, ShapeTable T, int M, int F,
+__global__ void __launch_bounds__(256) unet_tail_kernel(UNetParams U, ShapeTable T, int M, int F, int global_max,
                                                         const float* __restrict__ c4, const float* __restrict__ d1,
                                                         float* __restrict__ E, float* __restrict__ ctr) {
   extern __shared__ float sm[];
@@ -206,11 +206,16 @@ __global__ void __launch_bounds__(256) unet_tail_kernel(UNetParams U, ShapeTable
   float* gb = g + 128;             // [F]
   const int s = blockIdx.x, tid = threadIdx.x, nc = M * M * M, D = M - 2, n4 = D * D * D;
   for (int e = tid; e < F * 256; e += 256) pW[(e >> 8) * 257 + (e & 255)] = U.pW[e];
-  if (tid < 128) {
+  if (tid < 128) {  // global feature: average (default) or max of the last conv layer
     float acc = 0.f;
     const float* x = c4 + (int64_t)s * n4 * 128 + tid;
-    for (int q = 0; q < n4; ++q) acc += x[(int64_t)q * 128];
-    g[tid] = __fdiv_rn(acc, (float)n4);
+    if (global_max) {
+      for (int q = 0; q < n4; ++q) acc = fmaxf(acc, x[(int64_t)q * 128]);  // c4 >= 0 (ReLU)
+      g[tid] = acc;
+    } else {
+      for (int q = 0; q < n4; ++q) acc += x[(int64_t)q * 128];
+      g[tid] = __fdiv_rn(acc, (float)n4);
+    }
   }
   __syncthreads();
   if (tid < F) {
@@ -358,8 +363,8 @@ size_t unet_act_floats(int S, int M) {
   return (size_t)S * 128 * (7 * n4 + n6);
 }
 
-cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, int F, const float* G, float* act,
-                        float* E, float* ctr, cudaStream_t st) {
+cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, int F, int global_max, const float* G,
+                        float* act, float* E, float* ctr, cudaStream_t st) {
   const int D = M - 2, S = T.S;
   const size_t n4 = (size_t)S * D * D * D * 128;
   float* c[4];
@@ -390,7 +395,7 @@ cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, 
   static const cudaError_t attr =
       cudaFuncSetAttribute(unet_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float) * (64 * 257 + 128 + 64)));
   if (attr != cudaSuccess) return attr;
-  unet_tail_kernel<<<S, 256, sm, st>>>(U, T, M, F, c[3], d1, E, ctr);
+  unet_tail_kernel<<<S, 256, sm, st>>>(U, T, M, F, global_max, c[3], d1, E, ctr);
   return cudaGetLastError();
 }
 

@@ -123,6 +123,7 @@ struct locc_ctx {
   bool timed_overlap = false;  // the last timed query ran the overlapped crop pipeline
   // NEXT-1 encode-once mode
   bool has_unet = false, has_cells = false;
+  int unet_global_max = 0;  // U-Net global feature: 0 average, 1 max
   DevBuf unet_params, cells_E, cells_ctr, cells_emb;
   UNetParams U{};
   CellsTable cells{};
@@ -968,6 +969,17 @@ locc_status locc_load_unet_weights_mem(locc_ctx* c, const float* flat, size_t n)
   return LOCC_OK;
 }
 
+locc_status locc_set_unet_global_pool(locc_ctx* c, int32_t mode) {
+  if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
+  if (mode != 0 && mode != 1) return fail(LOCC_E_INVALID_ARG, "global pool mode must be 0 (average) or 1 (max)");
+  if (c->unet_global_max != mode) {
+    c->unet_global_max = mode;
+    c->has_cells = false;  // the grids must be re-encoded
+    ++c->generation;
+  }
+  return LOCC_OK;
+}
+
 locc_status locc_encode_shapes(locc_ctx* c) {
   if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
   if (!c->has_weights || !c->has_shapes || !c->has_unet)
@@ -987,7 +999,7 @@ locc_status locc_encode_shapes(locc_ctx* c) {
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, c->stream));
   CK(launch_grid_encode(c->P, c->T, M, G.as<float>(), c->stream));
-  CK(launch_unet(c->U, c->T, M, H, F, G.as<float>(), act.as<float>(), c->cells_E.as<float>(),
+  CK(launch_unet(c->U, c->T, M, H, F, c->unet_global_max, G.as<float>(), act.as<float>(), c->cells_E.as<float>(),
                  c->cells_ctr.as<float>(), c->stream));
   CK(cudaEventRecord(e1, c->stream));
   CK(cudaStreamSynchronize(c->stream));

@@ -19,7 +19,7 @@ LOCC_PREC_BF16 = 1
 
 EXPORTS = ("locc_create", "locc_load_weights", "locc_load_weights_mem", "locc_set_shapes", "locc_query",
            "locc_query_debug", "locc_query_grad", "locc_unet_n_params", "locc_load_unet_weights_mem",
-           "locc_encode_shapes", "locc_get_cell_embeddings", "locc_query_cells", "locc_sim_run", "locc_set_precision", "locc_set_timing", "locc_get_stats", "locc_destroy",
+           "locc_encode_shapes", "locc_set_unet_global_pool", "locc_get_cell_embeddings", "locc_query_cells", "locc_sim_run", "locc_set_precision", "locc_set_timing", "locc_get_stats", "locc_destroy",
            "locc_status_string", "locc_last_error", "locc_version")
 
 
@@ -78,6 +78,7 @@ def lib():
         L.locc_unet_n_params.restype = i64
         L.locc_load_unet_weights_mem.argtypes = [vp, vp, C.c_size_t]
         L.locc_encode_shapes.argtypes = [vp]
+        L.locc_set_unet_global_pool.argtypes = [vp, i32]
         L.locc_get_cell_embeddings.argtypes = [vp, vp, vp]
         L.locc_query_cells.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]
         L.locc_sim_run.argtypes = [vp, C.POINTER(SimConfig), i32, vp, vp, vp, C.c_double, vp, vp]
@@ -211,6 +212,10 @@ class Locc:
     def load_unet_weights_mem(self, flat):
         flat = np.ascontiguousarray(flat, np.float32)
         _check(lib().locc_load_unet_weights_mem(self._h, _ptr(flat), flat.size))
+
+    def set_unet_global_pool(self, mode):
+        """0 = average (default), 1 = max; re-run encode_shapes afterwards."""
+        _check(lib().locc_set_unet_global_pool(self._h, int(mode)))
 
     def encode_shapes(self):
         _check(lib().locc_encode_shapes(self._h))

@@ -176,3 +176,19 @@ def test_cells_empty_and_disjoint_batches(locc_mod, weights, wl):
         got = ctx.query_cells(pairs[:16], far, debug=True)
     assert np.all(got["nsel"] == 0) and np.all(got["probs"] == 0) and np.all(got["labels"] == 0)
     assert np.all(np.isneginf(got["logits"])) and np.all(got["emb"] == 0) and np.all(got["cells"] == 0)
+
+
+def test_cells_parity_global_max(locc_mod, oracle_mod, weights):
+    """The appendix's global max pooling (locc_set_unet_global_pool(1)) against the oracle's."""
+    w = ls.make_workload("C1", N=60, S=6)
+    ref = oracle_mod.query_cells(weights[0], weights[1], w.points, w.pairs, w.poses, global_max=True)
+    ctx = locc_mod.Locc(M=6, H=256, F=64, precision=0, device=0)
+    ctx.load_weights_mem(weights[0])
+    ctx.load_unet_weights_mem(weights[1])
+    ctx.set_shapes(w.points)
+    ctx.set_unet_global_pool(1)
+    ctx.encode_shapes()
+    E, _ = ctx.cell_embeddings()
+    got = ctx.query_cells(w.pairs, w.poses, debug=True)
+    ctx.close()
+    assert_cells_parity(got, ref, E, w.pairs)

@@ -253,3 +253,14 @@ def test_query_cells_symmetries(oracle_mod):
     r2 = oracle_mod.query_cells(w, u, pts, pairs, neg)
     for k in ("logits", "nsel", "cells", "emb"):
         assert np.array_equal(r0[k], r2[k]), k
+
+
+def test_unet_global_max_probe(oracle_mod):
+    """Q28's alternative reading (P:421 'max pooling to get global features'): with the delta-kernel
+    probe the global channel is the MAX of the block instead of its mean; everything else unchanged."""
+    pts, _ = ls.make_shapes(2, 600, seed=53)
+    G, E = oracle_mod.encode_grid(identity_encoder(), unet_probe(), pts[0], global_max=True)
+    _, E_avg = oracle_mod.encode_grid(identity_encoder(), unet_probe(), pts[0])
+    blk = G.reshape(6, 6, 6, H)[1:5, 0:4, 2:6, 0]
+    np.testing.assert_allclose(E[:, 1], np.full(216, blk.max()), rtol=0, atol=0)
+    assert np.array_equal(E[:, [0, 2]], E_avg[:, [0, 2]]) and blk.max() > blk.mean()
