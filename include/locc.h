@@ -149,8 +149,9 @@ locc_status locc_query_grad(locc_ctx* ctx, const int32_t* pairs, const float* po
  * transforms the M^3 cell centres of each object into the other's frame, selects the cells within
  * the own cell's half diagonal (the "margin ... distance from the center point to a vertex of a
  * cell") of the other AABB, average-pools the selected embeddings and runs the same
- * predictor.  Query cost is independent of K.  fp32 throughout (CUDA cores); readings
- * Q27-Q30 in DESIGN.md.  Requires 3 <= M <= 8, H = 256, F = 64.
+ * predictor.  Query cost is independent of K.  fp32 (bf16 contexts: the tensor-core 3xTF32
+ * predictor for F = 64); readings Q27-Q30 in DESIGN.md.  Requires 3 <= M <= 8, H a multiple of 32,
+ * F <= 64 (the appendix's F = 16 included).
  *
  * U-Net parameters, canonical order (each W then b [128]; kernels [out][in][27], tap k = kx + 3 (ky
  * + 3 kz)): c1 [128][H][27], c2, c3, c4 [128][128][27], d4 [128][128][27], d3, d2, d1 [128][256][27];

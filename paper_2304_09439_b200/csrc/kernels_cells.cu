@@ -305,6 +305,15 @@ __global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTa
     }
   }
   __syncwarp();
+  if (F != 64) {  // any F <= 256: lane owns features lane, lane + 32, ...; rows in ascending order
+    const float* Es = C.E + (int64_t)own * nc * F;
+    for (int f0 = 0; f0 < F; f0 += 32) {
+      const int f = f0 + lane;
+      float a = 0.f;
+      for (int i = 0; i < n; ++i) a = __fadd_rn(a, f < F ? __ldg(Es + (int64_t)list[i] * F + f) : 0.f);
+      if (f < F) e[f] = n ? __fdiv_rn(a, (float)n) : 0.f;
+    }
+  } else {
   const float4* Es4 = reinterpret_cast<const float4*>(C.E + (int64_t)own * nc * 64);
   const int half = lane >> 4, f4 = lane & 15;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -332,6 +341,7 @@ __global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTa
     float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
     if (n) r = make_float4(__fdiv_rn(acc.x, fn), __fdiv_rn(acc.y, fn), __fdiv_rn(acc.z, fn), __fdiv_rn(acc.w, fn));
     reinterpret_cast<float4*>(e)[f4] = r;
+  }
   }
   if (cells) {
 #pragma unroll

@@ -424,12 +424,19 @@ __global__ void __launch_bounds__(128) head_kernel(DevParams P, Batch b, float* 
   const int npairs = (int)min((int64_t)PB, b.B - i0);
   if (tid < NS) nside[tid] = tid < 2 * npairs ? b.counts[2 * i0 + tid] : 0;
   __syncthreads();
-  for (int idx = tid; idx < NS * H; idx += blockDim.x) {
-    const int s = idx / H, j = idx - s * H;
-    X[j * LD + s] = nside[s] > 0 ? b.pooled[(2 * i0 + s) * (int64_t)H + j] : 0.f;
+  if (b.emb_in) {  // encode-once mode: e is the selection's pooled cell embedding [G][F]
+    for (int idx = tid; idx < NS * F; idx += blockDim.x) {
+      const int s = idx / F, j = idx - s * F;
+      Z[j * LD + s] = nside[s] > 0 ? b.emb_in[(2 * i0 + s) * (int64_t)F + j] : 0.f;
+    }
+  } else {
+    for (int idx = tid; idx < NS * H; idx += blockDim.x) {
+      const int s = idx / H, j = idx - s * H;
+      X[j * LD + s] = nside[s] > 0 ? b.pooled[(2 * i0 + s) * (int64_t)H + j] : 0.f;
+    }
+    __syncthreads();
+    dense_t<NS / 2>(P.wfT, P.bf, H, F, X, (tid >> 6) * (NS / 2), Z, false, tid & 63, 64);
   }
-  __syncthreads();
-  dense_t<NS / 2>(P.wfT, P.bf, H, F, X, (tid >> 6) * (NS / 2), Z, false, tid & 63, 64);
   __syncthreads();
   if (tid < NS) {
     const int s = tid;
@@ -523,7 +530,7 @@ cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_
     if (b.emb_in) return run(head_tile_kernel<false, true>, sizeof(HeadSmem), nullptr);
     return run(head_tile_kernel<false, false>, sizeof(HeadSmem), nullptr);
   }
-  if (grad || b.emb_in) return cudaErrorNotSupported;  // the pose gradient and encode-once mode: H = 256, F = 64
+  if (grad) return cudaErrorNotSupported;  // the pose gradient is built for H = 256, F = 64
   const size_t sm = sizeof(float) * (size_t)(256 + 128 + P.F + 7) * LD;
   static const cudaError_t attr2 = cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                         (int)(sizeof(float) * (256 + 128 + 256 + 7) * LD));

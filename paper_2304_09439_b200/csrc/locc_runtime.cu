@@ -985,8 +985,8 @@ locc_status locc_encode_shapes(locc_ctx* c) {
   if (!c->has_weights || !c->has_shapes || !c->has_unet)
     return fail(LOCC_E_STATE, "weights, U-Net weights and shapes must be set before locc_encode_shapes");
   const int M = c->cfg.M, H = c->cfg.H, F = c->cfg.F, S = c->T.S;
-  if (M < 3 || M > 8 || H != 256 || F != 64)
-    return fail(LOCC_E_INVALID_ARG, "encode-once mode is built for 3 <= M <= 8, H = 256, F = 64");
+  if (M < 3 || M > 8 || H % 32 || F > 64)
+    return fail(LOCC_E_INVALID_ARG, "encode-once mode is built for 3 <= M <= 8, H a multiple of 32, F <= 64");
   CK(cudaSetDevice(c->device));
   const int nc = M * M * M;
   DevBuf G, act;

@@ -192,3 +192,22 @@ def test_cells_parity_global_max(locc_mod, oracle_mod, weights):
     got = ctx.query_cells(w.pairs, w.poses, debug=True)
     ctx.close()
     assert_cells_parity(got, ref, E, w.pairs)
+
+
+@pytest.mark.parametrize("H,F", [(256, 16), (128, 32)])
+def test_cells_parity_other_widths(locc_mod, oracle_mod, H, F):
+    """Encode-once at the appendix's F = 16 and a narrower point MLP: the generic selection and
+    predictor paths against the oracle."""
+    w = ls.flatten_weights(ls.make_weights("spread", H, F, calib=ls.load_calibration()), H, F)
+    u = ls.flatten_unet(ls.make_unet_weights("spread", H, F), H, F)
+    wl = ls.make_workload("C1", N=60, S=6)
+    ref = oracle_mod.query_cells(w, u, wl.points, wl.pairs, wl.poses, H=H, F=F)
+    ctx = locc_mod.Locc(M=6, H=H, F=F, precision=0, device=0)
+    ctx.load_weights_mem(w)
+    ctx.load_unet_weights_mem(u)
+    ctx.set_shapes(wl.points)
+    ctx.encode_shapes()
+    E, _ = ctx.cell_embeddings()
+    got = ctx.query_cells(wl.pairs, wl.poses, debug=True)
+    ctx.close()
+    assert_cells_parity(got, ref, E, wl.pairs)
