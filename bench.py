@@ -339,6 +339,24 @@ def main():
                              "unit": UNIT, "ms_per_step": gms, "overhead_vs_forward": gms / ms - 1.0,
                              "api": "locc_query_grad (grad [N][14] fp32)"}
 
+    # small-batch latency (SURVEY §8(d) C5's small-N floor): device time of one locc_query call
+    lat = {}
+    for n_small in (1024, 16384):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(3):
+            ctx.query_into(d_pairs[:n_small], d_poses[:n_small], d_probs[:n_small], d_labels[:n_small],
+                           stream=stream.cuda_stream)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        for _ in range(10):
+            ctx.query_into(d_pairs[:n_small], d_poses[:n_small], d_probs[:n_small], d_labels[:n_small],
+                           stream=stream.cuda_stream)
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        torch.cuda.synchronize()
+        lat[str(n_small)] = e0.elapsed_time(e1) / 10
+    line["latency_ms_per_query"] = lat
+
     # NEXT-1: the paper's encode-once inference on the same pairs (grids cached once per shape table)
     if not a.no_cells:
         import locc_synth as ls
