@@ -72,6 +72,8 @@ struct DevParams {
 struct UNetParams {
   const float* Wt[8];  // 0..3 = c1..c4, 4..7 = d4, d3, d2, d1
   const float* b[8];
+  const uint8_t* img[8];  // tensor-core (bf16 contexts) images: per layer 27 x C_in/32 chunks of
+                          // [128 out x 32 in] tf32 hi then lo, SW128 K-major (kernels_conv_tc.cu)
   const float* pW;     // [F][256] projection of [d1 ; g]
   const float* pb;     // [F]
 };
@@ -148,7 +150,9 @@ cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_
 // NEXT-1 encode-once mode (kernels_cells.cu)
 cudaError_t launch_grid_encode(const DevParams& P, const ShapeTable& T, int M, float* G, cudaStream_t st);
 cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, int F, int global_max, const float* G,
-                        float* act, float* E, float* ctr, cudaStream_t st);
+                        float* act, float* E, float* ctr, bool tc, int num_sms, cudaStream_t st);
+cudaError_t launch_conv_tc(const float* x1, int C1, const float* x2, int C2, int Di, int Do, int pad, int S,
+                           const uint8_t* img, const float* bias, float* y, int num_sms, cudaStream_t st);
 size_t unet_act_floats(int S, int M);
 cudaError_t launch_cells_select(const ShapeTable& T, const CellsTable& C, const Batch& b, int F, uint32_t* cells,
                                 float* emb_out, cudaStream_t st);

@@ -374,7 +374,7 @@ size_t unet_act_floats(int S, int M) {
 }
 
 cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, int F, int global_max, const float* G,
-                        float* act, float* E, float* ctr, cudaStream_t st) {
+                        float* act, float* E, float* ctr, bool tc, int num_sms, cudaStream_t st) {
   const int D = M - 2, S = T.S;
   const size_t n4 = (size_t)S * D * D * D * 128;
   float* c[4];
@@ -384,6 +384,7 @@ cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, 
   float* d2 = act + 6 * n4;
   float* d1 = act + 7 * n4;
   auto conv = [&](const float* x1, int C1, const float* x2, int C2, int Di, int Do, int pad, int l, float* y) {
+    if (tc) return launch_conv_tc(x1, C1, x2, C2, Di, Do, pad, S, U.img[l], U.b[l], y, num_sms, st);
     ConvArgs a{x1, x2, C1, C2, Di, Do, pad, U.Wt[l], U.b[l], y};
     dim3 grid((unsigned)((Do * Do * Do + kCvBM - 1) / kCvBM), (unsigned)S);
     conv3d_kernel<<<grid, 256, kCvSmem, st>>>(a);

@@ -1,0 +1,207 @@
+// kernels_conv_tc.cu — the encode-once U-Net's 3x3x3 layers on the 5th-generation tensor cores
+// (NEXT-1, readings Q28, Q32; the CUDA-core conv3d_kernel in kernels_cells.cu is the fp32
+// contexts' path).  Each layer is an implicit GEMM: rows = output positions over all shapes (flattened
+// (shape, position)), N = 128 output channels, K = 27 taps x C_in, in 32-channel chunks of one tap.
+// tcgen05.mma kind::tf32 with the 3xTF32 split (hi = tf32(x), lo = tf32(x - hi); hi hi + hi lo + lo hi),
+// fp32 accumulators in TMEM; deconvolutions run as convolutions with flipped taps (weights pre-flipped).
+//
+// Persistent CTAs, 128 output rows per tile, 6 warps:
+//   warp 0     weight producer: the layer's pre-split, pre-swizzled chunks [128 out x 32 K] (32 KB,
+//              hi then lo, SW128 K-major) through a 5-stage ring (cp.async.bulk)
+//   warp 1     MMA issuer: 12 TS MMAs per chunk (A from TMEM)
+//   warps 2-5  im2col producers (thread = row = TMEM lane): gather the 32 input channels of the row's
+//              tap position (zero outside the grid), split, tcgen05.st into a 4-stage A ring in TMEM;
+//              after the tile's last chunk, the epilogue: bias + ReLU and the output row to global
+// TMEM: D = columns 0..127, A stage s = 128 + 64 s (hi 32 columns, lo 32 columns).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+#include "tc_ptx.cuh"
+
+namespace locc {
+namespace {
+
+using namespace tc;
+
+constexpr int kCtStages = 5, kCtA = 4;
+constexpr int kCtChunk = 32768, kCtHalf = 16384;
+
+struct __align__(1024) ConvTcSmem {
+  uint8_t w[kCtStages][kCtChunk];
+  float bias[128];
+  uint64_t w_full[kCtStages], w_empty[kCtStages], a_full[kCtA], a_empty[kCtA], d_full, d_empty;
+  uint32_t tmem_base;
+};
+
+struct ConvTcArgs {
+  const float* x1;  // [S][Di^3][C1]
+  const float* x2;  // [S][Di^3][C2] or null (channels C1.. of the concatenation)
+  int C1, C2, Di, Do, pad, S;
+  const uint8_t* img;  // chunks (tap k, 32-channel block c) in order k-major
+  const float* bias;
+  float* y;            // [S][Do^3][128], ReLU applied
+};
+
+__device__ __forceinline__ float tf32r(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  ConvTcSmem& S = *reinterpret_cast<ConvTcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Cin = a.C1 + a.C2, nci = Cin / 32, nch = 27 * nci;
+  const int nq = a.Do * a.Do * a.Do;
+  const int64_t rows = (int64_t)a.S * nq, ntiles = (rows + 127) / 128;
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) S.bias[i] = a.bias[i];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kCtStages; ++i) {
+      mbar_init(&S.w_full[i], 1);
+      mbar_init(&S.w_empty[i], 1);
+    }
+    for (int i = 0; i < kCtA; ++i) {
+      mbar_init(&S.a_full[i], 128);
+      mbar_init(&S.a_empty[i], 1);
+    }
+    mbar_init(&S.d_full, 1);
+    mbar_init(&S.d_empty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_1cta(&S.tmem_base, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 0) {
+    uint32_t n = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int j = 0; j < nch; ++j, ++n) {
+        const uint32_t st = n % kCtStages;
+        if (lane == 0) {
+          if (n >= kCtStages) mbar_wait_spin(&S.w_empty[st], ((n / kCtStages) - 1) & 1);
+          mbar_arrive_expect_tx(&S.w_full[st], kCtChunk);
+          bulk_g2s(S.w[st], a.img + (size_t)j * kCtChunk, kCtChunk, &S.w_full[st]);
+        }
+        __syncwarp();
+      }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_tf32_f32(128, 128);
+    uint32_t n = 0, m = 0, it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      if (it > 0) {
+        mbar_wait_spin(&S.d_empty, (it - 1) & 1);  // the previous tile's accumulator has been read
+        tc_fence_after();
+      }
+      for (int j = 0; j < nch; ++j, ++n, ++m) {
+        const uint32_t sw = n % kCtStages, sa = m % kCtA;
+        mbar_wait_spin(&S.a_full[sa], (m / kCtA) & 1);
+        mbar_wait_spin(&S.w_full[sw], (n / kCtStages) & 1);
+        tc_fence_after();
+        const uint32_t bhi = smem_u32(S.w[sw]), blo = bhi + kCtHalf;
+        const uint32_t ahi = tmem + 128 + 64 * sa, alo = ahi + 32;
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            mma_tf32_ts(tmem, ahi + 8 * k, smem_desc_sw128(bhi + 32 * k, 1024), idesc, (j | k) != 0);
+            mma_tf32_ts(tmem, ahi + 8 * k, smem_desc_sw128(blo + 32 * k, 1024), idesc, 1);
+            mma_tf32_ts(tmem, alo + 8 * k, smem_desc_sw128(bhi + 32 * k, 1024), idesc, 1);
+          }
+          mma_commit_1cta(&S.w_empty[sw]);
+          mma_commit_1cta(&S.a_empty[sa]);
+          if (j == nch - 1) mma_commit_1cta(&S.d_full);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    const int q = warp & 3, r = 32 * q + lane;
+    const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
+    const int Di3 = a.Di * a.Di * a.Di;
+    uint32_t m = 0, it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const int64_t row = t * 128 + r;
+      const bool valid = row < rows;
+      const int s = valid ? (int)(row / nq) : 0, qp = valid ? (int)(row % nq) : 0;
+      const int qx = qp % a.Do, qy = (qp / a.Do) % a.Do, qz = qp / (a.Do * a.Do);
+      for (int j = 0; j < nch; ++j, ++m) {
+        const int k = j / nci, c = j - k * nci;
+        const int ix = qx + k % 3 - a.pad, iy = qy + (k / 3) % 3 - a.pad, iz = qz + k / 9 - a.pad;
+        const bool in = valid && ix >= 0 && iy >= 0 && iz >= 0 && ix < a.Di && iy < a.Di && iz < a.Di;
+        float x[32];
+        if (in) {
+          const int64_t pos = (int64_t)s * Di3 + (iz * a.Di + iy) * a.Di + ix;
+          const int ci = 32 * c;
+          const float4* src = ci < a.C1 ? reinterpret_cast<const float4*>(a.x1 + pos * a.C1 + ci)
+                                        : reinterpret_cast<const float4*>(a.x2 + pos * a.C2 + (ci - a.C1));
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const float4 f = __ldg(src + v);
+            x[4 * v] = f.x, x[4 * v + 1] = f.y, x[4 * v + 2] = f.z, x[4 * v + 3] = f.w;
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < 32; ++v) x[v] = 0.f;
+        }
+        uint32_t h[32], l[32];
+#pragma unroll
+        for (int v = 0; v < 32; ++v) {
+          const float hv = tf32r(x[v]);
+          h[v] = __float_as_uint(hv);
+          l[v] = __float_as_uint(tf32r(x[v] - hv));
+        }
+        const uint32_t sa = m % kCtA;
+        if (m >= kCtA) mbar_wait(&S.a_empty[sa], ((m / kCtA) - 1) & 1);  // the MMAs have read stage sa
+        tc_fence_after();
+        tmem_st32(trow + 128 + 64 * sa, h);
+        tmem_st32(trow + 128 + 64 * sa + 32, l);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&S.a_full[sa]);
+      }
+      // epilogue: ReLU(D + b) -> y[row]
+      mbar_wait(&S.d_full, it & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(trow + c0, v);
+        tmem_ld_wait();
+        if (valid) {
+          float4* yo = reinterpret_cast<float4*>(a.y + row * 128 + c0);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            yo[u] = make_float4(fmaxf(__uint_as_float(v[4 * u]) + S.bias[c0 + 4 * u], 0.f),
+                                fmaxf(__uint_as_float(v[4 * u + 1]) + S.bias[c0 + 4 * u + 1], 0.f),
+                                fmaxf(__uint_as_float(v[4 * u + 2]) + S.bias[c0 + 4 * u + 2], 0.f),
+                                fmaxf(__uint_as_float(v[4 * u + 3]) + S.bias[c0 + 4 * u + 3], 0.f));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&S.d_empty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc_1cta(tmem, 512);
+}
+
+}  // namespace
+
+cudaError_t launch_conv_tc(const float* x1, int C1, const float* x2, int C2, int Di, int Do, int pad, int S,
+                           const uint8_t* img, const float* bias, float* y, int num_sms, cudaStream_t st) {
+  const size_t sm = sizeof(ConvTcSmem) + 1024;
+  static const cudaError_t attr = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)(sizeof(ConvTcSmem) + 1024));
+  if (attr != cudaSuccess) return attr;
+  const int64_t rows = (int64_t)S * Do * Do * Do, ntiles = (rows + 127) / 128;
+  const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
+  ConvTcArgs a{x1, x2, C1, C2, Di, Do, pad, S, img, bias, y};
+  conv_tc_kernel<<<grid, 192, sm, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace locc

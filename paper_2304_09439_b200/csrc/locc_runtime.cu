@@ -124,7 +124,7 @@ struct locc_ctx {
   // NEXT-1 encode-once mode
   bool has_unet = false, has_cells = false;
   int unet_global_max = 0;  // U-Net global feature: 0 average, 1 max
-  DevBuf unet_params, cells_E, cells_ctr, cells_emb;
+  DevBuf unet_params, unet_img, cells_E, cells_ctr, cells_emb;
   UNetParams U{};
   CellsTable cells{};
   double encode_ms = 0.0;  // device time of the last locc_encode_shapes
@@ -949,6 +949,27 @@ locc_status locc_load_unet_weights_mem(locc_ctx* c, const float* flat, size_t n)
     img.insert(img.end(), q, q + C);
     q += C;
   }
+  // tensor-core images of the 8 layers: chunk (tap k, channel block cb) = [128 out x 32 in], tf32 hi then
+  // lo, SW128 K-major — from the conv-form Wt[k][i][o] above (deconv taps already flipped)
+  std::vector<uint8_t> timg;
+  size_t offT[8];
+  for (int l = 0; l < 8; ++l) {
+    offT[l] = timg.size();
+    const float* wt = img.data() + offW[l];
+    for (int k = 0; k < 27; ++k)
+      for (int cb = 0; cb < cin[l] / 32; ++cb) {
+        const size_t base = timg.size();
+        timg.resize(base + 32768, 0);
+        for (int o = 0; o < C; ++o)
+          for (int kk = 0; kk < 32; ++kk) {
+            const float w = wt[((size_t)k * cin[l] + 32 * cb + kk) * C + o];
+            const float hi = tf32_rna_host(w), lo = tf32_rna_host(w - hi);
+            const size_t off = tc::sw128_off((uint32_t)o, (uint32_t)(kk >> 2)) + (size_t)(kk & 3) * 4;
+            std::memcpy(&timg[base + off], &hi, 4);
+            std::memcpy(&timg[base + 16384 + off], &lo, 4);
+          }
+      }
+  }
   const size_t offP = img.size();
   img.insert(img.end(), q, q + (size_t)F * 2 * C);
   q += (size_t)F * 2 * C;
@@ -961,6 +982,9 @@ locc_status locc_load_unet_weights_mem(locc_ctx* c, const float* flat, size_t n)
     c->U.Wt[l] = d + offW[l];
     c->U.b[l] = d + offb[l];
   }
+  CK(c->unet_img.ensure(timg.size()));
+  CK(cudaMemcpy(c->unet_img.p, timg.data(), timg.size(), cudaMemcpyHostToDevice));
+  for (int l = 0; l < 8; ++l) c->U.img[l] = c->unet_img.as<uint8_t>() + offT[l];
   c->U.pW = d + offP;
   c->U.pb = d + offPb;
   c->has_unet = true;
@@ -999,8 +1023,10 @@ locc_status locc_encode_shapes(locc_ctx* c) {
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, c->stream));
   CK(launch_grid_encode(c->P, c->T, M, G.as<float>(), c->stream));
+  // the U-Net on the tensor cores (3xTF32) in bf16 contexts, on CUDA cores (fp32) in fp32 ones
+  const bool tc = c->cfg.precision == LOCC_PREC_BF16 && !getenv("LOCC_CONV_FFMA");
   CK(launch_unet(c->U, c->T, M, H, F, c->unet_global_max, G.as<float>(), act.as<float>(), c->cells_E.as<float>(),
-                 c->cells_ctr.as<float>(), c->stream));
+                 c->cells_ctr.as<float>(), tc, c->num_sms, c->stream));
   CK(cudaEventRecord(e1, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   float ms = 0.f;

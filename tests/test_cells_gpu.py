@@ -81,23 +81,28 @@ def test_cells_parity(locc_mod, wl, wl_oracle, weights):
     assert_cells_parity(got, wl_oracle, E, pairs)
 
 
-def test_cells_parity_tensor_core_predictor(locc_mod, wl, wl_oracle, weights):
-    """bf16 contexts run the predictor on the tensor cores (3xTF32 split, Q32): selection and
-    pooled e are the same kernels (bit-exact / 2e-5), probabilities within 2e-5 of the fp64 oracle."""
+def test_cells_parity_bf16_context(locc_mod, wl, wl_oracle, weights):
+    """bf16 contexts run the U-Net and the predictor on the tensor cores (3xTF32, Q32): the
+    selection is bit-exact; the grids within 5e-4 of max|E| (the tensor core's fp32 accumulation over
+    K = 27 x 256 truncates: measured ~1e-4), probabilities within 5e-4 of the fp64 oracle with identical
+    labels outside the 1e-3 band — the bf16 bar against an exact reference."""
     pts, pairs, poses = wl
     ctx = locc_mod.Locc(M=6, H=256, F=64, precision=1, device=0, max_batch=128)
     ctx.load_weights_mem(weights[0])
     ctx.load_unet_weights_mem(weights[1])
     ctx.set_shapes(pts)
     ctx.encode_shapes()
+    E, _ = ctx.cell_embeddings()
     got = ctx.query_cells(pairs, poses, debug=True)
     ctx.close()
     ref = wl_oracle
     assert np.array_equal(got["cells"], ref["cells"]) and np.array_equal(got["nsel"], ref["nsel"])
+    used = np.unique(pairs)
+    assert np.abs(E[used] - ref["grids"][used]).max() <= 5e-4 * np.abs(ref["grids"][used]).max()
     short = ref["nsel"].sum(1) == 0
     assert np.all(got["probs"][short] == 0) and np.all(np.isneginf(got["logits"][short]))
     dp = np.abs(got["probs"].astype(np.float64) - ref["probs"]).max()
-    assert dp <= 2e-5, f"max |dp| = {dp:.3g}"
+    assert dp <= 5e-4, f"max |dp| = {dp:.3g}"
     band = np.abs(ref["probs"] - 0.5) <= 1e-3
     assert np.array_equal(got["labels"][~band], ref["labels"][~band])
 

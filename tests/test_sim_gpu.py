@@ -39,7 +39,14 @@ def run_gpu(locc_mod, pts, ids, body, st, sim, unet=None, t0=0.0, precision=0):
     ctx.set_shapes(pts)
     if unet is not None:
         ctx.load_unet_weights_mem(unet)
-        ctx.encode_shapes()
+        # the loop's parity is about the step; the grids come from the fp32 U-Net in every context here
+        # (bf16 contexts otherwise encode on the tensor cores, whose accumulation is coarser, Q32)
+        import os
+        os.environ["LOCC_CONV_FFMA"] = "1"
+        try:
+            ctx.encode_shapes()
+        finally:
+            del os.environ["LOCC_CONV_FFMA"]
     d_ids = torch.from_numpy(ids).cuda()
     d_body = torch.from_numpy(body).cuda()
     d_st = torch.from_numpy(st.copy()).cuda()
