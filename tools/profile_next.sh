@@ -15,8 +15,8 @@ cap() {  # name regex skip
   ncu -i gpurun_out/next_${TAG}_$1.ncu-rep --page raw --csv > gpurun_out/next_raw_${TAG}_$1.csv 2>/dev/null || true
 }
 cap grid_encode grid_encode 0
-cap conv3d_c1 conv3d 0
-cap conv3d_d1 conv3d 7
+cap conv_c1 conv_tc 0
+cap conv_d1 conv_tc 7
 cap cells_select cells_select 0
 cap head_cells head_tc 0
 cap head_grad head_tc 1

@@ -11,6 +11,7 @@ KEYS = {
     "dram__bytes_read.sum": "dram_read",
     "dram__bytes_write.sum": "dram_write",
     "lts__t_sectors_srcunit_tex_op_read.sum": "l2_read_sectors",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_pct",
     "sm__issue_active.avg.pct_of_peak_sustained_elapsed": "issue_active_pct",
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
@@ -21,8 +22,8 @@ KEYS = {
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "ms": 1e-3, "us": 1e-6, "ns": 1e-9, "Ghz": 1e9,
          "Mhz": 1e6}
 CAPS = [("grid_encode", "point MLP over all K points, cell max (once per shape table)"),
-        ("conv3d_c1", "U-Net c1: valid 3^3 conv 256 -> 128 (once per shape table)"),
-        ("conv3d_d1", "U-Net d1: transposed valid conv [d2; c1] -> 128 (once per shape table)"),
+        ("conv_c1", "U-Net c1 on tcgen05 (3xTF32): valid 3^3 conv 256 -> 128 (once per shape table)"),
+        ("conv_d1", "U-Net d1 on tcgen05: transposed valid conv [d2; c1] -> 128 (once per shape table)"),
         ("cells_select", "encode-once query: cell selection + pooled embedding"),
         ("head_cells", "head_tc_kernel<0,0>: tensor-core predictor on pooled cell embeddings"),
         ("head_grad", "head_tc_kernel<1,1>: tensor-core predictor + pose gradient (crop path)"),
@@ -48,8 +49,8 @@ def main(tag="r1next"):
              "Workload: `python tools/next_modes.py` (262,144 C3-recipe pairs over 1030 shapes; grids encoded "
              "once; closed loop at 30,000 environments).  `ncu --set full --clock-control none`, one launch "
              "per kernel, 1 x B200.  Captured by `tools/profile_next.sh`.", "",
-             "| kernel | what | ms | DRAM R/W GB | L2 read GB | issue active | FMA pipe | occupancy | regs |",
-             "|---|---|---|---|---|---|---|---|---|"]
+             "| kernel | what | ms | DRAM R/W GB | L2 read GB | issue active | FMA pipe | tensor pipe | occupancy | regs |",
+             "|---|---|---|---|---|---|---|---|---|---|"]
     for k, what in CAPS:
         p = os.path.join(OUT, f"next_raw_{tag}_{k}.csv")
         if not os.path.exists(p):
@@ -59,6 +60,7 @@ def main(tag="r1next"):
         lines.append(f"| {k} | {what} | {1e3 * d.get('duration', 0):.3f} | {d.get('dram_read', 0) / 1e9:.3f} / "
                      f"{d.get('dram_write', 0) / 1e9:.3f} | {32 * d.get('l2_read_sectors', 0) / 1e9:.2f} | "
                      f"{d.get('issue_active_pct', 0):.0f}% | {d.get('fma_pipe_pct', 0):.0f}% | "
+                     f"{d.get('tensor_pct', 0):.0f}% | "
                      f"{d.get('occupancy_pct', 0):.0f}% | {d.get('registers', 0):.0f} |")
     json.dump(res, open(os.path.join(ROOT, "profiles", f"{tag}_summary.json"), "w"), indent=1)
     open(os.path.join(ROOT, "profiles", f"{tag}_summary.md"), "w").write("\n".join(lines) + "\n")
