@@ -138,7 +138,8 @@ locc_status locc_query_debug(locc_ctx* ctx, const int32_t* pairs, const float* p
  * to the side it selected (u_A > u_B -> A, ties -> B), and the raw quaternion's gradient includes
  * the normalisation and canonical sign: dq = s (dq^ - q^ (q^ . dq^)) / |q|.  Short-circuited pairs
  * (constant logit -inf): grad 0.  Computed in the same fused predictor kernel as the forward: fp32 on
- * CUDA cores in fp32 contexts, 3xTF32 on the tensor cores in bf16 contexts (Q32).  Requires H = 256, F = 64.  Same residency, stream and error rules as locc_query.
+ * CUDA cores in fp32 contexts, 3xTF32 on the tensor cores in bf16 contexts (Q32).
+ * Requires H = 256, F = 64.  Same residency, stream and error rules as locc_query.
  * Errors: INVALID_ARG (as locc_query, null grad, H/F not 256/64), STATE, CUDA, OOM. */
 locc_status locc_query_grad(locc_ctx* ctx, const int32_t* pairs, const float* poses, int64_t N,
                             float* probs, uint8_t* labels, float* logits, float* grad, void* stream);
