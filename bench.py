@@ -362,6 +362,8 @@ def main():
         import locc_synth as ls
         ctx.load_unet_weights_mem(ls.flatten_unet(ls.make_unet_weights()))
         ctx.encode_shapes()
+        enc_ms_first = ctx.encode_ms()  # includes the kernels' first-launch (module load) costs
+        ctx.encode_shapes()
         enc_ms = ctx.encode_ms()
 
         def cstep():
@@ -409,8 +411,10 @@ def main():
                                "kernels": {"cells_select_ms": cst["encoder_ms"], "head_ms": cst["head_ms"],
                                            "head_roofline": hroof},
                                "value": world * N / (cms / 1e3), "unit": UNIT, "ms_per_step": cms,
-                               "encode_ms_per_shape_table": enc_ms, "shapes": int(len(pts)),
-                               "note": "grids encoded once per shape table (not in the timed step); fp32"}
+                               "encode_ms_per_shape_table": enc_ms, "encode_ms_first_call": enc_ms_first,
+                               "shapes": int(len(pts)),
+                               "note": "grids encoded once per shape table (not in the timed step); grid layers "
+                                       "2-3 and U-Net on tcgen05 (3xTF32) in bf16 contexts, fp32 FFMA in fp32 ones"}
 
     # NEXT-3: closed-loop substeps (30,000 environments, dt = 0.01/4 s in 4 substeps)
     if not a.no_sim and not a.no_cells:

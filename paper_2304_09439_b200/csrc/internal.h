@@ -65,6 +65,8 @@ struct DevParams {
   const float* head_tc_bias;  // [6][128] layer biases, wout [128], bout, b_F [64]
   const void* tc_w2; // bf16 W2/W3 pre-arranged as the encoder_tc shared-memory image
   const void* tc_w3;
+  const uint8_t* grid_tc_img;  // tensor-core grid encode (H = 256): W2 then W3, each as 2 output halves
+                               // x 8 pre-split SW128 chunks [128 out x 32 in] (kernels_conv_tc.cu format)
 };
 
 // NEXT-1 (encode-once) U-Net parameters, rearranged for the implicit-GEMM conv kernel:
@@ -154,6 +156,12 @@ cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, 
 cudaError_t launch_conv_tc(const float* x1, int C1, const float* x2, int C2, int Di, int Do, int pad, int S,
                            const uint8_t* img, const float* bias, float* y, int num_sms, cudaStream_t st);
 size_t unet_act_floats(int S, int M);
+cudaError_t launch_gemm_tc(const float* x, int C, int64_t rows, const uint8_t* img, const float* bias, float* y,
+                           int ldy, int ycol, int num_sms, cudaStream_t st, const float4* pts = nullptr,
+                           const float4* w1b = nullptr);
+int64_t grid_tc_chunk_rows(const ShapeTable& T);
+cudaError_t launch_grid_encode_tc(const DevParams& P, const ShapeTable& T, int M, float* G, float* bufA, float* bufB,
+                                  int num_sms, cudaStream_t st);
 cudaError_t launch_cells_select(const ShapeTable& T, const CellsTable& C, const Batch& b, int F, uint32_t* cells,
                                 float* emb_out, cudaStream_t st);
 // NEXT-3 closed loop (kernels_sim.cu)

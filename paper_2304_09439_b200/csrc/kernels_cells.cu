@@ -3,7 +3,8 @@
 // :421-422); a query then only selects the cells near the other object and average-pools their
 // embeddings, so its cost does not depend on K.
 //
-//   grid_encode_kernel   point MLP over all K points of a shape, cell-wise max -> G [S][M^3][H]
+//   grid_encode_kernel   point MLP over all K points of a shape, cell-wise max -> G [S][M^3][H] (fp32
+//                        contexts; bf16 contexts: 2 x 2 tensor-core GEMMs, layer 1 fused -> cell_max)
 //   conv3d_kernel        one 3x3x3 layer of the U-Net as an implicit GEMM (fp32 FFMA2): rows = output
 //                        positions of one shape, columns = 128 output channels, K = 27 taps x C_in
 //                        (two inputs = the concatenation skip); deconv layers run as the equivalent
@@ -15,6 +16,9 @@
 // The predictor is head_tile_kernel reading e from the selection (Batch::emb_in).
 #include <cuda_runtime.h>
 #include <math.h>
+
+#include <algorithm>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "geom.cuh"
@@ -74,6 +78,44 @@ __global__ void __launch_bounds__(256) grid_encode_kernel(DevParams P, ShapeTabl
     }
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------- Q27 on the tensor cores (bf16 contexts)
+// The same grid as grid_encode_kernel, layer by layer over a chunk of shapes (all their points as flat
+// rows): layers 2 and 3 as 3xTF32 GEMMs on tcgen05 (launch_gemm_tc, kernels_conv_tc.cu; layer 2's A
+// rows are h1 = ReLU(W1 p + b1), K = 3, computed in its producers), then cell_max_kernel: per shape and feature, the running
+// max over the cell-sorted points, closed at each cell change.  h3 = ReLU(acc + b3) >= 0, so the max of
+// h3 equals ReLU(max acc + b3) and empty cells keep the cleared 0.
+__global__ void __launch_bounds__(256) cell_max_kernel(const float* __restrict__ h3, const float4* __restrict__ pts,
+                                                       int K, int nc, float* __restrict__ G) {
+  const int f = threadIdx.x;
+  const float* hs = h3 + (int64_t)blockIdx.x * K * 256 + f;
+  const float4* ps = pts + (int64_t)blockIdx.x * K;
+  float* Gs = G + (int64_t)blockIdx.x * nc * 256 + f;
+  if (K == 0) return;
+  int cell = __float_as_int(__ldg(&ps[0].w));
+  float run = 0.f;
+  for (int r0 = 0; r0 < K; r0 += 8) {
+    float v[8];
+    int cl[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = r0 + u;
+      v[u] = r < K ? __ldg(hs + (int64_t)r * 256) : 0.f;
+      cl[u] = r < K ? __float_as_int(__ldg(&ps[r].w)) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (cl[u] < 0) break;  // past the shape's last point
+      if (cl[u] != cell) {
+        Gs[(int64_t)cell * 256] = run;
+        run = 0.f;
+        cell = cl[u];
+      }
+      run = fmaxf(run, v[u]);
+    }
+  }
+  Gs[(int64_t)cell * 256] = run;
 }
 
 // ---------------------------------------------------------------- Q28: U-Net layers (implicit GEMM)
@@ -365,6 +407,41 @@ cudaError_t launch_grid_encode(const DevParams& P, const ShapeTable& T, int M, f
   if (e != cudaSuccess) return e;
   grid_encode_kernel<<<T.S, 256, sm, st>>>(P, T, M, G);
   return cudaGetLastError();
+}
+
+// Rows per chunk of the tensor-core grid encode: whole shapes, about 2^20 rows (1 GiB per activation;
+// LOCC_GRID_CHUNK=<rows> overrides, for the tests of the chunk boundaries).
+int64_t grid_tc_chunk_rows(const ShapeTable& T) {
+  const int64_t K = T.K > 0 ? T.K : 1;
+  const char* env = getenv("LOCC_GRID_CHUNK");
+  const int64_t target = env ? std::max<int64_t>(1, atoll(env)) : (int64_t(1) << 20);
+  const int64_t spc = std::max<int64_t>(1, std::min<int64_t>(T.S, target / K));
+  return spc * K;
+}
+
+cudaError_t launch_grid_encode_tc(const DevParams& P, const ShapeTable& T, int M, float* G, float* bufA, float* bufB,
+                                  int num_sms, cudaStream_t st) {
+  const int nc = M * M * M;
+  cudaError_t e = cudaMemsetAsync(G, 0, sizeof(float) * (size_t)T.S * nc * 256, st);
+  if (e != cudaSuccess || T.K == 0) return e;
+  const int64_t spc = grid_tc_chunk_rows(T) / T.K;
+  const uint8_t* w2 = P.grid_tc_img;
+  const uint8_t* w3 = P.grid_tc_img + 16 * 32768;
+  for (int64_t s0 = 0; s0 < T.S; s0 += spc) {
+    const int64_t ns = std::min<int64_t>(spc, T.S - s0), rows = ns * T.K;
+    const float4* pts = T.pts + s0 * T.K;
+    for (int half = 0; half < 2; ++half)
+      if ((e = launch_gemm_tc(nullptr, 256, rows, w2 + (size_t)half * 8 * 32768, P.b2 + 128 * half, bufB, 256,
+                              128 * half, num_sms, st, pts, P.w1b)) != cudaSuccess)
+        return e;
+    for (int half = 0; half < 2; ++half)
+      if ((e = launch_gemm_tc(bufB, 256, rows, w3 + (size_t)half * 8 * 32768, P.b3 + 128 * half, bufA, 256, 128 * half,
+                              num_sms, st)) != cudaSuccess)
+        return e;
+    cell_max_kernel<<<(unsigned)ns, 256, 0, st>>>(bufA, pts, T.K, nc, G + (size_t)s0 * nc * 256);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 // Activation scratch of the U-Net: c1..c4, d4, d3, d2 [S][(M-2)^3][128] and d1 [S][M^3][128].

@@ -10,9 +10,13 @@
 //              hi then lo, SW128 K-major) through a 5-stage ring (cp.async.bulk)
 //   warp 1     MMA issuer: 12 TS MMAs per chunk (A from TMEM)
 //   warps 2-5  im2col producers (thread = row = TMEM lane): gather the 32 input channels of the row's
-//              tap position (zero outside the grid), split, tcgen05.st into a 4-stage A ring in TMEM;
+//              tap position (zero outside the grid; issued one chunk ahead, so the loads overlap the
+//              split and store of the previous chunk), split, tcgen05.st into a 4-stage A ring in TMEM;
 //              after the tile's last chunk, the epilogue: bias + ReLU and the output row to global
 // TMEM: D = columns 0..127, A stage s = 128 + 64 s (hi 32 columns, lo 32 columns).
+// With ntaps = 1 the same kernel is a plain GEMM y = ReLU(x W^T + b) over flat rows: the tensor-core grid
+// encode's layers 2 and 3 (kernels_cells.cu, one launch per 128-column half of the 256 outputs); for
+// layer 2 the A rows are layer 1 of the rows' points, computed in the producers (pts mode).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -30,6 +34,7 @@ constexpr int kCtChunk = 32768, kCtHalf = 16384;
 struct __align__(1024) ConvTcSmem {
   uint8_t w[kCtStages][kCtChunk];
   float bias[128];
+  float4 w1b[256];  // layer-1 weights (w0, w1, w2, b) of the fused grid-encode layer 2 (pts mode)
   uint64_t w_full[kCtStages], w_empty[kCtStages], a_full[kCtA], a_empty[kCtA], d_full, d_empty;
   uint32_t tmem_base;
 };
@@ -40,7 +45,12 @@ struct ConvTcArgs {
   int C1, C2, Di, Do, pad, S;
   const uint8_t* img;  // chunks (tap k, 32-channel block c) in order k-major
   const float* bias;
-  float* y;            // [S][Do^3][128], ReLU applied
+  float* y;            // [S][Do^3][128], ReLU applied (row stride ldy, columns ycol..ycol+127)
+  int ntaps;           // 27: the 3x3x3 conv; 1: a plain GEMM, row r reads x1[r] (rows = flat_rows)
+  int64_t flat_rows;
+  int ldy, ycol;
+  const float4* pts;  // pts mode (ntaps = 1, C1 = 256): x1 is not read; the A row is computed on the fly
+  const float4* w1b;  // as h1 = ReLU(W1 p + b1) of the row's point (the grid encode's layer 1, fused)
 };
 
 __device__ __forceinline__ float tf32r(float x) {
@@ -53,10 +63,12 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   ConvTcSmem& S = *reinterpret_cast<ConvTcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int Cin = a.C1 + a.C2, nci = Cin / 32, nch = 27 * nci;
+  const int Cin = a.C1 + a.C2, nci = Cin / 32, nch = a.ntaps * nci;
   const int nq = a.Do * a.Do * a.Do;
-  const int64_t rows = (int64_t)a.S * nq, ntiles = (rows + 127) / 128;
+  const int64_t rows = a.ntaps == 1 ? a.flat_rows : (int64_t)a.S * nq, ntiles = (rows + 127) / 128;
   for (int i = threadIdx.x; i < 128; i += blockDim.x) S.bias[i] = a.bias[i];
+  if (a.pts)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) S.w1b[i] = a.w1b[i];
   if (threadIdx.x == 0) {
     for (int i = 0; i < kCtStages; ++i) {
       mbar_init(&S.w_full[i], 1);
@@ -121,31 +133,55 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
     const int q = warp & 3, r = 32 * q + lane;
     const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
     const int Di3 = a.Di * a.Di * a.Di;
+    // gather of chunk j (tap k, channels 32c..32c+31) of tile t's row r; zero outside the grid
+    auto gather = [&](int64_t t, int j, float (&x)[32]) {
+      const int64_t row = t * 128 + r;
+      const bool valid = row < rows;
+      const int k = j / nci, c = j - k * nci;
+      bool in = valid;
+      int64_t pos = row;
+      if (a.ntaps != 1) {
+        const int s = valid ? (int)(row / nq) : 0, qp = valid ? (int)(row % nq) : 0;
+        const int qx = qp % a.Do, qy = (qp / a.Do) % a.Do, qz = qp / (a.Do * a.Do);
+        const int ix = qx + k % 3 - a.pad, iy = qy + (k / 3) % 3 - a.pad, iz = qz + k / 9 - a.pad;
+        in = valid && ix >= 0 && iy >= 0 && iz >= 0 && ix < a.Di && iy < a.Di && iz < a.Di;
+        pos = (int64_t)s * Di3 + (iz * a.Di + iy) * a.Di + ix;
+      }
+      if (in && a.pts) {
+        const float4 p = __ldg(a.pts + row);
+#pragma unroll
+        for (int v = 0; v < 32; ++v) {
+          const float4 w = S.w1b[32 * c + v];
+          x[v] = fmaxf(fmaf(w.x, p.x, fmaf(w.y, p.y, fmaf(w.z, p.z, w.w))), 0.f);
+        }
+      } else if (in) {
+        const int ci = 32 * c;
+        const float4* src = ci < a.C1 ? reinterpret_cast<const float4*>(a.x1 + pos * a.C1 + ci)
+                                      : reinterpret_cast<const float4*>(a.x2 + pos * a.C2 + (ci - a.C1));
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const float4 f = __ldg(src + v);
+          x[4 * v] = f.x, x[4 * v + 1] = f.y, x[4 * v + 2] = f.z, x[4 * v + 3] = f.w;
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < 32; ++v) x[v] = 0.f;
+      }
+    };
     uint32_t m = 0, it = 0;
+    float xn[32];  // the next chunk's gather, issued one chunk ahead (across tiles too)
+    if ((int64_t)blockIdx.x < ntiles) gather(blockIdx.x, 0, xn);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const int64_t row = t * 128 + r;
       const bool valid = row < rows;
-      const int s = valid ? (int)(row / nq) : 0, qp = valid ? (int)(row % nq) : 0;
-      const int qx = qp % a.Do, qy = (qp / a.Do) % a.Do, qz = qp / (a.Do * a.Do);
       for (int j = 0; j < nch; ++j, ++m) {
-        const int k = j / nci, c = j - k * nci;
-        const int ix = qx + k % 3 - a.pad, iy = qy + (k / 3) % 3 - a.pad, iz = qz + k / 9 - a.pad;
-        const bool in = valid && ix >= 0 && iy >= 0 && iz >= 0 && ix < a.Di && iy < a.Di && iz < a.Di;
         float x[32];
-        if (in) {
-          const int64_t pos = (int64_t)s * Di3 + (iz * a.Di + iy) * a.Di + ix;
-          const int ci = 32 * c;
-          const float4* src = ci < a.C1 ? reinterpret_cast<const float4*>(a.x1 + pos * a.C1 + ci)
-                                        : reinterpret_cast<const float4*>(a.x2 + pos * a.C2 + (ci - a.C1));
 #pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            const float4 f = __ldg(src + v);
-            x[4 * v] = f.x, x[4 * v + 1] = f.y, x[4 * v + 2] = f.z, x[4 * v + 3] = f.w;
-          }
-        } else {
-#pragma unroll
-          for (int v = 0; v < 32; ++v) x[v] = 0.f;
-        }
+        for (int v = 0; v < 32; ++v) x[v] = xn[v];
+        if (j + 1 < nch)
+          gather(t, j + 1, xn);
+        else if (t + gridDim.x < ntiles)
+          gather(t + gridDim.x, 0, xn);
         uint32_t h[32], l[32];
 #pragma unroll
         for (int v = 0; v < 32; ++v) {
@@ -171,7 +207,7 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
         tmem_ld32(trow + c0, v);
         tmem_ld_wait();
         if (valid) {
-          float4* yo = reinterpret_cast<float4*>(a.y + row * 128 + c0);
+          float4* yo = reinterpret_cast<float4*>(a.y + row * a.ldy + a.ycol + c0);
 #pragma unroll
           for (int u = 0; u < 8; ++u)
             yo[u] = make_float4(fmaxf(__uint_as_float(v[4 * u]) + S.bias[c0 + 4 * u], 0.f),
@@ -199,7 +235,21 @@ cudaError_t launch_conv_tc(const float* x1, int C1, const float* x2, int C2, int
   if (attr != cudaSuccess) return attr;
   const int64_t rows = (int64_t)S * Do * Do * Do, ntiles = (rows + 127) / 128;
   const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
-  ConvTcArgs a{x1, x2, C1, C2, Di, Do, pad, S, img, bias, y};
+  ConvTcArgs a{x1, x2, C1, C2, Di, Do, pad, S, img, bias, y, 27, 0, 128, 0, nullptr, nullptr};
+  conv_tc_kernel<<<grid, 192, sm, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_tc(const float* x, int C, int64_t rows, const uint8_t* img, const float* bias, float* y,
+                           int ldy, int ycol, int num_sms, cudaStream_t st, const float4* pts, const float4* w1b) {
+  if (rows == 0) return cudaSuccess;
+  const size_t sm = sizeof(ConvTcSmem) + 1024;
+  static const cudaError_t attr = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)(sizeof(ConvTcSmem) + 1024));
+  if (attr != cudaSuccess) return attr;
+  const int64_t ntiles = (rows + 127) / 128;
+  const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
+  ConvTcArgs a{x, nullptr, C, 0, 1, 1, 0, 1, img, bias, y, 1, rows, ldy, ycol, pts, w1b};
   conv_tc_kernel<<<grid, 192, sm, st>>>(a);
   return cudaGetLastError();
 }

@@ -104,7 +104,7 @@ struct locc_ctx {
   bool timing = false;
   bool has_weights = false, has_shapes = false;
   // parameters
-  DevBuf params, tc_img, head_tc_img;
+  DevBuf params, tc_img, head_tc_img, grid_tc_img;
   DevParams P{};
   TcL1 tc_l1{};
   // shapes
@@ -328,6 +328,29 @@ locc_status upload_params(locc_ctx* c, const float* flat) {
   }
   D.tc_w2 = nullptr;
   D.tc_w3 = nullptr;
+  // tensor-core grid encode (encode-once, bf16 contexts): e2, e3 as [half][chunk] images, same format
+  D.grid_tc_img = nullptr;
+  if (H == 256) {
+    std::vector<uint8_t> gimg;
+    for (const L* l : {&e2, &e3})
+      for (int half = 0; half < 2; ++half)
+        for (int j = 0; j < 8; ++j) {
+          const size_t base = gimg.size();
+          gimg.resize(base + 32768, 0);
+          for (int n = 0; n < 128; ++n)
+            for (int k = 0; k < 32; ++k) {
+              const float w = l->W[(size_t)(128 * half + n) * H + 32 * j + k];
+              const float hi = tf32_rna_host(w);
+              const float lo = tf32_rna_host(w - hi);
+              const size_t off = tc::sw128_off((uint32_t)n, (uint32_t)(k >> 2)) + (size_t)(k & 3) * 4;
+              std::memcpy(&gimg[base + off], &hi, 4);
+              std::memcpy(&gimg[base + 16384 + off], &lo, 4);
+            }
+        }
+    CK(c->grid_tc_img.ensure(gimg.size()));
+    CK(cudaMemcpy(c->grid_tc_img.p, gimg.data(), gimg.size(), cudaMemcpyHostToDevice));
+    D.grid_tc_img = c->grid_tc_img.as<uint8_t>();
+  }
   c->has_weights = true;
   return LOCC_OK;
 }
@@ -1018,13 +1041,27 @@ locc_status locc_encode_shapes(locc_ctx* c) {
   CK(act.ensure(sizeof(float) * unet_act_floats(S, M)));
   CK(c->cells_E.ensure(sizeof(float) * (size_t)S * nc * F));
   CK(c->cells_ctr.ensure(sizeof(float) * (size_t)S * 24));
+  // the grid encode's layers 2-3 and the U-Net on the tensor cores (3xTF32) in bf16 contexts, on CUDA
+  // cores (fp32) in fp32 ones
+  const bool bf16 = c->cfg.precision == LOCC_PREC_BF16;
+  const bool grid_tc = bf16 && c->P.grid_tc_img && !getenv("LOCC_GRID_FFMA");
+  DevBuf bufA, bufB;  // the tensor-core grid encode's activations (allocated outside the timed region)
+  if (grid_tc) {
+    const size_t nb = sizeof(float) * 256 * (size_t)grid_tc_chunk_rows(c->T);
+    CK(bufA.ensure(nb));
+    CK(bufB.ensure(nb));
+  }
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, c->stream));
-  CK(launch_grid_encode(c->P, c->T, M, G.as<float>(), c->stream));
-  // the U-Net on the tensor cores (3xTF32) in bf16 contexts, on CUDA cores (fp32) in fp32 ones
-  const bool tc = c->cfg.precision == LOCC_PREC_BF16 && !getenv("LOCC_CONV_FFMA");
+  if (grid_tc) {
+    CK(launch_grid_encode_tc(c->P, c->T, M, G.as<float>(), bufA.as<float>(), bufB.as<float>(), c->num_sms,
+                             c->stream));
+  } else {
+    CK(launch_grid_encode(c->P, c->T, M, G.as<float>(), c->stream));
+  }
+  const bool tc = bf16 && !getenv("LOCC_CONV_FFMA");
   CK(launch_unet(c->U, c->T, M, H, F, c->unet_global_max, G.as<float>(), act.as<float>(), c->cells_E.as<float>(),
                  c->cells_ctr.as<float>(), tc, c->num_sms, c->stream));
   CK(cudaEventRecord(e1, c->stream));

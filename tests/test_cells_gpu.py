@@ -107,6 +107,35 @@ def test_cells_parity_bf16_context(locc_mod, wl, wl_oracle, weights):
     assert np.array_equal(got["labels"][~band], ref["labels"][~band])
 
 
+@pytest.mark.parametrize("chunk", [None, "1000", "4000"])
+def test_cells_grid_encode_tensor_cores(locc_mod, wl, wl_oracle, weights, monkeypatch, chunk):
+    """bf16 contexts encode the grid's layers 2-3 on the tensor cores (3xTF32, K = 256) in chunks of
+    whole shapes.  With the U-Net forced onto CUDA cores (LOCC_CONV_FFMA), E must meet the fp32 bar
+    (E_TOL of the fp64 oracle) for any chunking: one shape per chunk (1500 rows, a ragged last tile),
+    two shapes per chunk, and all 12 in one; and the fp32 grid path (LOCC_GRID_FFMA) must agree."""
+    pts, pairs, poses = wl
+    monkeypatch.setenv("LOCC_CONV_FFMA", "1")
+    if chunk:
+        monkeypatch.setenv("LOCC_GRID_CHUNK", chunk)
+    ctx = locc_mod.Locc(M=6, H=256, F=64, precision=1, device=0, max_batch=128)
+    ctx.load_weights_mem(weights[0])
+    ctx.load_unet_weights_mem(weights[1])
+    ctx.set_shapes(pts)
+    ctx.encode_shapes()
+    E_tc, _ = ctx.cell_embeddings()
+    monkeypatch.setenv("LOCC_GRID_FFMA", "1")
+    ctx.encode_shapes()
+    E_ff, _ = ctx.cell_embeddings()
+    ctx.close()
+    ref = wl_oracle["grids"]
+    used = np.unique(pairs)
+    scale = np.abs(ref[used]).max()
+    err_tc = np.abs(E_tc[used].astype(np.float64) - ref[used]).max()
+    err_ff = np.abs(E_ff[used].astype(np.float64) - ref[used]).max()
+    assert err_tc <= E_TOL * scale, f"tensor-core grid: E err {err_tc:.3g} (scale {scale:.3g}, fp32 path {err_ff:.3g})"
+    assert np.abs(E_tc - E_ff).max() <= E_TOL * scale
+
+
 def test_cells_probe_weights_gpu(locc_mod, oracle_mod, wl):
     """The identity-encoder / delta-kernel U-Net probe (closed form pinned in test_oracle_cells):
     the device grids reproduce the oracle's exactly up to fp32 rounding of the copied values."""

@@ -14,9 +14,12 @@ cap() {  # name regex skip
   ncu -i gpurun_out/next_${TAG}_$1.ncu-rep --page details > gpurun_out/next_details_${TAG}_$1.txt 2>/dev/null || true
   ncu -i gpurun_out/next_${TAG}_$1.ncu-rep --page raw --csv > gpurun_out/next_raw_${TAG}_$1.csv 2>/dev/null || true
 }
-cap grid_encode grid_encode 0
-cap conv_c1 conv_tc 0
-cap conv_d1 conv_tc 7
+# bf16 context: the grid encode is 4 conv_tc (ntaps = 1) GEMMs (layer 1 fused) -> cell_max per chunk of shapes
+# (2 chunks at 1030 x 1500 points), so the U-Net's c1 is the 9th conv_tc launch and d1 the 16th
+cap grid_gemm conv_tc 0
+cap grid_cellmax cell_max 0
+cap conv_c1 conv_tc 8
+cap conv_d1 conv_tc 15
 cap cells_select cells_select 0
 cap head_cells head_tc 0
 cap head_grad head_tc 1

@@ -21,7 +21,9 @@ KEYS = {
 }
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "ms": 1e-3, "us": 1e-6, "ns": 1e-9, "Ghz": 1e9,
          "Mhz": 1e6}
-CAPS = [("grid_encode", "point MLP over all K points, cell max (once per shape table)"),
+CAPS = [("grid_gemm", "grid encode layers 1+2 (one 128-column half, 699 shapes x 1500 points) on tcgen05 "
+                      "(3xTF32, conv_tc_kernel pts mode: layer 1 computed in the producers)"),
+        ("grid_cellmax", "grid encode: cell-wise max of layer 3 over the chunk's sorted points"),
         ("conv_c1", "U-Net c1 on tcgen05 (3xTF32): valid 3^3 conv 256 -> 128 (once per shape table)"),
         ("conv_d1", "U-Net d1 on tcgen05: transposed valid conv [d2; c1] -> 128 (once per shape table)"),
         ("cells_select", "encode-once query: cell selection + pooled embedding"),
