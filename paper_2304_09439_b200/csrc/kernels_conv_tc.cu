@@ -133,22 +133,36 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
     const int q = warp & 3, r = 32 * q + lane;
     const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
     const int Di3 = a.Di * a.Di * a.Di;
-    // gather of chunk j (tap k, channels 32c..32c+31) of tile t's row r; zero outside the grid
-    auto gather = [&](int64_t t, int j, float (&x)[32]) {
-      const int64_t row = t * 128 + r;
-      const bool valid = row < rows;
+    // the row's output position in tile t (computed once per tile)
+    struct Pos {
+      int64_t row;
+      bool valid;
+      int s, qx, qy, qz;
+    };
+    auto pos_of = [&](int64_t t) {
+      Pos P;
+      P.row = t * 128 + r;
+      P.valid = P.row < rows;
+      P.s = P.qx = P.qy = P.qz = 0;
+      if (a.ntaps != 1 && P.valid) {
+        P.s = (int)(P.row / nq);
+        const int qp = (int)(P.row % nq);
+        P.qx = qp % a.Do, P.qy = (qp / a.Do) % a.Do, P.qz = qp / (a.Do * a.Do);
+      }
+      return P;
+    };
+    // gather of chunk j (tap k, channels 32c..32c+31) of the row at P; zero outside the grid
+    auto gather = [&](const Pos& P, int j, float (&x)[32]) {
       const int k = j / nci, c = j - k * nci;
-      bool in = valid;
-      int64_t pos = row;
+      bool in = P.valid;
+      int64_t pos = P.row;
       if (a.ntaps != 1) {
-        const int s = valid ? (int)(row / nq) : 0, qp = valid ? (int)(row % nq) : 0;
-        const int qx = qp % a.Do, qy = (qp / a.Do) % a.Do, qz = qp / (a.Do * a.Do);
-        const int ix = qx + k % 3 - a.pad, iy = qy + (k / 3) % 3 - a.pad, iz = qz + k / 9 - a.pad;
-        in = valid && ix >= 0 && iy >= 0 && iz >= 0 && ix < a.Di && iy < a.Di && iz < a.Di;
-        pos = (int64_t)s * Di3 + (iz * a.Di + iy) * a.Di + ix;
+        const int ix = P.qx + k % 3 - a.pad, iy = P.qy + (k / 3) % 3 - a.pad, iz = P.qz + k / 9 - a.pad;
+        in = P.valid && ix >= 0 && iy >= 0 && iz >= 0 && ix < a.Di && iy < a.Di && iz < a.Di;
+        pos = (int64_t)P.s * Di3 + (iz * a.Di + iy) * a.Di + ix;
       }
       if (in && a.pts) {
-        const float4 p = __ldg(a.pts + row);
+        const float4 p = __ldg(a.pts + pos);
 #pragma unroll
         for (int v = 0; v < 32; ++v) {
           const float4 w = S.w1b[32 * c + v];
@@ -170,18 +184,20 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
     };
     uint32_t m = 0, it = 0;
     float xn[32];  // the next chunk's gather, issued one chunk ahead (across tiles too)
-    if ((int64_t)blockIdx.x < ntiles) gather(blockIdx.x, 0, xn);
+    Pos cur = pos_of(blockIdx.x);
+    if ((int64_t)blockIdx.x < ntiles) gather(cur, 0, xn);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const int64_t row = t * 128 + r;
-      const bool valid = row < rows;
+      const int64_t row = cur.row;
+      const bool valid = cur.valid;
+      const Pos nxt = pos_of(t + gridDim.x);
       for (int j = 0; j < nch; ++j, ++m) {
         float x[32];
 #pragma unroll
         for (int v = 0; v < 32; ++v) x[v] = xn[v];
         if (j + 1 < nch)
-          gather(t, j + 1, xn);
+          gather(cur, j + 1, xn);
         else if (t + gridDim.x < ntiles)
-          gather(t + gridDim.x, 0, xn);
+          gather(nxt, 0, xn);
         uint32_t h[32], l[32];
 #pragma unroll
         for (int v = 0; v < 32; ++v) {
@@ -218,6 +234,7 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
       }
       tc_fence_before();
       mbar_arrive(&S.d_empty);
+      cur = nxt;
     }
   }
   tc_fence_before();
