@@ -169,7 +169,9 @@ locc_status locc_load_unet_weights_mem(locc_ctx* ctx, const float* flat, size_t 
 locc_status locc_set_unet_global_pool(locc_ctx* ctx, int32_t mode);
 
 /* Encode every shape of the current table and cache the grids on the device (synchronous).  Must be
- * re-run after locc_set_shapes / locc_load_weights / locc_load_unet_weights_mem.
+ * re-run after locc_set_shapes / locc_load_weights / locc_load_unet_weights_mem.  fp32 contexts: CUDA
+ * cores (fp32); bf16 contexts: the point MLP's layers 2-3 (H = 256) and the U-Net on the tensor cores
+ * in 3xTF32 (Q30, Q32), with about 1 GiB of transient scratch per 2^20 points encoded.
  * Errors: STATE (weights, U-Net weights or shapes missing), INVALID_ARG (M, H, F), CUDA, OOM. */
 locc_status locc_encode_shapes(locc_ctx* ctx);
 
