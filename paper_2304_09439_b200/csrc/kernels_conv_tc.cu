@@ -5,15 +5,16 @@
 // tcgen05.mma kind::tf32 with the 3xTF32 split (hi = tf32(x), lo = tf32(x - hi); hi hi + hi lo + lo hi),
 // fp32 accumulators in TMEM; deconvolutions run as convolutions with flipped taps (weights pre-flipped).
 //
-// Persistent CTAs, 128 output rows per tile, 6 warps:
+// Persistent CTAs, a PAIR of 128-row tiles per pass (each weight chunk read from L2 once per 256 output
+// rows: at 128 rows the weight stream was the L2-bound half of the runtime), 6 warps:
 //   warp 0     weight producer: the layer's pre-split, pre-swizzled chunks [128 out x 32 K] (32 KB,
 //              hi then lo, SW128 K-major) through a 5-stage ring (cp.async.bulk)
-//   warp 1     MMA issuer: 12 TS MMAs per chunk (A from TMEM)
-//   warps 2-5  im2col producers (thread = row = TMEM lane): gather the 32 input channels of the row's
-//              tap position (zero outside the grid; issued one chunk ahead, so the loads overlap the
-//              split and store of the previous chunk), split, tcgen05.st into a 4-stage A ring in TMEM;
-//              after the tile's last chunk, the epilogue: bias + ReLU and the output row to global
-// TMEM: D = columns 0..127, A stage s = 128 + 64 s (hi 32 columns, lo 32 columns).
+//   warp 1     MMA issuer: 2 x 12 TS MMAs per chunk (A from TMEM), one accumulator per tile
+//   warps 2-5  im2col producers (thread = row r of both tiles = TMEM lane): gather the 32 input channels
+//              of the row's tap position (zero outside the grid; issued one chunk ahead, so the loads
+//              overlap the split and store of the previous chunk), split, tcgen05.st into a 2-stage A
+//              ring in TMEM; after the pair's last chunk, the epilogue: bias + ReLU, rows to global
+// TMEM: D_u = columns 128 u (u = 0, 1), A stage s = 256 + 128 s (tile 0 hi, lo; tile 1 hi, lo: 32 each).
 // With ntaps = 1 the same kernel is a plain GEMM y = ReLU(x W^T + b) over flat rows: the tensor-core grid
 // encode's layers 2 and 3 (kernels_cells.cu, one launch per 128-column half of the 256 outputs); for
 // layer 2 the A rows are layer 1 of the rows' points, computed in the producers (pts mode).
@@ -28,7 +29,7 @@ namespace {
 
 using namespace tc;
 
-constexpr int kCtStages = 5, kCtA = 4;
+constexpr int kCtStages = 5, kCtA = 2;
 constexpr int kCtChunk = 32768, kCtHalf = 16384;
 
 struct __align__(1024) ConvTcSmem {
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Cin = a.C1 + a.C2, nci = Cin / 32, nch = a.ntaps * nci;
   const int nq = a.Do * a.Do * a.Do;
-  const int64_t rows = a.ntaps == 1 ? a.flat_rows : (int64_t)a.S * nq, ntiles = (rows + 127) / 128;
+  const int64_t rows = a.ntaps == 1 ? a.flat_rows : (int64_t)a.S * nq, ntiles = (rows + 255) / 256;  // tile pairs
   for (int i = threadIdx.x; i < 128; i += blockDim.x) S.bias[i] = a.bias[i];
   if (a.pts)
     for (int i = threadIdx.x; i < 256; i += blockDim.x) S.w1b[i] = a.w1b[i];
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
     uint32_t n = 0, m = 0, it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       if (it > 0) {
-        mbar_wait_spin(&S.d_empty, (it - 1) & 1);  // the previous tile's accumulator has been read
+        mbar_wait_spin(&S.d_empty, (it - 1) & 1);  // the previous pair's accumulators have been read
         tc_fence_after();
       }
       for (int j = 0; j < nch; ++j, ++n, ++m) {
@@ -114,13 +115,16 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
         mbar_wait_spin(&S.w_full[sw], (n / kCtStages) & 1);
         tc_fence_after();
         const uint32_t bhi = smem_u32(S.w[sw]), blo = bhi + kCtHalf;
-        const uint32_t ahi = tmem + 128 + 64 * sa, alo = ahi + 32;
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            mma_tf32_ts(tmem, ahi + 8 * k, smem_desc_sw128(bhi + 32 * k, 1024), idesc, (j | k) != 0);
-            mma_tf32_ts(tmem, ahi + 8 * k, smem_desc_sw128(blo + 32 * k, 1024), idesc, 1);
-            mma_tf32_ts(tmem, alo + 8 * k, smem_desc_sw128(bhi + 32 * k, 1024), idesc, 1);
+          for (int u = 0; u < 2; ++u) {  // the weight chunk feeds both tiles of the pair
+            const uint32_t d = tmem + 128 * u, ahi = tmem + 256 + 128 * sa + 64 * u, alo = ahi + 32;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              mma_tf32_ts(d, ahi + 8 * k, smem_desc_sw128(bhi + 32 * k, 1024), idesc, (j | k) != 0);
+              mma_tf32_ts(d, ahi + 8 * k, smem_desc_sw128(blo + 32 * k, 1024), idesc, 1);
+              mma_tf32_ts(d, alo + 8 * k, smem_desc_sw128(bhi + 32 * k, 1024), idesc, 1);
+            }
           }
           mma_commit_1cta(&S.w_empty[sw]);
           mma_commit_1cta(&S.a_empty[sa]);
@@ -133,15 +137,15 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
     const int q = warp & 3, r = 32 * q + lane;
     const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
     const int Di3 = a.Di * a.Di * a.Di;
-    // the row's output position in tile t (computed once per tile)
+    // the row's output position in tile u of pair t (computed once per pair)
     struct Pos {
       int64_t row;
       bool valid;
       int s, qx, qy, qz;
     };
-    auto pos_of = [&](int64_t t) {
+    auto pos_of = [&](int64_t t, int u) {
       Pos P;
-      P.row = t * 128 + r;
+      P.row = t * 256 + 128 * u + r;
       P.valid = P.row < rows;
       P.s = P.qx = P.qy = P.qz = 0;
       if (a.ntaps != 1 && P.valid) {
@@ -182,59 +186,75 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
         for (int v = 0; v < 32; ++v) x[v] = 0.f;
       }
     };
+    auto split = [](const float (&x)[32], uint32_t (&h)[32], uint32_t (&l)[32]) {
+#pragma unroll
+      for (int v = 0; v < 32; ++v) {
+        const float hv = tf32r(x[v]);
+        h[v] = __float_as_uint(hv);
+        l[v] = __float_as_uint(tf32r(x[v] - hv));
+      }
+    };
     uint32_t m = 0, it = 0;
-    float xn[32];  // the next chunk's gather, issued one chunk ahead (across tiles too)
-    Pos cur = pos_of(blockIdx.x);
-    if ((int64_t)blockIdx.x < ntiles) gather(cur, 0, xn);
+    float xa[32], xb[32];  // the next chunk's gathers (tiles 0 and 1 of the pair), issued one chunk ahead
+    Pos ca = pos_of(blockIdx.x, 0), cb = pos_of(blockIdx.x, 1);
+    if ((int64_t)blockIdx.x < ntiles) {
+      gather(ca, 0, xa);
+      gather(cb, 0, xb);
+    }
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-      const int64_t row = cur.row;
-      const bool valid = cur.valid;
-      const Pos nxt = pos_of(t + gridDim.x);
+      const Pos na = pos_of(t + gridDim.x, 0), nb = pos_of(t + gridDim.x, 1);
+      const bool more = t + gridDim.x < ntiles;
       for (int j = 0; j < nch; ++j, ++m) {
-        float x[32];
-#pragma unroll
-        for (int v = 0; v < 32; ++v) x[v] = xn[v];
-        if (j + 1 < nch)
-          gather(cur, j + 1, xn);
-        else if (t + gridDim.x < ntiles)
-          gather(nxt, 0, xn);
-        uint32_t h[32], l[32];
-#pragma unroll
-        for (int v = 0; v < 32; ++v) {
-          const float hv = tf32r(x[v]);
-          h[v] = __float_as_uint(hv);
-          l[v] = __float_as_uint(tf32r(x[v] - hv));
-        }
         const uint32_t sa = m % kCtA;
+        const uint32_t col = trow + 256 + 128 * sa;
+        uint32_t h[32], l[32];
+        split(xa, h, l);
+        if (j + 1 < nch)
+          gather(ca, j + 1, xa);
+        else if (more)
+          gather(na, 0, xa);
         if (m >= kCtA) mbar_wait(&S.a_empty[sa], ((m / kCtA) - 1) & 1);  // the MMAs have read stage sa
         tc_fence_after();
-        tmem_st32(trow + 128 + 64 * sa, h);
-        tmem_st32(trow + 128 + 64 * sa + 32, l);
+        tmem_st32(col, h);
+        tmem_st32(col + 32, l);
+        tmem_st_wait();
+        split(xb, h, l);
+        if (j + 1 < nch)
+          gather(cb, j + 1, xb);
+        else if (more)
+          gather(nb, 0, xb);
+        tmem_st32(col + 64, h);
+        tmem_st32(col + 96, l);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&S.a_full[sa]);
       }
-      // epilogue: ReLU(D + b) -> y[row]
+      // epilogue: ReLU(D_u + b) -> y[row of tile u]
       mbar_wait(&S.d_full, it & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(trow + c0, v);
-        tmem_ld_wait();
-        if (valid) {
-          float4* yo = reinterpret_cast<float4*>(a.y + row * a.ldy + a.ycol + c0);
+      for (int u = 0; u < 2; ++u) {
+        const Pos& P = u == 0 ? ca : cb;
+#pragma unroll 1
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(trow + 128 * u + c0, v);
+          tmem_ld_wait();
+          if (P.valid) {
+            float4* yo = reinterpret_cast<float4*>(a.y + P.row * a.ldy + a.ycol + c0);
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            yo[u] = make_float4(fmaxf(__uint_as_float(v[4 * u]) + S.bias[c0 + 4 * u], 0.f),
-                                fmaxf(__uint_as_float(v[4 * u + 1]) + S.bias[c0 + 4 * u + 1], 0.f),
-                                fmaxf(__uint_as_float(v[4 * u + 2]) + S.bias[c0 + 4 * u + 2], 0.f),
-                                fmaxf(__uint_as_float(v[4 * u + 3]) + S.bias[c0 + 4 * u + 3], 0.f));
+            for (int w = 0; w < 8; ++w)
+              yo[w] = make_float4(fmaxf(__uint_as_float(v[4 * w]) + S.bias[c0 + 4 * w], 0.f),
+                                  fmaxf(__uint_as_float(v[4 * w + 1]) + S.bias[c0 + 4 * w + 1], 0.f),
+                                  fmaxf(__uint_as_float(v[4 * w + 2]) + S.bias[c0 + 4 * w + 2], 0.f),
+                                  fmaxf(__uint_as_float(v[4 * w + 3]) + S.bias[c0 + 4 * w + 3], 0.f));
+          }
         }
       }
       tc_fence_before();
       mbar_arrive(&S.d_empty);
-      cur = nxt;
+      ca = na;
+      cb = nb;
     }
   }
   tc_fence_before();
@@ -250,7 +270,7 @@ cudaError_t launch_conv_tc(const float* x1, int C1, const float* x2, int C2, int
   static const cudaError_t attr = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        (int)(sizeof(ConvTcSmem) + 1024));
   if (attr != cudaSuccess) return attr;
-  const int64_t rows = (int64_t)S * Do * Do * Do, ntiles = (rows + 127) / 128;
+  const int64_t rows = (int64_t)S * Do * Do * Do, ntiles = (rows + 255) / 256;
   const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
   ConvTcArgs a{x1, x2, C1, C2, Di, Do, pad, S, img, bias, y, 27, 0, 128, 0, nullptr, nullptr};
   conv_tc_kernel<<<grid, 192, sm, st>>>(a);
@@ -264,7 +284,7 @@ cudaError_t launch_gemm_tc(const float* x, int C, int64_t rows, const uint8_t* i
   static const cudaError_t attr = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        (int)(sizeof(ConvTcSmem) + 1024));
   if (attr != cudaSuccess) return attr;
-  const int64_t ntiles = (rows + 127) / 128;
+  const int64_t ntiles = (rows + 255) / 256;
   const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
   ConvTcArgs a{x, nullptr, C, 0, 1, 1, 0, 1, img, bias, y, 1, rows, ldy, ycol, pts, w1b};
   conv_tc_kernel<<<grid, 192, sm, st>>>(a);
