@@ -200,6 +200,24 @@ def test_cells_parity_other_grid_sizes(locc_mod, oracle_mod, weights, M):
     assert_cells_parity(got, ref, E, w.pairs)
 
 
+@pytest.mark.parametrize("M", [3, 8])
+def test_cells_grid_encode_tensor_cores_other_grid_sizes(locc_mod, oracle_mod, weights, monkeypatch, M):
+    """The tensor-core grid encode (bf16 context, U-Net on CUDA cores) at other grid edges: cell ids
+    0..M^3-1 (up to 511) in the cell-max kernel; E to the fp32 bar of the fp64 oracle."""
+    monkeypatch.setenv("LOCC_CONV_FFMA", "1")
+    w = ls.make_workload("C1", N=40, S=6)
+    ref = oracle_mod.query_cells(weights[0], weights[1], w.points, w.pairs, w.poses, M=M)
+    ctx = locc_mod.Locc(M=M, H=256, F=64, precision=1, device=0)
+    ctx.load_weights_mem(weights[0])
+    ctx.load_unet_weights_mem(weights[1])
+    ctx.set_shapes(w.points)
+    ctx.encode_shapes()
+    E, _ = ctx.cell_embeddings()
+    ctx.close()
+    scale = np.abs(ref["grids"]).max()
+    assert np.abs(E.astype(np.float64) - ref["grids"]).max() <= E_TOL * scale
+
+
 def test_cells_empty_and_disjoint_batches(locc_mod, weights, wl):
     pts, pairs, poses = wl
     with make_ctx(locc_mod, *weights, pts) as ctx:
