@@ -54,10 +54,10 @@ struct ConvTcArgs {
   const float4* w1b;  // as h1 = ReLU(W1 p + b1) of the row's point (the grid encode's layer 1, fused)
 };
 
+// fp32 -> nearest tf32 (ties away from zero) in an fp32 container: bit-identical to cvt.rna.tf32.f32,
+// but two integer ops on the ALU pipe instead of a conversion (a quarter-rate pipe, the producers' limit)
 __device__ __forceinline__ float tf32r(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {

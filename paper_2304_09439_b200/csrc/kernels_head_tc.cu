@@ -64,11 +64,10 @@ struct __align__(1024) HeadTcSmem {
   uint32_t tmem_base;
 };
 
-// Round to the nearest tf32 (ties away): a value the tensor core reads exactly.
+// Round to the nearest tf32 (ties away): a value the tensor core reads exactly.  Bit-identical to
+// cvt.rna.tf32.f32, as two integer ops on the ALU pipe instead of a conversion.
 __device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 // Split 32 values (this thread's row, K columns c0..c0+31) and store them as A_hi / A_lo.
