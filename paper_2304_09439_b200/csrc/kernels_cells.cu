@@ -266,20 +266,36 @@ __global__ void __launch_bounds__(256) unet_tail_kernel(UNetParams U, ShapeTable
     gb[tid] = acc;
   }
   __syncthreads();
-  for (int e = tid; e < nc * F; e += 256) {  // F consecutive threads share one d1 row (L1 broadcast)
-    const int c = e / F, f = e - c * F;
-    const float4* x = reinterpret_cast<const float4*>(d1 + ((int64_t)s * nc + c) * 128);
+  // thread (f, group): 4 cells at a time, so each weight read from shared memory feeds 4 FMAs; the d1
+  // rows are read by all threads of a feature group alike (L1 broadcast)
+  const int ngrp = 256 / F;
+  for (int e = tid; e < ngrp * F; e += 256) {
+    const int grp = e / F, f = e - grp * F;
     const float* w = pW + f * 257;
-    float a0 = 0.f, a1 = 0.f;
+    for (int c0 = 4 * grp; c0 < nc; c0 += 4 * ngrp) {
+      const float4* x[4];
+      float a0[4], a1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x[u] = reinterpret_cast<const float4*>(d1 + ((int64_t)s * nc + min(c0 + u, nc - 1)) * 128);
+        a0[u] = a1[u] = 0.f;
+      }
 #pragma unroll 4
-    for (int j = 0; j < 32; ++j) {
-      const float4 v = __ldg(x + j);
-      a0 = fmaf(w[4 * j], v.x, a0);
-      a1 = fmaf(w[4 * j + 1], v.y, a1);
-      a0 = fmaf(w[4 * j + 2], v.z, a0);
-      a1 = fmaf(w[4 * j + 3], v.w, a1);
+      for (int j = 0; j < 32; ++j) {
+        const float w0 = w[4 * j], w1 = w[4 * j + 1], w2 = w[4 * j + 2], w3 = w[4 * j + 3];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 v = __ldg(x[u] + j);
+          a0[u] = fmaf(w0, v.x, a0[u]);
+          a1[u] = fmaf(w1, v.y, a1[u]);
+          a0[u] = fmaf(w2, v.z, a0[u]);
+          a1[u] = fmaf(w3, v.w, a1[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c0 + u < nc) E[((int64_t)s * nc + c0 + u) * F + f] = (a0[u] + a1[u]) + gb[f];
     }
-    E[((int64_t)s * nc + c) * F + f] = (a0 + a1) + gb[f];
   }
   // the centres are separable: per axis d the M values lo_d + (i + 1/2) ext_d / M -> ctr[s][8 d + i]
   const float4 lo = T.lo[s], hi = T.hi[s];
