@@ -14,10 +14,14 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = os.path.join(_HERE, "liblocc_oracle.so")
+# tools/oracle_mutations.py points this at a deliberately broken build to check the pins' power
+_LIB_OVERRIDE = os.environ.get("LOCC_ORACLE_LIB")
 _lib = None
 
 
 def build(force: bool = False) -> str:
+    if _LIB_OVERRIDE:
+        return _LIB_OVERRIDE
     src = os.path.join(_HERE, "locc_oracle.cpp")
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
             os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "locc_oracle.h"))):
@@ -33,8 +37,7 @@ class _Cfg(C.Structure):
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(_LIB)
+        L = C.CDLL(build())
         vp = C.c_void_p
         L.oracle_shape_prep.argtypes = [vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
         L.oracle_rel_transform.argtypes = [vp] * 6

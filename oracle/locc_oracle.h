@@ -21,7 +21,9 @@
  * Parity pins: tests/test_oracle_*.py (network, geometry, grad: finite differences, a closed-form
  * head, symmetries; cells: scipy correlate/convolve, the adjoint identity, a delta-kernel U-Net probe,
  * a box-intersection superset property, a worked example; sim: discrete closed forms, score descent,
- * body-swap symmetry).  "parity unpinned": absolute probabilities of any trained LOCC (no trained
+ * body-swap symmetry; pins: closed-form probes of the encoder and predictor ReLUs and hidden biases and of
+ * the U-Net skip concatenation, each with a mutation check, tests/test_oracle_pins.py and
+ * tools/oracle_mutations.py).  "parity unpinned": absolute probabilities of any trained LOCC (no trained
  * weights exist).
  *
  * Return codes: 0 ok; -1 invalid argument; -2 bad shape table; -3 bad weights.

@@ -1,0 +1,291 @@
+"""Pins of the oracle parts round 1 left unpinned (VERDICT r1 "What's missing" 1):
+
+* the ReLU after enc.l2 and enc.l3 ("Relu activation ... across all layers");
+* the hidden-layer biases enc.l2/l3, obj.l1-l3, pair.l1-l3 (every layer has one);
+* the ReLUs of the object and pair MLPs;
+* the U-Net's skip concatenation order ("skip connection with concatenation").
+
+Each probe uses weights under which the network reduces to a closed form a reader can check by eye
+(group-by maxima of clipped coordinates, constants, a chain of sign flips and shifts, shifted delta
+blocks).  Each test also evaluates the closed form with the part in question removed (the ReLU
+dropped, the bias zeroed, the skips swapped) and asserts that this *mutated* value is far from the
+oracle's output, so the pin provably has the power to catch that mistake on this input."""
+import numpy as np
+import pytest
+
+import locc_synth as ls
+from conftest import cube26, pose
+from test_oracle_network import canon
+
+H, F, P, C = 256, 64, 128, 128
+
+
+def _keep_mask(r, i, side, K):
+    return np.array([(r["masks"][i, side, k // 32] >> (k % 32)) & 1 for k in range(K)], bool)
+
+
+def _cell_groupby(feats, cell):
+    """Textbook group-by: per-cell max of feats [n][j] (cells with no row stay -inf)."""
+    g = np.full((216, feats.shape[1]), -np.inf)
+    np.maximum.at(g, cell, feats)
+    return g
+
+
+# ----------------------------------------------------------------------------- encoder ReLUs
+def relu_probe(c, d):
+    """W1 = [I3; -I3; 0], b1 = 0  -> h1[0:6] = (x+, y+, z+, x-, y-, z-);
+    W2 = I, b2[0:6] = -c         -> h2 = ReLU(h1 - c);
+    W3 = -I, b3[0:6] = d         -> h3 = ReLU(d - h2);
+    W_F = [I6 | 0], b_F = 0      -> e[0:6] = mean over occupied cells of the cell max of h3."""
+    w = ls.make_weights("zero", H, F)
+    for i in range(3):
+        w["enc.l1.W"][i, i] = 1.0
+        w["enc.l1.W"][3 + i, i] = -1.0
+    w["enc.l2.W"][:] = np.eye(H, dtype=np.float32)
+    w["enc.l2.b"][:6] = -c
+    w["enc.l3.W"][:] = -np.eye(H, dtype=np.float32)
+    w["enc.l3.b"][:6] = d
+    for j in range(6):
+        w["enc.proj.W"][j, j] = 1.0
+    return ls.flatten_weights(w)
+
+
+def test_encoder_relu_probe(oracle_mod):
+    pts, _ = ls.make_shapes(10, 400, seed=70)
+    pairs, poses = ls.make_pairs_poses(pts, 40, s=0.5, seed=71)
+    # dyadic thresholds at the scale of the clouds' coordinates (a few cm)
+    c = (np.arange(1, 7) / 256.0).astype(np.float32)
+    d = (np.arange(6, 0, -1) / 512.0).astype(np.float32)
+    r = oracle_mod.query(relu_probe(c, d), pts, pairs, poses)
+    relu = lambda x: np.maximum(x, 0.0)
+    forms = {
+        "as defined": lambda h1: relu(d - relu(h1 - c)),
+        "enc.l2 ReLU dropped": lambda h1: relu(d - (h1 - c)),
+        "enc.l3 ReLU dropped": lambda h1: d - relu(h1 - c),
+    }
+    K = pts.shape[1]
+    dist = {k: 0.0 for k in forms}
+    checked = 0
+    for i in range(len(pairs)):
+        for side in range(2):
+            keep = _keep_mask(r, i, side, K)
+            if not keep.any():
+                continue
+            _, _, _, cell = oracle_mod.shape_prep(pts[pairs[i, side]])
+            p = pts[pairs[i, side]][keep].astype(np.float64)
+            h1 = np.concatenate([relu(p), relu(-p)], 1)
+            for name, f in forms.items():
+                g = _cell_groupby(f(h1), cell[keep])
+                occ = np.isfinite(g[:, 0])
+                want = g[occ].mean(0)
+                if name == "as defined":
+                    assert r["occ"][i, side] == occ.sum()
+                    np.testing.assert_allclose(r["emb"][i, side, :6], want, rtol=0, atol=1e-15)
+                    assert np.all(r["emb"][i, side, 6:] == 0)
+                dist[name] = max(dist[name], float(np.abs(r["emb"][i, side, :6] - want).max()))
+            checked += 1
+    assert checked > 30
+    assert dist["as defined"] <= 1e-15
+    for name in ("enc.l2 ReLU dropped", "enc.l3 ReLU dropped"):
+        assert dist[name] > 1e-4, name  # the probe separates the mutation from the definition
+
+
+# ----------------------------------------------------------------------------- encoder biases
+def test_encoder_bias_probe(oracle_mod):
+    """W2 = 0, W3 = P_tau (h3[tau(k)] = ReLU(h2[k] + b3[tau(k)])): every kept point has
+    h3[tau(k)] = ReLU(ReLU(b2[k]) + b3[tau(k)]), so every occupied cell's max is that constant and
+    e = W_F h3 + b_F for any non-empty side; an empty side gives e = 0."""
+    rng = np.random.default_rng(72)
+    w = ls.make_weights("he", H, F, seed=73)  # enc.l1 arbitrary: W2 = 0 cuts it off
+    tau = rng.permutation(H)
+    b2 = (rng.integers(-8, 9, H) / 16.0).astype(np.float32)
+    b3 = (rng.integers(-8, 9, H) / 16.0).astype(np.float32)
+    w["enc.l2.W"][:] = 0
+    w["enc.l2.b"][:] = b2
+    w["enc.l3.W"][:] = 0
+    w["enc.l3.W"][tau, np.arange(H)] = 1.0
+    w["enc.l3.b"][:] = b3
+    w["enc.proj.W"][:] = (rng.integers(-4, 5, (F, H)) / 8.0).astype(np.float32)
+    w["enc.proj.b"][:] = (rng.integers(-4, 5, F) / 8.0).astype(np.float32)
+    relu = lambda x: np.maximum(x, 0.0)
+    WF, bF = w["enc.proj.W"].astype(np.float64), w["enc.proj.b"].astype(np.float64)
+
+    def h3_of(b2_, b3_, relu2=True, relu3=True):
+        h2 = relu(b2_) if relu2 else b2_.astype(np.float64)
+        out = np.empty(H)
+        out[tau] = h2 + b3_[tau]
+        return relu(out) if relu3 else out
+
+    forms = {"as defined": h3_of(b2, b3), "enc.l2.b zeroed": h3_of(0 * b2, b3),
+             "enc.l3.b zeroed": h3_of(b2, 0 * b3), "enc.l2 ReLU dropped": h3_of(b2, b3, relu2=False),
+             "enc.l3 ReLU dropped": h3_of(b2, b3, relu3=False)}
+    pts, _ = ls.make_shapes(6, 300, seed=74)
+    pairs, poses = ls.make_pairs_poses(pts, 24, s=0.5, seed=75)
+    flat = ls.flatten_weights(w)
+    for emul in (False, True):  # dyadic biases and 0/1 weights are bf16-exact: emulation changes nothing
+        r = oracle_mod.query(flat, pts, pairs, poses, bf16_emul=emul)
+        nonempty = r["kept"] > 0
+        assert nonempty.sum() > 20 and (~nonempty).sum() > 0
+        for name, h3 in forms.items():
+            e = WF @ h3 + bF
+            dev = np.abs(r["emb"][nonempty] - e).max()
+            if name == "as defined":
+                assert dev <= 1e-12, dev
+            else:
+                assert dev > 1e-3, name
+        assert np.all(r["emb"][~nonempty] == 0)
+
+
+# ----------------------------------------------------------------------------- head ReLUs + biases
+HEAD_LAYERS = ("obj.l1", "obj.l2", "obj.l3", "pair.l1", "pair.l2", "pair.l3")
+
+
+def head_chain_weights(seed=76):
+    """Encoder = zero except b_F (so e = b_F on a non-empty side, 0 on an empty one);
+    obj.l1 unit u reads input col(u) = u mod 71 with sign s1[u];  obj.l2, obj.l3, pair.l1-l3 are
+    diagonal sign matrices diag(s_k); every layer has a signed dyadic bias; out = random dyadic.
+    Closed form per side: a = ReLU(s1 * z[col] + b1), a = ReLU(s_k * a + b_k) (k = 2, 3);
+    v = max(a_A, a_B); then three ReLU(s_k * v + b_k) and logit = W_out . v + b_out."""
+    rng = np.random.default_rng(seed)
+    w = ls.make_weights("zero", H, F)
+    w["enc.proj.b"][:] = (rng.integers(-8, 9, F) / 16.0).astype(np.float32)
+    signs, biases = {}, {}
+    for name in HEAD_LAYERS:
+        s = rng.choice([-1.0, 1.0], P).astype(np.float32)
+        b = (rng.integers(-8, 9, P) / 32.0).astype(np.float32)
+        signs[name], biases[name] = s, b
+        if name == "obj.l1":
+            w[name + ".W"][np.arange(P), np.arange(P) % (F + 7)] = s
+        else:
+            w[name + ".W"][:] = np.diag(s)
+        w[name + ".b"][:] = b
+    w["out.W"][0] = (rng.integers(-8, 9, P) / 8.0).astype(np.float32)
+    w["out.b"][0] = 0.375
+    return w, signs, biases
+
+
+def head_closed_form(w, signs, biases, z_A, z_B, drop_relu=None, zero_bias=None):
+    relu = lambda x: np.maximum(x, 0.0)
+
+    def layer(name, x):
+        b = 0 * biases[name] if name == zero_bias else biases[name].astype(np.float64)
+        y = signs[name] * x + b
+        return y if name == drop_relu else relu(y)
+
+    col = np.arange(P) % (F + 7)
+    u = []
+    for z in (z_A, z_B):
+        a = layer("obj.l1", z[col])
+        a = layer("obj.l2", a)
+        u.append(layer("obj.l3", a))
+    v = np.maximum(u[0], u[1])
+    for name in ("pair.l1", "pair.l2", "pair.l3"):
+        v = layer(name, v)
+    bout = 0.0 if zero_bias == "out" else float(w["out.b"][0])
+    return float(w["out.W"][0].astype(np.float64) @ v) + bout
+
+
+def test_head_relu_and_bias_chain(oracle_mod):
+    w, signs, biases = head_chain_weights()
+    pts, _ = ls.make_shapes(8, 300, seed=77)
+    pairs, poses = ls.make_pairs_poses(pts, 60, s=0.5, seed=78)
+    r = oracle_mod.query(ls.flatten_weights(w), pts, pairs, poses)
+    bF = w["enc.proj.b"].astype(np.float64)
+    mutations = [("drop_relu", n) for n in HEAD_LAYERS] + [("zero_bias", n) for n in HEAD_LAYERS + ("out",)]
+    dist = {m: 0.0 for m in mutations}
+    ev = 0
+    for i in range(len(pairs)):
+        if r["kept"][i].sum() == 0:
+            assert np.isneginf(r["logits"][i]) and r["probs"][i] == 0
+            continue
+        z = []
+        for side in range(2):
+            e = bF if r["kept"][i, side] > 0 else np.zeros(F)
+            z.append(np.concatenate([e, canon(poses[i, side, :4]), poses[i, side, 4:].astype(np.float64)]))
+        want = head_closed_form(w, signs, biases, z[0], z[1])
+        assert abs(r["logits"][i] - want) <= 1e-12, (i, r["logits"][i], want)
+        for kind, name in mutations:
+            alt = head_closed_form(w, signs, biases, z[0], z[1], **{kind: name})
+            dist[(kind, name)] = max(dist[(kind, name)], abs(r["logits"][i] - alt))
+        ev += 1
+    assert ev > 30
+    for m, dv in dist.items():
+        assert dv > 1e-3, m
+
+
+# ----------------------------------------------------------------------------- U-Net skips
+def unet_skip_probe():
+    """Channel-tagged delta kernels (centre tap 13 = identity for 'same' layers):
+    c1: ch0 <- G ch0 at tap (x, y, z) = (2, 0, 1) (valid)           => c1[0] = A (the 4^3 block)
+    c2: ch1 <- 2 c1[0];  ch7 <- -c1[0]  (ReLU -> 0)                   => c2[1] = 2A, c2[7] = 0
+    c3: ch2 <- 2 c2[1]                                                 => c3[2] = 4A
+    c4, d4: zero                                                       => g = 0, d4 = 0
+    d3 = deconv([d4; c3]): ch3 <- input 128 + 2 (= c3[2])             => d3[3] = 4A
+    d2 = deconv([d3; c2]): ch4 <- input 128 + 1 (= c2[1]); ch5 <- input 3 (= d3[3]);
+                           ch9 <- -input 128 + 7 (= -c2[7])           => d2[4] = 2A, d2[5] = 4A, d2[9] = 0
+    d1 = transposed valid deconv([d2; c1]), tap (0, 2, 1):
+         ch6 <- input 128 + 0 (= c1[0]); ch7 <- input 4; ch8 <- input 5; ch10 <- input 9
+    proj: E0..E3 = d1[6], d1[7], d1[8], d1[10]  => E = (A, 2A, 4A, 0) scattered to p + (0, 2, 1)."""
+    u = ls.make_unet_weights("zero", H, F)
+    k1 = 2 + 3 * (0 + 3 * 1)
+    kd = 0 + 3 * (2 + 3 * 1)
+    u["unet.c1.W"][0, 0, k1] = 1.0
+    u["unet.c2.W"][1, 0, 13] = 2.0
+    u["unet.c2.W"][7, 0, 13] = -1.0
+    u["unet.c3.W"][2, 1, 13] = 2.0
+    u["unet.d3.W"][3, C + 2, 13] = 1.0
+    u["unet.d2.W"][4, C + 1, 13] = 1.0
+    u["unet.d2.W"][5, 3, 13] = 1.0
+    u["unet.d2.W"][9, C + 7, 13] = -1.0
+    u["unet.d1.W"][6, C + 0, kd] = 1.0
+    u["unet.d1.W"][7, 4, kd] = 1.0
+    u["unet.d1.W"][8, 5, kd] = 1.0
+    u["unet.d1.W"][10, 9, kd] = 1.0
+    for j, ch in enumerate((6, 7, 8, 10)):
+        u["unet.proj.W"][j, ch] = 1.0
+    return ls.flatten_unet(u)
+
+
+def test_unet_skip_probe(oracle_mod):
+    from test_oracle_cells import identity_encoder
+    pts, _ = ls.make_shapes(3, 600, seed=79)
+    for s in range(3):
+        G, E = oracle_mod.encode_grid(identity_encoder(), unet_skip_probe(), pts[s])
+        A = G.reshape(6, 6, 6, H)[1:5, 0:4, 2:6, 0]  # G[p + (x2, y0, z1)] ch0, indexed [z][y][x]
+        assert A.max() > 0
+        Ez = E.reshape(6, 6, 6, F)
+        for ch, scale in ((0, 1.0), (1, 2.0), (2, 4.0), (3, 0.0)):
+            want = np.zeros((6, 6, 6))
+            want[1:5, 2:6, 0:4] = scale * A
+            np.testing.assert_array_equal(Ez[..., ch], want)
+        assert np.all(E[:, 4:] == 0)
+
+
+def test_unet_skip_probe_detects_swaps():
+    """The closed form above under each plausible wiring mistake (numpy, independent of the oracle):
+    every mistake changes at least one of E0..E3, so test_unet_skip_probe would fail on it."""
+    rng = np.random.default_rng(80)
+    A = rng.random((4, 4, 4))
+    relu = lambda x: np.maximum(x, 0)
+
+    def run(skip3="c3", skip2="c2", skip1="c1", swap_halves=False, relu_c2=True):
+        c1 = {0: A}
+        c2 = {1: 2 * c1[0], 7: relu(-c1[0]) if relu_c2 else -c1[0]}
+        c3 = {2: 2 * c2[1]}
+        T = {"c1": c1, "c2": c2, "c3": c3, "d4": {}}
+        get = lambda t, ch: T[t].get(ch, np.zeros((4, 4, 4)))
+        first3, second3 = ("d4", skip3) if not swap_halves else (skip3, "d4")
+        d3 = {3: get(second3, 2)}
+        T["d3"] = d3
+        first2, second2 = ("d3", skip2) if not swap_halves else (skip2, "d3")
+        d2 = {4: get(second2, 1), 5: get(first2, 3), 9: relu(-get(second2, 7))}
+        T["d2"] = d2
+        first1, second1 = ("d2", skip1) if not swap_halves else (skip1, "d2")
+        return np.stack([get(second1, 0), get(first1, 4), get(first1, 5), get(first1, 9)])
+
+    ok = run()
+    assert np.array_equal(ok, np.stack([A, 2 * A, 4 * A, 0 * A]))
+    for kw in (dict(skip3="c2"), dict(skip3="c1"), dict(skip2="c1"), dict(skip2="c3"), dict(skip1="c2"),
+               dict(skip1="c3"), dict(skip3="c1", skip1="c3"), dict(skip2="c1", skip1="c2"),
+               dict(swap_halves=True), dict(relu_c2=False)):
+        assert not np.array_equal(run(**kw), ok), kw
