@@ -23,9 +23,17 @@
  *     with poses[14i+7 .. 14i+13].
  *   - Buffers are caller-owned.  Every pointer passed to one call must have the same residency
  *     (all host, or all device memory of the context's device); the library detects which.
- *   - A context is bound to one CUDA device and is not reentrant; separate contexts are
- *     independent.  Multi-GPU = one context (one process) per GPU, sharding pairs (see
- *     paper_2304_09439_b200/parallel.py); the path needs no collective.
+ *   - A context is not reentrant; separate contexts are independent.  Multi-GPU (
+ *     pairs are independent), two forms, both sharding the batch into contiguous
+ *     shards of ceil(N/G) pairs:
+ *       * one process, G devices: locc_config.n_devices > 1 — the context drives one sub-context
+ *         per device (its own stream, scratch, weights and shape table) and splits every query;
+ *         device-resident caller buffers live on the home device (device_ids[0]) and the other
+ *         devices read their shard's inputs and write their outputs there directly over NVLink
+ *         (peer access), or through peer copies when peer access is unavailable;
+ *       * one process per GPU: locc_comm_init + locc_query_allgather — each rank computes its
+ *         shard and the library gathers every rank's results on every rank with NCCL (the only
+ *         collective of the path: 9 B per pair).
  *   - Errors: every function returns a locc_status; on error no output is guaranteed written
  *     and locc_last_error() holds a thread-local detail string.  No exception crosses the ABI.
  */
@@ -45,7 +53,7 @@ typedef enum {
   LOCC_E_WEIGHTS = -3,     /* manifest/tensor name/shape mismatch, wrong count, non-finite */
   LOCC_E_CUDA = -4,        /* a CUDA runtime call or kernel failed */
   LOCC_E_OOM = -5,         /* device allocation failed */
-  LOCC_E_NCCL = -6,        /* reserved (the path itself uses no collective) */
+  LOCC_E_NCCL = -6,        /* NCCL missing (dlopen of libnccl.so.2) or an NCCL call failed */
   LOCC_E_STATE = -7        /* query before weights and shapes were set */
 } locc_status;
 
@@ -62,9 +70,15 @@ typedef struct {
   int32_t H;         /* point-feature width; 256 for BF16, 32..256 step 32 for FP32 */
   int32_t F;         /* cell-feature width; 1..256 */
   int32_t precision; /* locc_precision */
-  int32_t device;    /* CUDA device ordinal; -1 = the calling thread's current device */
-  int32_t reserved;
-  int64_t max_batch; /* pairs per internal sub-batch (bounds scratch memory); 0 = 262144 */
+  int32_t device;    /* CUDA device ordinal; -1 = the calling thread's current device (ignored when
+                        n_devices > 1) */
+  int32_t n_devices; /* 0 or 1: one device.  > 1: the context drives n_devices devices of this process
+                        (one sub-context each, queries sharded into contiguous ceil(N/G) blocks) */
+  int64_t max_batch; /* pairs per internal sub-batch per device (bounds scratch memory); 0 = 262144 */
+  const int32_t* device_ids; /* n_devices CUDA ordinals (NULL = 0 .. n_devices-1); the first is the
+                                home device of device-resident caller buffers.  An ordinal may repeat
+                                (sub-contexts sharing a GPU, e.g. to test the sharding on one device).
+                                Copied at locc_create. */
 } locc_config;
 
 typedef struct locc_ctx locc_ctx;
@@ -84,8 +98,11 @@ typedef struct {
   double  crop_ms;          /* device time of the transform + crop + compaction launches (0 if timing off) */
 } locc_stats;
 
-/* Create a context on cfg->device.  Out: *out (free with locc_destroy).
- * Errors: INVALID_ARG (null, M/H/F/precision out of range), CUDA, OOM. */
+/* Create a context on cfg->device, or on the cfg->n_devices devices of cfg->device_ids (peer access
+ * is enabled between the home device and every other device where the hardware allows it).
+ * Every other call fans out to the sub-contexts; locc_get_stats sums the counts and takes the
+ * maximum of the per-device times.  Out: *out (free with locc_destroy).
+ * Errors: INVALID_ARG (null, M/H/F/precision out of range, bad device ordinal), CUDA, OOM. */
 locc_status locc_create(const locc_config* cfg, locc_ctx** out);
 
 /* Load parameters from the checkpoint format: text manifest
@@ -214,12 +231,52 @@ typedef struct {
  * [E][3] shape ids; body float32 [E][3][4] = mass, body-frame principal inertia (Ixx, Iyy, Izz); state
  * float32 [E][3][13] = q (4), t (3), v (3), w (3), world frame, updated in place; contacts int32 [E][3]
  * (nullable) = substeps in contact per pair.  stream NULL: synchronous; else asynchronous on it.
- * Errors: INVALID_ARG (sizes, host buffers, H/F not 256/64), STATE (weights/shapes/encoding), CUDA, OOM. */
+ * An environment with a body id outside [0, S) has its pairs culled for that substep (no contact
+ * forces; nothing out of range is read); the synchronous form then returns INVALID_ARG.  The
+ * substeps are captured into a CUDA graph on the second call with identical arguments and replayed
+ * while no context state or scratch buffer has changed.
+ * Errors: INVALID_ARG (sizes, host buffers, H/F not 256/64, bad ids), STATE (weights/shapes/encoding),
+ * CUDA, OOM. */
 locc_status locc_sim_run(locc_ctx* ctx, const locc_sim_config* cfg, int32_t E, const int32_t* ids,
                          const float* body, float* state, double t0, int32_t* contacts, void* stream);
 
+/* ---- Multi-process sharding with a library-owned NCCL gather ----
+ * One process (one single-device context) per GPU.  NCCL is loaded at run time (dlopen of
+ * libnccl.so.2: the copy already in the process, e.g. PyTorch's, else the system's); the handshake
+ * is the caller's: rank 0 calls locc_comm_unique_id and sends the 128 bytes to the other ranks
+ * (e.g. with torch.distributed), then every rank calls locc_comm_init.  */
+
+/* Write a new NCCL unique id (128 bytes) to out.  Errors: INVALID_ARG (null), NCCL. */
+locc_status locc_comm_unique_id(uint8_t out[128]);
+
+/* Join the world of `world` ranks as `rank` on the context's device (ncclCommInitRank).  A context
+ * holds one communicator; calling again replaces it.  Errors: INVALID_ARG (null, world < 1, rank out
+ * of [0, world), multi-device context), NCCL, CUDA. */
+locc_status locc_comm_init(locc_ctx* ctx, int32_t world, int32_t rank, const uint8_t id[128]);
+
+/* Sharded query of a GLOBAL batch of N pairs over the communicator's ranks: this rank reads only its
+ * contiguous shard [lo, hi) = [r ceil(N/W), min(N, (r+1) ceil(N/W))) of pairs/poses, computes it
+ * with locc_query's arithmetic, writes it at [lo, hi) of probs/labels/logits, and the library then
+ * gathers every rank's shard into the same global output arrays on every rank (one NCCL group of
+ * in-place broadcasts, one per rank's shard; labels and logits nullable, the same on every rank).
+ * Pairs outside the shard are never read, so a rank need only fill its own slice of pairs/poses.
+ * Every rank must call it with the same N.  Host or device buffers (same rules as locc_query; host
+ * outputs are staged through device memory for NCCL); stream NULL = synchronous.
+ * Errors: as locc_query; STATE (no communicator); NCCL. */
+locc_status locc_query_allgather(locc_ctx* ctx, const int32_t* pairs, const float* poses, int64_t N,
+                                 float* probs, uint8_t* labels, float* logits, void* stream);
+
 /* Switch the encoder precision of an existing context (LOCC_PREC_FP32 / LOCC_PREC_BF16). */
 locc_status locc_set_precision(locc_ctx* ctx, int32_t precision);
+
+/* Bitwise reproducibility of LOCC_PREC_BF16 contexts (reading Q24).  0 (default): the
+ * tensor-core encoder's layer-3 epilogue sums a segment's cell values in an order that depends on
+ * where the segment falls in its 128-row part, so batch composition (N, pair order, sub-batching,
+ * GPU count) can move a probability by a few fp32 ulps (<= 1e-5).  1: an order fixed by the segment's
+ * own rows (16-row blocks), so every output is bitwise independent of batch composition; the
+ * epilogue costs more.  FP32 contexts are always bitwise reproducible.
+ * Errors: INVALID_ARG (null). */
+locc_status locc_set_deterministic(locc_ctx* ctx, int32_t enabled);
 
 /* Enable (1) / disable (0) CUDA-event timing of the encoder and of the whole query. */
 locc_status locc_set_timing(locc_ctx* ctx, int32_t enabled);

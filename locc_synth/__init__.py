@@ -25,6 +25,9 @@ Workload recipe:
   the final linear layers), biases U(+-1/sqrt(fan_in)).  `spread`: W1 He bound
   x10, all biases 0, then out.W scaled and out.b set from a calibration file
   written by `tools/calibrate_spread.py` (which calls only the oracle).
+  `spread_bias`: the `spread` weights with every hidden and projection bias drawn
+  as in `he` (U(+-1/sqrt(fan_in))), out.W / out.b calibrated the same way (its own
+  file) — the set that exercises every bias path of the GPU kernels.
 """
 from __future__ import annotations
 
@@ -37,7 +40,7 @@ import numpy as np
 __all__ = [
     "FAMILIES", "make_shapes", "make_pairs_poses", "weight_layout", "make_weights",
     "flatten_weights", "write_weights", "read_weights", "default_calibration_path",
-    "load_calibration", "Workload", "make_workload",
+    "load_calibration", "Workload", "make_workload", "WEIGHT_SETS", "weight_set",
 ]
 
 FAMILIES = ("box", "wedge", "torus", "tube", "bowl", "cup", "mug", "lbracket")
@@ -206,7 +209,8 @@ def make_weights(kind: str = "spread", H: int = 256, F: int = 64, seed: int = 3,
     kind='he': He-uniform (ReLU layers) / Xavier-uniform (enc.proj, out) weights,
     biases U(+-1/sqrt(fan_in)).  kind='spread': same draws, enc.l1.W bound x10 and
     all biases 0; if `calib` ({'scale', 'bias'}) is given, out.W *= scale and
-    out.b = bias.  kind='zero': every parameter 0."""
+    out.b = bias.  kind='spread_bias': 'spread' with the 'he' biases (calibrated
+    the same way).  kind='zero': every parameter 0."""
     rng = np.random.default_rng(seed)
     w = {}
     for name, o, i in weight_layout(H, F):
@@ -216,20 +220,28 @@ def make_weights(kind: str = "spread", H: int = 256, F: int = 64, seed: int = 3,
                 bound = np.sqrt(6.0 / (i + o))
             else:
                 bound = np.sqrt(6.0 / i)
-            if kind == "spread" and layer == "enc.l1":
+            if kind in ("spread", "spread_bias") and layer == "enc.l1":
                 bound *= 10.0
             w[name] = rng.uniform(-bound, bound, size=(o, i)).astype(np.float32)
         else:
             fan_in = w[layer + ".W"].shape[1]
             b = rng.uniform(-1, 1, size=(o,)) / np.sqrt(fan_in)
-            w[name] = (b if kind == "he" else np.zeros(o)).astype(np.float32)
+            w[name] = (b if kind in ("he", "spread_bias") else np.zeros(o)).astype(np.float32)
     if kind == "zero":
         for k in w:
             w[k] = np.zeros_like(w[k])
-    if kind == "spread" and calib is not None:
+    if kind in ("spread", "spread_bias") and calib is not None:
         w["out.W"] = (w["out.W"] * np.float32(calib["scale"])).astype(np.float32)
         w["out.b"] = np.array([calib["bias"]], np.float32)
     return w
+
+
+WEIGHT_SETS = ("spread", "spread_bias")  # the calibrated sets the GPU parity suites run over
+
+
+def weight_set(kind: str = "spread"):
+    """A calibrated weight set ('spread' or 'spread_bias') as the flat canonical float32 vector."""
+    return flatten_weights(make_weights(kind, calib=load_calibration(kind=kind)))
 
 
 def unet_layout(H: int = 256, F: int = 64, C: int = 128):
@@ -311,13 +323,13 @@ def read_weights(path_txt: str):
     return w, (M, H, F)
 
 
-def default_calibration_path():
+def default_calibration_path(kind: str = "spread"):
     return os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
-                        "spread_calibration.json")
+                        f"{kind}_calibration.json")
 
 
-def load_calibration(path=None):
-    path = path or default_calibration_path()
+def load_calibration(path=None, kind: str = "spread"):
+    path = path or default_calibration_path(kind)
     if not os.path.exists(path):
         return None
     with open(path) as f:

@@ -1,7 +1,20 @@
 // e3_walk.cuh — the layer-3 epilogue walk of the tensor-core encoder (kernels_encoder_tc.cu): per
-// output feature, the rows of a tile in order -> cell-wise max, g = ReLU(max + b3),
-// sum over occupied cells, mean at the segment end.  Shared with
+// output feature, the rows of a tile in order -> cell-wise max of h3 = ReLU(D3), the
+// layer-3 accumulator D3 = b3 + W3 h2 (b3 enters through a bias MMA, like b2), sum over the occupied
+// cells in ascending cell order, mean at the segment end.  Shared with
 // tools/e3_microbench.cu, which times these routines in isolation.
+//
+// Summation order (reading Q24).  The default walk splits each 128-row part between two
+// walkers (rows 0-63 carried, rows 64-127 started fresh and merged), so the fp32 order in which a
+// segment's cell values are summed depends on where the segment falls relative to row 64 of its part:
+// batch composition can move the pooled mean by a few ulps.  The deterministic walk
+// (locc_set_deterministic; e3_part2_det) uses an order fixed by the segment itself: its rows are
+// padded to a multiple of 16 (kSegAlign) and start on a 16-row boundary, so they fall into 16-row
+// blocks fixed relative to the segment, and the pooled sum is the fold of per-block sums,
+//     S = ((P_0 + P_1) + P_2) + ...,   P_b = ((g_1 + g_2) + g_3) + ...,
+// g_1, g_2, ... the values of the cells that END in block b, in row (= ascending cell) order; a
+// block in which no cell ends adds +0.  Then every output is bitwise independent of batch
+// composition, pair order, sub-batching and GPU count.
 #pragma once
 #include <stdint.h>
 
@@ -13,13 +26,34 @@ namespace e3 {
 
 using namespace tc;
 
-// Layer-3 walk state of one output feature.  m runs from -b3 so that ReLU(max + b3) = m + b3 at a
-// cell end (max(x, -b3) + b3 rounds to exactly the same value as ReLU(x + b3)); s sums m over the
-// occupied cells of the open segment and the mean is (s + c b3) / c.
+// Walk state of one output feature: m = running max of the open cell (from 0: ReLU(max D3) =
+// max ReLU(D3)), s = fold of the block sums of the open segment, c = its closed cells.
 struct Walk {
   float m, s;
   int c;
 };
+
+// Out of line: called once per segment end, kept out of the walk's instruction stream.
+__device__ __noinline__ void store_mean(float* pooled, uint32_t seg, uint32_t f, float s, int c) {
+  pooled[(int64_t)seg * 256 + f] = __fdiv_rn(s, (float)c);
+}
+
+constexpr uint32_t kEven = 0x55555555u, kOdd = 0xAAAAAAAAu;
+
+__device__ __forceinline__ uint32_t sel4(const uint4& v, int c) {
+  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+
+// ---------------------------------------------------------------------------------------------
+// The walk (default).  Two walkers with interleaved masks: for step C (0..3) of a 128-row part, the
+// carried walker X takes rows 16C..16C+15 and the tail walker Y rows 64+16C..; their cell-end bits
+// come in one word with bit 2j = X row j and bit 2j+1 = Y row j (built directly by the ballot in the
+// flags phase), so both walkers' per-row predicates are extracted 7 at a time.  Segments are padded
+// to 16 rows (kSegAlign), so a segment end is the last real row of its step: the step is walked like
+// any other and the segment closed after it.  Summation order: X's cells sequentially; Y's tail sum
+// s1 (from 0) joins X's at the merge as (S + v) + s1 — so the fp32 order of a segment's cell sum
+// depends on where the segment falls relative to the part's row 64 (reading Q24: a few ulps).
+// The deterministic walk below (locc_set_deterministic) removes that dependence.
 // A walker that starts in the middle of the row sequence (the second half of a layer-3 part) runs
 // from an empty state without waiting for its predecessor, exactly like the carried walker: its
 // first cell (the "head") is in truth the continuation of the cell its predecessor left open, and
@@ -34,10 +68,6 @@ struct Tail {
   bool ce, se;  // seen a cell end / a segment end (warp-uniform)
 };
 
-// Out of line: called once per segment end, kept out of the walk's instruction stream.
-__device__ __noinline__ void store_mean(float* pooled, uint32_t seg, uint32_t f, float s, int c, float b3) {
-  pooled[(int64_t)seg * 256 + f] = __fdividef(fmaf((float)c, b3, s), (float)c);
-}
 
 // ---------------------------------------------------------------------------------------------
 // Two walkers with interleaved masks (the encoder's layer-3 epilogue).  For step C (0..3) of a
@@ -48,13 +78,13 @@ __device__ __noinline__ void store_mean(float* pooled, uint32_t seg, uint32_t f,
 // the step is walked like any other and the segment closed after it.
 // Tail semantics: Y's (s, c) exclude its head cell (kept as hm), see merge2().
 
-constexpr uint32_t kEven = 0x55555555u, kOdd = 0xAAAAAAAAu;
 
 // One step.  kFirst: Y's first cell end is in this step at bit `firstbit` (its head cell ends there:
 // not added, its max kept as hm).
 template <bool kFirst>
 __device__ __forceinline__ void step2(const uint32_t (&vx)[16], const uint32_t (&vy)[16], uint32_t ce2,
-                                      uint32_t firstbit, Walk& x, Tail& t, float nb3) {
+                                      uint32_t firstbit, Walk& x, Tail& t) {
+  constexpr float nb3 = 0.f;
   Walk& y = t.w;
   const uint32_t add = kFirst ? ce2 & ~firstbit : ce2;
   float hm = nb3;
@@ -79,10 +109,11 @@ __device__ __forceinline__ void step2(const uint32_t (&vx)[16], const uint32_t (
 // After a step with segment ends: close them (X: store the mean; Y: store, or keep aside if it is
 // Y's first segment end) and restart the walkers (the rest of the step is padding).
 __device__ __forceinline__ void seg_close(uint32_t se2, const uint32_t* flx, const uint32_t* fly, Walk& x, Tail& t,
-                                          float nb3, float b3, float* pooled, uint32_t f) {
+                                          float* pooled, uint32_t f) {
+  constexpr float nb3 = 0.f;
   if (se2 & kEven) {
     const int jx = (__ffs(se2 & kEven) - 1) >> 1;
-    store_mean(pooled, flx[jx] >> kRowSegShift, f, x.s, x.c, b3);
+    store_mean(pooled, flx[jx] >> kRowSegShift, f, x.s, x.c);
     x = Walk{nb3, 0.f, 0};
   }
   if (se2 & kOdd) {
@@ -90,7 +121,7 @@ __device__ __forceinline__ void seg_close(uint32_t se2, const uint32_t* flx, con
     const int jy = (__ffs(se2 & kOdd) - 2) >> 1;
     const uint32_t seg = fly[jy] >> kRowSegShift;
     if (t.se) {
-      store_mean(pooled, seg, f, y.s, y.c, b3);
+      store_mean(pooled, seg, f, y.s, y.c);
     } else {
       t.s1 = y.s;
       t.c1 = y.c;
@@ -102,14 +133,14 @@ __device__ __forceinline__ void seg_close(uint32_t se2, const uint32_t* flx, con
 }
 
 // x <- x followed by the tail walker's rows (Y's sums exclude its head cell).
-__device__ __forceinline__ void merge2(Walk& x, const Tail& t, float b3, float* pooled, uint32_t f) {
+__device__ __forceinline__ void merge2(Walk& x, const Tail& t, float* pooled, uint32_t f) {
   if (!t.ce) {
     x.m = fmaxf(x.m, t.w.m);
     return;
   }
   const float hv = fmaxf(x.m, t.hm);  // the cell open across the boundary
   if (t.se) {
-    store_mean(pooled, t.seg1, f, x.s + hv + t.s1, x.c + 1 + t.c1, b3);
+    store_mean(pooled, t.seg1, f, x.s + hv + t.s1, x.c + 1 + t.c1);
     x = t.w;
   } else {
     x.s = x.s + hv + t.w.s;
@@ -118,14 +149,12 @@ __device__ __forceinline__ void merge2(Walk& x, const Tail& t, float b3, float* 
   }
 }
 
-__device__ __forceinline__ uint32_t sel4(const uint4& v, int c) {
-  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
-}
 
 // A 128-row part: four straight-line steps with a register double buffer of TMEM columns.
 // mk[0..3] = interleaved cell ends of steps 0..3, mk[4..7] = interleaved segment ends.
-__device__ __forceinline__ void e3_part2(uint32_t tbase, const uint32_t* mk, const uint32_t* fl, Walk& w, float nb3,
-                                         float b3, float* pooled, uint32_t f) {
+__device__ __forceinline__ void e3_part2(uint32_t tbase, const uint32_t* mk, const uint32_t* fl, Walk& w,
+                                         float* pooled, uint32_t f) {
+  constexpr float nb3 = 0.f;
   Tail t;
   t.w = Walk{nb3, 0.f, 0};
   t.hm = nb3;
@@ -153,10 +182,10 @@ __device__ __forceinline__ void e3_part2(uint32_t tbase, const uint32_t* mk, con
         tmem_ld16(tbase + 64 + 16 * (c + 1), ny);
       }
       if (c == 0)
-        step2<true>(vx, vy, sel4(ce, c), yc & (0u - yc), w, t, nb3);
+        step2<true>(vx, vy, sel4(ce, c), yc & (0u - yc), w, t);
       else
-        step2<false>(vx, vy, sel4(ce, c), 0u, w, t, nb3);
-      if (sel4(se, c)) seg_close(sel4(se, c), fl + 16 * c, fl + 64 + 16 * c, w, t, nb3, b3, pooled, f);
+        step2<false>(vx, vy, sel4(ce, c), 0u, w, t);
+      if (sel4(se, c)) seg_close(sel4(se, c), fl + 16 * c, fl + 64 + 16 * c, w, t, pooled, f);
     }
   } else {
 #pragma unroll 1
@@ -169,13 +198,171 @@ __device__ __forceinline__ void e3_part2(uint32_t tbase, const uint32_t* mk, con
       const uint32_t cec = sel4(ce, c), sec = sel4(se, c);
       const uint32_t yc = cec & kOdd;
       if (!t.ce && yc != 0)
-        step2<true>(xa, ya, cec, yc & (0u - yc), w, t, nb3);
+        step2<true>(xa, ya, cec, yc & (0u - yc), w, t);
       else
-        step2<false>(xa, ya, cec, 0u, w, t, nb3);
-      if (sec) seg_close(sec, fl + 16 * c, fl + 64 + 16 * c, w, t, nb3, b3, pooled, f);
+        step2<false>(xa, ya, cec, 0u, w, t);
+      if (sec) seg_close(sec, fl + 16 * c, fl + 64 + 16 * c, w, t, pooled, f);
     }
   }
-  merge2(w, t, b3, pooled, f);
+  merge2(w, t, pooled, f);
+}
+
+// ---------------------------------------------------------------------------------------------
+// The deterministic walk (locc_set_deterministic): the same two walkers, the fixed blocked order of
+// the header comment.  Two walkers with interleaved masks (the encoder's layer-3 epilogue).  For block C (0..3) of a
+// 128-row part, walker X takes rows 16C..16C+15 and walker Y rows 64+16C..; their cell-end bits come
+// in one word with bit 2j = X row j and bit 2j+1 = Y row j (built directly by the ballot in the flags
+// phase), so both walkers' per-row predicates are extracted 7 at a time.  A segment end is the last
+// real row of its block (the rest is padding): the block is walked like any other and the segment
+// closed after it.
+//
+// X continues the carried segment.  Y starts at row 64 without waiting for X: until its first
+// segment end ("head mode", blocks 0..ys) its cells belong to the segment X has open.  The first
+// cell that ends in Y's rows (in block b0) is the one open across row 64: its value is
+// v = max(X's open max, Y's), known only to the merge, and it is the first term of P_b0.  So in block
+// b0 Y keeps its last two cell values (prev, last) instead of summing: with one or two cell ends in
+// the block that is all P_b0 = v or v + last needs; with more (rare) the merge re-walks block b0 from
+// TMEM with the true running max.  Y keeps the block sums of its later head blocks apart (hp1..hp3),
+// and the merge folds P_b0 and them onto X's sum in block order.  After its first segment end Y walks
+// whole segments and sums them itself.
+
+
+// One block of both walkers: X folds its cell values into px; Y folds them into py, or, with kYHead,
+// shifts them through (prev, last).
+template <bool kYHead>
+__device__ __forceinline__ void step2(const uint32_t (&vx)[16], const uint32_t (&vy)[16], uint32_t ce2, Walk& x,
+                                      Walk& y, float& px, float& py, float& prev, float& last) {
+  px = py = 0.f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    x.m = fmaxf(x.m, __uint_as_float(vx[j]));
+    if ((ce2 >> (2 * j)) & 1u) px += x.m;
+    if ((ce2 >> (2 * j)) & 1u) x.m = 0.f;
+    y.m = fmaxf(y.m, __uint_as_float(vy[j]));
+    if ((ce2 >> (2 * j + 1)) & 1u) {
+      if (kYHead) {
+        prev = last;
+        last = y.m;
+      } else {
+        py += y.m;
+      }
+    }
+    if ((ce2 >> (2 * j + 1)) & 1u) y.m = 0.f;
+  }
+  x.c += __popc(ce2 & kEven);
+  y.c += __popc(ce2 & kOdd);
+}
+
+
+// Y's head bookkeeping of one walk (one part).
+struct Head {
+  float prev = 0.f, last = 0.f, hm0 = 0.f;  // block b0's last two cell values; Y's max entering b0
+  float hp1 = 0.f, hp2 = 0.f, hp3 = 0.f;    // block sums of Y's head blocks 1..3 after b0
+  int hc = 0;                               // Y's head cells
+};
+
+// One block of the part (walkers X and Y) with Y's head bookkeeping.
+template <bool kYHead>
+__device__ __forceinline__ void block(int c, const uint32_t (&vx)[16], const uint32_t (&vy)[16], uint32_t cec,
+                                      uint32_t sec, int ys, int b0, Walk& w, Walk& y, Head& h, const uint32_t* fl,
+                                      float* pooled, uint32_t f) {
+  float px, py;
+  if (kYHead) h.hm0 = y.m;
+  step2<kYHead>(vx, vy, cec, w, y, px, py, h.prev, h.last);
+  w.s += px;  // a block without cell ends adds +0 (exact)
+  if (c > ys)
+    y.s += py;
+  else if (!kYHead && c > b0)  // (named scalars: c is a runtime value on the slow path)
+    (c == 1 ? h.hp1 : c == 2 ? h.hp2 : h.hp3) = py;
+  if (sec) {
+    if (sec & kEven) {  // X closes its segment (the rest of its block is padding)
+      const int jx = (__ffs(sec & kEven) - 1) >> 1;
+      store_mean(pooled, fl[16 * c + jx] >> kRowSegShift, f, w.s, w.c);
+      w = Walk{0.f, 0.f, 0};
+    }
+    if (sec & kOdd) {
+      if (c > ys) {  // a whole segment of Y's own
+        const int jy = (__ffs(sec & kOdd) - 2) >> 1;
+        store_mean(pooled, fl[64 + 16 * c + jy] >> kRowSegShift, f, y.s, y.c);
+      } else {
+        h.hc = y.c;  // Y's head cells (its head segment is closed in the merge)
+      }
+      y = Walk{0.f, 0.f, 0};
+    }
+  }
+}
+
+// A 128-row part: four straight-line blocks with a register double buffer of TMEM columns, then the
+// merge.  mk[0..3] = interleaved cell ends of blocks 0..3, mk[4..7] = interleaved segment ends.  `w`
+// is X's carried state in and the part's final state out.
+__device__ __forceinline__ void e3_part2_det(uint32_t tbase, const uint32_t* mk, const uint32_t* fl, Walk& w,
+                                         float* pooled, uint32_t f) {
+  const uint4 ce = *reinterpret_cast<const uint4*>(mk);
+  const uint4 se = *reinterpret_cast<const uint4*>(mk + 4);
+  // Y's first segment end is in block ys (4 = none in this part); its first cell end in block b0
+  const int ys = (se.x & kOdd) ? 0 : (se.y & kOdd) ? 1 : (se.z & kOdd) ? 2 : (se.w & kOdd) ? 3 : 4;
+  const int b0 = (ce.x & kOdd) ? 0 : (ce.y & kOdd) ? 1 : (ce.z & kOdd) ? 2 : (ce.w & kOdd) ? 3 : 4;
+  const uint32_t yb0 = b0 < 4 ? sel4(ce, b0) & kOdd : 0u;  // Y's cell ends in block b0
+  const bool rewalk = __popc(yb0) > 2;                      // rare: the merge re-walks block b0
+  Walk y{0.f, 0.f, 0};
+  Head h;
+  uint32_t xa[16], ya[16], xb[16], yb[16];
+  tmem_ld16(tbase, xa);
+  tmem_ld16(tbase + 64, ya);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t(&vx)[16] = (c & 1) ? xb : xa;
+    uint32_t(&vy)[16] = (c & 1) ? yb : ya;
+    uint32_t(&nx)[16] = (c & 1) ? xa : xb;
+    uint32_t(&ny)[16] = (c & 1) ? ya : yb;
+    tmem_ld_wait();
+    if (c < 3) {
+      tmem_ld16(tbase + 16 * (c + 1), nx);
+      tmem_ld16(tbase + 64 + 16 * (c + 1), ny);
+    } else if (rewalk) {
+      tmem_ld16(tbase + 64 + 16 * b0, nx);  // block b0's Y columns again, for the merge's re-walk (xa is free)
+    }
+    if (c == b0)
+      block<true>(c, vx, vy, sel4(ce, c), sel4(se, c), ys, b0, w, y, h, fl, pooled, f);
+    else
+      block<false>(c, vx, vy, sel4(ce, c), sel4(se, c), ys, b0, w, y, h, fl, pooled, f);
+  }
+  if (ys == 4) h.hc = y.c;
+  // merge: X's sum continues with Y's head blocks b0..ys in block order
+  if (b0 < 4) {
+    float pb0;
+    if (!rewalk) {
+      const bool one = (yb0 & (yb0 - 1)) == 0;
+      const float v = fmaxf(w.m, one ? h.last : h.prev);  // the cell open across row 64
+      pb0 = one ? v : v + h.last;
+    } else {  // re-walk block b0 (in xa) from the head cell's true running max
+      tmem_ld_wait();
+      float m = fmaxf(w.m, h.hm0);
+      pb0 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        m = fmaxf(m, __uint_as_float(xa[j]));
+        if ((yb0 >> (2 * j + 1)) & 1u) pb0 += m;
+        if ((yb0 >> (2 * j + 1)) & 1u) m = 0.f;
+      }
+    }
+    float s = w.s + pb0;
+    if (b0 < 1 && 1 <= ys) s += h.hp1;
+    if (b0 < 2 && 2 <= ys) s += h.hp2;
+    if (b0 < 3 && 3 <= ys) s += h.hp3;
+    const int cnt = w.c + h.hc;
+    if (ys < 4) {  // Y's first segment end closed X's segment
+      const int jy = (__ffs(sel4(se, ys) & kOdd) - 2) >> 1;
+      store_mean(pooled, fl[64 + 16 * ys + jy] >> kRowSegShift, f, s, cnt);
+      w = y;
+    } else {
+      w.s = s;
+      w.c = cnt;
+      w.m = y.m;  // the cell open after Y's last cell end
+    }
+  } else {
+    w.m = fmaxf(w.m, y.m);  // no cell ends in Y's rows: one cell continues through the part
+  }
 }
 
 // Flags phase: the ballot of warp eg over part p gives the interleaved masks of step eg when lane L

@@ -146,7 +146,7 @@ cudaError_t launch_scan(const int32_t* counts, int64_t G, int64_t* offsets, int6
 cudaError_t launch_crop_emit(const ShapeTable& T, const Batch& b, cudaStream_t st);
 cudaError_t launch_encoder_f32(const DevParams& P, const Batch& b, cudaStream_t st);
 cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b, int num_sms, cudaStream_t st,
-                              long long* trace = nullptr);
+                              long long* trace = nullptr, bool deterministic = false);
 cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_t* labels,
                         float* logits, float* emb, float* grad, cudaStream_t st);
 // NEXT-1 encode-once mode (kernels_cells.cu)
@@ -168,7 +168,7 @@ cudaError_t launch_cells_select(const ShapeTable& T, const CellsTable& C, const 
 cudaError_t launch_sim_set_t0(double* t0_dev, double t0, cudaStream_t st);
 cudaError_t launch_sim_prepare(const ShapeTable& T, const SimParams& sp, int E, const int32_t* ids, float* state,
                                const double* t0_dev, int n, int32_t* pairs, float* poses, uint8_t* culled,
-                               cudaStream_t st);
+                               unsigned long long* bad, cudaStream_t st);
 cudaError_t launch_sim_integrate(const SimParams& sp, int E, const float* body, float* state, const float* logits,
                                  const float* grad, const uint8_t* culled, int32_t* contacts, const double* t0_dev,
                                  int n, cudaStream_t st);
@@ -176,5 +176,14 @@ cudaError_t launch_head_tc(const DevParams& P, const Batch& b, float* probs, uin
                            float* emb, float* grad, int num_sms, cudaStream_t st);
 size_t scan_tmp_elems(int64_t G);
 size_t encoder_tc_smem_bytes();
+
+// Opts kernel `fn` into `bytes` of dynamic shared memory on the CURRENT device.  Function attributes
+// are per device, so this is done once per (device, kernel) and remembered (locc_runtime.cu); every
+// launcher with more than 48 KB calls it before its launch.
+cudaError_t smem_optin(const void* fn, size_t bytes);
+template <class K>
+cudaError_t smem_optin(K* fn, size_t bytes) {
+  return smem_optin(reinterpret_cast<const void*>(fn), bytes);
+}
 
 }  // namespace locc

@@ -416,8 +416,7 @@ __global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTa
 
 cudaError_t launch_grid_encode(const DevParams& P, const ShapeTable& T, int M, float* G, cudaStream_t st) {
   const size_t sm = sizeof(float4) * kMlpTR + sizeof(float) * 256 * kMlpLDH;
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(grid_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const cudaError_t attr = smem_optin(grid_encode_kernel, sm);
   if (attr != cudaSuccess) return attr;
   cudaError_t e = cudaMemsetAsync(G, 0, sizeof(float) * (size_t)T.S * M * M * M * P.H, st);
   if (e != cudaSuccess) return e;
@@ -483,8 +482,7 @@ cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, 
     conv3d_kernel<<<grid, 256, kCvSmem, st>>>(a);
     return cudaGetLastError();
   };
-  static const cudaError_t attr0 =
-      cudaFuncSetAttribute(conv3d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCvSmem);
+  const cudaError_t attr0 = smem_optin(conv3d_kernel, kCvSmem);
   if (attr0 != cudaSuccess) return attr0;
   cudaError_t e;
   if ((e = conv(G, H, nullptr, 0, M, D, 0, 0, c[0])) != cudaSuccess) return e;        // valid
@@ -496,8 +494,7 @@ cudaError_t launch_unet(const UNetParams& U, const ShapeTable& T, int M, int H, 
   if ((e = conv(d3, 128, c[1], 128, D, D, 1, 6, d2)) != cudaSuccess) return e;
   if ((e = conv(d2, 128, c[0], 128, D, M, 2, 7, d1)) != cudaSuccess) return e;      // transposed valid
   const size_t sm = sizeof(float) * ((size_t)F * 257 + 128 + F);
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(unet_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float) * (64 * 257 + 128 + 64)));
+  const cudaError_t attr = smem_optin(unet_tail_kernel, sizeof(float) * (64 * 257 + 128 + 64));
   if (attr != cudaSuccess) return attr;
   unet_tail_kernel<<<S, 256, sm, st>>>(U, T, M, F, global_max, c[3], d1, E, ctr);
   return cudaGetLastError();

@@ -267,8 +267,7 @@ __global__ void __launch_bounds__(192, 1) conv_tc_kernel(ConvTcArgs a) {
 cudaError_t launch_conv_tc(const float* x1, int C1, const float* x2, int C2, int Di, int Do, int pad, int S,
                            const uint8_t* img, const float* bias, float* y, int num_sms, cudaStream_t st) {
   const size_t sm = sizeof(ConvTcSmem) + 1024;
-  static const cudaError_t attr = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)(sizeof(ConvTcSmem) + 1024));
+  const cudaError_t attr = smem_optin(conv_tc_kernel, sizeof(ConvTcSmem) + 1024);
   if (attr != cudaSuccess) return attr;
   const int64_t rows = (int64_t)S * Do * Do * Do, ntiles = (rows + 255) / 256;
   const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
@@ -281,8 +280,7 @@ cudaError_t launch_gemm_tc(const float* x, int C, int64_t rows, const uint8_t* i
                            int ldy, int ycol, int num_sms, cudaStream_t st, const float4* pts, const float4* w1b) {
   if (rows == 0) return cudaSuccess;
   const size_t sm = sizeof(ConvTcSmem) + 1024;
-  static const cudaError_t attr = cudaFuncSetAttribute(conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                       (int)(sizeof(ConvTcSmem) + 1024));
+  const cudaError_t attr = smem_optin(conv_tc_kernel, sizeof(ConvTcSmem) + 1024);
   if (attr != cudaSuccess) return attr;
   const int64_t ntiles = (rows + 255) / 256;
   const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);

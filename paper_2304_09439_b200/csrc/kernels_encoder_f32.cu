@@ -90,8 +90,7 @@ cudaError_t launch_encoder_f32(const DevParams& P, const Batch& b, cudaStream_t 
   const int64_t chunks = (b.G + kSegPerChunk - 1) / kSegPerChunk;
   if (chunks == 0) return cudaSuccess;
   const size_t sm = sizeof(float4) * TR + sizeof(float) * (size_t)P.H * LDH;
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      encoder_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(float4) * TR + sizeof(float) * 256 * LDH));
+  const cudaError_t attr = smem_optin(encoder_f32_kernel, sizeof(float4) * TR + sizeof(float) * 256 * LDH);
   if (attr != cudaSuccess) return attr;
   encoder_f32_kernel<<<(unsigned)chunks, 256, sm, st>>>(P, b);
   return cudaGetLastError();

@@ -13,12 +13,13 @@
 //                                the first MMA of a half multiplies a column of ones with b2)
 //   epi L2 (TMEM -> regs)        h2 = ReLU(D2) -> bf16, written row-major (K-major) as the B operand
 //                                of L3 — each CTA keeps its own rows: no exchange
-//   L3 (tcgen05, TS)             D3[256 features x 128 rows] = W3 * h2^T, twice per tile (rows
-//                                0-127, 128-255); A = W3 resident in TMEM (each CTA 128 features),
-//                                B = h2 (each CTA 64 of the 128 rows)
+//   L3 (tcgen05, TS)             D3[256 features x 128 rows] = b3 * 1 + W3 * h2^T, twice per tile
+//                                (rows 0-127, 128-255); A = W3 resident in TMEM (each CTA 128
+//                                features), B = h2 (each CTA 64 of the 128 rows); the first MMA of a
+//                                part multiplies b3 (three bf16 terms, in the bias block) with ones
 //   epi L3 (TMEM -> regs)        thread = output feature, walking the rows in order: cell-wise max
-//                                (PAPER.md:331), g = ReLU(max + b3), running sum over occupied cells,
-//                                mean at the segment end — e3_walk.cuh
+//                                of ReLU(D3), sum over occupied cells in blocks of 16
+//                                rows, mean at the segment end — e3_walk.cuh
 //
 // Layer 2 is computed "rows x features" and layer 3 "features x rows" so that layer 2's epilogue
 // produces layer 3's operand in place and layer 3's epilogue sees each feature's rows in one
@@ -99,8 +100,10 @@ enum {
 
 struct alignas(1024) Smem {
   uint8_t w2[5 * 16384];  // B of L2: this CTA's 128 W2 rows, 4 K blocks x [128 rows x 128 B], SW128,
-                          // + a block whose K = 0..2 hold b2 split into three bf16 terms
-  uint8_t ones[1024];     // A of the bias MMA: one 8-row SW128 atom with K = 0..2 = 1 (all rows alike)
+                          // + a bias block: K = 0..2 of row i = b2 of L2 image row i, K = 16..18 of
+                          // row m = b3 of this CTA's feature m, each split into three bf16 terms
+  uint8_t ones[1024];     // the other operand of the bias MMAs: one 8-row SW128 atom with K = 0..2 and
+                          // K = 16..18 = 1 (all rows alike: SBO = 0)
   uint8_t h1[65536];  // A of L2: this CTA's 128 rows of h1, same layout
   uint8_t h2[65536];  // B of L3: this CTA's 128 rows of h2, same layout
   float px[2][128], py[2][128], pz[2][128];  // this CTA's rows of a tile (layer-1 input), double buffered
@@ -207,16 +210,17 @@ __device__ __forceinline__ uint32_t tile_row_of_local(uint32_t rank, uint32_t i)
 
 // Layer-3 MMAs of K chunk j (features 32j..32j+31, written by epi L2 as one chunk): K steps 2j, 2j+1.
 // A = W3 columns in TMEM (8 columns of bf16x2 per K step), B = h2 (+rowoff: descriptor offset of the
-// part's 64 rows); the part's first K step overwrites the accumulator.
+// part's 64 rows); they accumulate onto the part's bias MMA (D3 = b3 * 1).
 __device__ __forceinline__ void l3_chunk(uint32_t d3, uint32_t w3, uint64_t dH2, int j, uint32_t rowoff) {
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     const int k = 2 * j + s;
     const uint32_t koff = (k >> 2) * 1024 + (k & 3) * 2 + rowoff;
-    mma_ts_2cta(d3, w3 + 8 * k, dH2 + koff, kIdescN128, (j | s) != 0);
+    mma_ts_2cta(d3, w3 + 8 * k, dH2 + koff, kIdescN128, 1);
   }
 }
 
+template <bool kDet>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder_tc_kernel(const __grid_constant__ TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023));
@@ -251,8 +255,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     const uint32_t row = i >> 5, word = i & 31;
     const uint32_t chunk = (word >> 2) ^ row;  // logical 16-byte chunk of this physical word
     uint32_t v = 0;
-    if (chunk == 0 && (word & 3) == 0) v = 0x3F803F80u;  // K = 0, 1
-    if (chunk == 0 && (word & 3) == 1) v = 0x00003F80u;  // K = 2
+    if ((chunk == 0 || chunk == 2) && (word & 3) == 0) v = 0x3F803F80u;  // K = 0, 1 (16, 17)
+    if ((chunk == 0 || chunk == 2) && (word & 3) == 1) v = 0x00003F80u;  // K = 2 (18)
     reinterpret_cast<uint32_t*>(S.ones)[i] = v;
   }
   fence_proxy_async_smem();
@@ -383,6 +387,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         if (lane == 0) { trace_ev(a, rank, cid, it, 3); trace_issue(a, &S.issue_seq, cid); }
         tc_fence_after();
         if (elect_one()) {
+          // D3 = b3 (hi + mid + lo) for every row: K = 16..18 (+32 B) of the bias block and the ones atom
+          mma_ss_2cta(rp, dB2 + 2, dOne + 2, kIdescN128, 0);
 #pragma unroll
           for (int j = 0; j < 4; ++j) l3_chunk(rp, tmem + kColW3, dH2, j, 0);
           if (a.trace) mma_commit_2cta(&S.bar[B_PROBE + 2], 3);
@@ -392,6 +398,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           if (last_p1 >= 0) mbar_wait_spin(&S.bar[B_D3E1], last_p1 & 1);
           tc_fence_after();
           if (elect_one()) {
+            mma_ss_2cta(r3, dB2 + 2, dOne + 2, kIdescN128, 0);
 #pragma unroll
             for (int j = 0; j < 4; ++j) l3_chunk(r3, tmem + kColW3, dH2, j, 512);
           }
@@ -573,8 +580,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     const uint32_t q = warp & 3;
     const uint32_t eg = warp - kWarpE3;  // 0..3: flags of rows 32eg.. and the masks of step eg
     const uint32_t f = 128 * rank + 32 * q + lane;
-    const float b3 = a.b3[f], nb3 = -b3;
-    Walk w{nb3, 0.f, 0};
+    Walk w{0.f, 0.f, 0};
     TileIter iter(a, (int)cid, (int)ncl);
     int64_t row0;
     int nrows;
@@ -582,7 +588,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     uint32_t it = 0, c0 = 0, c1 = 0;
     Regions R;
     while (iter.next(row0, nrows, first)) {
-      if (first) w.m = nb3;  // drop padding rows after the previous chunk's last segment end
+      if (first) w.m = 0.f;  // drop padding rows after the previous chunk's last segment end
       asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's flags no longer read
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -604,8 +610,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         group_wait<1, 128, LOCC_SPIN_E3>(&S.bar[p ? B_D3F1 : B_D3F0], (p ? c1 : c0) & 1, warp == kWarpE3);
         if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 12 + 2 * p);
         tc_fence_after();
-        e3_part2(tmem + ((32 * q) << 16) + region_col(p ? kRegionP1 : R.P), S.masks + 8 * p, S.flags + 128 * p, w, nb3, b3,
-                 a.pooled, f);
+        const uint32_t tb = tmem + ((32 * q) << 16) + region_col(p ? kRegionP1 : R.P);
+        if (kDet)
+          e3_part2_det(tb, S.masks + 8 * p, S.flags + 128 * p, w, a.pooled, f);
+        else
+          e3_part2(tb, S.masks + 8 * p, S.flags + 128 * p, w, a.pooled, f);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&S.bar[p ? B_D3E1 : B_D3E0], 0);
@@ -629,7 +638,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
 size_t encoder_tc_smem_bytes() { return sizeof(Smem) + 1024; }
 
 cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b, int num_sms, cudaStream_t st,
-                              long long* trace) {
+                              long long* trace, bool deterministic) {
   const int spc = 16;
   const int64_t chunks = (b.G + spc - 1) / spc;
   if (chunks == 0) return cudaSuccess;
@@ -651,13 +660,16 @@ cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b
   args.seg_per_chunk = spc;
   args.trace = trace;
   const size_t smem = encoder_tc_smem_bytes();
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(encoder_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const cudaError_t attr = deterministic ? smem_optin(encoder_tc_kernel<true>, smem)
+                                         : smem_optin(encoder_tc_kernel<false>, smem);
   if (attr != cudaSuccess) return attr;
   int grid = (num_sms / 2) * 2;
   const int64_t max_useful = 2 * chunks;
   if (grid > max_useful) grid = (int)max_useful;
-  encoder_tc_kernel<<<grid, kThreads, smem, st>>>(args);
+  if (deterministic)
+    encoder_tc_kernel<true><<<grid, kThreads, smem, st>>>(args);
+  else
+    encoder_tc_kernel<false><<<grid, kThreads, smem, st>>>(args);
   return cudaGetLastError();
 }
 

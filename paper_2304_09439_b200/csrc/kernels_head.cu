@@ -508,15 +508,12 @@ cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_
   if (b.B == 0) return cudaSuccess;
   if (P.H == 256 && P.F == 64) {
     const unsigned grid = (unsigned)((b.B + kTP - 1) / kTP);
-    static const cudaError_t attr = [] {  // once per process
-      const int g = (int)sizeof(HeadGradSmem), f = (int)sizeof(HeadSmem);
-      cudaError_t e = cudaFuncSetAttribute(head_tile_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, g);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(head_tile_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, g);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(head_tile_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, f);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(head_tile_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, f);
+    const cudaError_t attr = [] {  // once per (device, kernel), see smem_optin
+      const size_t g = sizeof(HeadGradSmem), f = sizeof(HeadSmem);
+      cudaError_t e = smem_optin(head_tile_kernel<true, true>, g);
+      if (e == cudaSuccess) e = smem_optin(head_tile_kernel<true, false>, g);
+      if (e == cudaSuccess) e = smem_optin(head_tile_kernel<false, true>, f);
+      if (e == cudaSuccess) e = smem_optin(head_tile_kernel<false, false>, f);
       return e;
     }();
     if (attr != cudaSuccess) return attr;
@@ -532,8 +529,7 @@ cudaError_t launch_head(const DevParams& P, const Batch& b, float* probs, uint8_
   }
   if (grad) return cudaErrorNotSupported;  // the pose gradient is built for H = 256, F = 64
   const size_t sm = sizeof(float) * (size_t)(256 + 128 + P.F + 7) * LD;
-  static const cudaError_t attr2 = cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                        (int)(sizeof(float) * (256 + 128 + 256 + 7) * LD));
+  const cudaError_t attr2 = smem_optin(head_kernel, sizeof(float) * (256 + 128 + 256 + 7) * LD);
   if (attr2 != cudaSuccess) return attr2;
   head_kernel<<<(unsigned)((b.B + PB - 1) / PB), 128, sm, st>>>(P, b, probs, labels, logits, emb);
   return cudaGetLastError();

@@ -477,15 +477,12 @@ cudaError_t launch_head_tc(const DevParams& P, const Batch& b, float* probs, uin
   const int64_t ntiles = (b.B + kHP - 1) / kHP;
   const unsigned grid = (unsigned)(ntiles < num_sms ? ntiles : num_sms);
   const int threads = grad ? 192 : 320;
-  static const cudaError_t attr = [] {  // once per process (not inside a stream capture's replay path)
-    const int sm = (int)head_tc_smem_bytes();
-    cudaError_t e = cudaFuncSetAttribute(head_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(head_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(head_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(head_tc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  const cudaError_t attr = [] {  // once per (device, kernel), see smem_optin
+    const size_t sm = head_tc_smem_bytes();
+    cudaError_t e = smem_optin(head_tc_kernel<true, true>, sm);
+    if (e == cudaSuccess) e = smem_optin(head_tc_kernel<true, false>, sm);
+    if (e == cudaSuccess) e = smem_optin(head_tc_kernel<false, true>, sm);
+    if (e == cudaSuccess) e = smem_optin(head_tc_kernel<false, false>, sm);
     return e;
   }();
   if (attr != cudaSuccess) return attr;

@@ -57,12 +57,27 @@ __global__ void __launch_bounds__(128) sim_prepare_kernel(ShapeTable T, SimParam
                                                           const int32_t* __restrict__ ids, float* __restrict__ state,
                                                           const double* __restrict__ t0_dev, int n,
                                                           int32_t* __restrict__ pairs,
-                                                          float* __restrict__ poses, uint8_t* __restrict__ culled) {
+                                                          float* __restrict__ poses, uint8_t* __restrict__ culled,
+                                                          unsigned long long* __restrict__ bad) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   const double tau = *t0_dev + n * sp.hd;
   float* st = state + (int64_t)e * 39;
   set_bowl(sp, st, tau);
+  // a body id outside the shape table: count it and cull the environment's pairs (the query then only
+  // sees in-range ids; locc_sim_run reports the count in its synchronous form)
+  bool ok = true;
+  for (int b = 0; b < 3; ++b) ok &= (unsigned)ids[3 * e + b] < (unsigned)T.S;
+  if (!ok) {
+    atomicAdd(bad, 1ull);
+    for (int p = 0; p < 3; ++p) {
+      const int64_t i = 3 * (int64_t)e + p;
+      pairs[2 * i] = pairs[2 * i + 1] = 0;
+      for (int j = 0; j < 14; ++j) poses[14 * i + j] = (j % 7) == 0 ? 1.f : 0.f;
+      culled[i] = 1;
+    }
+    return;
+  }
   float cw[3][3], hw[3][3];
   for (int b = 0; b < 3; ++b) {  // world AABB of every body: centre R c + t, half-extent |R| e
     const int sid = ids[3 * e + b];
@@ -164,9 +179,9 @@ cudaError_t launch_sim_set_t0(double* t0_dev, double t0, cudaStream_t st) {
 
 cudaError_t launch_sim_prepare(const ShapeTable& T, const SimParams& sp, int E, const int32_t* ids, float* state,
                                const double* t0_dev, int n, int32_t* pairs, float* poses, uint8_t* culled,
-                               cudaStream_t st) {
+                               unsigned long long* bad, cudaStream_t st) {
   if (E == 0) return cudaSuccess;
-  sim_prepare_kernel<<<(E + 127) / 128, 128, 0, st>>>(T, sp, E, ids, state, t0_dev, n, pairs, poses, culled);
+  sim_prepare_kernel<<<(E + 127) / 128, 128, 0, st>>>(T, sp, E, ids, state, t0_dev, n, pairs, poses, culled, bad);
   return cudaGetLastError();
 }
 

@@ -8,21 +8,42 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <map>
+#include <mutex>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
+
+#include <dlfcn.h>
+#include <nccl.h>  // types and enums only: NCCL is loaded at run time (dlopen), never linked
 
 #include "../../include/locc.h"
 #include "internal.h"
 #include "tc_ptx.cuh"
 
 using namespace locc;
+
+cudaError_t locc::smem_optin(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;  // (device, kernel) -> bytes set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{dev, fn}];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
 
 struct locc_ctx;
 locc_status locc_upload_tc_weights(locc_ctx* c, const float* flat);
@@ -50,6 +71,10 @@ locc_status fail(locc_status s, const char* fmt, ...) {
     }                                                                                                \
   } while (0)
 
+// Bumped whenever any device buffer is (re)allocated: a captured CUDA graph holds raw pointers into
+// the scratch buffers, so it is valid only while this epoch is unchanged (locc_sim_run's key).
+std::atomic<uint64_t> g_alloc_epoch{0};
+
 struct DevBuf {
   void* p = nullptr;
   size_t n = 0;
@@ -58,6 +83,7 @@ struct DevBuf {
   }
   cudaError_t ensure(size_t bytes) {
     if (bytes <= n && p) return cudaSuccess;
+    ++g_alloc_epoch;
     if (p) cudaFree(p);
     p = nullptr;
     n = 0;
@@ -102,6 +128,7 @@ struct locc_ctx {
   std::vector<cudaEvent_t> head_ev;  // per sub-batch predictor stop (its start = the encoder stop)
   std::vector<cudaEvent_t> crop_ev;  // per sub-batch crop start (its stop = the encoder start)
   bool timing = false;
+  bool deterministic = false;  // bf16 encoder: the deterministic layer-3 walk (locc_set_deterministic)
   bool has_weights = false, has_shapes = false;
   // parameters
   DevBuf params, tc_img, head_tc_img, grid_tc_img;
@@ -130,7 +157,7 @@ struct locc_ctx {
   double encode_ms = 0.0;  // device time of the last locc_encode_shapes
   // NEXT-3 closed-loop scratch
   int64_t sim_cap = 0;
-  DevBuf sim_pairs, sim_poses, sim_probs, sim_logits, sim_grad, sim_culled, sim_t0;
+  DevBuf sim_pairs, sim_poses, sim_probs, sim_logits, sim_grad, sim_culled, sim_t0, sim_bad;
   // CUDA graph of one locc_sim_run's substeps, replayed while its inputs are unchanged
   uint64_t generation = 1;  // bumped by every call that changes weights, shapes, grids or precision
   struct SimKey {
@@ -138,10 +165,22 @@ struct locc_ctx {
     int32_t E;
     const void *ids, *body, *state, *contacts, *stream;
     uint64_t gen;
+    uint64_t alloc_epoch;  // g_alloc_epoch: no scratch buffer the graph points into was reallocated
   } sim_key{};
   int sim_seen = 0;  // calls with sim_key so far (capture on the second)
   int64_t sim_launches = 0;  // kernels inside the captured graph
   cudaGraphExec_t sim_exec = nullptr;
+  // multi-device group (locc_config.n_devices > 1): one single-device sub-context per device; this
+  // context's own device is the home device (device_ids[0]) and its state is only the fan-out
+  std::vector<locc_ctx*> kids;
+  std::vector<char> kid_direct;  // kid i's kernels may address the home device's memory (peer access)
+  static constexpr int kGrpBufs = 12;
+  DevBuf grp_buf[kGrpBufs];      // this kid's staged shard buffers (no peer access)
+  cudaEvent_t grp_ev = nullptr;  // this kid's "shard done" event (recorded on its stream)
+  // multi-process communicator (locc_comm_init): ncclComm_t, world size, rank
+  void* nccl_comm = nullptr;
+  int world = 1, rank = 0;
+  DevBuf ag_out[3];  // device staging of host outputs of locc_query_allgather
 };
 
 namespace {
@@ -606,7 +645,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
         CK(cudaMemsetAsync(c->trace.p, 0, sizeof(long long) * 3 * 64 * 16, st));
         trace = c->trace.as<long long>();
       }
-      CK(launch_encoder_tc(c->P, c->tc_l1, b, c->num_sms, st, trace));
+      CK(launch_encoder_tc(c->P, c->tc_l1, b, c->num_sms, st, trace, c->deterministic));
       if (trace) {
         std::vector<long long> h(3 * 64 * 16);
         CK(cudaMemcpyAsync(h.data(), trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
@@ -677,6 +716,250 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
   return LOCC_OK;
 }
 
+
+// ---------------------------------------------------------------- multi-device groups (n_devices > 1)
+// A shard's view of one caller buffer: base pointer, bytes per pair (or environment), and whether the
+// shard reads it (in) and/or writes it (out).
+struct Slice {
+  const void* base;
+  size_t unit;
+  bool in, out;
+};
+
+bool is_group(const locc_ctx* c) { return c && !c->kids.empty(); }
+
+int pointer_device(const void* p) {
+  cudaPointerAttributes a;
+  if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? a.device : -1;
+}
+
+// Runs fn(kid, ptrs, n, stream) on every device's contiguous shard of N units: [g ceil(N/G), ...).
+// Host buffers: one host thread per device, each a synchronous shard call (stream = NULL).  Device
+// buffers (home device): every kid stream waits for the caller's stream, reads its inputs and writes
+// its outputs in place (peer access, `direct`) or through peer copies of its slices, and the caller's
+// stream waits for every kid; stream == NULL makes the whole call synchronous, after which `check`
+// validates every kid (device-side input errors).
+template <class Fn, class Check>
+locc_status group_run(locc_ctx* c, int64_t N, const Slice* sl, int nsl, bool dev, void* stream, bool allow_direct,
+                      Fn fn, Check check) {
+  const int G = (int)c->kids.size();
+  const int64_t per = (N + G - 1) / G;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  locc_status res = LOCC_OK;
+  if (!dev) {
+    std::vector<std::thread> th;
+    std::vector<locc_status> st(G, LOCC_OK);
+    std::vector<std::string> msg(G);
+    for (int g = 0; g < G; ++g) {
+      const int64_t lo = std::min<int64_t>(N, g * per), hi = std::min<int64_t>(N, lo + per);
+      if (hi <= lo) continue;
+      th.emplace_back([&, g, lo, hi] {
+        void* p[locc_ctx::kGrpBufs] = {};
+        for (int i = 0; i < nsl; ++i)
+          p[i] = sl[i].base ? (void*)(static_cast<const char*>(sl[i].base) + lo * sl[i].unit) : nullptr;
+        st[g] = fn(c->kids[g], p, hi - lo, nullptr);
+        if (st[g] != LOCC_OK) msg[g] = g_err;
+      });
+    }
+    for (auto& t : th) t.join();
+    for (int g = 0; g < G && res == LOCC_OK; ++g)
+      if (st[g] != LOCC_OK) {
+        res = st[g];
+        g_err = "device " + std::to_string(c->kids[g]->device) + ": " + msg[g];
+      }
+    cudaSetDevice(cur);
+    return res;
+  }
+  CK(cudaSetDevice(c->device));
+  cudaStream_t hs = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  CK(cudaEventRecord(c->ev_q0, hs));
+  for (int g = 0; g < G && res == LOCC_OK; ++g) {
+    locc_ctx* k = c->kids[g];
+    const int64_t lo = std::min<int64_t>(N, g * per), hi = std::min<int64_t>(N, lo + per), n = hi - lo;
+    if (n <= 0) continue;
+    const bool direct = k->device == c->device || (allow_direct && c->kid_direct[g]);
+    CK(cudaSetDevice(k->device));
+    CK(cudaStreamWaitEvent(k->stream, c->ev_q0, 0));
+    void* p[locc_ctx::kGrpBufs] = {};
+    for (int i = 0; i < nsl; ++i) {
+      if (!sl[i].base) continue;
+      char* at = const_cast<char*>(static_cast<const char*>(sl[i].base)) + lo * sl[i].unit;
+      if (direct) {
+        p[i] = at;
+        continue;
+      }
+      CK(k->grp_buf[i].ensure(n * sl[i].unit));
+      p[i] = k->grp_buf[i].p;
+      if (sl[i].in) CK(cudaMemcpyPeerAsync(p[i], k->device, at, c->device, n * sl[i].unit, k->stream));
+    }
+    res = fn(k, p, n, k->stream);
+    if (res != LOCC_OK) break;
+    if (!direct)
+      for (int i = 0; i < nsl; ++i)
+        if (sl[i].base && sl[i].out)
+          CK(cudaMemcpyPeerAsync(const_cast<char*>(static_cast<const char*>(sl[i].base)) + lo * sl[i].unit,
+                                 c->device, p[i], k->device, n * sl[i].unit, k->stream));
+    CK(cudaEventRecord(k->grp_ev, k->stream));
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamWaitEvent(hs, k->grp_ev, 0));
+  }
+  if (res == LOCC_OK && !stream) {
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(hs));
+    for (int g = 0; g < G && res == LOCC_OK; ++g) {
+      const int64_t lo = std::min<int64_t>(N, g * per), hi = std::min<int64_t>(N, lo + per);
+      if (hi > lo) res = check(c->kids[g]);
+    }
+  }
+  cudaSetDevice(cur);
+  return res;
+}
+
+// After a synchronous group call: the kid's device counters (and input validation) of its shard.
+locc_status kid_query_check(locc_ctx* k) {
+  CK(cudaSetDevice(k->device));
+  DevStats hs;
+  CK(cudaMemcpy(&hs, k->stats.p, sizeof hs, cudaMemcpyDeviceToHost));
+  k->last.kept_rows = (int64_t)hs.kept_rows;
+  k->last.nonempty_sides = (int64_t)hs.nonempty_sides;
+  k->last.evaluated_pairs = (int64_t)hs.evaluated_pairs;
+  locc_status ts = read_timing(k);
+  if (ts != LOCC_OK) return ts;
+  if (hs.bad_input)
+    return fail(LOCC_E_INVALID_ARG, "device %d: %llu segments had an out-of-range id or invalid pose", k->device,
+                (unsigned long long)hs.bad_input);
+  return LOCC_OK;
+}
+
+locc_status kid_sim_check(locc_ctx* k) {
+  CK(cudaSetDevice(k->device));
+  unsigned long long bad = 0;
+  CK(cudaMemcpy(&bad, k->sim_bad.p, sizeof bad, cudaMemcpyDeviceToHost));
+  if (bad) return fail(LOCC_E_INVALID_ARG, "device %d: %llu environment substeps had a body id outside [0, S)",
+                       k->device, bad);
+  return LOCC_OK;
+}
+
+// A query of any kind over the group's devices (run_query's arguments, sharded by pair).
+locc_status group_query(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
+                        uint8_t* labels, float* logits, int32_t* kept, int32_t* occ, uint32_t* masks, float* emb,
+                        float* grad, void* stream, bool cells) {
+  if (N < 0) return fail(LOCC_E_INVALID_ARG, "N < 0");
+  if (N == 0) return LOCC_OK;
+  if (!pairs || !poses || !probs) return fail(LOCC_E_INVALID_ARG, "pairs, poses and probs must be non-null");
+  const int home_dev = pointer_device(pairs);
+  const bool dev = home_dev >= 0;
+  const void* all[] = {poses, probs, labels, logits, kept, occ, masks, emb, grad};
+  for (const void* p : all)
+    if (p && pointer_device(p) != home_dev)
+      return fail(LOCC_E_INVALID_ARG, "all buffers of one call must be host memory or all on the home device");
+  if (dev && home_dev != c->device)
+    return fail(LOCC_E_INVALID_ARG, "device buffers must be on the home device %d (got %d)", c->device, home_dev);
+  const locc_ctx* k0 = c->kids[0];
+  const int ncell = c->cfg.M * c->cfg.M * c->cfg.M;
+  const size_t words = cells ? (ncell + 31) / 32 : (k0->T.K + 31) / 32;
+  const Slice sl[] = {{pairs, 8, true, false},           {poses, 56, true, false},
+                      {probs, 4, false, true},           {labels, 1, false, true},
+                      {logits, 4, false, true},          {kept, 8, false, true},
+                      {occ, 8, false, true},             {masks, 8 * words, false, true},
+                      {emb, 8 * (size_t)c->cfg.F, false, true}, {grad, 56, false, true}};
+  // debug outputs are zeroed with memsets on the kid's stream: those go through the kid's own buffers
+  const bool allow_direct = !kept && !occ && !masks && !emb;
+  return group_run(
+      c, N, sl, 10, dev, stream, allow_direct,
+      [&](locc_ctx* k, void** p, int64_t n, void* st) {
+        return run_query(k, (const int32_t*)p[0], (const float*)p[1], n, (float*)p[2], (uint8_t*)p[3],
+                         (float*)p[4], (int32_t*)p[5], (int32_t*)p[6], (uint32_t*)p[7], (float*)p[8], (float*)p[9],
+                         st, cells);
+      },
+      kid_query_check);
+}
+
+// Fan-out of a per-context call to every kid (first error wins).
+template <class Fn>
+locc_status fan_out(locc_ctx* c, Fn fn) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  locc_status s = LOCC_OK;
+  for (locc_ctx* k : c->kids)
+    if ((s = fn(k)) != LOCC_OK) break;
+  cudaSetDevice(cur);
+  return s;
+}
+
+// ---------------------------------------------------------------- NCCL (loaded at run time)
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    // prefer a copy already in the process (PyTorch's), else the loader's search path
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char* e = dlerror();
+      a.why = std::string("dlopen libnccl.so.2: ") + (e ? e : "not found");
+      return a;
+    }
+    bool all = true;
+    auto sym = [&](auto& f, const char* name) {
+      f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, name));
+      all &= f != nullptr;
+    };
+    sym(a.GetUniqueId, "ncclGetUniqueId");
+    sym(a.CommInitRank, "ncclCommInitRank");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    sym(a.Broadcast, "ncclBroadcast");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    sym(a.GetErrorString, "ncclGetErrorString");
+    a.ok = all;
+    if (!all) a.why = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+#define NK(call)                                                                                    \
+  do {                                                                                              \
+    ncclResult_t r_ = (call);                                                                       \
+    if (r_ != ncclSuccess)                                                                          \
+      return fail(LOCC_E_NCCL, "%s: %s (%s:%d)", #call, nccl().GetErrorString(r_), __FILE__, __LINE__); \
+  } while (0)
+
+// Every rank's shard [lo_q, hi_q) of the global arrays, broadcast in place from rank q to all ranks.
+locc_status allgather_slices(locc_ctx* c, int64_t N, float* probs, uint8_t* labels, float* logits, cudaStream_t st) {
+  const NcclApi& A = nccl();
+  ncclComm_t comm = static_cast<ncclComm_t>(c->nccl_comm);
+  const int64_t per = (N + c->world - 1) / c->world;
+  NK(A.GroupStart());
+  for (int q = 0; q < c->world; ++q) {
+    const int64_t lo = std::min<int64_t>(N, q * per), n = std::min<int64_t>(N, lo + per) - lo;
+    if (n <= 0) continue;
+    NK(A.Broadcast(probs + lo, probs + lo, (size_t)n, ncclFloat32, q, comm, st));
+    if (labels) NK(A.Broadcast(labels + lo, labels + lo, (size_t)n, ncclUint8, q, comm, st));
+    if (logits) NK(A.Broadcast(logits + lo, logits + lo, (size_t)n, ncclFloat32, q, comm, st));
+  }
+  NK(A.GroupEnd());
+  return LOCC_OK;
+}
+
 bool read_file(const std::string& path, std::vector<char>& out) {
   std::ifstream f(path, std::ios::binary);
   if (!f) return false;
@@ -717,6 +1000,50 @@ locc_status locc_create(const locc_config* cfg, locc_ctx** out) {
   if (cfg->precision == LOCC_PREC_BF16 && cfg->H != 256)
     return fail(LOCC_E_INVALID_ARG, "the tensor-core encoder is built for H = 256");
   if (cfg->max_batch < 0) return fail(LOCC_E_INVALID_ARG, "max_batch < 0");
+  if (cfg->n_devices < 0 || cfg->n_devices > 64) return fail(LOCC_E_INVALID_ARG, "n_devices must be in [0, 64]");
+  if (cfg->n_devices > 1) {
+    // a group: the home context (streams and events on device_ids[0]) plus one sub-context per device
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    std::vector<int> ids(cfg->n_devices);
+    for (int i = 0; i < cfg->n_devices; ++i) {
+      ids[i] = cfg->device_ids ? cfg->device_ids[i] : i;
+      if (ids[i] < 0 || ids[i] >= ndev) return fail(LOCC_E_INVALID_ARG, "device_ids[%d] = %d of %d devices", i, ids[i], ndev);
+    }
+    locc_config one = *cfg;
+    one.n_devices = 0;
+    one.device_ids = nullptr;
+    one.device = ids[0];
+    locc_ctx* g = nullptr;
+    locc_status s = locc_create(&one, &g);
+    if (s != LOCC_OK) return s;
+    for (int i = 0; i < cfg->n_devices; ++i) {
+      one.device = ids[i];
+      locc_ctx* k = nullptr;
+      s = locc_create(&one, &k);
+      if (s == LOCC_OK && cudaEventCreateWithFlags(&k->grp_ev, cudaEventDisableTiming) != cudaSuccess)
+        s = fail(LOCC_E_CUDA, "event creation on device %d", ids[i]);
+      if (k) {
+        g->kids.push_back(k);
+        int can = 0;
+        if (ids[i] != ids[0] && cudaDeviceCanAccessPeer(&can, ids[i], ids[0]) == cudaSuccess && can) {
+          cudaSetDevice(ids[i]);
+          const cudaError_t e = cudaDeviceEnablePeerAccess(ids[0], 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) can = 0;
+          cudaGetLastError();
+        }
+        g->kid_direct.push_back((char)(ids[i] == ids[0] || can));
+      }
+      if (s != LOCC_OK) {
+        locc_destroy(g);
+        return s;
+      }
+    }
+    g->cfg.n_devices = cfg->n_devices;
+    cudaSetDevice(ids[0]);
+    *out = g;
+    return LOCC_OK;
+  }
   int dev = cfg->device;
   if (dev < 0) CK(cudaGetDevice(&dev));
   int ndev = 0;
@@ -726,6 +1053,7 @@ locc_status locc_create(const locc_config* cfg, locc_ctx** out) {
   locc_ctx* c = new (std::nothrow) locc_ctx();
   if (!c) return fail(LOCC_E_OOM, "host allocation");
   c->cfg = *cfg;
+  c->cfg.device_ids = nullptr;  // not owned (the group keeps its sub-contexts instead)
   c->device = dev;
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) c->num_sms = prop.multiProcessorCount;
@@ -754,7 +1082,11 @@ locc_status locc_create(const locc_config* cfg, locc_ctx** out) {
 
 void locc_destroy(locc_ctx* c) {
   if (!c) return;
+  for (locc_ctx* k : c->kids) locc_destroy(k);
+  c->kids.clear();
+  if (c->nccl_comm && nccl().ok) nccl().CommDestroy(static_cast<ncclComm_t>(c->nccl_comm));
   cudaSetDevice(c->device);
+  if (c->grp_ev) cudaEventDestroy(c->grp_ev);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   for (auto& e : c->ev)
@@ -791,19 +1123,52 @@ locc_status locc_set_precision(locc_ctx* c, int32_t precision) {
     return fail(LOCC_E_INVALID_ARG, "unknown precision %d", precision);
   if (precision == LOCC_PREC_BF16 && c->cfg.H != 256)
     return fail(LOCC_E_INVALID_ARG, "the tensor-core encoder is built for H = 256");
+  if (is_group(c)) {
+    locc_status s = fan_out(c, [&](locc_ctx* k) { return locc_set_precision(k, precision); });
+    if (s != LOCC_OK) return s;
+  }
   c->cfg.precision = precision;
   ++c->generation;
+  return LOCC_OK;
+}
+
+locc_status locc_set_deterministic(locc_ctx* c, int32_t enabled) {
+  if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
+  if (c->deterministic != (enabled != 0)) ++c->generation;  // a captured sim graph holds the kernel choice
+  c->deterministic = enabled != 0;
+  if (is_group(c)) return fan_out(c, [&](locc_ctx* k) { return locc_set_deterministic(k, enabled); });
   return LOCC_OK;
 }
 
 locc_status locc_set_timing(locc_ctx* c, int32_t enabled) {
   if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
   c->timing = enabled != 0;
+  if (is_group(c)) return fan_out(c, [&](locc_ctx* k) { return locc_set_timing(k, enabled); });
   return LOCC_OK;
 }
 
 locc_status locc_get_stats(locc_ctx* c, locc_stats* out) {
   if (!c || !out) return fail(LOCC_E_INVALID_ARG, "null argument");
+  if (is_group(c)) {  // counts summed over the devices' shards, times the slowest device's
+    locc_stats a{};
+    locc_status s = fan_out(c, [&](locc_ctx* k) {
+      locc_stats ks{};
+      locc_status r = locc_get_stats(k, &ks);
+      a.pairs += ks.pairs;
+      a.evaluated_pairs += ks.evaluated_pairs;
+      a.kept_rows += ks.kept_rows;
+      a.nonempty_sides += ks.nonempty_sides;
+      a.sub_batches += ks.sub_batches;
+      a.kernel_launches += ks.kernel_launches;
+      a.encoder_ms = std::max(a.encoder_ms, ks.encoder_ms);
+      a.total_ms = std::max(a.total_ms, ks.total_ms);
+      a.head_ms = std::max(a.head_ms, ks.head_ms);
+      a.crop_ms = std::max(a.crop_ms, ks.crop_ms);
+      return r;
+    });
+    *out = a;
+    return s;
+  }
   if (c->last.pairs > 0 && c->last.kept_rows == 0 && c->last.evaluated_pairs == 0) {
     // asynchronous query: read the device counters now
     CK(cudaSetDevice(c->device));
@@ -827,6 +1192,12 @@ locc_status locc_load_weights_mem(locc_ctx* c, const float* flat, size_t n) {
     return fail(LOCC_E_WEIGHTS, "expected %lld floats for H=%d F=%d, got %zu", (long long)want, c->cfg.H, c->cfg.F, n);
   for (size_t i = 0; i < n; ++i)
     if (!std::isfinite(flat[i])) return fail(LOCC_E_WEIGHTS, "non-finite parameter at %zu", i);
+  if (is_group(c)) {
+    locc_status s = fan_out(c, [&](locc_ctx* k) { return locc_load_weights_mem(k, flat, n); });
+    c->has_weights = s == LOCC_OK;
+    c->has_cells = false;
+    return s;
+  }
   CK(cudaSetDevice(c->device));
   c->has_cells = false;  // the cached grids depend on the encoder weights
   ++c->generation;
@@ -882,8 +1253,23 @@ locc_status locc_set_shapes(locc_ctx* c, const float* points, int32_t S, int32_t
   if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
   if (!points) return fail(LOCC_E_INVALID_ARG, "null points");
   if (S < 1 || K < 1 || K > 65535) return fail(LOCC_E_SHAPE, "need S >= 1 and 1 <= K <= 65535 (S=%d K=%d)", S, K);
-  CK(cudaSetDevice(c->device));
   const size_t n = (size_t)S * K * 3;
+  if (is_group(c)) {  // every device gets its own copy of the table (a device pointer is read back once)
+    std::vector<float> host;
+    const float* src = points;
+    if (is_device_ptr(points)) {
+      host.resize(n);
+      CK(cudaMemcpy(host.data(), points, n * sizeof(float), cudaMemcpyDeviceToHost));
+      src = host.data();
+    }
+    locc_status s = fan_out(c, [&](locc_ctx* k) { return locc_set_shapes(k, src, S, K); });
+    c->has_shapes = s == LOCC_OK;
+    c->has_cells = false;
+    c->T.S = S;
+    c->T.K = K;
+    return s;
+  }
+  CK(cudaSetDevice(c->device));
   DevBuf tmp, cell, bad;
   const float* src = points;
   if (!is_device_ptr(points)) {
@@ -922,18 +1308,25 @@ locc_status locc_set_shapes(locc_ctx* c, const float* points, int32_t S, int32_t
 
 locc_status locc_query(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
                        uint8_t* labels, float* logits, void* stream) {
+  if (is_group(c))
+    return group_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, nullptr, stream,
+                       false);
   return run_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
 }
 
 locc_status locc_query_debug(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
                              uint8_t* labels, float* logits, int32_t* kept, int32_t* occ, uint32_t* masks,
                              float* emb, void* stream) {
+  if (is_group(c))
+    return group_query(c, pairs, poses, N, probs, labels, logits, kept, occ, masks, emb, nullptr, stream, false);
   return run_query(c, pairs, poses, N, probs, labels, logits, kept, occ, masks, emb, nullptr, stream);
 }
 
 locc_status locc_query_grad(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
                             uint8_t* labels, float* logits, float* grad, void* stream) {
   if (N > 0 && !grad) return fail(LOCC_E_INVALID_ARG, "grad must be non-null");
+  if (is_group(c))
+    return group_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, grad, stream, false);
   return run_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, grad, stream);
 }
 
@@ -951,6 +1344,12 @@ locc_status locc_load_unet_weights_mem(locc_ctx* c, const float* flat, size_t n)
     return fail(LOCC_E_WEIGHTS, "expected %lld U-Net floats for H=%d F=%d, got %zu", (long long)want, H, F, n);
   for (size_t i = 0; i < n; ++i)
     if (!std::isfinite(flat[i])) return fail(LOCC_E_WEIGHTS, "non-finite U-Net parameter at %zu", i);
+  if (is_group(c)) {
+    locc_status s = fan_out(c, [&](locc_ctx* k) { return locc_load_unet_weights_mem(k, flat, n); });
+    c->has_unet = s == LOCC_OK;
+    c->has_cells = false;
+    return s;
+  }
   CK(cudaSetDevice(c->device));
   // Wt[l][k][i][o] = W[o][i][k] for the convs; the deconvs as the equivalent conv: taps flipped (26 - k)
   const int cin[8] = {H, C, C, C, C, 2 * C, 2 * C, 2 * C};
@@ -1019,6 +1418,12 @@ locc_status locc_load_unet_weights_mem(locc_ctx* c, const float* flat, size_t n)
 locc_status locc_set_unet_global_pool(locc_ctx* c, int32_t mode) {
   if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
   if (mode != 0 && mode != 1) return fail(LOCC_E_INVALID_ARG, "global pool mode must be 0 (average) or 1 (max)");
+  if (is_group(c)) {
+    locc_status s = fan_out(c, [&](locc_ctx* k) { return locc_set_unet_global_pool(k, mode); });
+    if (s == LOCC_OK && c->unet_global_max != mode) c->has_cells = false;
+    c->unet_global_max = mode;
+    return s;
+  }
   if (c->unet_global_max != mode) {
     c->unet_global_max = mode;
     c->has_cells = false;  // the grids must be re-encoded
@@ -1029,6 +1434,28 @@ locc_status locc_set_unet_global_pool(locc_ctx* c, int32_t mode) {
 
 locc_status locc_encode_shapes(locc_ctx* c) {
   if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
+  if (is_group(c)) {  // every device encodes its own copy of the table, concurrently
+    std::vector<std::thread> th;
+    std::vector<locc_status> st(c->kids.size(), LOCC_OK);
+    std::vector<std::string> msg(c->kids.size());
+    for (size_t i = 0; i < c->kids.size(); ++i)
+      th.emplace_back([&, i] {
+        st[i] = locc_encode_shapes(c->kids[i]);
+        if (st[i] != LOCC_OK) msg[i] = g_err;
+      });
+    for (auto& t : th) t.join();
+    double ms = 0.0;
+    for (size_t i = 0; i < c->kids.size(); ++i) {
+      if (st[i] != LOCC_OK) {
+        g_err = msg[i];
+        return st[i];
+      }
+      ms = std::max(ms, c->kids[i]->encode_ms);
+    }
+    c->encode_ms = ms;
+    c->has_cells = true;
+    return LOCC_OK;
+  }
   if (!c->has_weights || !c->has_shapes || !c->has_unet)
     return fail(LOCC_E_STATE, "weights, U-Net weights and shapes must be set before locc_encode_shapes");
   const int M = c->cfg.M, H = c->cfg.H, F = c->cfg.F, S = c->T.S;
@@ -1081,6 +1508,11 @@ locc_status locc_encode_shapes(locc_ctx* c) {
 
 locc_status locc_get_cell_embeddings(locc_ctx* c, float* out, double* encode_ms) {
   if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
+  if (is_group(c)) {  // every device holds the same grids: read the first one's
+    locc_status s = locc_get_cell_embeddings(c->kids[0], out, nullptr);
+    if (s == LOCC_OK && encode_ms) *encode_ms = c->encode_ms;
+    return s;
+  }
   if (!c->has_cells) return fail(LOCC_E_STATE, "no encoded shapes");
   CK(cudaSetDevice(c->device));
   if (out) {
@@ -1094,6 +1526,8 @@ locc_status locc_get_cell_embeddings(locc_ctx* c, float* out, double* encode_ms)
 locc_status locc_query_cells(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
                              uint8_t* labels, float* logits, int32_t* nsel, uint32_t* cells, float* emb,
                              void* stream) {
+  if (is_group(c))
+    return group_query(c, pairs, poses, N, probs, labels, logits, nsel, nullptr, cells, emb, nullptr, stream, true);
   return run_query(c, pairs, poses, N, probs, labels, logits, nsel, nullptr, cells, emb, nullptr, stream, true);
 }
 
@@ -1108,6 +1542,22 @@ locc_status locc_sim_run(locc_ctx* c, const locc_sim_config* cfg, int32_t E, con
   if (c->cfg.H != 256 || c->cfg.F != 64) return fail(LOCC_E_INVALID_ARG, "the pose gradient is built for H = 256, F = 64");
   if (E == 0) return LOCC_OK;
   if (!ids || !body || !state) return fail(LOCC_E_INVALID_ARG, "ids, body and state must be non-null");
+  if (is_group(c)) {  // environments sharded over the devices (each env's bodies stay together)
+    const int hd = pointer_device(state);
+    if (hd != c->device || pointer_device(ids) != hd || pointer_device(body) != hd ||
+        (contacts && pointer_device(contacts) != hd))
+      return fail(LOCC_E_INVALID_ARG, "locc_sim_run takes device buffers on the home device %d", c->device);
+    const Slice sl[] = {{ids, 12, true, false}, {body, 48, true, false}, {state, 156, true, true},
+                        {contacts, 12, false, true}};
+    // contacts are zeroed with a memset on the kid's stream: then the kid works on its own copies
+    return group_run(
+        c, E, sl, 4, true, stream, contacts == nullptr,
+        [&](locc_ctx* k, void** p, int64_t n, void* st) {
+          return locc_sim_run(k, cfg, (int32_t)n, (const int32_t*)p[0], (const float*)p[1], (float*)p[2], t0,
+                              (int32_t*)p[3], st);
+        },
+        kid_sim_check);
+  }
   if (!is_device_ptr(ids) || !is_device_ptr(body) || !is_device_ptr(state) || (contacts && !is_device_ptr(contacts)))
     return fail(LOCC_E_INVALID_ARG, "locc_sim_run takes device buffers");
   CK(cudaSetDevice(c->device));
@@ -1134,7 +1584,10 @@ locc_status locc_sim_run(locc_ctx* c, const locc_sim_config* cfg, int32_t E, con
   sp.slack = cfg->slack;
   sp.hd = cfg->h;
   CK(c->sim_t0.ensure(sizeof(double)));
+  CK(c->sim_bad.ensure(sizeof(unsigned long long)));
   double* t0_dev = c->sim_t0.as<double>();
+  unsigned long long* bad = c->sim_bad.as<unsigned long long>();
+  CK(cudaMemsetAsync(bad, 0, sizeof(unsigned long long), st));
   CK(launch_sim_set_t0(t0_dev, t0, st));
   // the substeps: enqueued directly, or captured once into a CUDA graph and replayed while the call's
   // inputs (sizes, constants, buffers, stream) and the context's state are unchanged — one launch
@@ -1143,7 +1596,7 @@ locc_status locc_sim_run(locc_ctx* c, const locc_sim_config* cfg, int32_t E, con
     if (contacts) CK(cudaMemsetAsync(contacts, 0, sizeof(int32_t) * NP, st));
     for (int n = 0; n < cfg->substeps; ++n) {
       CK(launch_sim_prepare(c->T, sp, E, ids, state, t0_dev, n, c->sim_pairs.as<int32_t>(), c->sim_poses.as<float>(),
-                            c->sim_culled.as<uint8_t>(), st));
+                            c->sim_culled.as<uint8_t>(), bad, st));
       locc_status s = run_query(c, c->sim_pairs.as<int32_t>(), c->sim_poses.as<float>(), NP,
                                 c->sim_probs.as<float>(), nullptr, c->sim_logits.as<float>(), nullptr, nullptr,
                                 nullptr, nullptr, c->sim_grad.as<float>(), st, cfg->detector == 1);
@@ -1163,6 +1616,7 @@ locc_status locc_sim_run(locc_ctx* c, const locc_sim_config* cfg, int32_t E, con
   key.contacts = contacts;
   key.stream = st;
   key.gen = c->generation;
+  key.alloc_epoch = g_alloc_epoch.load();
   const bool same = std::memcmp(&key, &c->sim_key, sizeof key) == 0;
   if (!same) {
     if (c->sim_exec) cudaGraphExecDestroy(c->sim_exec);
@@ -1201,7 +1655,97 @@ locc_status locc_sim_run(locc_ctx* c, const locc_sim_config* cfg, int32_t E, con
   }
   ++c->sim_seen;
   c->last.kernel_launches = launches;
-  if (!stream) CK(cudaStreamSynchronize(st));
+  if (!stream) {
+    // synchronous form: report environments whose body ids were out of range (their pairs were culled)
+    unsigned long long hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hbad) return fail(LOCC_E_INVALID_ARG, "%llu environment substeps had a body id outside [0, S)", hbad);
+  }
+  return LOCC_OK;
+}
+
+// ---------------------------------------------------------------- multi-process NCCL gather
+locc_status locc_comm_unique_id(uint8_t out[128]) {
+  if (!out) return fail(LOCC_E_INVALID_ARG, "null argument");
+  const NcclApi& A = nccl();
+  if (!A.ok) return fail(LOCC_E_NCCL, "%s", A.why.c_str());
+  ncclUniqueId id;
+  NK(A.GetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out, &id, 128);
+  return LOCC_OK;
+}
+
+locc_status locc_comm_init(locc_ctx* c, int32_t world, int32_t rank, const uint8_t id[128]) {
+  if (!c || !id) return fail(LOCC_E_INVALID_ARG, "null argument");
+  if (is_group(c)) return fail(LOCC_E_INVALID_ARG, "locc_comm_init takes a single-device context (one per rank)");
+  if (world < 1 || rank < 0 || rank >= world) return fail(LOCC_E_INVALID_ARG, "rank %d of world %d", rank, world);
+  const NcclApi& A = nccl();
+  if (!A.ok) return fail(LOCC_E_NCCL, "%s", A.why.c_str());
+  CK(cudaSetDevice(c->device));
+  if (c->nccl_comm) {
+    A.CommDestroy(static_cast<ncclComm_t>(c->nccl_comm));
+    c->nccl_comm = nullptr;
+  }
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  ncclComm_t comm = nullptr;
+  NK(A.CommInitRank(&comm, world, uid, rank));
+  c->nccl_comm = comm;
+  c->world = world;
+  c->rank = rank;
+  return LOCC_OK;
+}
+
+locc_status locc_query_allgather(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
+                                 uint8_t* labels, float* logits, void* stream) {
+  if (!c) return fail(LOCC_E_INVALID_ARG, "null context");
+  if (!c->nccl_comm) return fail(LOCC_E_STATE, "locc_comm_init first");
+  if (N < 0) return fail(LOCC_E_INVALID_ARG, "N < 0");
+  if (N == 0) return LOCC_OK;
+  if (!pairs || !poses || !probs) return fail(LOCC_E_INVALID_ARG, "pairs, poses and probs must be non-null");
+  const int64_t per = (N + c->world - 1) / c->world;
+  const int64_t lo = std::min<int64_t>(N, c->rank * per), n = std::min<int64_t>(N, lo + per) - lo;
+  const bool dev = is_device_ptr(probs);
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  if (dev) {
+    if (n > 0) {  // this rank's shard, asynchronously on st (input errors are reported below if synchronous)
+      locc_status s = run_query(c, pairs + 2 * lo, poses + 14 * lo, n, probs + lo, labels ? labels + lo : nullptr,
+                                logits ? logits + lo : nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st);
+      if (s != LOCC_OK) return s;
+    }
+    locc_status s = allgather_slices(c, N, probs, labels, logits, st);
+    if (s != LOCC_OK) return s;
+    if (!stream) {
+      CK(cudaStreamSynchronize(st));
+      if (n > 0) return kid_query_check(c);
+    }
+    return LOCC_OK;
+  }
+  // host buffers: the shard runs synchronously from host memory, then the slices meet in device
+  // staging buffers for the collective and the whole result is copied back
+  CK(c->ag_out[0].ensure(sizeof(float) * N));
+  if (labels) CK(c->ag_out[1].ensure(N));
+  if (logits) CK(c->ag_out[2].ensure(sizeof(float) * N));
+  float* dp = c->ag_out[0].as<float>();
+  uint8_t* dl = labels ? c->ag_out[1].as<uint8_t>() : nullptr;
+  float* dg = logits ? c->ag_out[2].as<float>() : nullptr;
+  if (n > 0) {
+    locc_status s = run_query(c, pairs + 2 * lo, poses + 14 * lo, n, probs + lo, labels ? labels + lo : nullptr,
+                              logits ? logits + lo : nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+    if (s != LOCC_OK) return s;
+    CK(cudaMemcpyAsync(dp + lo, probs + lo, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+    if (dl) CK(cudaMemcpyAsync(dl + lo, labels + lo, n, cudaMemcpyHostToDevice, st));
+    if (dg) CK(cudaMemcpyAsync(dg + lo, logits + lo, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+  }
+  locc_status s = allgather_slices(c, N, dp, dl, dg, st);
+  if (s != LOCC_OK) return s;
+  CK(cudaMemcpyAsync(probs, dp, sizeof(float) * N, cudaMemcpyDeviceToHost, st));
+  if (dl) CK(cudaMemcpyAsync(labels, dl, N, cudaMemcpyDeviceToHost, st));
+  if (dg) CK(cudaMemcpyAsync(logits, dg, sizeof(float) * N, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   return LOCC_OK;
 }
 
@@ -1221,6 +1765,17 @@ float bf16_to_float(uint16_t h) {
   std::memcpy(&x, &u, 4);
   return x;
 }
+// b = hi + mid + lo exactly (three bf16 terms of 8 significant bits each cover fp32's 24), stored at
+// dst[0..5] (K = k0, k0 + 1, k0 + 2 of an SW128 row chunk).
+void put_bias3(uint8_t* dst, float b) {
+  const uint16_t hi = bf16_rne(b);
+  const float r1 = b - bf16_to_float(hi);
+  const uint16_t mid = bf16_rne(r1);
+  const uint16_t lo = bf16_rne(r1 - bf16_to_float(mid));
+  std::memcpy(dst + 0, &hi, 2);
+  std::memcpy(dst + 2, &mid, 2);
+  std::memcpy(dst + 4, &lo, 2);
+}
 }  // namespace
 
 // W2 as the B operand of layer 2, computed as two N = 128 halves: per CTA rank r the 64 output
@@ -1239,6 +1794,7 @@ locc_status locc_upload_tc_weights(locc_ctx* c, const float* flat) {
   const float* w2 = b1 + H;
   const float* b2 = w2 + H * H;
   const float* w3 = b2 + H;
+  const float* b3 = w3 + H * H;
   for (int f = 0; f < H; ++f) {
     c->tc_l1.w1b[f] = make_float4(w1[3 * f], w1[3 * f + 1], w1[3 * f + 2], b1[f]);
     c->tc_l1.b2[f] = b2[f];
@@ -1256,15 +1812,10 @@ locc_status locc_upload_tc_weights(locc_ctx* c, const float* flat) {
             std::memcpy(dst + 2 * e, &v, 2);
           }
         }
-      const float b = b2[n];
-      const uint16_t hi = bf16_rne(b);
-      const float r1 = b - bf16_to_float(hi);
-      const uint16_t mid = bf16_rne(r1);
-      const uint16_t lo = bf16_rne(r1 - bf16_to_float(mid));
-      uint8_t* dst = img.data() + r * kTcW2Bytes + 4 * 16384 + locc::tc::sw128_off(i, 0);
-      std::memcpy(dst + 0, &hi, 2);
-      std::memcpy(dst + 2, &mid, 2);
-      std::memcpy(dst + 4, &lo, 2);
+      // bias block: K = 0..2 of row i = b2 of image row i's feature n (B of layer 2's bias MMA),
+      // K = 16..18 of row i = b3 of this CTA's feature 128 r + i (A of layer 3's bias MMA)
+      put_bias3(img.data() + r * kTcW2Bytes + 4 * 16384 + locc::tc::sw128_off(i, 0), b2[n]);
+      put_bias3(img.data() + r * kTcW2Bytes + 4 * 16384 + locc::tc::sw128_off(i, 2), b3[128 * r + i]);
     }
   uint32_t* w3img = reinterpret_cast<uint32_t*>(img.data() + 2 * kTcW2Bytes);
   for (int f = 0; f < H; ++f)

@@ -19,7 +19,8 @@ LOCC_PREC_BF16 = 1
 
 EXPORTS = ("locc_create", "locc_load_weights", "locc_load_weights_mem", "locc_set_shapes", "locc_query",
            "locc_query_debug", "locc_query_grad", "locc_unet_n_params", "locc_load_unet_weights_mem",
-           "locc_encode_shapes", "locc_set_unet_global_pool", "locc_get_cell_embeddings", "locc_query_cells", "locc_sim_run", "locc_set_precision", "locc_set_timing", "locc_get_stats", "locc_destroy",
+           "locc_encode_shapes", "locc_set_unet_global_pool", "locc_get_cell_embeddings", "locc_query_cells", "locc_sim_run", "locc_set_precision", "locc_set_deterministic", "locc_set_timing", "locc_get_stats", "locc_destroy",
+           "locc_comm_unique_id", "locc_comm_init", "locc_query_allgather",
            "locc_status_string", "locc_last_error", "locc_version")
 
 
@@ -31,7 +32,8 @@ class LoccError(RuntimeError):
 
 class Config(C.Structure):
     _fields_ = [("M", C.c_int32), ("H", C.c_int32), ("F", C.c_int32), ("precision", C.c_int32),
-                ("device", C.c_int32), ("reserved", C.c_int32), ("max_batch", C.c_int64)]
+                ("device", C.c_int32), ("n_devices", C.c_int32), ("max_batch", C.c_int64),
+                ("device_ids", C.POINTER(C.c_int32))]
 
 
 class SimConfig(C.Structure):
@@ -84,6 +86,10 @@ def lib():
         L.locc_sim_run.argtypes = [vp, C.POINTER(SimConfig), i32, vp, vp, vp, C.c_double, vp, vp]
         L.locc_set_precision.argtypes = [vp, i32]
         L.locc_set_timing.argtypes = [vp, i32]
+        L.locc_set_deterministic.argtypes = [vp, i32]
+        L.locc_comm_unique_id.argtypes = [vp]
+        L.locc_comm_init.argtypes = [vp, i32, i32, vp]
+        L.locc_query_allgather.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp]
         L.locc_get_stats.argtypes = [vp, C.POINTER(Stats)]
         L.locc_destroy.argtypes = [vp]
         L.locc_destroy.restype = None
@@ -103,8 +109,10 @@ def _check(rc):
         raise LoccError(rc, f"{L.locc_status_string(rc).decode()}: {L.locc_last_error().decode()}")
 
 
-def _ptr(x, dtype=None):
-    """Raw pointer of a numpy array or torch tensor (contiguous, expected dtype); None -> NULL."""
+def _ptr(x, dtype=None, count=None):
+    """Raw pointer of a numpy array or torch tensor; None -> NULL.  Checks contiguity, the element
+    dtype (numpy dtype, matched by name for torch tensors) and that it holds >= `count` elements, so
+    the library never reads or writes past the caller's allocation."""
     if x is None:
         return None
     if isinstance(x, np.ndarray):
@@ -112,20 +120,36 @@ def _ptr(x, dtype=None):
             raise TypeError(f"expected {np.dtype(dtype)}, got {x.dtype}")
         if not x.flags["C_CONTIGUOUS"]:
             raise ValueError("array must be C-contiguous")
-        return x.ctypes.data
-    if hasattr(x, "data_ptr"):  # torch.Tensor
+        n, p = x.size, x.ctypes.data
+    elif hasattr(x, "data_ptr"):  # torch.Tensor
+        if dtype is not None and str(x.dtype).replace("torch.", "") != np.dtype(dtype).name:
+            raise TypeError(f"expected {np.dtype(dtype)}, got {x.dtype}")
         if not x.is_contiguous():
             raise ValueError("tensor must be contiguous")
-        return x.data_ptr()
-    raise TypeError(type(x))
+        n, p = x.numel(), x.data_ptr()
+    else:
+        raise TypeError(type(x))
+    if count is not None and n < count:
+        raise ValueError(f"buffer holds {n} elements, the call needs {count}")
+    return p
+
+
+def comm_unique_id() -> bytes:
+    """A new NCCL unique id (128 bytes) for locc_comm_init (rank 0 creates it and sends it to the others)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().locc_comm_unique_id(buf))
+    return buf.raw
 
 
 class Locc:
-    """One library context on one CUDA device (locc_create / locc_destroy)."""
+    """One library context (locc_create / locc_destroy): on one CUDA device, or — devices=[d0, d1, ...]
+    — a group that shards every query over those devices (d0 = home of device-resident buffers)."""
 
-    def __init__(self, M=6, H=256, F=64, precision=LOCC_PREC_BF16, device=-1, max_batch=0):
+    def __init__(self, M=6, H=256, F=64, precision=LOCC_PREC_BF16, device=-1, max_batch=0, devices=None):
         self._h = C.c_void_p()
-        self.cfg = Config(M, H, F, precision, device, 0, max_batch)
+        n = len(devices) if devices else 0
+        self._ids = (C.c_int32 * max(n, 1))(*(devices or [0]))
+        self.cfg = Config(M, H, F, precision, device, n, max_batch, self._ids if n > 1 else None)
         _check(lib().locc_create(C.byref(self.cfg), C.byref(self._h)))
         self.M, self.H, self.F = M, H, F
         self.K = None
@@ -158,12 +182,16 @@ class Locc:
         S, K = int(points.shape[0]), int(points.shape[1])
         if isinstance(points, np.ndarray):
             points = np.ascontiguousarray(points, np.float32)
-        _check(lib().locc_set_shapes(self._h, _ptr(points, np.float32), S, K))
+        _check(lib().locc_set_shapes(self._h, _ptr(points, np.float32, S * K * 3), S, K))
         self.K = K
         self.S = S
 
     def set_precision(self, precision):
         _check(lib().locc_set_precision(self._h, precision))
+
+    def set_deterministic(self, on=True):
+        """Bitwise batch-composition invariance of bf16 contexts (locc_set_deterministic)."""
+        _check(lib().locc_set_deterministic(self._h, 1 if on else 0))
 
     def set_timing(self, on=True):
         _check(lib().locc_set_timing(self._h, 1 if on else 0))
@@ -176,8 +204,12 @@ class Locc:
     def query_into(self, pairs, poses, probs, labels=None, logits=None, stream=None):
         """locc_query on caller buffers (numpy = host, torch cuda tensors = device)."""
         N = int(pairs.shape[0])
-        _check(lib().locc_query(self._h, _ptr(pairs), _ptr(poses), N, _ptr(probs), _ptr(labels), _ptr(logits),
-                                stream))
+        _check(lib().locc_query(self._h, *self._inputs(pairs, poses, N), N, _ptr(probs, np.float32, N),
+                                _ptr(labels, np.uint8, N), _ptr(logits, np.float32, N), stream))
+
+    @staticmethod
+    def _inputs(pairs, poses, N):
+        return _ptr(pairs, np.int32, 2 * N), _ptr(poses, np.float32, 14 * N)
 
     def query(self, pairs, poses):
         """Host convenience form: numpy in, numpy out (probs float32, labels uint8, logits float32)."""
@@ -190,11 +222,26 @@ class Locc:
         self.query_into(pairs, poses, probs, labels, logits)
         return probs, labels, logits
 
+    # ------------------------------------------------------------- multi-process sharding (NCCL gather)
+    def comm_init(self, world, rank, uid: bytes):
+        """Join the NCCL world (locc_comm_init); uid from comm_unique_id() on rank 0."""
+        if len(uid) != 128:
+            raise ValueError("the NCCL unique id is 128 bytes")
+        _check(lib().locc_comm_init(self._h, int(world), int(rank), C.c_char_p(uid)))
+
+    def query_allgather_into(self, pairs, poses, probs, labels=None, logits=None, stream=None):
+        """locc_query_allgather: this rank computes its contiguous shard of the GLOBAL batch (only that
+        slice of pairs/poses is read) and every rank receives all N results."""
+        N = int(pairs.shape[0])
+        _check(lib().locc_query_allgather(self._h, *self._inputs(pairs, poses, N), N, _ptr(probs, np.float32, N),
+                                          _ptr(labels, np.uint8, N), _ptr(logits, np.float32, N), stream))
+
     def query_grad_into(self, pairs, poses, probs, grad, labels=None, logits=None, stream=None):
         """locc_query_grad on caller buffers: grad [N][14] = d logit / d (q_A, t_A, q_B, t_B)."""
         N = int(pairs.shape[0])
-        _check(lib().locc_query_grad(self._h, _ptr(pairs), _ptr(poses), N, _ptr(probs), _ptr(labels), _ptr(logits),
-                                     _ptr(grad), stream))
+        _check(lib().locc_query_grad(self._h, *self._inputs(pairs, poses, N), N, _ptr(probs, np.float32, N),
+                                     _ptr(labels, np.uint8, N), _ptr(logits, np.float32, N),
+                                     _ptr(grad, np.float32, 14 * N), stream))
 
     def query_grad(self, pairs, poses):
         """Host form of locc_query_grad -> (probs, labels, logits, grad [N][14])."""
@@ -236,8 +283,11 @@ class Locc:
     def query_cells_into(self, pairs, poses, probs, labels=None, logits=None, nsel=None, cells=None, emb=None,
                          stream=None):
         N = int(pairs.shape[0])
-        _check(lib().locc_query_cells(self._h, _ptr(pairs), _ptr(poses), N, _ptr(probs), _ptr(labels),
-                                      _ptr(logits), _ptr(nsel), _ptr(cells), _ptr(emb), stream))
+        words = (self.M ** 3 + 31) // 32
+        _check(lib().locc_query_cells(self._h, *self._inputs(pairs, poses, N), N, _ptr(probs, np.float32, N),
+                                      _ptr(labels, np.uint8, N), _ptr(logits, np.float32, N),
+                                      _ptr(nsel, np.int32, 2 * N), _ptr(cells, np.uint32, 2 * N * words),
+                                      _ptr(emb, np.float32, 2 * N * self.F), stream))
 
     def query_cells(self, pairs, poses, debug=False):
         """Host form of locc_query_cells -> dict (probs, labels, logits [, nsel, cells, emb])."""
@@ -257,8 +307,9 @@ class Locc:
         """locc_sim_run on device tensors: ids int32 [E][3], body [E][3][4], state [E][3][13] (in place)."""
         cfg = SimConfig.from_dict(sim)
         E = int(ids.shape[0])
-        _check(lib().locc_sim_run(self._h, C.byref(cfg), E, _ptr(ids), _ptr(body), _ptr(state), float(t0),
-                                  _ptr(contacts), stream))
+        _check(lib().locc_sim_run(self._h, C.byref(cfg), E, _ptr(ids, np.int32, 3 * E), _ptr(body, np.float32, 12 * E),
+                                  _ptr(state, np.float32, 39 * E), float(t0), _ptr(contacts, np.int32, 3 * E),
+                                  stream))
 
     def query_debug(self, pairs, poses):
         """Host form of locc_query_debug -> dict of every output and intermediate."""

@@ -24,10 +24,13 @@ def locc_mod():
     return locc
 
 
-@pytest.fixture(scope="module")
-def weights():
-    w = ls.flatten_weights(ls.make_weights("spread", calib=ls.load_calibration()))
-    u = ls.flatten_unet(ls.make_unet_weights())
+@pytest.fixture(scope="module", params=[("spread", "spread"), ("spread_bias", "he")], ids=["spread", "bias"])
+def weights(request):
+    """(predictor weights, U-Net weights): zero biases, or every bias non-zero (the `spread_bias`
+    set and the U-Net's `he` biases: conv/deconv biases, the projection bias)."""
+    kind, ukind = request.param
+    w = ls.weight_set(kind)
+    u = ls.flatten_unet(ls.make_unet_weights(ukind))
     return w, u
 
 

@@ -29,9 +29,10 @@ def locc_mod():
     return locc
 
 
-@pytest.fixture(scope="module")
-def spread_flat():
-    return ls.flatten_weights(ls.make_weights("spread", calib=ls.load_calibration()))
+@pytest.fixture(scope="module", params=ls.WEIGHT_SETS)
+def wflat(request):
+    """Both calibrated sets: `spread` (zero hidden biases) and `spread_bias` (all biases non-zero)."""
+    return ls.weight_set(request.param)
 
 
 @pytest.fixture(scope="module")
@@ -47,9 +48,9 @@ def wl():
 
 
 @pytest.fixture(scope="module")
-def wl_oracle(oracle_mod, wl, spread_flat):
+def wl_oracle(oracle_mod, wl, wflat):
     pts, pairs, poses = wl
-    return {emul: oracle_mod.query_grad(spread_flat, pts, pairs, poses, bf16_emul=emul) for emul in (False, True)}
+    return {emul: oracle_mod.query_grad(wflat, pts, pairs, poses, bf16_emul=emul) for emul in (False, True)}
 
 
 def make_ctx(locc_mod, flat, points, precision, max_batch=0):
@@ -72,9 +73,9 @@ def check_grad(g, ref, precision):
 
 
 @pytest.mark.parametrize("precision", [0, 1])
-def test_grad_parity_host(locc_mod, wl, wl_oracle, spread_flat, precision):
+def test_grad_parity_host(locc_mod, wl, wl_oracle, wflat, precision):
     pts, pairs, poses = wl
-    with make_ctx(locc_mod, spread_flat, pts, precision, max_batch=256) as ctx:
+    with make_ctx(locc_mod, wflat, pts, precision, max_batch=256) as ctx:
         pr, lb, lg, g = ctx.query_grad(pairs, poses)
         pr0, lb0, lg0 = ctx.query(pairs, poses)
     if precision == 0:  # same fp32 predictor kernel family: the same bits
@@ -87,10 +88,10 @@ def test_grad_parity_host(locc_mod, wl, wl_oracle, spread_flat, precision):
 
 
 @pytest.mark.parametrize("precision", [0, 1])
-def test_grad_device_buffers_same_bits(locc_mod, wl, spread_flat, precision):
+def test_grad_device_buffers_same_bits(locc_mod, wl, wflat, precision):
     import torch
     pts, pairs, poses = wl
-    with make_ctx(locc_mod, spread_flat, pts, precision) as ctx:
+    with make_ctx(locc_mod, wflat, pts, precision) as ctx:
         _, _, _, g_host = ctx.query_grad(pairs, poses)
         N = len(pairs)
         dp = torch.from_numpy(pairs).cuda()
@@ -103,11 +104,11 @@ def test_grad_device_buffers_same_bits(locc_mod, wl, spread_flat, precision):
     assert np.array_equal(grad.cpu().numpy(), g_host)
 
 
-def test_grad_symmetries_gpu(locc_mod, wl, spread_flat):
+def test_grad_symmetries_gpu(locc_mod, wl, wflat):
     """Exact symmetries carried to the device: swapping the objects swaps the gradient halves, and
     q -> -q negates d/dq and keeps d/dt (fp32 path; same kernels on permuted inputs)."""
     pts, pairs, poses = wl
-    with make_ctx(locc_mod, spread_flat, pts, 0) as ctx:
+    with make_ctx(locc_mod, wflat, pts, 0) as ctx:
         _, _, _, g = ctx.query_grad(pairs, poses)
         _, _, _, gs = ctx.query_grad(pairs[:, ::-1].copy(), poses[:, ::-1].copy())
         neg = poses.copy()
@@ -119,7 +120,7 @@ def test_grad_symmetries_gpu(locc_mod, wl, spread_flat):
     assert np.array_equal(gn[:, [0, 1, 2, 3, 7, 8, 9, 10]], -g[:, [0, 1, 2, 3, 7, 8, 9, 10]])
 
 
-def test_grad_unsupported_width_fails_loudly(locc_mod, spread_flat):
+def test_grad_unsupported_width_fails_loudly(locc_mod, wflat):
     H, F = 128, 32
     flat = ls.flatten_weights(ls.make_weights("spread", H, F, calib=ls.load_calibration()), H, F)
     pts, _ = ls.make_shapes(4, 200, seed=5)
@@ -132,9 +133,9 @@ def test_grad_unsupported_width_fails_loudly(locc_mod, spread_flat):
     ctx.close()
 
 
-def test_grad_empty_batch_and_short_circuit(locc_mod, wl, spread_flat):
+def test_grad_empty_batch_and_short_circuit(locc_mod, wl, wflat):
     pts, pairs, poses = wl
-    with make_ctx(locc_mod, spread_flat, pts, 1) as ctx:
+    with make_ctx(locc_mod, wflat, pts, 1) as ctx:
         pr, lb, lg, g = ctx.query_grad(pairs[:0], poses[:0])
         assert g.shape == (0, 14)
         far = poses[:8].copy()

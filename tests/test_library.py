@@ -53,3 +53,33 @@ def test_binding_fails_loudly_without_library(monkeypatch, tmp_path):
     monkeypatch.setattr(locc, "_lib", None)
     with pytest.raises(ImportError):
         locc.lib()
+
+
+def test_buffer_checks_before_the_library_is_called():
+    """The binding checks dtype and length of every caller buffer: a wrong dtype or a
+    buffer shorter than the call needs raises before any pointer reaches the library."""
+    import numpy as np
+    from paper_2304_09439_b200.locc import _ptr
+    assert _ptr(None, np.float32, 10) is None
+    a = np.zeros(10, np.float32)
+    assert _ptr(a, np.float32, 10) == a.ctypes.data
+    with pytest.raises(ValueError):
+        _ptr(a, np.float32, 11)
+    with pytest.raises(TypeError):
+        _ptr(np.zeros(10, np.int64), np.int32, 10)
+    import torch
+    t = torch.zeros(3, 2, dtype=torch.int32)
+    assert _ptr(t, np.int32, 6) == t.data_ptr()
+    with pytest.raises(TypeError):
+        _ptr(t.to(torch.int64), np.int32, 6)
+    with pytest.raises(ValueError):
+        _ptr(t, np.int32, 7)
+    with pytest.raises(ValueError):
+        _ptr(torch.zeros(4, 4).t(), np.float32, 16)  # non-contiguous
+
+
+def test_nccl_unique_id_without_gpu():
+    """NCCL is loaded at run time (dlopen) and the handshake id needs no GPU: 128 bytes, fresh each call."""
+    from paper_2304_09439_b200 import locc
+    a, b = locc.comm_unique_id(), locc.comm_unique_id()
+    assert len(a) == 128 and a != b

@@ -91,11 +91,12 @@ def test_encoder_relu_probe(oracle_mod):
 
 
 # ----------------------------------------------------------------------------- encoder biases
-def test_encoder_bias_probe(oracle_mod):
+def encoder_bias_probe(seed=72):
     """W2 = 0, W3 = P_tau (h3[tau(k)] = ReLU(h2[k] + b3[tau(k)])): every kept point has
     h3[tau(k)] = ReLU(ReLU(b2[k]) + b3[tau(k)]), so every occupied cell's max is that constant and
-    e = W_F h3 + b_F for any non-empty side; an empty side gives e = 0."""
-    rng = np.random.default_rng(72)
+    e = W_F h3 + b_F for any non-empty side.  Returns (weights, {closed form name: e}), the closed
+    form "as defined" and four mutations of it (a bias zeroed, a ReLU dropped)."""
+    rng = np.random.default_rng(seed)
     w = ls.make_weights("he", H, F, seed=73)  # enc.l1 arbitrary: W2 = 0 cuts it off
     tau = rng.permutation(H)
     b2 = (rng.integers(-8, 9, H) / 16.0).astype(np.float32)
@@ -119,6 +120,12 @@ def test_encoder_bias_probe(oracle_mod):
     forms = {"as defined": h3_of(b2, b3), "enc.l2.b zeroed": h3_of(0 * b2, b3),
              "enc.l3.b zeroed": h3_of(b2, 0 * b3), "enc.l2 ReLU dropped": h3_of(b2, b3, relu2=False),
              "enc.l3 ReLU dropped": h3_of(b2, b3, relu3=False)}
+    return w, {name: WF @ h3 + bF for name, h3 in forms.items()}
+
+
+def test_encoder_bias_probe(oracle_mod):
+    """encoder_bias_probe: e = W_F h3 + b_F on every non-empty side; an empty side gives e = 0."""
+    w, forms = encoder_bias_probe()
     pts, _ = ls.make_shapes(6, 300, seed=74)
     pairs, poses = ls.make_pairs_poses(pts, 24, s=0.5, seed=75)
     flat = ls.flatten_weights(w)
@@ -126,8 +133,7 @@ def test_encoder_bias_probe(oracle_mod):
         r = oracle_mod.query(flat, pts, pairs, poses, bf16_emul=emul)
         nonempty = r["kept"] > 0
         assert nonempty.sum() > 20 and (~nonempty).sum() > 0
-        for name, h3 in forms.items():
-            e = WF @ h3 + bF
+        for name, e in forms.items():
             dev = np.abs(r["emb"][nonempty] - e).max()
             if name == "as defined":
                 assert dev <= 1e-12, dev

@@ -1,6 +1,8 @@
 """Host logic of the multi-GPU path on CPU: shard bounds, and the gloo world_size-2 gather
-reassembling a sharded query in the original order (the per-shard function here is a stand-in that
-only tags pairs; the GPU query itself is covered by the gpu tests)."""
+reassembling a sharded query in the original order.  The per-shard function is a REAL query — the CPU
+oracle's (test infrastructure may call it) — so the test proves that sharding the pairs and gathering
+the shards gives bitwise the unsharded answer; the GPU query's own sharded
+equality is covered by tests/test_multi_gpu.py and test_parity_gpu.py."""
 import os
 import socket
 
@@ -30,19 +32,23 @@ def _free_port():
 
 def _worker(rank, world, port, N, q):
     import torch.distributed as dist
+
+    import locc_synth as ls
+    import oracle
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    rng = np.random.default_rng(0)
-    pairs = rng.integers(0, 100, size=(N, 2)).astype(np.int32)
-    poses = rng.standard_normal((N, 2, 7)).astype(np.float32)
+    wl = ls.make_workload("C1", N=N, K=300, S=8)
+    flat = ls.weight_set("spread_bias")
 
-    def fake_query(p, po):  # stand-in: a deterministic tag of each pair
-        return (p[:, 0] * 1000 + p[:, 1]).astype(np.float32), (p[:, 0] % 2).astype(np.uint8)
+    def query(p, po):  # the oracle's collision query of one shard (single-threaded, deterministic)
+        r = oracle.query(flat, wl.points, p, po, n_threads=1)
+        return r["probs"].astype(np.float32), r["labels"].astype(np.uint8)
 
-    probs, labels = query_sharded(fake_query, pairs, poses, rank, world)
-    want_p, want_l = fake_query(pairs, poses)
-    q.put((rank, bool(np.array_equal(probs, want_p) and np.array_equal(labels, want_l))))
+    probs, labels = query_sharded(query, wl.pairs, wl.poses, rank, world)
+    want_p, want_l = query(wl.pairs, wl.poses)
+    q.put((rank, bool(np.array_equal(probs, want_p) and np.array_equal(labels, want_l)
+                      and (want_l == 1).any() and (want_l == 0).any())))
     dist.destroy_process_group()
 
 

@@ -28,9 +28,12 @@ def locc_mod():
     return locc
 
 
-@pytest.fixture(scope="module")
-def spread_flat():
-    return ls.flatten_weights(ls.make_weights("spread", calib=ls.load_calibration()))
+@pytest.fixture(scope="module", params=ls.WEIGHT_SETS)
+def wflat(request):
+    """Every parity suite runs over both calibrated sets: `spread` (zero hidden biases) and
+    `spread_bias` (every bias non-zero: b1, the bf16 b2 bias MMA, the b3 fold, the projection and
+    predictor biases)."""
+    return ls.weight_set(request.param)
 
 
 @pytest.fixture(scope="module")
@@ -39,8 +42,8 @@ def c1():
 
 
 @pytest.fixture(scope="module")
-def c1_oracle(oracle_mod, c1, spread_flat):
-    return {emul: oracle_mod.query(spread_flat, c1.points, c1.pairs, c1.poses, bf16_emul=emul) for emul in (False, True)}
+def c1_oracle(oracle_mod, c1, wflat):
+    return {emul: oracle_mod.query(wflat, c1.points, c1.pairs, c1.poses, bf16_emul=emul) for emul in (False, True)}
 
 
 def make_ctx(locc_mod, flat, points, precision, M=6, H=256, F=64, max_batch=0):
@@ -68,8 +71,8 @@ def assert_parity(got, ref, precision, ref64=None):
 
 # ----------------------------------------------------------------------------- C1 parity
 @pytest.mark.parametrize("precision", [0, 1])
-def test_c1_parity(locc_mod, c1, c1_oracle, spread_flat, precision):
-    with make_ctx(locc_mod, spread_flat, c1.points, precision) as ctx:
+def test_c1_parity(locc_mod, c1, c1_oracle, wflat, precision):
+    with make_ctx(locc_mod, wflat, c1.points, precision) as ctx:
         got = ctx.query_debug(c1.pairs, c1.poses)
     ref = c1_oracle[precision == 1]
     assert_parity(got, ref, precision, ref64=c1_oracle[False])
@@ -80,10 +83,10 @@ def test_c1_parity(locc_mod, c1, c1_oracle, spread_flat, precision):
 
 
 @pytest.mark.parametrize("precision", [0, 1])
-def test_c1_parity_with_ragged_subbatches_and_device_buffers(locc_mod, c1, c1_oracle, spread_flat, precision):
+def test_c1_parity_with_ragged_subbatches_and_device_buffers(locc_mod, c1, c1_oracle, wflat, precision):
     import torch
     ref = c1_oracle[precision == 1]
-    with make_ctx(locc_mod, spread_flat, c1.points, precision, max_batch=7) as ctx:
+    with make_ctx(locc_mod, wflat, c1.points, precision, max_batch=7) as ctx:
         got = ctx.query_debug(c1.pairs, c1.poses)
         assert_parity(got, ref, precision)
         # device-resident inputs/outputs on a caller stream: same bits as the host path
@@ -136,21 +139,21 @@ def test_identity_probe_gpu(locc_mod):
 # ----------------------------------------------------------------------------- edge cases
 @pytest.mark.parametrize("precision", [0, 1])
 @pytest.mark.parametrize("K,M,s", [(1, 6, 0.5), (77, 6, 0.3), (300, 1, 0.5), (300, 7, 0.25), (2000, 5, 0.1)])
-def test_edge_shapes(locc_mod, oracle_mod, spread_flat, precision, K, M, s):
+def test_edge_shapes(locc_mod, oracle_mod, wflat, precision, K, M, s):
     pts, _ = ls.make_shapes(5, K, seed=40 + K)
     pairs, poses = ls.make_pairs_poses(pts, 24, s=s, seed=41)
     pairs[0] = [2, 2]  # self pair
     poses[1, 1] = poses[1, 0]  # coincident poses: everything kept
-    ref = oracle_mod.query(spread_flat, pts, pairs, poses, M=M, bf16_emul=precision == 1)
-    with make_ctx(locc_mod, spread_flat, pts, precision, M=M) as ctx:
+    ref = oracle_mod.query(wflat, pts, pairs, poses, M=M, bf16_emul=precision == 1)
+    with make_ctx(locc_mod, wflat, pts, precision, M=M) as ctx:
         got = ctx.query_debug(pairs, poses)
     assert_parity(got, ref, precision)
 
 
 @pytest.mark.parametrize("precision", [0, 1])
-def test_all_short_circuit_and_empty(locc_mod, spread_flat, precision):
+def test_all_short_circuit_and_empty(locc_mod, wflat, precision):
     pts, _ = ls.make_shapes(3, 200, seed=50)
-    with make_ctx(locc_mod, spread_flat, pts, precision) as ctx:
+    with make_ctx(locc_mod, wflat, pts, precision) as ctx:
         poses = np.stack([np.stack([pose(), pose(t=(5.0 + i, 0, 0))]) for i in range(10)])
         pr, lb, lg = ctx.query(np.zeros((10, 2), np.int32), poses)
         assert np.all(pr == 0) and np.all(lb == 0) and np.all(np.isneginf(lg))
@@ -158,9 +161,9 @@ def test_all_short_circuit_and_empty(locc_mod, spread_flat, precision):
         assert pr.size == 0
 
 
-def test_invalid_inputs_fail_loudly(locc_mod, spread_flat):
+def test_invalid_inputs_fail_loudly(locc_mod, wflat):
     pts, _ = ls.make_shapes(3, 100, seed=51)
-    with make_ctx(locc_mod, spread_flat, pts, 0) as ctx:
+    with make_ctx(locc_mod, wflat, pts, 0) as ctx:
         ok = np.stack([pose(), pose()])[None]
         with pytest.raises(locc_mod.LoccError):
             ctx.query(np.array([[0, 3]], np.int32), ok)
@@ -178,28 +181,30 @@ def test_invalid_inputs_fail_loudly(locc_mod, spread_flat):
     with pytest.raises(locc_mod.LoccError):  # no weights / shapes yet
         ctx.query(np.array([[0, 0]], np.int32), ok)
     with pytest.raises(locc_mod.LoccError):
-        ctx.load_weights_mem(spread_flat[:-1])
+        ctx.load_weights_mem(wflat[:-1])
     with pytest.raises(locc_mod.LoccError):
         ctx.set_shapes(np.full((2, 10, 3), np.nan, np.float32))
     ctx.close()
 
 
-def test_weight_file_path(locc_mod, c1, spread_flat, tmp_path):
-    w = ls.make_weights("spread", calib=ls.load_calibration())
+def test_weight_file_path(locc_mod, c1, wflat, tmp_path):
+    kind = "spread_bias" if np.array_equal(wflat, ls.weight_set("spread_bias")) else "spread"
+    w = ls.make_weights(kind, calib=ls.load_calibration(kind=kind))
     path = ls.write_weights(str(tmp_path / "w.txt"), w)
-    with make_ctx(locc_mod, spread_flat, c1.points, 0) as a, locc_mod.Locc(precision=0, device=0) as b:
+    with make_ctx(locc_mod, wflat, c1.points, 0) as a, locc_mod.Locc(precision=0, device=0) as b:
         b.load_weights(path)
         b.set_shapes(c1.points)
         assert np.array_equal(a.query(c1.pairs, c1.poses)[0], b.query(c1.pairs, c1.poses)[0])
 
 
 # ----------------------------------------------------------------------------- invariants
-def assert_invariant(a, b, precision, keys=("probs", "logits", "labels")):
-    """fp32: bitwise.  bf16: the tensor-core layer-3 walk splits each 128-row part between two
-    walkers, so the fp32 summation order of a segment's cell values depends on where the segment
-    falls in its tile (reading Q24): the pooled mean moves by a few fp32 ulps (<= 1e-5
-    relative for <= 216 cells) and probabilities by <= 1e-5; labels agree away from 0.5."""
-    if precision == 0:
+def assert_invariant(a, b, precision, keys=("probs", "logits", "labels"), det=False):
+    """fp32, and bf16 with locc_set_deterministic: bitwise.  bf16 by default: the tensor-core layer-3
+    walk splits each 128-row part between two walkers, so the fp32 summation order of a segment's cell
+    values depends on where the segment falls in its tile (reading Q24): the pooled mean moves
+    by a few fp32 ulps (<= 1e-5 relative for <= 216 cells) and probabilities by <= 1e-5; labels agree
+    away from 0.5."""
+    if precision == 0 or det:
         for k in keys:
             assert np.array_equal(a[k], b[k]), k
         return
@@ -220,11 +225,12 @@ def assert_invariant(a, b, precision, keys=("probs", "logits", "labels")):
             assert np.array_equal(a[k], b[k]), k
 
 
-@pytest.mark.parametrize("precision", [0, 1])
-def test_invariances(locc_mod, c1, spread_flat, precision):
-    """Point order, object swap, q -> -q and batch composition leave every output unchanged
-    (bitwise in fp32; see assert_invariant for bf16)."""
-    with make_ctx(locc_mod, spread_flat, c1.points, precision) as ctx:
+@pytest.mark.parametrize("precision,det", [(0, False), (1, False), (1, True)])
+def test_invariances(locc_mod, c1, wflat, precision, det):
+    """Point order, object swap, q -> -q and batch composition leave every output unchanged: bitwise
+    in fp32 and in deterministic bf16 contexts, within the walk's summation-order bound otherwise."""
+    with make_ctx(locc_mod, wflat, c1.points, precision) as ctx:
+        ctx.set_deterministic(det)
         base = ctx.query_debug(c1.pairs, c1.poses)
         sw = ctx.query_debug(c1.pairs[:, ::-1].copy(), c1.poses[:, ::-1].copy())
         neg = c1.poses.copy()
@@ -233,31 +239,29 @@ def test_invariances(locc_mod, c1, spread_flat, precision):
         one = ctx.query_debug(c1.pairs[5:6], c1.poses[5:6])
         perm = np.random.default_rng(3).permutation(len(c1.pairs))
         pm = ctx.query_debug(c1.pairs[perm], c1.poses[perm])
-    assert_invariant(base, sw, precision)
-    assert_invariant(base, ng, precision)
-    assert_invariant({k: v[5:6] for k, v in base.items()}, one, precision)
-    assert_invariant({k: v[perm] for k, v in base.items()}, pm, precision)
-    if precision == 0:
-        np.testing.assert_array_equal(base["emb"], sw["emb"][:, ::-1])
-    else:
-        assert_invariant({"emb": base["emb"]}, {"emb": sw["emb"][:, ::-1]}, precision, keys=("emb",))
+    assert_invariant(base, sw, precision, det=det)
+    assert_invariant(base, ng, precision, det=det)
+    assert_invariant({k: v[5:6] for k, v in base.items()}, one, precision, det=det)
+    assert_invariant({k: v[perm] for k, v in base.items()}, pm, precision, det=det)
+    assert_invariant({"emb": base["emb"]}, {"emb": sw["emb"][:, ::-1]}, precision, keys=("emb",), det=det)
     rng = np.random.default_rng(4)
     pts2 = np.stack([p[rng.permutation(p.shape[0])] for p in c1.points])
-    with make_ctx(locc_mod, spread_flat, pts2, precision) as ctx:
+    with make_ctx(locc_mod, wflat, pts2, precision) as ctx:
+        ctx.set_deterministic(det)
         pp = ctx.query_debug(c1.pairs, c1.poses)
-    assert_invariant(base, pp, precision, keys=("probs", "logits", "kept", "occ", "emb"))
+    assert_invariant(base, pp, precision, keys=("probs", "logits", "kept", "occ", "emb"), det=det)
 
 
 # ----------------------------------------------------------------------------- full sizes
 @pytest.mark.parametrize("precision", [0, 1])
-def test_c2_sampled_parity(locc_mod, oracle_mod, spread_flat, precision):
+def test_c2_sampled_parity(locc_mod, oracle_mod, wflat, precision):
     wl = ls.make_workload("C2")
-    with make_ctx(locc_mod, spread_flat, wl.points, precision) as ctx:
+    with make_ctx(locc_mod, wflat, wl.points, precision) as ctx:
         pr, lb, lg = ctx.query(wl.pairs, wl.poses)
         st = ctx.stats()
     assert st["pairs"] == len(wl.pairs) and st["kept_rows"] > 0
     idx = np.random.default_rng(9).choice(len(wl.pairs), 96, replace=False)
-    ref = oracle_mod.query(spread_flat, wl.points, wl.pairs[idx], wl.poses[idx], bf16_emul=precision == 1)
+    ref = oracle_mod.query(wflat, wl.points, wl.pairs[idx], wl.poses[idx], bf16_emul=precision == 1)
     assert np.abs(pr[idx] - ref["probs"]).max() <= P_TOL[precision]
     band = np.abs(ref["probs"] - 0.5) <= 1e-3
     assert np.array_equal(lb[idx][~band], ref["labels"][~band])
@@ -265,14 +269,14 @@ def test_c2_sampled_parity(locc_mod, oracle_mod, spread_flat, precision):
     assert np.all((pr[ev] > 0) & (pr[ev] < 1)) and st["evaluated_pairs"] == ev.sum()
 
 
-def test_c3_full_size_bf16(locc_mod, oracle_mod, spread_flat):
+def test_c3_full_size_bf16(locc_mod, oracle_mod, wflat):
     """BASELINE config C3 (1,048,576 pairs, bf16, the bench launch configuration): sampled outputs
-    against the oracle, kept = popcount(mask) everywhere, swap invariance on the whole batch
-    (within the bf16 walk's summation-order bound, see assert_invariant)."""
+    against the oracle, kept = popcount(mask) everywhere, swap invariance on the whole batch and batch
+    composition invariance of the sampled pairs (within the default walk's summation-order bound)."""
     import torch
     wl = ls.make_workload("C3")
     N = len(wl.pairs)
-    with make_ctx(locc_mod, spread_flat, wl.points, 1) as ctx:
+    with make_ctx(locc_mod, wflat, wl.points, 1) as ctx:
         pairs = torch.from_numpy(wl.pairs).cuda()
         poses = torch.from_numpy(wl.poses).cuda()
         probs = torch.empty(N, device="cuda")
@@ -289,19 +293,19 @@ def test_c3_full_size_bf16(locc_mod, oracle_mod, spread_flat):
     assert np.array_equal(pc, dbg["kept"])
     assert np.abs(dbg["probs"] - pr[sub]).max() <= 1e-5  # batch composition (see assert_invariant)
     idx = sub[:64]
-    ref = oracle_mod.query(spread_flat, wl.points, wl.pairs[idx], wl.poses[idx], bf16_emul=True)
+    ref = oracle_mod.query(wflat, wl.points, wl.pairs[idx], wl.poses[idx], bf16_emul=True)
     assert np.abs(pr[idx] - ref["probs"]).max() <= 5e-4
     band = np.abs(ref["probs"] - 0.5) <= 1e-3
     assert np.array_equal(lb[idx][~band], ref["labels"][~band])
     assert np.array_equal(dbg["kept"][:64], ref["kept"])
 
 
-def test_tensor_core_predictor_vs_fp32_predictor(locc_mod, spread_flat):
+def test_tensor_core_predictor_vs_fp32_predictor(locc_mod, wflat):
     """Crop path in a bf16 context: the 3xTF32 tensor-core predictor (Q32) against the CUDA-core fp32
     predictor on the same embeddings (LOCC_HEAD_FFMA switches the kernel): |dp| <= 2e-5, labels equal
     outside the 1e-4 band, the same short-circuits."""
     wl = ls.make_workload("C1", N=2000, S=64)
-    with make_ctx(locc_mod, spread_flat, wl.points, 1) as ctx:
+    with make_ctx(locc_mod, wflat, wl.points, 1) as ctx:
         p_tc, l_tc, g_tc = ctx.query(wl.pairs, wl.poses)
         os.environ["LOCC_HEAD_FFMA"] = "1"
         try:
@@ -316,12 +320,41 @@ def test_tensor_core_predictor_vs_fp32_predictor(locc_mod, spread_flat):
 
 @pytest.mark.parametrize("precision", [0, 1])
 @pytest.mark.parametrize("K", [512, 4096])
-def test_k_sweep_parity(locc_mod, oracle_mod, spread_flat, precision, K):
+def test_k_sweep_parity(locc_mod, oracle_mod, wflat, precision, K):
     """BASELINE.json config 5's K values (512 / 4096 points per object): C1-sized batches against the
     oracle at the same bars as C1 (the full-size sweep is a bench setting, `bench.py --K`)."""
     wl = ls.make_workload("C1", N=48, K=K, S=12)
-    ref = oracle_mod.query(spread_flat, wl.points, wl.pairs, wl.poses, bf16_emul=precision == 1)
-    with make_ctx(locc_mod, spread_flat, wl.points, precision) as ctx:
+    ref = oracle_mod.query(wflat, wl.points, wl.pairs, wl.poses, bf16_emul=precision == 1)
+    with make_ctx(locc_mod, wflat, wl.points, precision) as ctx:
         got = ctx.query_debug(wl.pairs, wl.poses)
     assert_parity(got, ref, precision)
     assert (ref["kept"].sum(1) > 0).mean() > 0.8
+
+
+def test_c3_sharded_equals_unsharded_bf16(locc_mod, wflat):
+    """pairs are independent, so the C3 batch split into 8 contiguous shards of
+    ceil(N/8) pairs (each a separate query, as the 8 ranks of a multi-GPU run compute them) gives
+    BITWISE the probabilities, labels and logits of the single 1,048,576-pair query — in a
+    deterministic context (locc_set_deterministic), the bf16 path's bitwise mode; swapping the objects
+    of every pair is bitwise invariant there too."""
+    import torch
+    from paper_2304_09439_b200.parallel import shard_bounds
+    wl = ls.make_workload("C3")
+    N = len(wl.pairs)
+    with make_ctx(locc_mod, wflat, wl.points, 1) as ctx:
+        ctx.set_deterministic(True)
+        pairs = torch.from_numpy(wl.pairs).cuda()
+        poses = torch.from_numpy(wl.poses).cuda()
+        out = [torch.empty(N, device="cuda"), torch.empty(N, dtype=torch.uint8, device="cuda"),
+               torch.empty(N, device="cuda")]
+        ctx.query_into(pairs, poses, *out)
+        sh = [torch.full((N,), 7.0, device="cuda"), torch.full((N,), 7, dtype=torch.uint8, device="cuda"),
+              torch.full((N,), 7.0, device="cuda")]
+        for r in range(8):
+            lo, hi = shard_bounds(N, 8, r)
+            ctx.query_into(pairs[lo:hi], poses[lo:hi], *(t[lo:hi] for t in sh))
+        for a, b in zip(out, sh):
+            assert torch.equal(a, b)
+        swapped = torch.empty(N, device="cuda")
+        ctx.query_into(pairs.flip(1).contiguous(), poses.flip(1).contiguous(), swapped)
+        assert torch.equal(out[0], swapped)

@@ -32,10 +32,10 @@ def world():
     return pts, ids, body, st
 
 
-def run_gpu(locc_mod, pts, ids, body, st, sim, unet=None, t0=0.0, precision=0):
+def run_gpu(locc_mod, pts, ids, body, st, sim, unet=None, t0=0.0, precision=0, weights=None):
     import torch
     ctx = locc_mod.Locc(M=6, H=256, F=64, precision=precision, device=0)
-    ctx.load_weights_mem(spread())
+    ctx.load_weights_mem(spread() if weights is None else weights)
     ctx.set_shapes(pts)
     if unet is not None:
         ctx.load_unet_weights_mem(unet)
@@ -58,9 +58,9 @@ def run_gpu(locc_mod, pts, ids, body, st, sim, unet=None, t0=0.0, precision=0):
     return out, con
 
 
-def compare(out, con, ref, st):
+def compare(out, con, ref, st, relu_margin=1e-5):
     rst, rcon, mg = ref
-    ok = (mg[:, 0] > 1e-3) & (mg[:, 1] > 1e-5) & (mg[:, 2] > 1e-5) & (mg[:, 3] > 1e-4)
+    ok = (mg[:, 0] > 1e-3) & (mg[:, 1] > relu_margin) & (mg[:, 2] > 1e-5) & (mg[:, 3] > 1e-4)
     assert ok.mean() >= 0.6, f"only {ok.mean():.2f} of the environments away from every decision"
     assert np.array_equal(con[ok], rcon[ok])
     d = np.abs(rst[ok] - st[ok].astype(np.float64)).max(axis=(1, 2), keepdims=True)
@@ -70,16 +70,21 @@ def compare(out, con, ref, st):
     return ok
 
 
+@pytest.mark.parametrize("kind", ls.WEIGHT_SETS)
 @pytest.mark.parametrize("detector,precision", [("crop", 0), ("cells", 0), ("cells", 1)])
-def test_sim_parity(locc_mod, oracle_mod, world, detector, precision):
+def test_sim_parity(locc_mod, oracle_mod, world, detector, precision, kind):
     """(cells, 1): a bf16 context, whose encode-once detector runs the tensor-core (3xTF32) predictor and
     gradient (reading Q32); the encode-once embeddings are fp32 in both precisions."""
     pts, ids, body, st = world
     sim = dict(SIM, substeps=2, detector=detector, ks=2.0)
-    unet = ls.flatten_unet(ls.make_unet_weights()) if detector == "cells" else None
-    out, con = run_gpu(locc_mod, pts, ids, body, st, sim, unet, t0=0.1, precision=precision)
-    ref = oracle_mod.sim_run(spread(), pts, sim, ids, body, st.astype(np.float64), t0=0.1, unet_flat=unet)
-    compare(out, con, ref, st)
+    w = ls.weight_set(kind)
+    ukind = "he" if kind == "spread_bias" else "spread"
+    unet = ls.flatten_unet(ls.make_unet_weights(ukind)) if detector == "cells" else None
+    out, con = run_gpu(locc_mod, pts, ids, body, st, sim, unet, t0=0.1, precision=precision, weights=w)
+    ref = oracle_mod.sim_run(w, pts, sim, ids, body, st.astype(np.float64), t0=0.1, unet_flat=unet)
+    # a bf16 context's predictor is the 3xTF32 tensor-core kernel, ~1e-5 off the fp64 oracle in the logit
+    # (DESIGN.md Q32): a ReLU decision closer than that may flip, so such environments are not compared
+    compare(out, con, ref, st, relu_margin=1e-5 if precision == 0 else 1e-4)
 
 
 def test_sim_free_fall_gpu(locc_mod, world):
@@ -147,3 +152,44 @@ def test_sim_graph_replay_same_bits(locc_mod, world, detector):
         finally:
             os.environ.pop("LOCC_NO_GRAPH", None)
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("detector", ["crop", "cells"])
+def test_sim_graph_survives_scratch_regrowth(locc_mod, world, detector):
+    """sim, sim (captured), a larger query that regrows the context's scratch buffers, then sim again:
+    the graph must not replay into the freed buffers — the trajectory is bitwise the direct
+    path's (LOCC_NO_GRAPH), and bad body ids are reported by the synchronous form, not read."""
+    import os
+    import torch
+    pts, ids, body, st = world
+    unet = ls.flatten_unet(ls.make_unet_weights()) if detector == "cells" else None
+    sim = dict(SIM, detector=detector)
+    big = ls.make_pairs_poses(pts, 5000, s=0.5, seed=83)
+    outs = []
+    for no_graph in (False, True):
+        if no_graph:
+            os.environ["LOCC_NO_GRAPH"] = "1"
+        try:
+            ctx = locc_mod.Locc(M=6, H=256, F=64, precision=1, device=0)
+            ctx.load_weights_mem(spread())
+            ctx.set_shapes(pts)
+            if unet is not None:
+                ctx.load_unet_weights_mem(unet)
+                ctx.encode_shapes()
+            d_ids, d_body = torch.from_numpy(ids).cuda(), torch.from_numpy(body).cuda()
+            d_st = torch.from_numpy(st.copy()).cuda()
+            s = torch.cuda.Stream()
+            for k in range(5):
+                if k == 2:
+                    ctx.query(*big) if detector == "crop" else ctx.query_cells(*big)
+                ctx.sim_run(sim, d_ids, d_body, d_st, t0=k * sim["h"] * sim["substeps"], stream=s.cuda_stream)
+            s.synchronize()
+            outs.append(d_st.cpu().numpy())
+            bad = d_ids.clone()
+            bad[3, 1] = len(pts)
+            with pytest.raises(locc_mod.LoccError):
+                ctx.sim_run(sim, bad, d_body, d_st.clone())
+            ctx.close()
+        finally:
+            os.environ.pop("LOCC_NO_GRAPH", None)
+    assert np.array_equal(outs[0], outs[1])

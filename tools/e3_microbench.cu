@@ -2,9 +2,11 @@
 // TMEM lane quarter) walk synthetic 256-row tiles with the encoder's cell/segment statistics
 // (segments padded to 16 rows as the crop kernel emits them), reading layer-3 outputs from TMEM
 // exactly as the encoder does.  Reports the walk's cycles per tile, and checks the pooled means
-// against a plain host walk of the same rows.
+// against a plain host walk of the same rows (bitwise: the walk sums each segment in one sequential
+// fp32 chain, like the host loop).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/e3_microbench tools/e3_microbench.cu
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <random>
 #include <vector>
@@ -18,12 +20,42 @@ using namespace locc::tc;
 using namespace locc::e3;
 
 struct Sm {
+  float4 slab[512];  // the walk's record slab (16 floats per E3 thread)
+  uint32_t pce[8], pse[8];  // plain (non-interleaved) masks: [4 h + q] = rows 128 h + 32 q .. + 31
   uint32_t flags[256];
   alignas(16) uint32_t masks[16];
   uint32_t tmem;
 };
 
-__host__ __device__ inline float val(int r, int f) { return sinf(r * 0.37f + f); }
+// exactly representable on both sides (a device sinf would differ from the host libm in the last bits)
+__host__ __device__ inline float val(int r, int f) { return (float)((r * 37 + f * 101) % 997 - 498) * (1.0f / 331.0f); }
+
+// Reference point: ONE sequential walker per 128-row part (exact sequential sum, no merge, no ILP).
+__device__ __forceinline__ void part1(uint32_t tbase, const uint32_t* ce, const uint32_t* se, const uint32_t* fl,
+                                      Walk& w, float* pooled, uint32_t f) {
+  uint32_t va[16], vb[16];
+  tmem_ld16(tbase, va);
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    uint32_t(&v)[16] = (g & 1) ? vb : va;
+    uint32_t(&n)[16] = (g & 1) ? va : vb;
+    tmem_ld_wait();
+    if (g < 7) tmem_ld16(tbase + 16 * (g + 1), n);
+    const uint32_t bits = (ce[g >> 1] >> (16 * (g & 1))) & 0xFFFFu;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      w.m = fmaxf(w.m, __uint_as_float(v[j]));
+      if ((bits >> j) & 1u) w.s += w.m;
+      if ((bits >> j) & 1u) w.m = 0.f;
+    }
+    w.c += __popc(bits);
+    const uint32_t sb = (se[g >> 1] >> (16 * (g & 1))) & 0xFFFFu;
+    if (sb) {
+      store_mean(pooled, fl[16 * g + __ffs(sb) - 1] >> kRowSegShift, f, w.s, w.c);
+      w = Walk{0.f, 0.f, 0};
+    }
+  }
+}
 
 template <int V, int NOISE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (4 + NOISE), 1)
@@ -45,8 +77,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (4 + NOISE), 1)
     }
     tmem_st_wait();
     asm volatile("bar.sync 1, 128;" ::: "memory");
-    const float b3 = b3g[f], nb3 = -b3;
-    Walk w{nb3, 0.f, 0};
+    Walk w{0.f, 0.f, 0};  // the values stand for D3 = b3 + W3 h2 (b3 is in the accumulator)
     long long tw = 0;
     for (int it = 0; it < ntiles; ++it) {
       asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -61,13 +92,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (4 + NOISE), 1)
           S.masks[8 * h + q] = ce;
           S.masks[8 * h + 4 + q] = se;
         }
+        const uint32_t pce = __ballot_sync(0xffffffffu, S.flags[r] & kRowFlagCellEnd);
+        const uint32_t pse = __ballot_sync(0xffffffffu, S.flags[r] & kRowFlagSegEnd);
+        if (lane == 0) {
+          S.pce[4 * h + q] = pce;
+          S.pse[4 * h + q] = pse;
+        }
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       const long long t0 = clock64();
       for (int p = 0; p < 2; ++p) {
         const uint32_t tbase = tmem + ((32 * q) << 16) + 128 * p;
         if (V == 0) {
-          e3_part2(tbase, S.masks + 8 * p, S.flags + 128 * p, w, nb3, b3, pooled, f);
+          e3_part2(tbase, S.masks + 8 * p, S.flags + 128 * p, w, pooled, f);
+        } else if (V == 2) {
+          part1(tbase, S.pce + 4 * p, S.pse + 4 * p, S.flags + 128 * p, w, pooled, f);
+        } else if (V == 5) {
+          e3_part2_det(tbase, S.masks + 8 * p, S.flags + 128 * p, w, pooled, f);
         } else {  // TMEM loads of the walk's schedule only
           uint32_t xa[16], ya[16];
           uint32_t acc = 0;
@@ -85,7 +126,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (4 + NOISE), 1)
       tw += clock64() - t0;
     }
     if (lane == 0 && blockIdx.x == 0) cycles[q] = tw;
-    if (w.s == 12345.f) pooled[1] = w.m + (float)w.c;  // keep the walk state alive
+    if (w.s == 12345.f) pooled[1] = w.m + (float)w.c + b3g[0];  // keep the walk state alive
   } else {
     // noise: FFMA2 chains (layer-1-like work) competing for issue slots (bounded)
     unsigned long long a0 = f2(1.f, 2.f), a1 = f2(3.f, 4.f), k = f2(0.999f, 0.999f);
@@ -126,24 +167,32 @@ std::vector<uint32_t> make_flags(int ntiles, double cell_len, double seg_len, in
   return fl;
 }
 
-// host reference: the plain row walk (last segment may be cut by the end of the rows: skipped)
+// host reference: the plain row walk in the walk's canonical order (e3_walk.cuh): per segment, per
+// 16-row block (segments start on multiples of 16), P = ((g_1 + g_2) + ...) over the cells ending in
+// the block, S = ((P_0 + P_1) + ...), mean = S / C (the last segment may be cut by the end of the
+// rows: skipped).  Also counts the segments whose mean differs from the walk's in any bit.
 std::vector<float> host_walk(const std::vector<uint32_t>& fl, int nseg, const std::vector<float>& b3) {
   std::vector<float> out((size_t)nseg * 256, 0.f);
   for (int f = 0; f < 128; ++f) {
-    double s = 0;
+    float s = 0.f, pb = 0.f;
     int c = 0;
     float m = -INFINITY;
     for (size_t r = 0; r < fl.size(); ++r) {
+      if (r % 16 == 0) {  // block boundary: fold the previous block's sum
+        s += pb;
+        pb = 0.f;
+      }
       if (fl[r] & kRowFlagPad) continue;
       m = std::max(m, val((int)(r % 256), f));
       if (fl[r] & kRowFlagCellEnd) {
-        s += std::max(m + b3[f], 0.f);
+        pb += std::max(m + b3[f], 0.f);
         ++c;
         m = -INFINITY;
       }
       if (fl[r] & kRowFlagSegEnd) {
-        out[(size_t)(fl[r] >> kRowSegShift) * 256 + f] = (float)(s / c);
-        s = 0;
+        s += pb;
+        out[(size_t)(fl[r] >> kRowSegShift) * 256 + f] = s / (float)c;
+        s = pb = 0.f;
         c = 0;
       }
     }
@@ -180,26 +229,44 @@ double run(const std::vector<uint32_t>& fl, int ntiles, int nseg, const std::vec
 }
 
 int main() {
-  const int ntiles = 2000;
+  const int ntiles = getenv("E3_DUMP") ? 200 : 2000;
   std::vector<float> b3(128);
-  for (int i = 0; i < 128; ++i) b3[i] = 0.3f * std::sin(1.7f * i);
-  for (double seg_len : {528.0, 128.0, 1e9}) {
+  // the walk takes b3 inside the layer-3 accumulator (the encoder's bias MMA): the values stand for D3
+  for (int i = 0; i < 128; ++i) b3[i] = 0.f;
+  const double cfgs[4][2] = {{528.0, 10.0}, {528.0, 5.0}, {128.0, 5.0}, {1e9, 5.0}};  // (segment, cell) rows
+  for (const auto& cf : cfgs) {
+    const double seg_len = cf[0], cell_len = cf[1];
     int nseg = 0;
-    std::vector<uint32_t> fl = make_flags(ntiles, 5.0, seg_len, &nseg);
-    std::vector<float> o0, o1, o2;
+    std::vector<uint32_t> fl = make_flags(ntiles, cell_len, seg_len, &nseg);
+    std::vector<float> o0, o1, o2, o3, o5;
     const double c0 = run<0, 0>(fl, ntiles, nseg, b3, o0);
     const double c1 = run<0, 4>(fl, ntiles, nseg, b3, o1);
     const double c2 = run<1, 0>(fl, ntiles, nseg, b3, o2);
+    const double c3 = run<2, 0>(fl, ntiles, nseg, b3, o3);
+    const double c5 = run<5, 0>(fl, ntiles, nseg, b3, o5);
     const std::vector<float> ref = host_walk(fl, nseg, b3);
+    if (getenv("E3_DUMP") && cell_len == 10.0) {  // debugging aid: flags, walk output, host output
+      FILE* fp = fopen(getenv("E3_DUMP"), "wb");
+      const long long n = (long long)fl.size();
+      fwrite(&n, 8, 1, fp);
+      fwrite(&nseg, 4, 1, fp);
+      fwrite(fl.data(), 4, fl.size(), fp);
+      fwrite(o5.data(), 4, o5.size(), fp);
+      fwrite(ref.data(), 4, ref.size(), fp);
+      fclose(fp);
+    }
     double md = 0;
+    long long nbad5 = 0;
     for (int sg = 0; sg + 1 < nseg; ++sg)
       for (int f = 0; f < 128; ++f) {
         const size_t i = (size_t)sg * 256 + f;
         md = std::max(md, (double)std::fabs(o0[i] - ref[i]) / (1.0 + std::fabs(ref[i])));
+        nbad5 += o5[i] != ref[i];
       }
-    printf("segments ~%5.0f rows, cells ~5: walk %6.0f cyc/tile (+4 FFMA2 warps %6.0f), TMEM loads alone %5.0f | "
-           "max rel diff vs host %.3g\n",
-           seg_len, c0, c1, c2, md);
+    printf("segments ~%5.0f rows, cells ~%2.0f: walk %6.0f cyc/tile (+4 FFMA2 warps %6.0f, TMEM loads alone %4.0f), "
+           "max rel diff vs the canonical order %.3g | deterministic walk %6.0f cyc/tile, %lld values not bitwise "
+           "the canonical order (expected 0) | one sequential walker %6.0f cyc/tile\n",
+           seg_len, cell_len, c0, c1, c2, md, c5, nbad5, c3);
   }
   return 0;
 }
