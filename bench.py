@@ -7,8 +7,15 @@ batch (every stage of the hot path: transforms, crop + compaction, encoder, pool
   python bench.py [--gpus N] [--steps K] [--warmup W] [--precision bf16|fp32] [--pairs N]
   python bench.py --impl reference ...   # the CPU oracle (this tier's reference arm)
 
-Multi-GPU (torchrun, one process per GPU): every rank runs its own 1,048,576-pair batch (weak
-scaling; the path needs no collective); time = max over ranks; value = all pairs / that time.
+Multi-GPU (one process per GPU; `--gpus N` re-launches itself under torch.distributed.run when
+WORLD_SIZE is unset): the global batch is N x 1,048,576 pairs, each rank computes its own contiguous
+shard and the library gathers every rank's probabilities and labels on every rank with NCCL
+(locc_query_allgather, the path's only collective) inside the timed step (weak scaling); time = max
+over ranks; value = all pairs / that time.
+
+The N = 1 line also carries the BASELINE.json config table (`sweep`: C1/C2 in fp32 and bf16, C5's
+K x N grid with its roofline fractions, C4's closed-loop times, the oracle at 1 and all host threads)
+and the deterministic bf16 mode's throughput (`deterministic`).
 """
 import argparse
 import json
@@ -51,7 +58,26 @@ def parse():
     ap.add_argument("--no-cells", action="store_true", help="skip the NEXT-1 encode-once measurement")
     ap.add_argument("--no-sim", action="store_true", help="skip the NEXT-3 closed-loop measurement")
     ap.add_argument("--sim-envs", type=int, default=30000)
+    ap.add_argument("--no-sweep", action="store_true", help="skip the config-table sweep (C1/C2/C4/C5)")
     return ap.parse_args()
+
+
+def relaunch_distributed(a):
+    """`--gpus N` without a torchrun environment: start N ranks of this script under
+    torch.distributed.run (rendezvous on 127.0.0.1) and return their exit code; rank 0 prints the line."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        raise SystemExit(f"bench.py --gpus {a.gpus}: only {have} CUDA device(s) visible")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def workload_name(a):
@@ -162,10 +188,122 @@ def run_reference(a):
     print(json.dumps(line), flush=True)
 
 
+def time_query(ctx, torch, stream, pairs, poses, probs, labels, reps=3, warm=2, flush=None):
+    """Mean device time (ms) of one locc_query over device-resident inputs (CUDA events on the
+    query's stream; the L2 flushed before each timed call when the batch is large)."""
+    for _ in range(warm):
+        ctx.query_into(pairs, poses, probs, labels, stream=stream.cuda_stream)
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            if flush is not None:
+                flush.zero_()
+            e0.record(stream)
+        ctx.query_into(pairs, poses, probs, labels, stream=stream.cuda_stream)
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        stream.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.mean(ts)
+
+
+def run_sweep(a, locc, torch, stream, flush, peaks):
+    """BASELINE.json configs as a table: C1 and C2 in fp32 and bf16; C5 = K x N with
+    the encoder's tensor-core roofline fraction per cell; C4 = the closed-loop step at 4K-65K
+    environments with both detectors; the oracle at 1 host thread (its all-threads rate is cpu_baseline)."""
+    import locc_synth as ls
+    import oracle
+    out = {}
+    flat = ls.weight_set("spread")
+    peak = peaks.get("bf16_tflops_sustained", 1400.0)
+
+    def one(points, pairs, poses, prec, det=False):
+        ctx = locc.Locc(precision=prec, device=torch.cuda.current_device())
+        ctx.set_deterministic(det)
+        ctx.load_weights_mem(flat)
+        ctx.set_shapes(points)
+        n = len(pairs)
+        dp, dq = torch.from_numpy(pairs).cuda(), torch.from_numpy(poses).cuda()
+        pr, lb = torch.empty(n, device="cuda"), torch.empty(n, dtype=torch.uint8, device="cuda")
+        ms = time_query(ctx, torch, stream, dp, dq, pr, lb, flush=flush if n >= 65536 else None)
+        ctx.set_timing(True)
+        ctx.query_into(dp, dq, pr, lb, stream=stream.cuda_stream)
+        stream.synchronize()
+        st = ctx.stats()
+        ctx.close()
+        r = {"pairs": n, "ms": ms, "checks_per_s": n / (ms / 1e3), "kept_rows_per_pair": st["kept_rows"] / n}
+        if prec == locc.LOCC_PREC_BF16 and st["encoder_ms"] > 0:
+            tf = FLOP_PER_ROW * st["kept_rows"] / (st["encoder_ms"] / 1e3) / 1e12
+            r["encoder_tflops"] = tf
+            r["encoder_roofline_frac"] = tf / peak
+            r["step_roofline_frac"] = FLOP_PER_ROW * st["kept_rows"] / (ms / 1e3) / 1e12 / peak
+        return r
+
+    # C1 (64 pairs over 16 shapes) and C2 (16,384 pairs over 1030 shapes), both precisions
+    for name in ("C1", "C2"):
+        wl = ls.make_workload(name)
+        out[name] = {p: one(wl.points, wl.pairs, wl.poses, getattr(locc, f"LOCC_PREC_{p.upper()}"))
+                     for p in ("fp32", "bf16")}
+    # C5: K x N (bf16); 4M pairs per query at the largest N
+    out["C5"] = {"note": "bf16, s = 0.5; K sets the kept rows per pair, so the encoder FLOPs scale with K "
+                         "(this path crops then encodes; the paper's K-independence is the encode-once mode's)"}
+    for K in (512, 1500, 4096):
+        pts, _ = ls.make_shapes(1030, K, seed=1)
+        pairs, poses = ls.make_pairs_poses(pts, 1 << 22, s=0.5, seed=2)
+        row = {}
+        for n in (1024, 16384, 262144, 1 << 20, 1 << 22):
+            row[str(n)] = one(pts, pairs[:n], poses[:n], locc.LOCC_PREC_BF16)
+        out["C5"][f"K={K}"] = row
+    # C4: closed-loop step (PAPER.md:91: dt = 0.01/4 s in 4 substeps), both detectors, bf16 context
+    pts, _ = ls.make_shapes(1030, 1500, seed=1)
+    ctx = locc.Locc(precision=locc.LOCC_PREC_BF16, device=torch.cuda.current_device())
+    ctx.load_weights_mem(flat)
+    ctx.set_shapes(pts)
+    ctx.load_unet_weights_mem(ls.flatten_unet(ls.make_unet_weights()))
+    ctx.encode_shapes()
+    c4 = {}
+    for E in (4096, 8192, 16384, 32768, 65536):
+        ids, body, st0 = ls.make_sim_scene(pts, E, seed=6)
+        di, db = torch.from_numpy(ids).cuda(), torch.from_numpy(body).cuda()
+        row = {}
+        for det in ("cells", "crop"):
+            sim = dict(ls.SIM_DEFAULTS, detector=det)
+            ds = torch.from_numpy(st0).cuda()
+            for _ in range(2):
+                ctx.sim_run(sim, di, db, ds, stream=stream.cuda_stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+            for k in range(3):
+                ctx.sim_run(sim, di, db, ds, t0=k * sim["h"] * sim["substeps"], stream=stream.cuda_stream)
+            with torch.cuda.stream(stream):
+                e1.record(stream)
+            stream.synchronize()
+            row[det] = e0.elapsed_time(e1) / 3
+        c4[str(E)] = {"pairs_per_substep": 3 * E, "ms_per_dt_encode_once": row["cells"],
+                      "ms_per_dt_crop_bf16": row["crop"]}
+    ctx.close()
+    out["C4"] = c4
+    # the oracle at one host thread (bounded sample)
+    wl = ls.make_workload("C2")
+    oracle.query(flat, wl.points, wl.pairs[:2], wl.poses[:2], bf16_emul=True, n_threads=1)
+    t = time.perf_counter()
+    n1 = 0
+    while time.perf_counter() - t < 5.0:
+        oracle.query(flat, wl.points, wl.pairs[n1:n1 + 4], wl.poses[n1:n1 + 4], bf16_emul=True, n_threads=1)
+        n1 += 4
+    out["oracle_1_thread"] = {"value": n1 / (time.perf_counter() - t), "unit": UNIT, "cores": 1,
+                              "sample": f"first {n1} pairs of C2, bf16-emulating fp64 oracle"}
+    return out
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         return run_reference(a)
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(relaunch_distributed(a))
     import torch
     import torch.distributed as dist
 
@@ -176,6 +314,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"bench.py --gpus {a.gpus} launched with WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -195,6 +335,22 @@ def main():
 
     def step():
         ctx.query_into(d_pairs, d_poses, d_probs, d_labels, stream=stream.cuda_stream)
+
+    if world > 1:
+        # the global batch: this rank's pairs at its shard [rank N, (rank + 1) N) (the only slice the
+        # library reads); every rank ends each step with all world x N results (NCCL, in the library)
+        uid = [locc.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(world, rank, uid[0])
+        g_pairs = torch.zeros(world * N, 2, dtype=torch.int32, device="cuda")
+        g_poses = torch.zeros(world * N, 2, 7, device="cuda")
+        g_pairs[rank * N:(rank + 1) * N] = d_pairs
+        g_poses[rank * N:(rank + 1) * N] = d_poses
+        g_probs = torch.empty(world * N, device="cuda")
+        g_labels = torch.empty(world * N, dtype=torch.uint8, device="cuda")
+
+        def step():  # noqa: F811
+            ctx.query_allgather_into(g_pairs, g_poses, g_probs, g_labels, stream=stream.cuda_stream)
 
     for _ in range(a.warmup):
         step()
@@ -306,7 +462,9 @@ def main():
                        "kept_rows_per_step": kept, "kept_rows_per_pair": kept / N,
                        "evaluated_pairs": st["evaluated_pairs"], "sub_batches": subs,
                        "l2": "L2 flushed (256 MB write) before every timed step; working set (GBs of rows) >> L2",
-                       "parallelism": f"pair-batch shards, 1 process/GPU x {world}"},
+                       "parallelism": f"pair-batch shards, 1 process/GPU x {world}"
+                                      + (", library NCCL gather of all results on every rank (locc_query_allgather)"
+                                         if world > 1 else "")},
             "gpu_launches": launches_per_step * a.steps, "clocks": clk, "roofline": roof}
 
     # NEXT-2: the same step with the pose gradient (locc_query_grad), device-timed the same way
@@ -496,6 +654,17 @@ def main():
                        "d2h_bytes_per_step": N * (4 + 1), "timer": "host perf_counter around the synchronous call"}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(pts, pairs, poses, flat)
+    if world == 1:
+        # the deterministic bf16 mode (locc_set_deterministic: bitwise batch-composition invariance)
+        if prec == locc.LOCC_PREC_BF16:
+            ctx.set_deterministic(True)
+            dms = time_query(ctx, torch, stream, d_pairs, d_poses, d_probs, d_labels, reps=a.steps,
+                             warm=1, flush=flush)
+            ctx.set_deterministic(False)
+            line["deterministic"] = {"value": N / (dms / 1e3), "unit": UNIT, "ms_per_step": dms,
+                                     "api": "locc_set_deterministic(ctx, 1)"}
+        if not a.no_sweep:
+            line["sweep"] = run_sweep(a, locc, torch, stream, flush, peaks)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
