@@ -98,7 +98,7 @@ class Clocks:
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.limit")
 
     def __init__(self, dev):
         self.dev = dev
@@ -117,7 +117,7 @@ class Clocks:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
         out, _ = self.p.communicate(timeout=10)
-        sm, mx, reasons = [], [], set()
+        sm, mx, reasons, pw, lim, capped = [], [], set(), [], [], 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in out.strip().splitlines():
             f = [x.strip() for x in ln.split(",")]
@@ -128,11 +128,21 @@ class Clocks:
                 mx.append(float(f[2]))
             except ValueError:
                 continue
+            try:
+                pw.append(float(f[3]))
+                lim.append(float(f[9]))
+            except (ValueError, IndexError):
+                pass
             for n, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(n)
+            capped += f[8].lower() == "active"
+        # the power trace: draw against the enforced limit while the encoder runs (the sw_power_cap
+        # samples are the ones where the driver lowered the SM clock to stay under the limit)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_median": statistics.median(pw) if pw else None, "power_w_max": max(pw) if pw else None,
+                "power_limit_w": statistics.median(lim) if lim else None, "sw_power_cap_samples": capped}
 
 
 def cpu_baseline(pts, pairs, poses, flat, target_s=15.0):

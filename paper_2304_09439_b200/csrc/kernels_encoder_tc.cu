@@ -34,6 +34,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "internal.h"
 #include "tc_ptx.cuh"
 #include "e3_walk.cuh"
@@ -639,7 +641,10 @@ size_t encoder_tc_smem_bytes() { return sizeof(Smem) + 1024; }
 
 cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b, int num_sms, cudaStream_t st,
                               long long* trace, bool deterministic) {
-  const int spc = 16;
+  // Work unit: a chunk of spc whole segments.  16 segments (~33 tiles at C3) keep the partial last tile
+  // of a chunk cheap; small batches use fewer so that every cluster gets >= 4 chunks to balance.
+  const int64_t clusters = num_sms / 2;
+  const int spc = (int)std::min<int64_t>(16, std::max<int64_t>(1, b.G / (4 * clusters)));
   const int64_t chunks = (b.G + spc - 1) / spc;
   if (chunks == 0) return cudaSuccess;
   if (!P.tc_w2 || !P.tc_w3) return cudaErrorInvalidValue;
