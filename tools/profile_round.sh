@@ -3,7 +3,7 @@
 # of each hot kernel.  Usage: tools/profile_round.sh <tag> [pairs]
 set -e
 TAG=${1:-r1}; PAIRS=${2:-262144}
-CMD="python bench.py --pairs $PAIRS --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+CMD="python bench.py --pairs $PAIRS --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-grad --no-cells --no-sim --no-sweep"
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain_$TAG.log 2>&1
 # launch list: skip shape prep (2 launches) + the warm-up step (7 per sub-batch); capture one step
