@@ -33,9 +33,12 @@ struct Walk {
   int c;
 };
 
-// Out of line: called once per segment end, kept out of the walk's instruction stream.
-__device__ __noinline__ void store_mean(float* pooled, uint32_t seg, uint32_t f, float s, int c) {
-  pooled[(int64_t)seg * 256 + f] = __fdiv_rn(s, (float)c);
+// A segment's pooled features leave the walk as the cell SUM with the cell count (written once, by
+// feature 0); the predictor divides (IEEE, off the walk: a division here sits on the encoder's
+// critical loop).  Out of line: called once per segment end, kept out of the walk's instruction stream.
+__device__ __noinline__ void store_sum(float* pooled, int32_t* cells_c, uint32_t seg, uint32_t f, float s, int c) {
+  pooled[(int64_t)seg * 256 + f] = s;
+  if (f == 0) cells_c[seg] = c;
 }
 
 constexpr uint32_t kEven = 0x55555555u, kOdd = 0xAAAAAAAAu;
@@ -109,11 +112,11 @@ __device__ __forceinline__ void step2(const uint32_t (&vx)[16], const uint32_t (
 // After a step with segment ends: close them (X: store the mean; Y: store, or keep aside if it is
 // Y's first segment end) and restart the walkers (the rest of the step is padding).
 __device__ __forceinline__ void seg_close(uint32_t se2, const uint32_t* flx, const uint32_t* fly, Walk& x, Tail& t,
-                                          float* pooled, uint32_t f) {
+                                          float* pooled, int32_t* cellc, uint32_t f) {
   constexpr float nb3 = 0.f;
   if (se2 & kEven) {
     const int jx = (__ffs(se2 & kEven) - 1) >> 1;
-    store_mean(pooled, flx[jx] >> kRowSegShift, f, x.s, x.c);
+    store_sum(pooled, cellc, flx[jx] >> kRowSegShift, f, x.s, x.c);
     x = Walk{nb3, 0.f, 0};
   }
   if (se2 & kOdd) {
@@ -121,7 +124,7 @@ __device__ __forceinline__ void seg_close(uint32_t se2, const uint32_t* flx, con
     const int jy = (__ffs(se2 & kOdd) - 2) >> 1;
     const uint32_t seg = fly[jy] >> kRowSegShift;
     if (t.se) {
-      store_mean(pooled, seg, f, y.s, y.c);
+      store_sum(pooled, cellc, seg, f, y.s, y.c);
     } else {
       t.s1 = y.s;
       t.c1 = y.c;
@@ -133,14 +136,14 @@ __device__ __forceinline__ void seg_close(uint32_t se2, const uint32_t* flx, con
 }
 
 // x <- x followed by the tail walker's rows (Y's sums exclude its head cell).
-__device__ __forceinline__ void merge2(Walk& x, const Tail& t, float* pooled, uint32_t f) {
+__device__ __forceinline__ void merge2(Walk& x, const Tail& t, float* pooled, int32_t* cellc, uint32_t f) {
   if (!t.ce) {
     x.m = fmaxf(x.m, t.w.m);
     return;
   }
   const float hv = fmaxf(x.m, t.hm);  // the cell open across the boundary
   if (t.se) {
-    store_mean(pooled, t.seg1, f, x.s + hv + t.s1, x.c + 1 + t.c1);
+    store_sum(pooled, cellc, t.seg1, f, x.s + hv + t.s1, x.c + 1 + t.c1);
     x = t.w;
   } else {
     x.s = x.s + hv + t.w.s;
@@ -153,7 +156,7 @@ __device__ __forceinline__ void merge2(Walk& x, const Tail& t, float* pooled, ui
 // A 128-row part: four straight-line steps with a register double buffer of TMEM columns.
 // mk[0..3] = interleaved cell ends of steps 0..3, mk[4..7] = interleaved segment ends.
 __device__ __forceinline__ void e3_part2(uint32_t tbase, const uint32_t* mk, const uint32_t* fl, Walk& w,
-                                         float* pooled, uint32_t f) {
+                                         float* pooled, int32_t* cellc, uint32_t f) {
   constexpr float nb3 = 0.f;
   Tail t;
   t.w = Walk{nb3, 0.f, 0};
@@ -185,7 +188,7 @@ __device__ __forceinline__ void e3_part2(uint32_t tbase, const uint32_t* mk, con
         step2<true>(vx, vy, sel4(ce, c), yc & (0u - yc), w, t);
       else
         step2<false>(vx, vy, sel4(ce, c), 0u, w, t);
-      if (sel4(se, c)) seg_close(sel4(se, c), fl + 16 * c, fl + 64 + 16 * c, w, t, pooled, f);
+      if (sel4(se, c)) seg_close(sel4(se, c), fl + 16 * c, fl + 64 + 16 * c, w, t, pooled, cellc, f);
     }
   } else {
 #pragma unroll 1
@@ -201,10 +204,10 @@ __device__ __forceinline__ void e3_part2(uint32_t tbase, const uint32_t* mk, con
         step2<true>(xa, ya, cec, yc & (0u - yc), w, t);
       else
         step2<false>(xa, ya, cec, 0u, w, t);
-      if (sec) seg_close(sec, fl + 16 * c, fl + 64 + 16 * c, w, t, pooled, f);
+      if (sec) seg_close(sec, fl + 16 * c, fl + 64 + 16 * c, w, t, pooled, cellc, f);
     }
   }
-  merge2(w, t, pooled, f);
+  merge2(w, t, pooled, cellc, f);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -265,7 +268,7 @@ struct Head {
 template <bool kYHead>
 __device__ __forceinline__ void block(int c, const uint32_t (&vx)[16], const uint32_t (&vy)[16], uint32_t cec,
                                       uint32_t sec, int ys, int b0, Walk& w, Walk& y, Head& h, const uint32_t* fl,
-                                      float* pooled, uint32_t f) {
+                                      float* pooled, int32_t* cellc, uint32_t f) {
   float px, py;
   if (kYHead) h.hm0 = y.m;
   step2<kYHead>(vx, vy, cec, w, y, px, py, h.prev, h.last);
@@ -277,13 +280,13 @@ __device__ __forceinline__ void block(int c, const uint32_t (&vx)[16], const uin
   if (sec) {
     if (sec & kEven) {  // X closes its segment (the rest of its block is padding)
       const int jx = (__ffs(sec & kEven) - 1) >> 1;
-      store_mean(pooled, fl[16 * c + jx] >> kRowSegShift, f, w.s, w.c);
+      store_sum(pooled, cellc, fl[16 * c + jx] >> kRowSegShift, f, w.s, w.c);
       w = Walk{0.f, 0.f, 0};
     }
     if (sec & kOdd) {
       if (c > ys) {  // a whole segment of Y's own
         const int jy = (__ffs(sec & kOdd) - 2) >> 1;
-        store_mean(pooled, fl[64 + 16 * c + jy] >> kRowSegShift, f, y.s, y.c);
+        store_sum(pooled, cellc, fl[64 + 16 * c + jy] >> kRowSegShift, f, y.s, y.c);
       } else {
         h.hc = y.c;  // Y's head cells (its head segment is closed in the merge)
       }
@@ -296,7 +299,7 @@ __device__ __forceinline__ void block(int c, const uint32_t (&vx)[16], const uin
 // merge.  mk[0..3] = interleaved cell ends of blocks 0..3, mk[4..7] = interleaved segment ends.  `w`
 // is X's carried state in and the part's final state out.
 __device__ __forceinline__ void e3_part2_det(uint32_t tbase, const uint32_t* mk, const uint32_t* fl, Walk& w,
-                                         float* pooled, uint32_t f) {
+                                         float* pooled, int32_t* cellc, uint32_t f) {
   const uint4 ce = *reinterpret_cast<const uint4*>(mk);
   const uint4 se = *reinterpret_cast<const uint4*>(mk + 4);
   // Y's first segment end is in block ys (4 = none in this part); its first cell end in block b0
@@ -323,9 +326,9 @@ __device__ __forceinline__ void e3_part2_det(uint32_t tbase, const uint32_t* mk,
       tmem_ld16(tbase + 64 + 16 * b0, nx);  // block b0's Y columns again, for the merge's re-walk (xa is free)
     }
     if (c == b0)
-      block<true>(c, vx, vy, sel4(ce, c), sel4(se, c), ys, b0, w, y, h, fl, pooled, f);
+      block<true>(c, vx, vy, sel4(ce, c), sel4(se, c), ys, b0, w, y, h, fl, pooled, cellc, f);
     else
-      block<false>(c, vx, vy, sel4(ce, c), sel4(se, c), ys, b0, w, y, h, fl, pooled, f);
+      block<false>(c, vx, vy, sel4(ce, c), sel4(se, c), ys, b0, w, y, h, fl, pooled, cellc, f);
   }
   if (ys == 4) h.hc = y.c;
   // merge: X's sum continues with Y's head blocks b0..ys in block order
@@ -353,7 +356,7 @@ __device__ __forceinline__ void e3_part2_det(uint32_t tbase, const uint32_t* mk,
     const int cnt = w.c + h.hc;
     if (ys < 4) {  // Y's first segment end closed X's segment
       const int jy = (__ffs(sel4(se, ys) & kOdd) - 2) >> 1;
-      store_mean(pooled, fl[64 + 16 * ys + jy] >> kRowSegShift, f, s, cnt);
+      store_sum(pooled, cellc, fl[64 + 16 * ys + jy] >> kRowSegShift, f, s, cnt);
       w = y;
     } else {
       w.s = s;

@@ -119,7 +119,9 @@ struct Batch {
   uint2* rows;           // [sum pad16(n)] kept rows: (flags, point index k in the own shape's sorted table)
   const float4* pts;     // the shape table's sorted points [S][K] (the rows' coordinates: pts[own K + k])
   int K;
-  float* pooled;         // [G][H] mean over occupied cells of the cell-max features
+  float* pooled;         // [G][H] mean over occupied cells of the cell-max features, or their SUM when
+                         // cells_c is set (the tensor-core encoder; the predictor divides)
+  int32_t* cells_c;      // [G] occupied cells C of each non-empty segment when pooled holds sums, else null
   const float* emb_in;   // encode-once mode: [G][F] pooled cell embeddings (the predictor's e); else null
   float4* xf;            // [G][4] per-segment transform into the other object's frame (segment_xf_kernel):
                          // rows (R00 R01 R02 t0), (R10 R11 R12 t1), (R20 R21 R22 t2), (own, other, -, -) as ints;

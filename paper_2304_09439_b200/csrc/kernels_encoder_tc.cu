@@ -128,7 +128,8 @@ struct TcArgs {
   const float4* xf;       // per-segment transforms (own shape id in [4 seg + 3].x)
   int K;
   const int64_t* offsets;
-  float* pooled;
+  float* pooled;     // [G][256] cell sums (the predictor divides by cells_c)
+  int32_t* cells_c;  // [G] occupied cells per segment
   int64_t G;
   int64_t n_chunks;
   int seg_per_chunk;
@@ -614,9 +615,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         tc_fence_after();
         const uint32_t tb = tmem + ((32 * q) << 16) + region_col(p ? kRegionP1 : R.P);
         if (kDet)
-          e3_part2_det(tb, S.masks + 8 * p, S.flags + 128 * p, w, a.pooled, f);
+          e3_part2_det(tb, S.masks + 8 * p, S.flags + 128 * p, w, a.pooled, a.cells_c, f);
         else
-          e3_part2(tb, S.masks + 8 * p, S.flags + 128 * p, w, a.pooled, f);
+          e3_part2(tb, S.masks + 8 * p, S.flags + 128 * p, w, a.pooled, a.cells_c, f);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&S.bar[p ? B_D3E1 : B_D3E0], 0);
@@ -660,6 +661,8 @@ cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b
   args.K = b.K;
   args.offsets = b.offsets;
   args.pooled = b.pooled;
+  args.cells_c = b.cells_c;
+  if (!b.cells_c) return cudaErrorInvalidValue;
   args.G = b.G;
   args.n_chunks = chunks;
   args.seg_per_chunk = spc;

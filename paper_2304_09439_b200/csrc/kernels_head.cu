@@ -291,7 +291,13 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_tile_kernel(DevParams P,
       for (int i = 0; i < 8; ++i) {
         const int e = e0 + i * kHeadThreads + tid, s = e / 64, j4 = e % 64;
         x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (S.nside[s] > 0) x[i] = __ldg(reinterpret_cast<const float4*>(b.pooled + (2 * i0 + s) * (int64_t)256) + j4);
+        if (S.nside[s] > 0) {
+          x[i] = __ldg(reinterpret_cast<const float4*>(b.pooled + (2 * i0 + s) * (int64_t)256) + j4);
+          if (b.cells_c) {  // the tensor-core encoder leaves cell sums: m = S / C
+            const float c = (float)b.cells_c[2 * i0 + s];
+            x[i] = make_float4(__fdiv_rn(x[i].x, c), __fdiv_rn(x[i].y, c), __fdiv_rn(x[i].z, c), __fdiv_rn(x[i].w, c));
+          }
+        }
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -432,7 +438,10 @@ __global__ void __launch_bounds__(128) head_kernel(DevParams P, Batch b, float* 
   } else {
     for (int idx = tid; idx < NS * H; idx += blockDim.x) {
       const int s = idx / H, j = idx - s * H;
-      X[j * LD + s] = nside[s] > 0 ? b.pooled[(2 * i0 + s) * (int64_t)H + j] : 0.f;
+      X[j * LD + s] = nside[s] > 0 ? (b.cells_c ? __fdiv_rn(b.pooled[(2 * i0 + s) * (int64_t)H + j],
+                                                             (float)b.cells_c[2 * i0 + s])
+                                                  : b.pooled[(2 * i0 + s) * (int64_t)H + j])
+                                   : 0.f;
     }
     __syncthreads();
     dense_t<NS / 2>(P.wfT, P.bf, H, F, X, (tid >> 6) * (NS / 2), Z, false, tid & 63, 64);

@@ -198,6 +198,8 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
       if constexpr (kProj) {
         // m (the pooled 256-vector) in two K halves through A; e = D + b_F afterwards
         const float4* m4 = reinterpret_cast<const float4*>(b.pooled + g * 256);
+        // the tensor-core encoder leaves cell sums: m = S / C (IEEE division)
+        const float cnt = (b.cells_c && ns > 0) ? (float)b.cells_c[g] : 1.f;
         for (int h = 0; h < 2; ++h) {
           if (h == 1) {  // the first half has been consumed
             mbar_wait(&S.d_full, dph);
@@ -210,7 +212,11 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
 #pragma unroll
             for (int k = 0; k < 32; k += 4) {
               float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (ns > 0) v = __ldg(m4 + ((128 * h + c0 + k) >> 2));
+              if (ns > 0) {
+                v = __ldg(m4 + ((128 * h + c0 + k) >> 2));
+                if (b.cells_c)
+                  v = make_float4(__fdiv_rn(v.x, cnt), __fdiv_rn(v.y, cnt), __fdiv_rn(v.z, cnt), __fdiv_rn(v.w, cnt));
+              }
               x[k] = v.x, x[k + 1] = v.y, x[k + 2] = v.z, x[k + 3] = v.w;
             }
             put32(trow, c0, x);

@@ -140,9 +140,10 @@ struct locc_ctx {
   // scratch for one sub-batch
   int64_t cap_B = 0;
   DevBuf trace;
-  DevBuf in_pairs, in_poses, in_pairs2, in_poses2, counts, occ, offsets, scan_tmp, rows, pooled, stats, xf, kbits;
+  DevBuf in_pairs, in_poses, in_pairs2, in_poses2, counts, occ, offsets, scan_tmp, rows, pooled, stats, xf, kbits,
+      cellc;
   // second buffer set of the overlapped crop pipeline (sub-batches alternate between the two)
-  DevBuf counts2, offsets2, scan_tmp2, rows2, pooled2, xf2, kbits2;
+  DevBuf counts2, offsets2, scan_tmp2, rows2, pooled2, xf2, kbits2, cellc2;
   int64_t cap_B2 = 0;
   DevBuf out_probs, out_labels, out_logits, out_kept, out_occ, out_masks, out_emb, out_grad;
   locc_stats last{};
@@ -404,6 +405,7 @@ locc_status ensure_scratch2(locc_ctx* c, int64_t B) {
     CK(c->scan_tmp2.ensure(sizeof(int64_t) * scan_tmp_elems(G)));
     CK(c->rows2.ensure(sizeof(uint2) * (size_t)G * seg_rows(K)));
     CK(c->pooled2.ensure(sizeof(float) * (size_t)G * c->cfg.H));
+    CK(c->cellc2.ensure(sizeof(int32_t) * G));
     CK(c->xf2.ensure(sizeof(float4) * 4 * G));
     CK(c->kbits2.ensure(sizeof(uint32_t) * G * ((K + 31) / 32)));
     c->cap_B2 = B;
@@ -427,6 +429,7 @@ locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks, bool need_gr
     CK(c->scan_tmp.ensure(sizeof(int64_t) * scan_tmp_elems(G)));
     CK(c->rows.ensure(sizeof(uint2) * (size_t)G * seg_rows(K)));
     CK(c->pooled.ensure(sizeof(float) * (size_t)G * c->cfg.H));
+    CK(c->cellc.ensure(sizeof(int32_t) * G));
     CK(c->out_probs.ensure(sizeof(float) * B));
     CK(c->out_labels.ensure(B));
     CK(c->out_logits.ensure(sizeof(float) * B));
@@ -586,6 +589,8 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     b.pts = c->T.pts;
     b.K = c->T.K;
     b.pooled = (set2 ? c->pooled2 : c->pooled).as<float>();
+    // the tensor-core encoder leaves cell sums and counts (the predictor divides); fp32: means
+    b.cells_c = (!cells && c->cfg.precision == LOCC_PREC_BF16) ? (set2 ? c->cellc2 : c->cellc).as<int32_t>() : nullptr;
     b.stats = dstats;
     b.xf = (set2 ? c->xf2 : c->xf).as<float4>();
     b.kbits = (set2 ? c->kbits2 : c->kbits).as<uint32_t>();

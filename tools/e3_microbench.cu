@@ -32,7 +32,7 @@ __host__ __device__ inline float val(int r, int f) { return (float)((r * 37 + f 
 
 // Reference point: ONE sequential walker per 128-row part (exact sequential sum, no merge, no ILP).
 __device__ __forceinline__ void part1(uint32_t tbase, const uint32_t* ce, const uint32_t* se, const uint32_t* fl,
-                                      Walk& w, float* pooled, uint32_t f) {
+                                      Walk& w, float* pooled, int32_t* cellc, uint32_t f) {
   uint32_t va[16], vb[16];
   tmem_ld16(tbase, va);
 #pragma unroll
@@ -51,7 +51,7 @@ __device__ __forceinline__ void part1(uint32_t tbase, const uint32_t* ce, const 
     w.c += __popc(bits);
     const uint32_t sb = (se[g >> 1] >> (16 * (g & 1))) & 0xFFFFu;
     if (sb) {
-      store_mean(pooled, fl[16 * g + __ffs(sb) - 1] >> kRowSegShift, f, w.s, w.c);
+      store_sum(pooled, cellc, fl[16 * g + __ffs(sb) - 1] >> kRowSegShift, f, w.s, w.c);
       w = Walk{0.f, 0.f, 0};
     }
   }
@@ -59,7 +59,7 @@ __device__ __forceinline__ void part1(uint32_t tbase, const uint32_t* ce, const 
 
 template <int V, int NOISE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (4 + NOISE), 1)
-    kern(const uint32_t* __restrict__ gflags, int ntiles, const float* __restrict__ b3g, float* pooled,
+    kern(const uint32_t* __restrict__ gflags, int ntiles, const float* __restrict__ b3g, float* pooled, int32_t* cellc,
          long long* cycles) {
   __shared__ Sm S;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -104,11 +104,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(32 * (4 + NOISE), 1)
       for (int p = 0; p < 2; ++p) {
         const uint32_t tbase = tmem + ((32 * q) << 16) + 128 * p;
         if (V == 0) {
-          e3_part2(tbase, S.masks + 8 * p, S.flags + 128 * p, w, pooled, f);
+          e3_part2(tbase, S.masks + 8 * p, S.flags + 128 * p, w, pooled, cellc, f);
         } else if (V == 2) {
-          part1(tbase, S.pce + 4 * p, S.pse + 4 * p, S.flags + 128 * p, w, pooled, f);
+          part1(tbase, S.pce + 4 * p, S.pse + 4 * p, S.flags + 128 * p, w, pooled, cellc, f);
         } else if (V == 5) {
-          e3_part2_det(tbase, S.masks + 8 * p, S.flags + 128 * p, w, pooled, f);
+          e3_part2_det(tbase, S.masks + 8 * p, S.flags + 128 * p, w, pooled, cellc, f);
         } else {  // TMEM loads of the walk's schedule only
           uint32_t xa[16], ya[16];
           uint32_t acc = 0;
@@ -212,13 +212,22 @@ double run(const std::vector<uint32_t>& fl, int ntiles, int nseg, const std::vec
   cudaMalloc(&dp, (size_t)nseg * 256 * 4);
   cudaMemset(dp, 0, (size_t)nseg * 256 * 4);
   cudaMalloc(&dc, 8 * 8);
-  kern<V, NOISE><<<2, 32 * (4 + NOISE)>>>(dfl, ntiles, db3, dp, dc);
+  int32_t* dcell;
+  cudaMalloc(&dcell, (size_t)nseg * 4);
+  cudaMemset(dcell, 0, (size_t)nseg * 4);
+  kern<V, NOISE><<<2, 32 * (4 + NOISE)>>>(dfl, ntiles, db3, dp, dcell, dc);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
   long long c[8];
   cudaMemcpy(c, dc, 64, cudaMemcpyDeviceToHost);
   out.resize((size_t)nseg * 256);
   cudaMemcpy(out.data(), dp, out.size() * 4, cudaMemcpyDeviceToHost);
+  std::vector<int32_t> cc(nseg);
+  cudaMemcpy(cc.data(), dcell, (size_t)nseg * 4, cudaMemcpyDeviceToHost);
+  cudaFree(dcell);
+  for (int sg = 0; sg < nseg; ++sg)  // the walk leaves cell sums and counts: the mean, as the predictor forms it
+    for (int f = 0; f < 128; ++f)
+      if (cc[sg] > 0) out[(size_t)sg * 256 + f] /= (float)cc[sg];
   cudaFree(dfl);
   cudaFree(db3);
   cudaFree(dp);
