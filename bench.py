@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-sim", action="store_true", help="skip the NEXT-3 closed-loop measurement")
     ap.add_argument("--sim-envs", type=int, default=30000)
     ap.add_argument("--no-sweep", action="store_true", help="skip the config-table sweep (C1/C2/C4/C5)")
+    ap.add_argument("--allgather", action="store_true",
+                    help="time the library NCCL gather (locc_query_allgather) even in a world of one rank")
     return ap.parse_args()
 
 
@@ -346,11 +348,12 @@ def main():
     def step():
         ctx.query_into(d_pairs, d_poses, d_probs, d_labels, stream=stream.cuda_stream)
 
-    if world > 1:
+    if world > 1 or a.allgather:
         # the global batch: this rank's pairs at its shard [rank N, (rank + 1) N) (the only slice the
         # library reads); every rank ends each step with all world x N results (NCCL, in the library)
         uid = [locc.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
         ctx.comm_init(world, rank, uid[0])
         g_pairs = torch.zeros(world * N, 2, dtype=torch.int32, device="cuda")
         g_poses = torch.zeros(world * N, 2, 7, device="cuda")
@@ -474,7 +477,7 @@ def main():
                        "l2": "L2 flushed (256 MB write) before every timed step; working set (GBs of rows) >> L2",
                        "parallelism": f"pair-batch shards, 1 process/GPU x {world}"
                                       + (", library NCCL gather of all results on every rank (locc_query_allgather)"
-                                         if world > 1 else "")},
+                                         if world > 1 or a.allgather else "")},
             "gpu_launches": launches_per_step * a.steps, "clocks": clk, "roofline": roof}
 
     # NEXT-2: the same step with the pose gradient (locc_query_grad), device-timed the same way
