@@ -179,6 +179,14 @@ cudaError_t launch_head_tc(const DevParams& P, const Batch& b, float* probs, uin
 size_t scan_tmp_elems(int64_t G);
 size_t encoder_tc_smem_bytes();
 
+// x / c for a pooled cell sum x and a cell count c (1 <= c <= 216): x * RN(1/c) corrected once with the
+// exact FMA residual (Markstein) — bitwise the IEEE quotient __fdiv_rn(x, c) (tools/div_check.cu checks
+// every fp32 mantissa in two binades against it for c = 1..216; normal range) at a multiply and two FMAs.
+__device__ __forceinline__ float div_count(float x, float c, float rc) {
+  const float q0 = x * rc;
+  return fmaf(fmaf(-q0, c, x), rc, q0);
+}
+
 // Opts kernel `fn` into `bytes` of dynamic shared memory on the CURRENT device.  Function attributes
 // are per device, so this is done once per (device, kernel) and remembered (locc_runtime.cu); every
 // launcher with more than 48 KB calls it before its launch.

@@ -294,8 +294,9 @@ __global__ void __launch_bounds__(kHeadThreads, 1) head_tile_kernel(DevParams P,
         if (S.nside[s] > 0) {
           x[i] = __ldg(reinterpret_cast<const float4*>(b.pooled + (2 * i0 + s) * (int64_t)256) + j4);
           if (b.cells_c) {  // the tensor-core encoder leaves cell sums: m = S / C
-            const float c = (float)b.cells_c[2 * i0 + s];
-            x[i] = make_float4(__fdiv_rn(x[i].x, c), __fdiv_rn(x[i].y, c), __fdiv_rn(x[i].z, c), __fdiv_rn(x[i].w, c));
+            const float c = (float)b.cells_c[2 * i0 + s], rc = __frcp_rn(c);
+            x[i] = make_float4(div_count(x[i].x, c, rc), div_count(x[i].y, c, rc), div_count(x[i].z, c, rc),
+                               div_count(x[i].w, c, rc));
           }
         }
       }
@@ -441,7 +442,7 @@ __global__ void __launch_bounds__(128) head_kernel(DevParams P, Batch b, float* 
       X[j * LD + s] = nside[s] > 0 ? (b.cells_c ? __fdiv_rn(b.pooled[(2 * i0 + s) * (int64_t)H + j],
                                                              (float)b.cells_c[2 * i0 + s])
                                                   : b.pooled[(2 * i0 + s) * (int64_t)H + j])
-                                   : 0.f;
+                                   : 0.f;  // (head_kernel: configurations other than H = 256, F = 64)
     }
     __syncthreads();
     dense_t<NS / 2>(P.wfT, P.bf, H, F, X, (tid >> 6) * (NS / 2), Z, false, tid & 63, 64);

@@ -14,8 +14,11 @@
 //   warps 2+   epilogue (TMEM lane quadrant = warp % 4, thread = row r): per layer tcgen05.ld the
 //              accumulator row, bias + ReLU, split, and tcgen05.st the next layer's A row (hi, lo);
 //              8 warps (two column halves per row) in the forward variants, 4 with the gradient
-// TMEM (512 columns): D = 0..127, A_hi = 128..255, A_lo = 256..383 (A: row = lane, K = column), so the
-// operands never touch shared memory and 160 KB of it holds the weight ring.
+// TMEM (512 columns): two accumulators D0 = 0..127 and D1 = 384..511 used by alternate layers,
+// A_hi = 128..255, A_lo = 256..383 (A: row = lane, K = column), so the operands never touch shared
+// memory and 160 KB of it holds the weight ring.  The epilogue hands the next layer's A over per
+// 32-column K chunk (one mbarrier per chunk) and the MMA warp issues that chunk's products at once, into
+// the other accumulator: layer l + 1's MMAs overlap layer l's epilogue.
 // Rows: side s of the tile in row s (pair p = sides 2p, 2p+1); the pair layers keep pair p in row 2p
 // and zeros in the odd rows, so the max across the pair and the gradient's routing back to the two
 // sides are shuffles between adjacent lanes.
@@ -43,7 +46,9 @@ constexpr int kStages = 5;          // weight ring
 constexpr int kLayers = 6;
 constexpr int kChunks = 23;         // obj1 3 (K = 71 padded to 96), obj2, obj3, pair1..3 4 each
 constexpr int kBwd = 5;             // reverse GEMMs: pair3^T, pair2^T, pair1^T, obj3^T, obj2^T (4 chunks each)
-constexpr uint32_t kColD = 0, kColAH = 128, kColAL = 256;
+constexpr uint32_t kColD0 = 0, kColD1 = 384, kColAH = 128, kColAL = 256;
+// Accumulator of the stage with D counter sd (both projection halves share one stage's accumulator).
+__device__ __forceinline__ uint32_t dcol(uint32_t sd) { return (sd & 1) ? kColD1 : kColD0; }
 __constant__ int kLayerChunks[kLayers + kBwd] = {3, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4};
 
 struct __align__(1024) HeadTcSmem {
@@ -60,7 +65,7 @@ struct __align__(1024) HeadTcSmem {
   uint32_t mask[kLayers][128][4];
   uint32_t selA[64][4];
   float o1p[7][128];
-  uint64_t w_full[kStages], w_empty[kStages], a_full, d_full;
+  uint64_t w_full[kStages], w_empty[kStages], a_full[4], d_full;  // a_full[j]: A's K chunk j written
   uint32_t tmem_base;
 };
 
@@ -83,10 +88,13 @@ __device__ __forceinline__ void put32(uint32_t arow, int c0, const float (&x)[32
   tmem_st32(arow + kColAL + c0, l);
 }
 
-__device__ __forceinline__ void a_ready(HeadTcSmem& S) {
+// This warp's rows of A's K chunk (columns c0 .. c0 + 31) are written: one arrival per warp (a chunk is
+// written by the 4 warps of one column group, one per TMEM lane quadrant).
+__device__ __forceinline__ void chunk_ready(HeadTcSmem& S, int c0) {
   tmem_st_wait();
   tc_fence_before();
-  mbar_arrive(&S.a_full);
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&S.a_full[c0 >> 5]);
 }
 
 // kGrad variants keep 4 epilogue warps (their register footprint); the forward variants run 8, two per
@@ -116,7 +124,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
       mbar_init(&S.w_full[i], 1);
       mbar_init(&S.w_empty[i], 1);
     }
-    mbar_init(&S.a_full, 32 * kEW);
+    for (int j = 0; j < 4; ++j) mbar_init(&S.a_full[j], 4);
     mbar_init(&S.d_full, 1);
     fence_mbar_init();
   }
@@ -150,16 +158,16 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
     // ---------------------------------------------------------------- MMA issuer
     constexpr int kL0 = kProj ? -2 : 0;
     constexpr int kLEnd = kGrad ? kLayers + kBwd : kLayers;
-    uint32_t n = 0, aph = 0;
+    uint32_t n = 0, aph = 0, sd = 0;  // aph bit j: phase of a_full[j]; sd: accumulator counter
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
       for (int l = kL0; l < kLEnd; ++l) {
         // l = -2, -1: the projection's two K halves (N = 64; the second accumulates onto the first)
         const uint32_t idesc = l < 0 ? idesc_tf32_f32(128, 64) : idesc_tf32_f32(128, 128);
         const int nch = l < 0 ? 4 : kLayerChunks[l];
-        mbar_wait_spin(&S.a_full, aph);
-        aph ^= 1;
-        tc_fence_after();
+        const uint32_t d = tmem + dcol(sd);
         for (int j = 0; j < nch; ++j, ++n) {
+          mbar_wait_spin(&S.a_full[j], (aph >> j) & 1);  // A's chunk j of this stage
+          aph ^= 1u << j;
           const uint32_t st = n % kStages;
           mbar_wait_spin(&S.w_full[st], (n / kStages) & 1);
           tc_fence_after();
@@ -168,16 +176,16 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint32_t kc = (uint32_t)(32 * j + 8 * k), bo = 32u * k;
-              mma_tf32_ts(tmem + kColD, tmem + kColAH + kc, smem_desc_sw128(bhi + bo, 1024), idesc,
-                          (l == -1) || (j | k) != 0);
-              mma_tf32_ts(tmem + kColD, tmem + kColAH + kc, smem_desc_sw128(blo + bo, 1024), idesc, 1);
-              mma_tf32_ts(tmem + kColD, tmem + kColAL + kc, smem_desc_sw128(bhi + bo, 1024), idesc, 1);
+              mma_tf32_ts(d, tmem + kColAH + kc, smem_desc_sw128(bhi + bo, 1024), idesc, (l == -1) || (j | k) != 0);
+              mma_tf32_ts(d, tmem + kColAH + kc, smem_desc_sw128(blo + bo, 1024), idesc, 1);
+              mma_tf32_ts(d, tmem + kColAL + kc, smem_desc_sw128(bhi + bo, 1024), idesc, 1);
             }
             mma_commit_1cta(&S.w_empty[st]);
             if (j == nch - 1) mma_commit_1cta(&S.d_full);
           }
           __syncwarp();
         }
+        if (l != -2) ++sd;
       }
   } else {
     // ---------------------------------------------------------------- epilogue (warps 2..5)
@@ -186,7 +194,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
     const int cb = half * kCols, eb = half * (kCols / 2);  // first column of 128-wide / 64-wide rows
     const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
     const bool odd = r & 1;
-    uint32_t dph = 0;
+    uint32_t dph = 0, sd = 0;  // d_full phase; accumulator counter (as the MMA warp's)
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int64_t i0 = t * kHP;
       const int npairs = (int)min((int64_t)kHP, b.B - i0);
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
         // m (the pooled 256-vector) in two K halves through A; e = D + b_F afterwards
         const float4* m4 = reinterpret_cast<const float4*>(b.pooled + g * 256);
         // the tensor-core encoder leaves cell sums: m = S / C (IEEE division)
-        const float cnt = (b.cells_c && ns > 0) ? (float)b.cells_c[g] : 1.f;
+        const float cnt = (b.cells_c && ns > 0) ? (float)b.cells_c[g] : 1.f, rcnt = __frcp_rn(cnt);
         for (int h = 0; h < 2; ++h) {
           if (h == 1) {  // the first half has been consumed
             mbar_wait(&S.d_full, dph);
@@ -215,13 +223,14 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
               if (ns > 0) {
                 v = __ldg(m4 + ((128 * h + c0 + k) >> 2));
                 if (b.cells_c)
-                  v = make_float4(__fdiv_rn(v.x, cnt), __fdiv_rn(v.y, cnt), __fdiv_rn(v.z, cnt), __fdiv_rn(v.w, cnt));
+                  v = make_float4(div_count(v.x, cnt, rcnt), div_count(v.y, cnt, rcnt), div_count(v.z, cnt, rcnt),
+                                  div_count(v.w, cnt, rcnt));
               }
               x[k] = v.x, x[k + 1] = v.y, x[k + 2] = v.z, x[k + 3] = v.w;
             }
             put32(trow, c0, x);
+            chunk_ready(S, c0);
           }
-          a_ready(S);
         }
         mbar_wait(&S.d_full, dph);
         dph ^= 1;
@@ -229,17 +238,19 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
 #pragma unroll 1
         for (int c0 = eb; c0 < eb + kCols / 2; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(trow + kColD + c0, v);
+          tmem_ld32(trow + dcol(sd) + c0, v);
           tmem_ld_wait();
           float x[32];
 #pragma unroll
           for (int k = 0; k < 32; ++k) x[k] = ns > 0 ? __uint_as_float(v[k]) + S.bf[c0 + k] : 0.f;
           put32(trow, c0, x);
+          chunk_ready(S, c0);
           if (emb && live)
 #pragma unroll
             for (int k = 0; k < 32; k += 4)
               *reinterpret_cast<float4*>(emb + g * 64 + c0 + k) = make_float4(x[k], x[k + 1], x[k + 2], x[k + 3]);
         }
+        ++sd;
       } else {
         const float4* e4 = reinterpret_cast<const float4*>(b.emb_in + g * 64);
 #pragma unroll 1
@@ -252,6 +263,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
             x[k] = v.x, x[k + 1] = v.y, x[k + 2] = v.z, x[k + 3] = v.w;
           }
           put32(trow, c0, x);
+          chunk_ready(S, c0);
         }
       }
       {
@@ -273,10 +285,12 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
 #pragma unroll
           for (int c = 0; c < 3; ++c) x[4 + c] = pose[4 + c];
         }
-        if (half == kHalves - 1) put32(trow, 64, x);
+        if (half == kHalves - 1) {
+          put32(trow, 64, x);
+          chunk_ready(S, 64);
+        }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEW) : "memory");  // nside of every side visible to the pair rows
-      a_ready(S);
       // ---- forward layers
       for (int l = 0; l < kLayers; ++l) {
         mbar_wait(&S.d_full, dph);
@@ -288,7 +302,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
 #pragma unroll 1
           for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
             uint32_t v[32];
-            tmem_ld32(trow + kColD + c0, v);
+            tmem_ld32(trow + dcol(sd) + c0, v);
             tmem_ld_wait();
             float x[32];
             uint32_t bits = 0;
@@ -298,6 +312,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
               bits |= (uint32_t)(x[k] > 0.f) << k;
             }
             put32(trow, c0, x);
+            chunk_ready(S, c0);
             if (kGrad) S.mask[l][r][c0 >> 5] = bits;
           }
         } else if (l == 2) {
@@ -305,7 +320,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
 #pragma unroll 1
           for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
             uint32_t v[32];
-            tmem_ld32(trow + kColD + c0, v);
+            tmem_ld32(trow + dcol(sd) + c0, v);
             tmem_ld_wait();
             float x[32];
             uint32_t mb = 0, sb = 0;
@@ -318,6 +333,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
               sb |= (uint32_t)(mine > other) << k;  // even lane: u_A > u_B (ties -> B)
             }
             put32(trow, c0, x);
+            chunk_ready(S, c0);
             if (kGrad) {
               S.mask[2][r][c0 >> 5] = mb;
               if (!odd) S.selA[r >> 1][c0 >> 5] = sb;
@@ -329,7 +345,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
 #pragma unroll 1
           for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
             uint32_t v[32];
-            tmem_ld32(trow + kColD + c0, v);
+            tmem_ld32(trow + dcol(sd) + c0, v);
             tmem_ld_wait();
             float x[32];
             uint32_t bits = 0;
@@ -339,6 +355,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
               bits |= (uint32_t)(x[k] > 0.f) << k;
             }
             put32(trow, c0, x);
+            chunk_ready(S, c0);
             if (kGrad) S.mask[l][r][c0 >> 5] = bits;
           }
         } else {
@@ -347,7 +364,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
 #pragma unroll 1
           for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
             uint32_t v[32];
-            tmem_ld32(trow + kColD + c0, v);
+            tmem_ld32(trow + dcol(sd) + c0, v);
             tmem_ld_wait();
             float x[32];
 #pragma unroll
@@ -356,7 +373,10 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
               acc = fmaf(S.wout[c0 + k], fmaxf(pre, 0.f), acc);
               x[k] = (!odd && pre > 0.f) ? S.wout[c0 + k] : 0.f;
             }
-            if (kGrad) put32(trow, c0, x);
+            if (kGrad) {
+              put32(trow, c0, x);
+              chunk_ready(S, c0);
+            }
           }
           if constexpr (kHalves == 2) {
             S.part[half][r] = acc;
@@ -380,7 +400,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
             if (logits) logits[i] = lg;
           }
         }
-        if (kGrad || l < kLayers - 1) a_ready(S);
+        ++sd;
       }
       if constexpr (kGrad) {
         // ---- reverse GEMMs: B1 (pair3^T) -> d/d c2, B2 -> d/d c1, B3 (pair1^T) -> d/d v,
@@ -395,20 +415,21 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
 #pragma unroll 1
             for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
               uint32_t v[32];
-              tmem_ld32(trow + kColD + c0, v);
+              tmem_ld32(trow + dcol(sd) + c0, v);
               tmem_ld_wait();
               const uint32_t m = S.mask[ml][r][c0 >> 5];
               float x[32];
 #pragma unroll
               for (int k = 0; k < 32; ++k) x[k] = (m >> k) & 1u ? __uint_as_float(v[k]) : 0.f;
               put32(trow, c0, x);
+              chunk_ready(S, c0);
             }
           } else if (l == 2) {
             // d/d v of pair p (row 2p) routed to the side the max selected, masked by u > 0
 #pragma unroll 1
             for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
               uint32_t v[32];
-              tmem_ld32(trow + kColD + c0, v);
+              tmem_ld32(trow + dcol(sd) + c0, v);
               tmem_ld_wait();
               const uint32_t sa = S.selA[r >> 1][c0 >> 5];
               const uint32_t m = S.mask[2][r][c0 >> 5] & (odd ? ~sa : sa);
@@ -419,6 +440,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
                 x[k] = (m >> k) & 1u ? gv : 0.f;
               }
               put32(trow, c0, x);
+              chunk_ready(S, c0);
             }
           } else {
             // d/d a1 masked by a1 > 0 = d/d pre1; d/d z[F + c] = sum_o O1[o][F + c] d/d pre1[o]
@@ -426,7 +448,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
 #pragma unroll 1
             for (int c0 = cb; c0 < cb + kCols; c0 += 32) {
               uint32_t v[32];
-              tmem_ld32(trow + kColD + c0, v);
+              tmem_ld32(trow + dcol(sd) + c0, v);
               tmem_ld_wait();
               const uint32_t m = S.mask[0][r][c0 >> 5];
 #pragma unroll
@@ -460,7 +482,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
               }
             }
           }
-          if (l < kBwd - 1) a_ready(S);
+          ++sd;
         }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEW) : "memory");  // this tile's nside reads precede the next tile's writes
