@@ -96,6 +96,8 @@ typedef struct {
   double  head_ms;          /* device time of the predictor launches (0 if timing off); in the
                                encode-once mode encoder_ms is the cell selection's time */
   double  crop_ms;          /* device time of the transform + crop + compaction launches (0 if timing off) */
+  int64_t graph_replay;     /* 1 if the query was replayed from the context's CUDA graph (asynchronous
+                               device-buffer queries of one sub-batch; see locc_query) */
 } locc_stats;
 
 /* Create a context on cfg->device, or on the cfg->n_devices devices of cfg->device_ids (peer access
@@ -134,6 +136,11 @@ locc_status locc_set_shapes(locc_ctx* ctx, const float* points, int32_t S, int32
  * with stream == NULL the call returns after completion; with a caller stream it is
  * asynchronous on that stream (and validation of ids/poses happens on the device: an invalid
  * id or pose makes the call return INVALID_ARG only in the synchronous form).
+ * CUDA graph: an asynchronous device-buffer call whose N fits one internal sub-batch is captured
+ * on the second call with the same arguments (pointers, N, stream) and context state (weights,
+ * shapes, grids, precision, determinism, no scratch reallocated since), then replayed as one graph
+ * launch; the buffers' CONTENTS may change between calls.  Same for locc_query_grad and
+ * locc_query_cells (without its debug outputs).  LOCC_NO_GRAPH=1 disables it.
  * Errors: INVALID_ARG (N < 0, null buffers, id out of range, non-finite pose, |q|^2 < 1e-12),
  * STATE (no weights or no shapes), CUDA, OOM. */
 locc_status locc_query(locc_ctx* ctx, const int32_t* pairs, const float* poses, int64_t N,

@@ -171,6 +171,19 @@ struct locc_ctx {
   int sim_seen = 0;  // calls with sim_key so far (capture on the second)
   int64_t sim_launches = 0;  // kernels inside the captured graph
   cudaGraphExec_t sim_exec = nullptr;
+  // CUDA graph of one asynchronous device-buffer query of a single sub-batch (locc_query,
+  // locc_query_grad, locc_query_cells), replayed while the call's arguments and the context's state
+  // are unchanged: the ~8 launches of a small query become one
+  struct QueryKey {
+    int32_t kind;  // 0 query, 1 grad, 2 cells
+    int32_t precision, det;
+    int64_t N;
+    const void *pairs, *poses, *probs, *labels, *logits, *extra, *stream;
+    uint64_t gen, alloc_epoch;
+  } q_key{};
+  int q_seen = 0;
+  locc_stats q_last{};  // the stats the captured call left
+  cudaGraphExec_t q_exec = nullptr;
   // multi-device group (locc_config.n_devices > 1): one single-device sub-context per device; this
   // context's own device is the home device (device_ids[0]) and its state is only the fan-out
   std::vector<locc_ctx*> kids;
@@ -1115,6 +1128,7 @@ void locc_destroy(locc_ctx* c) {
     if (c->ev_ce[i]) cudaEventDestroy(c->ev_ce[i]);
   }
   if (c->sim_exec) cudaGraphExecDestroy(c->sim_exec);
+  if (c->q_exec) cudaGraphExecDestroy(c->q_exec);
   for (auto& e : c->enc_ev) cudaEventDestroy(e);
   for (auto& e : c->head_ev) cudaEventDestroy(e);
   for (auto& e : c->crop_ev) cudaEventDestroy(e);
@@ -1169,6 +1183,7 @@ locc_status locc_get_stats(locc_ctx* c, locc_stats* out) {
       a.total_ms = std::max(a.total_ms, ks.total_ms);
       a.head_ms = std::max(a.head_ms, ks.head_ms);
       a.crop_ms = std::max(a.crop_ms, ks.crop_ms);
+      a.graph_replay += ks.graph_replay;
       return r;
     });
     *out = a;
@@ -1311,12 +1326,83 @@ locc_status locc_set_shapes(locc_ctx* c, const float* points, int32_t S, int32_t
   return LOCC_OK;
 }
 
+// An asynchronous query of device buffers that fits one sub-batch runs from a CUDA graph: the first
+// call with a given key runs directly (allocating any scratch), the second is captured, later ones
+// replay it.  The key holds every argument and the context's generation (weights, shapes, grids,
+// precision, determinism) and allocation epoch (no scratch buffer the graph points into was
+// reallocated); anything else — host buffers, the synchronous form, timing, LOCC_NO_GRAPH=1 — runs
+// directly.
+extern "C++" {
+template <class Run>
+locc_status graphed_query(locc_ctx* c, int32_t kind, const int32_t* pairs, const float* poses, int64_t N,
+                          const float* probs, const void* labels, const float* logits, const void* extra,
+                          void* stream, Run&& run) {
+  const bool eligible = c && stream && N > 0 && pairs && poses && probs && c->has_weights && c->has_shapes &&
+                        !c->timing && N <= batch_cap(c) && is_device_ptr(pairs) && !getenv("LOCC_NO_GRAPH") &&
+                        !getenv("LOCC_TC_TRACE");
+  if (!eligible) return run();
+  locc_ctx::QueryKey key;
+  std::memset(&key, 0, sizeof key);
+  key.kind = kind;
+  key.precision = c->cfg.precision;
+  key.det = c->deterministic;
+  key.N = N;
+  key.pairs = pairs;
+  key.poses = poses;
+  key.probs = probs;
+  key.labels = labels;
+  key.logits = logits;
+  key.extra = extra;
+  key.stream = stream;
+  key.gen = c->generation;
+  key.alloc_epoch = g_alloc_epoch.load();
+  if (std::memcmp(&key, &c->q_key, sizeof key) != 0) {
+    if (c->q_exec) cudaGraphExecDestroy(c->q_exec);
+    c->q_exec = nullptr;
+    c->q_key = key;
+    c->q_seen = 0;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (c->q_exec) {
+    CK(cudaSetDevice(c->device));
+    CK(cudaGraphLaunch(c->q_exec, st));
+    c->last = c->q_last;
+    c->last.graph_replay = 1;
+    return LOCC_OK;
+  }
+  if (c->q_seen < 1) {
+    locc_status s = run();
+    if (s == LOCC_OK) ++c->q_seen;
+    return s;
+  }
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const locc_status s = run();
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(st, &graph);
+  if (s == LOCC_OK && ec == cudaSuccess && graph && cudaGraphInstantiate(&c->q_exec, graph, 0) != cudaSuccess)
+    c->q_exec = nullptr;
+  if (graph) cudaGraphDestroy(graph);
+  cudaGetLastError();
+  if (!c->q_exec || s != LOCC_OK) {  // not capturable: this key stays on the direct path
+    c->q_seen = -(1 << 30);
+    return run();
+  }
+  c->q_last = c->last;
+  CK(cudaGraphLaunch(c->q_exec, st));
+  c->last.graph_replay = 1;
+  return LOCC_OK;
+}
+}  // extern "C++"
+
 locc_status locc_query(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
                        uint8_t* labels, float* logits, void* stream) {
   if (is_group(c))
     return group_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, nullptr, stream,
                        false);
-  return run_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
+  return graphed_query(c, 0, pairs, poses, N, probs, labels, logits, nullptr, stream, [&] {
+    return run_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
+  });
 }
 
 locc_status locc_query_debug(locc_ctx* c, const int32_t* pairs, const float* poses, int64_t N, float* probs,
@@ -1332,7 +1418,9 @@ locc_status locc_query_grad(locc_ctx* c, const int32_t* pairs, const float* pose
   if (N > 0 && !grad) return fail(LOCC_E_INVALID_ARG, "grad must be non-null");
   if (is_group(c))
     return group_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, grad, stream, false);
-  return run_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, grad, stream);
+  return graphed_query(c, 1, pairs, poses, N, probs, labels, logits, grad, stream, [&] {
+    return run_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, grad, stream);
+  });
 }
 
 // ---------------------------------------------------------------- NEXT-1: encode-once mode
@@ -1533,7 +1621,12 @@ locc_status locc_query_cells(locc_ctx* c, const int32_t* pairs, const float* pos
                              void* stream) {
   if (is_group(c))
     return group_query(c, pairs, poses, N, probs, labels, logits, nsel, nullptr, cells, emb, nullptr, stream, true);
-  return run_query(c, pairs, poses, N, probs, labels, logits, nsel, nullptr, cells, emb, nullptr, stream, true);
+  if (nsel || cells || emb)  // debug outputs: direct
+    return run_query(c, pairs, poses, N, probs, labels, logits, nsel, nullptr, cells, emb, nullptr, stream, true);
+  return graphed_query(c, 2, pairs, poses, N, probs, labels, logits, nullptr, stream, [&] {
+    return run_query(c, pairs, poses, N, probs, labels, logits, nullptr, nullptr, nullptr, nullptr, nullptr, stream,
+                     true);
+  });
 }
 
 // ---------------------------------------------------------------- NEXT-3: closed-loop substeps

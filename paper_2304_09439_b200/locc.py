@@ -52,7 +52,7 @@ class Stats(C.Structure):
     _fields_ = [("pairs", C.c_int64), ("evaluated_pairs", C.c_int64), ("kept_rows", C.c_int64),
                 ("nonempty_sides", C.c_int64), ("sub_batches", C.c_int64), ("kernel_launches", C.c_int64),
                 ("encoder_ms", C.c_double), ("total_ms", C.c_double), ("head_ms", C.c_double),
-                ("crop_ms", C.c_double)]
+                ("crop_ms", C.c_double), ("graph_replay", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
