@@ -431,11 +431,12 @@ def main():
         peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
         roof = {"bound": "alu", "unit": "TFLOP/s",
                 "peak_source": f"148 SM x 128 FP32 FMA/clk x 2 x {mhz:.0f} MHz (median SM clock under load)"}
-    traffic = None
+    traffic, crop_ncu = None, None
     tp = os.path.join(ROOT, "profiles", "encoder_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(a.precision)
+            tj = json.load(open(tp))
+            traffic, crop_ncu = tj.get(a.precision), tj.get("crop_bytes_per_pair")
         except Exception:
             traffic = None
     roof.update({"achieved": achieved, "peak": peak, "frac": (achieved / peak) if achieved else None,
@@ -466,7 +467,11 @@ def main():
                         "ms_per_step": st["crop_ms"], "unit": "GB/s",
                         "achieved": cb / (st["crop_ms"] / 1e3) / 1e9, "peak": hbm,
                         "frac": cb / (st["crop_ms"] / 1e3) / 1e9 / hbm,
-                        "algorithmic_bytes_per_pair": 2 * a.K * 12 + 69}
+                        "algorithmic_bytes_per_pair": 2 * a.K * 12 + 69,
+                        # DRAM bytes per pair of crop_count + crop_emit from ncu --set full (the
+                        # row-buffer write dominates; the point reads hit L2)
+                        "dram_bytes_per_pair_ncu": crop_ncu,
+                        "dram_bytes_source": "profiles/encoder_traffic.json (from the round's ncu capture)"}
 
     line = {"metric": METRIC, "value": world * N / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

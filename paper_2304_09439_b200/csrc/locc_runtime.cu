@@ -1373,6 +1373,7 @@ locc_status graphed_query(locc_ctx* c, int32_t kind, const int32_t* pairs, const
   if (c->q_seen < 1) {
     locc_status s = run();
     if (s == LOCC_OK) ++c->q_seen;
+    c->q_key.alloc_epoch = g_alloc_epoch.load();  // what this direct call allocated is what a capture uses
     return s;
   }
   CK(cudaSetDevice(c->device));
@@ -1752,6 +1753,7 @@ locc_status locc_sim_run(locc_ctx* c, const locc_sim_config* cfg, int32_t E, con
     if (s != LOCC_OK) return s;
   }
   ++c->sim_seen;
+  c->sim_key.alloc_epoch = g_alloc_epoch.load();  // the scratch this call allocated is what a capture uses
   c->last.kernel_launches = launches;
   if (!stream) {
     // synchronous form: report environments whose body ids were out of range (their pairs were culled)

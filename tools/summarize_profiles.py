@@ -88,6 +88,9 @@ def main(tag="r1"):
         traffic = {"bf16": e.get("dram_read", 0) + e.get("dram_write", 0),
                    "source": f"profiles/{tag}_summary.json (ncu --set full, one 262,144-pair launch)",
                    "pairs_per_launch": 262144}
+        cr = [kern[k] for k in ("crop_count", "crop_emit") if k in kern]
+        if cr:  # the crop's measured DRAM bytes per pair (crop_count + crop_emit, one sub-batch)
+            traffic["crop_bytes_per_pair"] = sum(k.get("dram_read", 0) + k.get("dram_write", 0) for k in cr) / 262144
         json.dump(traffic, open(os.path.join(ROOT, "profiles", "encoder_traffic.json"), "w"), indent=1)
     print(md)
 
