@@ -23,14 +23,17 @@ def deps():
         os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "locc.h")]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(p) for p in deps()):
-        return LIB
-    extra = os.environ.get("LOCC_NVCC_FLAGS", "").split()  # experiment switches, e.g. -DLOCC_E3_TWO_WALKERS=1
-    cmd = [NVCC] + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB + ".tmp"] + sources()
+def build(force: bool = False, verbose: bool = False, out: str = LIB, flags: tuple = ()) -> str:
+    """Compile every csrc/*.cu into `out` (default: the in-tree liblocc.so) unless it is newer than all
+    sources.  `flags` (and $LOCC_NVCC_FLAGS) add experiment or diagnostic switches, e.g.
+    -DLOCC_TRACE_BUILD=1 for the encoder's event trace."""
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(p) for p in deps()):
+        return out
+    extra = list(flags) + os.environ.get("LOCC_NVCC_FLAGS", "").split()
+    cmd = [NVCC] + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", out + ".tmp"] + sources()
     subprocess.check_call(cmd, cwd=HERE)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -25,10 +25,10 @@
 // produces layer 3's operand in place and layer 3's epilogue sees each feature's rows in one
 // thread — the segmented cell max needs no cross-lane reduction.
 //
-// Roles (17 warps): warps 0-3 = layer 1, warps 4-11 = epi L2 (4 per half), warps 12-15 = epi L3,
-// warp 16 = TMEM allocation + MMA issue (leader CTA).  mbarriers link the roles across both CTAs.
-// h1 is handed over per 64-feature K block in both directions (layer 1 of tile t+1 overwrites K
-// block kb as soon as L2 of tile t has consumed it); layer 3 accumulates per 32-feature K chunk as
+// Roles (17 warps): warps 0-7 = layer 1 (a warp pair per 64-feature K block of h1, the weights of its
+// features in registers), warps 8-11 = epi L2, warps 12-15 = epi L3, warp 16 = TMEM allocation + MMA
+// issue (leader CTA).  mbarriers link the roles across both CTAs.  h1 is handed over per K block in
+// both directions (layer 1 of tile t+1 overwrites K block kb as soon as L2 of tile t has consumed it); layer 3 accumulates per 32-feature K chunk as
 // epi L2 writes them; accumulators rotate over three TMEM regions (struct Regions) so that the
 // tensor core runs the next tile's first layer-2 half while the epilogues still drain this one.
 #include <cuda_runtime.h>
@@ -52,21 +52,10 @@ using namespace e3;
 // group starts at a multiple of 4.  The warp scheduler favours higher warp ids, so the sequential
 // layer-3 walk and the MMA issuer get the high ids and layer 1 (which has the most slack) the low.
 // 17 warps = at most 5 per scheduler, which leaves 96 registers per thread.
-#ifndef LOCC_L1_WARPS
-#define LOCC_L1_WARPS 8
-#endif
-constexpr int kL1Warps = LOCC_L1_WARPS;  // 8: layer 1 on warps 0-7, epi L2 on 8-11 (both halves)
-                                         // 4: layer 1 on warps 0-3, epi L2 on 4-11 (one half each)
+constexpr int kL1Warps = 8;  // layer 1: warps 0-7, a warp pair per K block
 constexpr int kL1Threads = 32 * kL1Warps;
-constexpr int kE2Warps = 12 - kL1Warps;
-#ifndef LOCC_WARP_ORDER
-#define LOCC_WARP_ORDER 0
-#endif
-// Role order by warp id (the scheduler favours higher ids).  0: L1 < E2 < E3 < MMA; 1: E2 < L1 < E3;
-// 2: E2 < E3 < L1.  TMEM-reading groups (E2, E3) start at multiples of 4.
-constexpr int kWarpL1 = LOCC_WARP_ORDER == 0 ? 0 : LOCC_WARP_ORDER == 1 ? kE2Warps : kE2Warps + 4;
-constexpr int kWarpE2 = LOCC_WARP_ORDER == 0 ? kL1Warps : 0;
-constexpr int kWarpE3 = LOCC_WARP_ORDER == 2 ? kE2Warps : 12;
+constexpr int kE2Warps = 4;  // epi L2: warps 8-11, both halves in turn
+constexpr int kWarpL1 = 0, kWarpE2 = 8, kWarpE3 = 12;
 constexpr int kWarpMMA = 16;  // warp 16: TMEM allocation + MMA issue (leader CTA)
 constexpr int kWarps = 17;
 constexpr int kThreads = 32 * kWarps;
@@ -109,7 +98,6 @@ struct alignas(1024) Smem {
   uint8_t h1[65536];  // A of L2: this CTA's 128 rows of h1, same layout
   uint8_t h2[65536];  // B of L3: this CTA's 128 rows of h2, same layout
   float px[2][128], py[2][128], pz[2][128];  // this CTA's rows of a tile (layer-1 input), double buffered
-  float4 w1b[256];  // (w0, w1, w2, b1) of feature 64kb + 4fq + k at [(4kb + k) 16 + fq] (conflict-free reads)
   uint32_t flags[kTileRows];  // row flags of the whole tile (epi L3)
   alignas(16) uint32_t masks[16];  // per part p: [8p + C] cell ends, [8p + 4 + C] segment ends of step C (interleaved)
   uint64_t bar[kNumBars];
@@ -136,11 +124,17 @@ struct TcArgs {
   long long* trace;  // debug timeline (LOCC_TC_TRACE): [2 ranks][64 tiles][16 events] of cluster 0
 };
 
+// The per-tile event trace (LOCC_TC_TRACE=1 at run time) is compiled in only with -DLOCC_TRACE_BUILD=1
+// (tools/trace_run.py builds it): its checks cost ~2 % of the step in the hot loops.
+#ifndef LOCC_TRACE_BUILD
+#define LOCC_TRACE_BUILD 0
+#endif
 constexpr int kTraceTiles = 64;
+constexpr int kTraceEv = 32;  // events per tile (see tools/trace_summary.py)
 // Issuer trace points are also signalled to CTA 1's idle MMA warp, which timestamps them in the same
 // clock domain as the tensor-core completion probes.
 __device__ __forceinline__ void trace_issue(const TcArgs& a, uint32_t* seq, int64_t cid) {
-  if (a.trace && cid == 0) {
+  if (LOCC_TRACE_BUILD && a.trace && cid == 0) {
     const uint32_t v = *seq + 1;  // the issuer's local copy counts its trace points
     *seq = v;
     asm volatile(
@@ -152,7 +146,7 @@ __device__ __forceinline__ void trace_issue(const TcArgs& a, uint32_t* seq, int6
 }
 
 __device__ __forceinline__ void trace_ev(const TcArgs& a, uint32_t rank, int64_t cid, uint32_t tile, int ev) {
-  if (a.trace && cid == 0 && tile < kTraceTiles) a.trace[(rank * kTraceTiles + tile) * 16 + ev] = clock64();
+  if (LOCC_TRACE_BUILD && a.trace && cid == 0 && tile < kTraceTiles) a.trace[(rank * kTraceTiles + tile) * kTraceEv + ev] = clock64();
 }
 
 // Iterates the (chunk, tile) sequence of this cluster; every role walks the same sequence.  Only
@@ -234,7 +228,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
   // ---------------------------------------------------------------- setup
   if (threadIdx.x == 0) {
     for (int kb = 0; kb < 4; ++kb) {
-      mbar_init(&S.bar[B_H1F0 + kb], 2 * kL1Warps);  // layer-1 warps x 2 CTAs (the leader's copy is used)
+      mbar_init(&S.bar[B_H1F0 + kb], 4);  // the 2 layer-1 warps of K block kb x 2 CTAs (the leader's copy is used)
       mbar_init(&S.bar[B_H1E0 + kb], 1);   // MMA commits
     }
     mbar_init(&S.bar[B_D2AF], 1);
@@ -253,7 +247,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     for (int kb = 0; kb < 5; ++kb)
       bulk_g2s(S.w2 + kb * 16384, a.w2img + (size_t)rank * 5 * 16384 + kb * 16384, 16384, &S.bar[B_WLOAD]);
   }
-  for (int i = threadIdx.x; i < 256; i += kThreads) S.w1b[((i >> 6) * 4 + (i & 3)) * 16 + ((i & 63) >> 2)] = a.w1b[i];
   for (int i = threadIdx.x; i < 256; i += kThreads) {  // ones atom: row i>>5, 4-byte word i&31
     const uint32_t row = i >> 5, word = i & 31;
     const uint32_t chunk = (word >> 2) ^ row;  // logical 16-byte chunk of this physical word
@@ -286,7 +279,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
 
   // ---------------------------------------------------------------- roles
   if (warp == kWarpMMA && rank == 1) {
-    if (a.trace && cid == 0 && lane == 0) {
+    if (LOCC_TRACE_BUILD && a.trace && cid == 0 && lane == 0) {
       // debug: one thread timestamps tensor-core completions (probe barriers) and issuer trace points
       // (sequence numbers stored remotely by the issuer) in this SM's clock
       TileIter pit(a, (int)cid, (int)ncl), iit(a, (int)cid, (int)ncl);
@@ -298,7 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         if (pmore) {
           const uint32_t ng = pn > 128 ? 5 : 4;  // L2a, L2b, L3p0 first K half, L3p0, L3p1
           if (mbar_try_wait(&S.bar[B_PROBE + pg], (pg == 4 ? np1 : ptile) & 1)) {
-            if (ptile < kTraceTiles) a.trace[(2 * kTraceTiles + ptile) * 16 + pg] = clock64();
+            if (ptile < kTraceTiles) a.trace[(2 * kTraceTiles + ptile) * kTraceEv + pg] = clock64();
             if (++pg == ng) {
               if (ng == 5) ++np1;
               pg = 0;
@@ -312,7 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           const uint32_t v = *reinterpret_cast<volatile uint32_t*>(&S.issue_seq);
           const long long now = clock64();
           while (imore && seen < v) {
-            if (itile < kTraceTiles) a.trace[(2 * kTraceTiles + itile) * 16 + 8 + ig] = now;
+            if (itile < kTraceTiles) a.trace[(2 * kTraceTiles + itile) * kTraceEv + 8 + ig] = now;
             ++seen;
             if (++ig == ng) {
               ig = 0;
@@ -362,9 +355,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         }
         if (elect_one()) {
           mma_commit_2cta(&S.bar[B_D2AF], 3);
-          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE + 0], 3);
+          if (LOCC_TRACE_BUILD && a.trace) mma_commit_2cta(&S.bar[B_PROBE + 0], 3);
         }
         __syncwarp();
+        if (lane == 0) trace_ev(a, rank, cid, it, 20);  // L2a issued
         // L2b -> Q: the previous tile's L3p0 region
         if (it > 0) mbar_wait_spin(&S.bar[B_D3E0], (n0 - 1) & 1);
         if (lane == 0) { trace_ev(a, rank, cid, it, 2); trace_issue(a, &S.issue_seq, cid); }
@@ -380,9 +374,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
             mma_commit_2cta(&S.bar[B_H1E0 + kb], 3);  // h1 K block kb read by both halves
           }
           mma_commit_2cta(&S.bar[B_D2BF], 3);
-          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE + 1], 3);
+          if (LOCC_TRACE_BUILD && a.trace) mma_commit_2cta(&S.bar[B_PROBE + 1], 3);
         }
         __syncwarp();
+        if (lane == 0) trace_ev(a, rank, cid, it, 21);  // L2b issued
         // Layer 3, first K half (features 0-127, from L2a): L3p0 -> P once epi L2 has drained all of
         // it, L3p1 -> R(2) once the layer-3 epilogue has walked its previous part there
 #pragma unroll 1
@@ -394,9 +389,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           mma_ss_2cta(rp, dB2 + 2, dOne + 2, kIdescN128, 0);
 #pragma unroll
           for (int j = 0; j < 4; ++j) l3_chunk(rp, tmem + kColW3, dH2, j, 0);
-          if (a.trace) mma_commit_2cta(&S.bar[B_PROBE + 2], 3);
+          if (LOCC_TRACE_BUILD && a.trace) mma_commit_2cta(&S.bar[B_PROBE + 2], 3);
         }
         __syncwarp();
+        if (lane == 0) trace_ev(a, rank, cid, it, 22);  // L3p0 first half issued
         if (p1) {
           if (last_p1 >= 0) mbar_wait_spin(&S.bar[B_D3E1], last_p1 & 1);
           tc_fence_after();
@@ -406,17 +402,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
             for (int j = 0; j < 4; ++j) l3_chunk(r3, tmem + kColW3, dH2, j, 512);
           }
           __syncwarp();
+          if (lane == 0) trace_ev(a, rank, cid, it, 23);  // L3p1 first half issued
         }
         // second K half (features 128-255) chunk by chunk as epi L2 writes it
 #pragma unroll 1
         for (int j = 4; j < 8; ++j) {
           mbar_wait_spin(&S.bar[B_E2K0 + j], par);
+          if (lane == 0) trace_ev(a, rank, cid, it, 12 + j);  // 16..19: chunk j of h2 seen
           tc_fence_after();
           if (elect_one()) {
             l3_chunk(rp, tmem + kColW3, dH2, j, 0);
             if (j == 7) {
               mma_commit_2cta(&S.bar[B_D3F0], 3);
-              if (a.trace) mma_commit_2cta(&S.bar[B_PROBE + 3], 3);
+              if (LOCC_TRACE_BUILD && a.trace) mma_commit_2cta(&S.bar[B_PROBE + 3], 3);
             }
             if (p1) l3_chunk(r3, tmem + kColW3, dH2, j, 512);
           }
@@ -426,7 +424,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         if (elect_one()) {
           if (p1) {
             mma_commit_2cta(&S.bar[B_D3F1], 3);
-            if (a.trace) mma_commit_2cta(&S.bar[B_PROBE + 4], 3);
+            if (LOCC_TRACE_BUILD && a.trace) mma_commit_2cta(&S.bar[B_PROBE + 4], 3);
           }
           mma_commit_2cta(&S.bar[B_H2_EMPTY], 3);
         }
@@ -442,11 +440,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       }
     }
   } else if (warp >= kWarpL1 && warp < kWarpL1 + kL1Warps) {
-    // ============ layer 1: K block kb -> thread = features 64kb + 4fq..+3, rows 8rq + {0..7, 64..71} ====
-    const uint32_t lt = threadIdx.x - 32 * kWarpL1;  // 0..kL1Threads-1
-    const uint32_t fq = lt & 15, rq = lt >> 4;  // 8 warps: rows 8rq..8rq+7; 4 warps: also 64 + 8rq..
-    const uint32_t h1 = smem_u32(S.h1) + rq * 1024 + ((4 * fq) & 7) * 2;
-    const uint32_t chunk = (4 * fq) >> 3;  // 16-byte chunk of the 128-byte row (same in every K block)
+    // ============ layer 1: a warp pair per K block kb; thread = features 64kb + 4fq .. +3 (their
+    // weights in registers for the whole launch, as fp32 pairs of adjacent features) x local rows
+    // 32rg .. 32rg + 31; FFMA2 with the row's coordinate as the broadcast operand ============
+    const uint32_t lt = threadIdx.x - 32 * kWarpL1;  // 0..255
+    const uint32_t wl = lt >> 5, kb = wl >> 1;
+    const uint32_t fq = lane & 15, rg = 2 * (wl & 1) + (lane >> 4);
+    unsigned long long wA[4], wB[4];  // (w0, w1, w2, b1) of features (4fq, 4fq+1) and (4fq+2, 4fq+3)
+    {
+      const float4* w = a.w1b + 64 * kb + 4 * fq;
+      const float4 f0 = w[0], f1 = w[1], f2_ = w[2], f3 = w[3];
+      wA[0] = f2(f0.x, f1.x); wA[1] = f2(f0.y, f1.y); wA[2] = f2(f0.z, f1.z); wA[3] = f2(f0.w, f1.w);
+      wB[0] = f2(f2_.x, f3.x); wB[1] = f2(f2_.y, f3.y); wB[2] = f2(f2_.z, f3.z); wB[3] = f2(f2_.w, f3.w);
+    }
+    const uint32_t h1 = smem_u32(S.h1) + kb * 16384 + ((4 * fq) & 7) * 2;
+    const uint32_t chunk = (4 * fq) >> 3;  // 16-byte chunk of the 128-byte row
     TileIter iter(a, (int)cid, (int)ncl), ahead(a, (int)cid, (int)ncl);
     int64_t row0, nrow0;
     int nrows, nnrows;
@@ -477,54 +485,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       asm volatile("bar.sync 2, %0;" ::"n"(kL1Threads) : "memory");  // rows of tile it staged; buffer buf^1 free
       have_next = ahead.next(nrow0, nnrows);
       const float4 pf = fetch(have_next, nrow0, nnrows);  // next tile's row, in flight during this tile
-#pragma unroll 1
-      for (uint32_t kb = 0; kb < 4; ++kb) {
-        unsigned long long wx[4], wy[4], wz[4], wb[4];
+      // K block kb free (layer 2 of the previous tile has read it): one warp of the pair polls
+      if ((wl & 1) == 0) mbar_wait(&S.bar[B_H1E0 + kb], (it & 1) ^ 1);
+      __syncwarp();
+      asm volatile("bar.sync %0, 64;" ::"r"(5 + kb) : "memory");
+      if (lt == 0) trace_ev(a, rank, cid, it, 6);
+#pragma unroll 2
+      for (uint32_t g = 0; g < 8; ++g) {  // local rows lr .. lr + 3
+        const uint32_t lr = 32 * rg + 4 * g;
+        const float4 x = *reinterpret_cast<const float4*>(&S.px[buf][lr]);
+        const float4 y = *reinterpret_cast<const float4*>(&S.py[buf][lr]);
+        const float4 z = *reinterpret_cast<const float4*>(&S.pz[buf][lr]);
+        const float xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w}, zs[4] = {z.x, z.y, z.z, z.w};
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float4 w = S.w1b[(4 * kb + k) * 16 + fq];
-          wx[k] = f2(w.x, w.x);
-          wy[k] = f2(w.y, w.y);
-          wz[k] = f2(w.z, w.z);
-          wb[k] = f2(w.w, w.w);
+        for (int v = 0; v < 4; ++v) {
+          const unsigned long long X = f2(xs[v], xs[v]), Y = f2(ys[v], ys[v]), Z = f2(zs[v], zs[v]);
+          const unsigned long long hA = ffma2(wA[0], X, ffma2(wA[1], Y, ffma2(wA[2], Z, wA[3])));
+          const unsigned long long hB = ffma2(wB[0], X, ffma2(wB[1], Y, ffma2(wB[2], Z, wB[3])));
+          st_shared_v2(h1 + sw128_off(lr + v, chunk),
+                       pack_relu_bf16x2(f2_lo(hA), f2_hi(hA)), pack_relu_bf16x2(f2_lo(hB), f2_hi(hB)));
         }
-        group_wait<2, kL1Threads, LOCC_SPIN_L1>(&S.bar[B_H1E0 + kb], (it & 1) ^ 1, warp == kWarpL1);
-        if (lt == 0 && kb == 0) trace_ev(a, rank, cid, it, 6);
-#pragma unroll
-        for (uint32_t g = 0; g < 128 / (8 * (kL1Threads / 16)); ++g) {  // local rows 64g + 8rq .. +7
-          const uint32_t lr = 64 * g + 8 * rq;
-          const float4 xa = *reinterpret_cast<const float4*>(&S.px[buf][lr]);
-          const float4 xb = *reinterpret_cast<const float4*>(&S.px[buf][lr + 4]);
-          const float4 ya = *reinterpret_cast<const float4*>(&S.py[buf][lr]);
-          const float4 yb = *reinterpret_cast<const float4*>(&S.py[buf][lr + 4]);
-          const float4 za = *reinterpret_cast<const float4*>(&S.pz[buf][lr]);
-          const float4 zb = *reinterpret_cast<const float4*>(&S.pz[buf][lr + 4]);
-          const unsigned long long x2[4] = {f2(xa.x, xa.y), f2(xa.z, xa.w), f2(xb.x, xb.y), f2(xb.z, xb.w)};
-          const unsigned long long y2[4] = {f2(ya.x, ya.y), f2(ya.z, ya.w), f2(yb.x, yb.y), f2(yb.z, yb.w)};
-          const unsigned long long z2[4] = {f2(za.x, za.y), f2(za.z, za.w), f2(zb.x, zb.y), f2(zb.z, zb.w)};
-          const uint32_t base = h1 + kb * 16384 + g * 8192;
-#pragma unroll
-          for (uint32_t v = 0; v < 4; ++v) {  // rows lr + 2v, lr + 2v + 1
-            unsigned long long h[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) h[k] = ffma2(wx[k], x2[v], ffma2(wy[k], y2[v], ffma2(wz[k], z2[v], wb[k])));
-            const uint32_t r = 2 * v;  // row within the 8-row group
-            st_shared_v2(base + r * 128 + ((chunk ^ r) << 4), pack_relu_bf16x2(f2_lo(h[0]), f2_lo(h[1])),
-                         pack_relu_bf16x2(f2_lo(h[2]), f2_lo(h[3])));
-            st_shared_v2(base + (r + 1) * 128 + ((chunk ^ (r + 1)) << 4), pack_relu_bf16x2(f2_hi(h[0]), f2_hi(h[1])),
-                         pack_relu_bf16x2(f2_hi(h[2]), f2_hi(h[3])));
-          }
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&S.bar[B_H1F0 + kb], 0);
       }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&S.bar[B_H1F0 + kb], 0);
       if (lt == 0) trace_ev(a, rank, cid, it, 7);
       stage(pf, buf ^ 1);
       ++it;
     }
   } else if (warp >= kWarpE2 && warp < kWarpE2 + kE2Warps) {
-    // ============ epi L2: thread = row; 8 warps: one half each, 4 warps: both halves in turn ============
+    // ============ epi L2: thread = row; the two halves in turn ============
     const uint32_t q = warp & 3;  // TMEM lane quarter (rows 32q..32q+31)
     const uint32_t row = 32 * q + lane;
     const uint32_t lt = threadIdx.x - 32 * kWarpE2;
@@ -536,19 +526,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     Regions R;
     while (iter.next(row0, nrows)) {
 #pragma unroll 1
-      for (uint32_t hh = 0; hh < (kE2Warps == 4 ? 2u : 1u); ++hh) {
-        const uint32_t half = kE2Warps == 4 ? hh : (warp - kWarpE2) >> 2;
+      for (uint32_t half = 0; half < 2; ++half) {
         if ((warp & 3) == 0) {  // one warp per group polls; the group waits on a named barrier
           if (LOCC_SPIN_E2) mbar_wait_spin(&S.bar[half ? B_D2BF : B_D2AF], it & 1); else mbar_wait(&S.bar[half ? B_D2BF : B_D2AF], it & 1);
           if (lt == 0) trace_ev(a, rank, cid, it, half ? 11 : 8);  // D2AF / D2BF seen
-          if (hh == 0) mbar_wait(&S.bar[B_H2_EMPTY], (it & 1) ^ 1);
+          if (half == 0) mbar_wait(&S.bar[B_H2_EMPTY], (it & 1) ^ 1);
           if (lt == 0 && half == 0) trace_ev(a, rank, cid, it, 9);
         }
         __syncwarp();
-        if (half && kE2Warps == 8)
-          asm volatile("bar.sync 4, 128;" ::: "memory");
-        else
-          asm volatile("bar.sync 3, 128;" ::: "memory");
+        asm volatile("bar.sync 3, 128;" ::: "memory");
         tc_fence_after();
         const uint32_t tbase = tmem + ((32 * q) << 16) + region_col(half ? R.Q : R.P);
         uint32_t va[32], vb[32];
@@ -621,6 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&S.bar[p ? B_D3E1 : B_D3E0], 0);
+        if (lane == 0) trace_ev(a, rank, cid, it, 24 + 4 * p + eg);  // 24..31: each E3 warp's part p done
         if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 13 + 2 * p);
         if (p) ++c1; else ++c0;
       }

@@ -659,21 +659,21 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     if (c->cfg.precision == LOCC_PREC_BF16) {
       long long* trace = nullptr;
       if (getenv("LOCC_TC_TRACE") && subs == 0) {
-        CK(c->trace.ensure(sizeof(long long) * 3 * 64 * 16));
-        CK(cudaMemsetAsync(c->trace.p, 0, sizeof(long long) * 3 * 64 * 16, st));
+        CK(c->trace.ensure(sizeof(long long) * 3 * 64 * 32));
+        CK(cudaMemsetAsync(c->trace.p, 0, sizeof(long long) * 3 * 64 * 32, st));
         trace = c->trace.as<long long>();
       }
       CK(launch_encoder_tc(c->P, c->tc_l1, b, c->num_sms, st, trace, c->deterministic));
       if (trace) {
-        std::vector<long long> h(3 * 64 * 16);
+        std::vector<long long> h(3 * 64 * 32);
         CK(cudaMemcpyAsync(h.data(), trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         for (int rk = 0; rk < 3; ++rk) {  // rank 0, rank 1, tensor-core probes (rank 1 clock)
           const long long t0 = 0;  // raw clock64 (ranks 1 and 2 share the clock of CTA 1's SM)
           for (int t = 0; t < 64; ++t) {
             fprintf(stderr, "trace r%d t%02d", rk, t);
-            for (int e = 0; e < 16; ++e) {
-              long long v = h[(rk * 64 + t) * 16 + e];
+            for (int e = 0; e < 32; ++e) {
+              long long v = h[(rk * 64 + t) * 32 + e];
               fprintf(stderr, " %7lld", v ? v - t0 : -1);
             }
             fprintf(stderr, "\n");

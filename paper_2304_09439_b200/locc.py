@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblocc.so")
+LIB_PATH = os.environ.get("LOCC_LIB") or os.path.join(HERE, "liblocc.so")  # LOCC_LIB: a diagnostic build
 
 LOCC_PREC_FP32 = 0
 LOCC_PREC_BF16 = 1
