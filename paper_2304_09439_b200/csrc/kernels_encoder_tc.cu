@@ -64,6 +64,12 @@ constexpr uint32_t kTmemCols = 512;
 // TMEM columns: W3 (A of L3: this CTA's 128 features as bf16x2) and three 128-column regions
 // R(i) = 128 + 128 i, assigned per tile as described at struct Regions.
 constexpr uint32_t kColW3 = 0, kColR0 = 128;
+// The per-tile event trace (LOCC_TC_TRACE=1 at run time) is compiled in only with -DLOCC_TRACE_BUILD=1
+// (tools/trace_run.py builds it; its checks cost several % of the step in the hot loops).  Events go
+// to shared memory (cheap stores) and are copied out at the end of the launch.
+#ifndef LOCC_TRACE_BUILD
+#define LOCC_TRACE_BUILD 0
+#endif
 constexpr uint32_t kIdescN128 = idesc_bf16_f32(256, 128);
 
 __device__ __forceinline__ uint32_t region_col(uint32_t i) { return kColR0 + 128 * i; }
@@ -102,7 +108,9 @@ struct alignas(1024) Smem {
   alignas(16) uint32_t masks[16];  // per part p: [8p + C] cell ends, [8p + 4 + C] segment ends of step C (interleaved)
   uint64_t bar[kNumBars];
   uint32_t tmem_base;
-  uint32_t issue_seq;  // LOCC_TC_TRACE: issuer trace points (written remotely into CTA 1)
+#if LOCC_TRACE_BUILD
+  long long tr[32][32];  // LOCC_TC_TRACE: event clocks of the first 32 tiles, copied out at the end
+#endif
 };
 
 
@@ -124,30 +132,18 @@ struct TcArgs {
   long long* trace;  // debug timeline (LOCC_TC_TRACE): [2 ranks][64 tiles][16 events] of cluster 0
 };
 
-// The per-tile event trace (LOCC_TC_TRACE=1 at run time) is compiled in only with -DLOCC_TRACE_BUILD=1
-// (tools/trace_run.py builds it): its checks cost ~2 % of the step in the hot loops.
-#ifndef LOCC_TRACE_BUILD
-#define LOCC_TRACE_BUILD 0
+constexpr int kTraceTiles = 64;  // tiles per rank in the trace buffer (the kernel records the first 32)
+constexpr int kTraceEv = 32;     // events per tile (see tools/trace_events.py)
+#if LOCC_TRACE_BUILD
+#define TRACE_EV(it, ev)                                                     \
+  do {                                                                       \
+    if (a.trace && cid == 0 && (it) < 32) S.tr[(it)][(ev)] = clock64();     \
+  } while (0)
+#else
+#define TRACE_EV(it, ev) \
+  do {                   \
+  } while (0)
 #endif
-constexpr int kTraceTiles = 64;
-constexpr int kTraceEv = 32;  // events per tile (see tools/trace_summary.py)
-// Issuer trace points are also signalled to CTA 1's idle MMA warp, which timestamps them in the same
-// clock domain as the tensor-core completion probes.
-__device__ __forceinline__ void trace_issue(const TcArgs& a, uint32_t* seq, int64_t cid) {
-  if (LOCC_TRACE_BUILD && a.trace && cid == 0) {
-    const uint32_t v = *seq + 1;  // the issuer's local copy counts its trace points
-    *seq = v;
-    asm volatile(
-        "{\n\t.reg .b32 ra;\n\t"
-        "mapa.shared::cluster.u32 ra, %0, 1;\n\t"
-        "st.shared::cluster.u32 [ra], %1;\n\t}" ::"r"(smem_u32(seq)), "r"(v)
-        : "memory");
-  }
-}
-
-__device__ __forceinline__ void trace_ev(const TcArgs& a, uint32_t rank, int64_t cid, uint32_t tile, int ev) {
-  if (LOCC_TRACE_BUILD && a.trace && cid == 0 && tile < kTraceTiles) a.trace[(rank * kTraceTiles + tile) * kTraceEv + ev] = clock64();
-}
 
 // Iterates the (chunk, tile) sequence of this cluster; every role walks the same sequence.  Only
 // the cursor lives in registers (the launch constants stay in the parameter bank).
@@ -241,7 +237,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     mbar_init(&S.bar[B_D3E1], 8);
     mbar_init(&S.bar[B_WLOAD], 1);
     for (int g = 0; g < 5; ++g) mbar_init(&S.bar[B_PROBE + g], 1);  // LOCC_TC_TRACE: completion probes
-    S.issue_seq = 0;
+#if LOCC_TRACE_BUILD
+    for (int i = 0; i < 32 * 32; ++i) S.tr[i / 32][i % 32] = 0;
+#endif
     fence_mbar_init();
     mbar_arrive_expect_tx(&S.bar[B_WLOAD], 5 * 16384);
     for (int kb = 0; kb < 5; ++kb)
@@ -280,38 +278,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
   // ---------------------------------------------------------------- roles
   if (warp == kWarpMMA && rank == 1) {
     if (LOCC_TRACE_BUILD && a.trace && cid == 0 && lane == 0) {
-      // debug: one thread timestamps tensor-core completions (probe barriers) and issuer trace points
-      // (sequence numbers stored remotely by the issuer) in this SM's clock
-      TileIter pit(a, (int)cid, (int)ncl), iit(a, (int)cid, (int)ncl);
+      // debug: one thread timestamps tensor-core completions (probe barriers) in this SM's clock
+      TileIter pit(a, (int)cid, (int)ncl);
       int64_t r0;
-      int pn = 0, in_ = 0;
-      bool pmore = pit.next(r0, pn), imore = iit.next(r0, in_);
-      uint32_t ptile = 0, pg = 0, np1 = 0, itile = 0, ig = 0, seen = 0;
-      while (pmore || imore) {
-        if (pmore) {
-          const uint32_t ng = pn > 128 ? 5 : 4;  // L2a, L2b, L3p0 first K half, L3p0, L3p1
-          if (mbar_try_wait(&S.bar[B_PROBE + pg], (pg == 4 ? np1 : ptile) & 1)) {
-            if (ptile < kTraceTiles) a.trace[(2 * kTraceTiles + ptile) * kTraceEv + pg] = clock64();
-            if (++pg == ng) {
-              if (ng == 5) ++np1;
-              pg = 0;
-              ++ptile;
-              pmore = pit.next(r0, pn);
-            }
-          }
-        }
-        if (imore) {
-          const uint32_t ng = in_ > 128 ? 6 : 5;
-          const uint32_t v = *reinterpret_cast<volatile uint32_t*>(&S.issue_seq);
-          const long long now = clock64();
-          while (imore && seen < v) {
-            if (itile < kTraceTiles) a.trace[(2 * kTraceTiles + itile) * kTraceEv + 8 + ig] = now;
-            ++seen;
-            if (++ig == ng) {
-              ig = 0;
-              ++itile;
-              imore = iit.next(r0, in_);
-            }
+      int pn = 0;
+      bool pmore = pit.next(r0, pn);
+      uint32_t ptile = 0, pg = 0, np1 = 0;
+      while (pmore) {
+        const uint32_t ng = pn > 128 ? 5 : 4;  // L2a, L2b, L3p0 first K half, L3p0, L3p1
+        if (mbar_try_wait(&S.bar[B_PROBE + pg], (pg == 4 ? np1 : ptile) & 1)) {
+          if (ptile < 32) a.trace[(2 * kTraceTiles + ptile) * kTraceEv + pg] = clock64();
+          if (++pg == ng) {
+            if (ng == 5) ++np1;
+            pg = 0;
+            ++ptile;
+            pmore = pit.next(r0, pn);
           }
         }
       }
@@ -337,14 +318,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         const bool p1 = nrows > 128;
         const uint32_t rp = tmem + region_col(R.P), rq = tmem + region_col(R.Q);
         // L2a -> P: the previous tile's L2b region, drained before that tile's L3 was issued
-        if (lane == 0) { trace_ev(a, rank, cid, it, 1); trace_issue(a, &S.issue_seq, cid); }
+        if (lane == 0) { TRACE_EV(it, 1); }
         tc_fence_after();
         if (elect_one()) mma_ss_2cta(rp, dOne, dB2, kIdescN128, 0);  // D = 1 * b2 (hi + mid + lo)
         __syncwarp();
 #pragma unroll 1
         for (int kb = 0; kb < 4; ++kb) {
           mbar_wait_spin(&S.bar[B_H1F0 + kb], par);
-          if (kb == 0 && lane == 0) { trace_ev(a, rank, cid, it, 0); trace_issue(a, &S.issue_seq, cid); }
+          if (kb == 0 && lane == 0) { TRACE_EV(it, 0); }
           tc_fence_after();
           if (elect_one()) {
             const uint32_t koff = kb * 1024;
@@ -358,10 +339,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           if (LOCC_TRACE_BUILD && a.trace) mma_commit_2cta(&S.bar[B_PROBE + 0], 3);
         }
         __syncwarp();
-        if (lane == 0) trace_ev(a, rank, cid, it, 20);  // L2a issued
+        if (lane == 0) TRACE_EV(it, 20);  // L2a issued
         // L2b -> Q: the previous tile's L3p0 region
         if (it > 0) mbar_wait_spin(&S.bar[B_D3E0], (n0 - 1) & 1);
-        if (lane == 0) { trace_ev(a, rank, cid, it, 2); trace_issue(a, &S.issue_seq, cid); }
+        if (lane == 0) { TRACE_EV(it, 2); }
         tc_fence_after();
         if (elect_one()) {
           mma_ss_2cta(rq, dOne, dB2 + 512, kIdescN128, 0);
@@ -377,12 +358,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           if (LOCC_TRACE_BUILD && a.trace) mma_commit_2cta(&S.bar[B_PROBE + 1], 3);
         }
         __syncwarp();
-        if (lane == 0) trace_ev(a, rank, cid, it, 21);  // L2b issued
+        if (lane == 0) TRACE_EV(it, 21);  // L2b issued
         // Layer 3, first K half (features 0-127, from L2a): L3p0 -> P once epi L2 has drained all of
         // it, L3p1 -> R(2) once the layer-3 epilogue has walked its previous part there
 #pragma unroll 1
         for (int j = 0; j < 4; ++j) mbar_wait_spin(&S.bar[B_E2K0 + j], par);
-        if (lane == 0) { trace_ev(a, rank, cid, it, 3); trace_issue(a, &S.issue_seq, cid); }
+        if (lane == 0) { TRACE_EV(it, 3); }
         tc_fence_after();
         if (elect_one()) {
           // D3 = b3 (hi + mid + lo) for every row: K = 16..18 (+32 B) of the bias block and the ones atom
@@ -392,7 +373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           if (LOCC_TRACE_BUILD && a.trace) mma_commit_2cta(&S.bar[B_PROBE + 2], 3);
         }
         __syncwarp();
-        if (lane == 0) trace_ev(a, rank, cid, it, 22);  // L3p0 first half issued
+        if (lane == 0) TRACE_EV(it, 22);  // L3p0 first half issued
         if (p1) {
           if (last_p1 >= 0) mbar_wait_spin(&S.bar[B_D3E1], last_p1 & 1);
           tc_fence_after();
@@ -402,13 +383,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
             for (int j = 0; j < 4; ++j) l3_chunk(r3, tmem + kColW3, dH2, j, 512);
           }
           __syncwarp();
-          if (lane == 0) trace_ev(a, rank, cid, it, 23);  // L3p1 first half issued
+          if (lane == 0) TRACE_EV(it, 23);  // L3p1 first half issued
         }
         // second K half (features 128-255) chunk by chunk as epi L2 writes it
 #pragma unroll 1
         for (int j = 4; j < 8; ++j) {
           mbar_wait_spin(&S.bar[B_E2K0 + j], par);
-          if (lane == 0) trace_ev(a, rank, cid, it, 12 + j);  // 16..19: chunk j of h2 seen
+          if (lane == 0) TRACE_EV(it, 12 + j);  // 16..19: chunk j of h2 seen
           tc_fence_after();
           if (elect_one()) {
             l3_chunk(rp, tmem + kColW3, dH2, j, 0);
@@ -420,7 +401,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           }
           __syncwarp();
         }
-        if (lane == 0) { trace_ev(a, rank, cid, it, 4); trace_issue(a, &S.issue_seq, cid); }
+        if (lane == 0) { TRACE_EV(it, 4); }
         if (elect_one()) {
           if (p1) {
             mma_commit_2cta(&S.bar[B_D3F1], 3);
@@ -430,7 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         }
         __syncwarp();
         if (p1) {
-          if (lane == 0) { trace_ev(a, rank, cid, it, 5); trace_issue(a, &S.issue_seq, cid); }
+          if (lane == 0) { TRACE_EV(it, 5); }
           last_p1 = (int)n1;
           ++n1;
         }
@@ -489,7 +470,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       if ((wl & 1) == 0) mbar_wait(&S.bar[B_H1E0 + kb], (it & 1) ^ 1);
       __syncwarp();
       asm volatile("bar.sync %0, 64;" ::"r"(5 + kb) : "memory");
-      if (lt == 0) trace_ev(a, rank, cid, it, 6);
+      if (lt == 0) TRACE_EV(it, 6);
 #pragma unroll 2
       for (uint32_t g = 0; g < 8; ++g) {  // local rows lr .. lr + 3
         const uint32_t lr = 32 * rg + 4 * g;
@@ -509,7 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&S.bar[B_H1F0 + kb], 0);
-      if (lt == 0) trace_ev(a, rank, cid, it, 7);
+      if (lt == 0) TRACE_EV(it, 7);
       stage(pf, buf ^ 1);
       ++it;
     }
@@ -529,9 +510,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       for (uint32_t half = 0; half < 2; ++half) {
         if ((warp & 3) == 0) {  // one warp per group polls; the group waits on a named barrier
           if (LOCC_SPIN_E2) mbar_wait_spin(&S.bar[half ? B_D2BF : B_D2AF], it & 1); else mbar_wait(&S.bar[half ? B_D2BF : B_D2AF], it & 1);
-          if (lt == 0) trace_ev(a, rank, cid, it, half ? 11 : 8);  // D2AF / D2BF seen
+          if (lt == 0) TRACE_EV(it, half ? 11 : 8);  // D2AF / D2BF seen
           if (half == 0) mbar_wait(&S.bar[B_H2_EMPTY], (it & 1) ^ 1);
-          if (lt == 0 && half == 0) trace_ev(a, rank, cid, it, 9);
+          if (lt == 0 && half == 0) TRACE_EV(it, 9);
         }
         __syncwarp();
         asm volatile("bar.sync 3, 128;" ::: "memory");
@@ -560,7 +541,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
           if (lane == 0) mbar_arrive_cluster(&S.bar[B_E2K0 + 4 * half + c], 0);
         }
       }
-      if (lt == 0) trace_ev(a, rank, cid, it, 10);
+      if (lt == 0) TRACE_EV(it, 10);
       ++it;
       R.next();
     }
@@ -597,7 +578,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
 #pragma unroll 1
       for (int p = 0; p < np; ++p) {
         group_wait<1, 128, LOCC_SPIN_E3>(&S.bar[p ? B_D3F1 : B_D3F0], (p ? c1 : c0) & 1, warp == kWarpE3);
-        if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 12 + 2 * p);
+        if (lane == 0 && eg == 0) TRACE_EV(it, 12 + 2 * p);
         tc_fence_after();
         const uint32_t tb = tmem + ((32 * q) << 16) + region_col(p ? kRegionP1 : R.P);
         if (kDet)
@@ -607,8 +588,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&S.bar[p ? B_D3E1 : B_D3E0], 0);
-        if (lane == 0) trace_ev(a, rank, cid, it, 24 + 4 * p + eg);  // 24..31: each E3 warp's part p done
-        if (lane == 0 && eg == 0) trace_ev(a, rank, cid, it, 13 + 2 * p);
+        if (lane == 0) TRACE_EV(it, 24 + 4 * p + eg);  // 24..31: each E3 warp's part p done
+        if (lane == 0 && eg == 0) TRACE_EV(it, 13 + 2 * p);
         if (p) ++c1; else ++c0;
       }
       ++it;
@@ -621,6 +602,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
   cluster_sync();
   tc_fence_after();
   if (warp == kWarpMMA) tmem_dealloc_2cta(tmem, kTmemCols);
+#if LOCC_TRACE_BUILD
+  if (a.trace && cid == 0)
+    for (int i = threadIdx.x; i < 32 * 32; i += kThreads) a.trace[(rank * kTraceTiles + i / 32) * kTraceEv + i % 32] = S.tr[i / 32][i % 32];
+#endif
 }
 
 }  // namespace
