@@ -107,6 +107,7 @@ struct alignas(1024) Smem {
   uint32_t flags[kTileRows];  // row flags of the whole tile (epi L3)
   alignas(16) uint32_t masks[16];  // per part p: [8p + C] cell ends, [8p + 4 + C] segment ends of step C (interleaved)
   uint64_t bar[kNumBars];
+  int64_t range[2];  // this cluster's rows [range[0], range[1]) (whole segments)
   uint32_t tmem_base;
 #if LOCC_TRACE_BUILD
   long long tr[32][32];  // LOCC_TC_TRACE: event clocks of the first 32 tiles, copied out at the end
@@ -127,8 +128,6 @@ struct TcArgs {
   float* pooled;     // [G][256] cell sums (the predictor divides by cells_c)
   int32_t* cells_c;  // [G] occupied cells per segment
   int64_t G;
-  int64_t n_chunks;
-  int seg_per_chunk;
   long long* trace;  // debug timeline (LOCC_TC_TRACE): [2 ranks][64 tiles][16 events] of cluster 0
 };
 
@@ -145,25 +144,28 @@ constexpr int kTraceEv = 32;     // events per tile (see tools/trace_events.py)
   } while (0)
 #endif
 
-// Iterates the (chunk, tile) sequence of this cluster; every role walks the same sequence.  Only
-// the cursor lives in registers (the launch constants stay in the parameter bank).
+// First row of the first segment whose rows start at or after `target` (offsets[G] = all rows).
+__device__ int64_t seg_boundary_at(const TcArgs& a, int64_t target) {
+  int64_t lo = 0, hi = a.G;  // offsets[hi] >= target always
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a.offsets[mid] >= target) hi = mid; else lo = mid + 1;
+  }
+  return a.offsets[lo];
+}
+
+// Iterates the tiles of this cluster's rows; every role walks the same sequence.  Each cluster owns
+// one contiguous range of whole segments holding ~1/nclusters of the batch's rows (computed once per
+// CTA in the setup), so only its last tile is partial.
 struct TileIter {
-  const TcArgs& a;
-  int chunk;
-  int64_t r1 = 0, t0 = 0;
-  __device__ TileIter(const TcArgs& args, int first, int stride) : a(args), chunk(first - stride) {}
-  // first = true for the first tile of a chunk (a chunk starts on a segment boundary)
+  int64_t t0, r1;
+  bool started = false;
+  __device__ TileIter(int64_t begin, int64_t end) : t0(begin), r1(end) {}
+  // first = true for the cluster's first tile (a range starts on a segment boundary)
   __device__ bool next(int64_t& row0, int& nrows, bool& first) {
-    first = false;
-    while (t0 >= r1) {
-      chunk += (int)nclusters_x();
-      if (chunk >= a.n_chunks) return false;
-      const int64_t s0 = (int64_t)chunk * a.seg_per_chunk;
-      const int64_t s1 = min(s0 + a.seg_per_chunk, a.G);
-      t0 = a.offsets[s0];
-      r1 = a.offsets[s1];
-      first = true;
-    }
+    if (t0 >= r1) return false;
+    first = !started;
+    started = true;
     row0 = t0;
     nrows = (int)min((int64_t)kTileRows, r1 - t0);
     t0 += kTileRows;
@@ -240,6 +242,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
 #if LOCC_TRACE_BUILD
     for (int i = 0; i < 32 * 32; ++i) S.tr[i / 32][i % 32] = 0;
 #endif
+    const int64_t R = a.offsets[a.G];
+    S.range[0] = cid == 0 ? 0 : seg_boundary_at(a, R * cid / ncl);
+    S.range[1] = cid + 1 == ncl ? R : seg_boundary_at(a, R * (cid + 1) / ncl);
     fence_mbar_init();
     mbar_arrive_expect_tx(&S.bar[B_WLOAD], 5 * 16384);
     for (int kb = 0; kb < 5; ++kb)
@@ -279,7 +284,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
   if (warp == kWarpMMA && rank == 1) {
     if (LOCC_TRACE_BUILD && a.trace && cid == 0 && lane == 0) {
       // debug: one thread timestamps tensor-core completions (probe barriers) in this SM's clock
-      TileIter pit(a, (int)cid, (int)ncl);
+      TileIter pit(S.range[0], S.range[1]);
       int64_t r0;
       int pn = 0;
       bool pmore = pit.next(r0, pn);
@@ -300,7 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
   } else if (warp == kWarpMMA) {
     // ============ MMA issuer (leader CTA, whole warp; one elected lane issues) ============
     if (rank == 0) {
-      TileIter iter(a, (int)cid, (int)ncl);
+      TileIter iter(S.range[0], S.range[1]);
       int64_t row0;
       int nrows;
       uint32_t it = 0, n0 = 0, n1 = 0;
@@ -436,7 +441,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     }
     const uint32_t h1 = smem_u32(S.h1) + kb * 16384 + ((4 * fq) & 7) * 2;
     const uint32_t chunk = (4 * fq) >> 3;  // 16-byte chunk of the 128-byte row
-    TileIter iter(a, (int)cid, (int)ncl), ahead(a, (int)cid, (int)ncl);
+    TileIter iter(S.range[0], S.range[1]), ahead(S.range[0], S.range[1]);
     int64_t row0, nrow0;
     int nrows, nnrows;
     auto stage = [&](float4 p, uint32_t buf) {
@@ -500,7 +505,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     const uint32_t row = 32 * q + lane;
     const uint32_t lt = threadIdx.x - 32 * kWarpE2;
     const uint32_t h2 = smem_u32(S.h2);
-    TileIter iter(a, (int)cid, (int)ncl);
+    TileIter iter(S.range[0], S.range[1]);
     int64_t row0;
     int nrows;
     uint32_t it = 0;
@@ -551,14 +556,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
     const uint32_t eg = warp - kWarpE3;  // 0..3: flags of rows 32eg.. and the masks of step eg
     const uint32_t f = 128 * rank + 32 * q + lane;
     Walk w{0.f, 0.f, 0};
-    TileIter iter(a, (int)cid, (int)ncl);
+    TileIter iter(S.range[0], S.range[1]);
     int64_t row0;
     int nrows;
     bool first;
     uint32_t it = 0, c0 = 0, c1 = 0;
     Regions R;
     while (iter.next(row0, nrows, first)) {
-      if (first) w.m = 0.f;  // drop padding rows after the previous chunk's last segment end
+      if (first) w.m = 0.f;
       asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's flags no longer read
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -614,12 +619,10 @@ size_t encoder_tc_smem_bytes() { return sizeof(Smem) + 1024; }
 
 cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b, int num_sms, cudaStream_t st,
                               long long* trace, bool deterministic) {
-  // Work unit: a chunk of spc whole segments.  16 segments (~33 tiles at C3) keep the partial last tile
-  // of a chunk cheap; small batches use fewer so that every cluster gets >= 4 chunks to balance.
-  const int64_t clusters = num_sms / 2;
-  const int spc = (int)std::min<int64_t>(16, std::max<int64_t>(1, b.G / (4 * clusters)));
-  const int64_t chunks = (b.G + spc - 1) / spc;
-  if (chunks == 0) return cudaSuccess;
+  // Work unit: each cluster takes one contiguous range of whole segments with ~1/clusters of the rows
+  // (the kernel splits the batch by its row offsets); a batch of G segments needs at most G clusters.
+  if (b.G == 0) return cudaSuccess;
+  const int64_t clusters = std::min<int64_t>(num_sms / 2, b.G);
   if (!P.tc_w2 || !P.tc_w3) return cudaErrorInvalidValue;
   (void)l1;
   TcArgs args;
@@ -636,16 +639,12 @@ cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b
   args.cells_c = b.cells_c;
   if (!b.cells_c) return cudaErrorInvalidValue;
   args.G = b.G;
-  args.n_chunks = chunks;
-  args.seg_per_chunk = spc;
   args.trace = trace;
   const size_t smem = encoder_tc_smem_bytes();
   const cudaError_t attr = deterministic ? smem_optin(encoder_tc_kernel<true>, smem)
                                          : smem_optin(encoder_tc_kernel<false>, smem);
   if (attr != cudaSuccess) return attr;
-  int grid = (num_sms / 2) * 2;
-  const int64_t max_useful = 2 * chunks;
-  if (grid > max_useful) grid = (int)max_useful;
+  const int grid = (int)(2 * clusters);
   if (deterministic)
     encoder_tc_kernel<true><<<grid, kThreads, smem, st>>>(args);
   else
