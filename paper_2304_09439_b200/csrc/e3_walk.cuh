@@ -312,23 +312,44 @@ __device__ __forceinline__ void e3_part2_det(uint32_t tbase, const uint32_t* mk,
   uint32_t xa[16], ya[16], xb[16], yb[16];
   tmem_ld16(tbase, xa);
   tmem_ld16(tbase + 64, ya);
+  if (b0 == 0) {  // Y's first cell end in block 0 (the common case): the head bookkeeping in block 0 only
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    uint32_t(&vx)[16] = (c & 1) ? xb : xa;
-    uint32_t(&vy)[16] = (c & 1) ? yb : ya;
-    uint32_t(&nx)[16] = (c & 1) ? xa : xb;
-    uint32_t(&ny)[16] = (c & 1) ? ya : yb;
-    tmem_ld_wait();
-    if (c < 3) {
-      tmem_ld16(tbase + 16 * (c + 1), nx);
-      tmem_ld16(tbase + 64 + 16 * (c + 1), ny);
-    } else if (rewalk) {
-      tmem_ld16(tbase + 64 + 16 * b0, nx);  // block b0's Y columns again, for the merge's re-walk (xa is free)
+    for (int c = 0; c < 4; ++c) {
+      uint32_t(&vx)[16] = (c & 1) ? xb : xa;
+      uint32_t(&vy)[16] = (c & 1) ? yb : ya;
+      uint32_t(&nx)[16] = (c & 1) ? xa : xb;
+      uint32_t(&ny)[16] = (c & 1) ? ya : yb;
+      tmem_ld_wait();
+      if (c < 3) {
+        tmem_ld16(tbase + 16 * (c + 1), nx);
+        tmem_ld16(tbase + 64 + 16 * (c + 1), ny);
+      } else if (rewalk) {
+        tmem_ld16(tbase + 64, nx);  // block 0's Y columns again, for the merge's re-walk (xa is free)
+      }
+      if (c == 0)
+        block<true>(c, vx, vy, sel4(ce, c), sel4(se, c), ys, 0, w, y, h, fl, pooled, cellc, f);
+      else
+        block<false>(c, vx, vy, sel4(ce, c), sel4(se, c), ys, 0, w, y, h, fl, pooled, cellc, f);
     }
-    if (c == b0)
-      block<true>(c, vx, vy, sel4(ce, c), sel4(se, c), ys, b0, w, y, h, fl, pooled, cellc, f);
-    else
-      block<false>(c, vx, vy, sel4(ce, c), sel4(se, c), ys, b0, w, y, h, fl, pooled, cellc, f);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t(&vx)[16] = (c & 1) ? xb : xa;
+      uint32_t(&vy)[16] = (c & 1) ? yb : ya;
+      uint32_t(&nx)[16] = (c & 1) ? xa : xb;
+      uint32_t(&ny)[16] = (c & 1) ? ya : yb;
+      tmem_ld_wait();
+      if (c < 3) {
+        tmem_ld16(tbase + 16 * (c + 1), nx);
+        tmem_ld16(tbase + 64 + 16 * (c + 1), ny);
+      } else if (rewalk) {
+        tmem_ld16(tbase + 64 + 16 * b0, nx);  // block b0's Y columns again, for the merge's re-walk (xa is free)
+      }
+      if (c == b0)
+        block<true>(c, vx, vy, sel4(ce, c), sel4(se, c), ys, b0, w, y, h, fl, pooled, cellc, f);
+      else
+        block<false>(c, vx, vy, sel4(ce, c), sel4(se, c), ys, b0, w, y, h, fl, pooled, cellc, f);
+    }
   }
   if (ys == 4) h.hc = y.c;
   // merge: X's sum continues with Y's head blocks b0..ys in block order
