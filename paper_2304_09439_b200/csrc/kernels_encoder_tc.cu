@@ -476,7 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       __syncwarp();
       asm volatile("bar.sync %0, 64;" ::"r"(5 + kb) : "memory");
       if (lt == 0) TRACE_EV(it, 6);
-#pragma unroll 2
+#pragma unroll 1  // (unrolled x2 was 0.5 % slower: instruction-cache footprint)
       for (uint32_t g = 0; g < 8; ++g) {  // local rows lr .. lr + 3
         const uint32_t lr = 32 * rg + 4 * g;
         const float4 x = *reinterpret_cast<const float4*>(&S.px[buf][lr]);
