@@ -497,6 +497,17 @@ locc_status read_timing(locc_ctx* c) {
   c->last.encoder_ms = enc;
   c->last.head_ms = head;
   c->last.crop_ms = crop;
+  if (getenv("LOCC_TIMELINE")) {  // diagnostic: each sub-batch's stages relative to the query start (ms)
+    auto at = [&](cudaEvent_t e) {
+      float t = 0.f;
+      return cudaEventElapsedTime(&t, c->ev[0], e) == cudaSuccess ? t : -1.f;
+    };
+    for (int64_t s = 0; s < c->timed_subs; ++s)
+      fprintf(stderr, "timeline sub %lld: crop %.2f-%.2f encoder %.2f-%.2f head end %.2f\n", (long long)s,
+              c->timed_overlap && s < 64 ? at(c->ev_cs[s]) : at(c->crop_ev[s]),
+              c->timed_overlap && s < 64 ? at(c->ev_ce[s]) : at(c->enc_ev[2 * s]), at(c->enc_ev[2 * s]),
+              at(c->enc_ev[2 * s + 1]), at(c->head_ev[s]));
+  }
   c->timed_subs = 0;
   return LOCC_OK;
 }
