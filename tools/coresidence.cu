@@ -12,8 +12,8 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
-template <bool kCluster>
-__global__ void __launch_bounds__(544, 1) hog(unsigned long long ns, unsigned long long* end) {
+template <bool kCluster, int kT = 544>
+__global__ void __launch_bounds__(kT, 1) hog(unsigned long long ns, unsigned long long* end) {
   extern __shared__ char sm[];
   const unsigned long long t0 = gtime();
   float r[84];
@@ -30,7 +30,6 @@ __global__ void __launch_bounds__(544, 1) hog(unsigned long long ns, unsigned lo
   sm[threadIdx.x] = (char)x;
   if (threadIdx.x == 0) atomicMax(end, gtime());
 }
-template __global__ void hog<true>(unsigned long long, unsigned long long*);
 
 template <int kThreadsPerBlock, int kMinBlocks>
 __global__ void __launch_bounds__(kThreadsPerBlock, kMinBlocks) small(unsigned long long* done_before,
@@ -52,14 +51,14 @@ __global__ void __launch_bounds__(kThreadsPerBlock, kMinBlocks) small(unsigned l
   if (threadIdx.x == 0 && x != 0.f) atomicAdd(done_before, 1ull);
 }
 
-template <int T, int MB>
+template <int T, int MB, int HT = 544>
 void run(const char* name, cudaStream_t s0, cudaStream_t s1, unsigned long long* d, int nsm) {
-  cudaFuncSetAttribute(hog<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220160);
+  cudaFuncSetAttribute(hog<true, HT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220160);
   unsigned long long init[3] = {0, 0, ~0ull};
   cudaMemcpy(d, init, 24, cudaMemcpyHostToDevice);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nsm);
-  cfg.blockDim = dim3(544);
+  cfg.blockDim = dim3(HT);
   cfg.dynamicSmemBytes = 220160;
   cfg.stream = s0;
   cudaLaunchAttribute at[1];
@@ -69,14 +68,14 @@ void run(const char* name, cudaStream_t s0, cudaStream_t s1, unsigned long long*
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, hog<true>, 20000000ull, d);
+  cudaLaunchKernelEx(&cfg, hog<true, HT>, 20000000ull, d);
   small<T, MB><<<nsm * 20 * 128 / T, T, 0, s1>>>(d + 1, d, d + 2);
   cudaDeviceSynchronize();
   unsigned long long r[3];
   cudaMemcpy(r, d, 24, cudaMemcpyDeviceToHost);
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, small<T, MB>);
-  printf("%s (%d threads/block, %d regs): first block %+.2f ms relative to the hog's end (%s)\n", name, T, fa.numRegs,
+  printf("hog %d threads; %s (%d threads/block, %d regs): first block %+.2f ms relative to the hog's end (%s)\n", HT, name, T, fa.numRegs,
          ((double)r[2] - (double)r[0]) / 1e6, cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -94,5 +93,8 @@ int main() {
   run<128, 16>("128-thread blocks <= 32 regs", s0, s1, d, nsm);
   run<64, 20>("64-thread blocks <= 48 regs", s0, s1, d, nsm);
   run<32, 40>("32-thread blocks <= 48 regs", s0, s1, d, nsm);
+  run<128, 10, 512>("128-thread blocks <= 48 regs", s0, s1, d, nsm);
+  run<128, 16, 512>("128-thread blocks <= 32 regs", s0, s1, d, nsm);
+  run<128, 10, 416>("128-thread blocks <= 48 regs", s0, s1, d, nsm);
   return 0;
 }
