@@ -178,23 +178,10 @@ struct TileIter {
 };
 
 // One warp of a role group polls the mbarrier; the others wait on a named barrier (no issue slots).
-#ifndef LOCC_SPIN_E2
-#define LOCC_SPIN_E2 0
-#endif
-#ifndef LOCC_SPIN_E3
-#define LOCC_SPIN_E3 0
-#endif
-#ifndef LOCC_SPIN_L1
-#define LOCC_SPIN_L1 0
-#endif
-template <int ID, int NTHREADS, bool kSpin = false>
+// (Spinning instead of the sleeping try_wait made no difference.)
+template <int ID, int NTHREADS>
 __device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool poller) {
-  if (poller) {
-    if (kSpin)
-      mbar_wait_spin(bar, parity);
-    else
-      mbar_wait(bar, parity);
-  }
+  if (poller) mbar_wait(bar, parity);
   __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(NTHREADS) : "memory");
 }
@@ -514,7 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
 #pragma unroll 1
       for (uint32_t half = 0; half < 2; ++half) {
         if ((warp & 3) == 0) {  // one warp per group polls; the group waits on a named barrier
-          if (LOCC_SPIN_E2) mbar_wait_spin(&S.bar[half ? B_D2BF : B_D2AF], it & 1); else mbar_wait(&S.bar[half ? B_D2BF : B_D2AF], it & 1);
+          mbar_wait(&S.bar[half ? B_D2BF : B_D2AF], it & 1);
           if (lt == 0) TRACE_EV(it, half ? 11 : 8);  // D2AF / D2BF seen
           if (half == 0) mbar_wait(&S.bar[B_H2_EMPTY], (it & 1) ^ 1);
           if (lt == 0 && half == 0) TRACE_EV(it, 9);
@@ -582,7 +569,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       const int np = nrows > 128 ? 2 : 1;
 #pragma unroll 1
       for (int p = 0; p < np; ++p) {
-        group_wait<1, 128, LOCC_SPIN_E3>(&S.bar[p ? B_D3F1 : B_D3F0], (p ? c1 : c0) & 1, warp == kWarpE3);
+        group_wait<1, 128>(&S.bar[p ? B_D3F1 : B_D3F0], (p ? c1 : c0) & 1, warp == kWarpE3);
         if (lane == 0 && eg == 0) TRACE_EV(it, 12 + 2 * p);
         tc_fence_after();
         const uint32_t tb = tmem + ((32 * q) << 16) + region_col(p ? kRegionP1 : R.P);
