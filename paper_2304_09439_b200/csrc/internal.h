@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+
 namespace locc {
 
 constexpr int kPredW = 128;        // predictor width, "3 layers of 128 neurons"
@@ -16,6 +18,39 @@ constexpr int kRowSegShift = 3;    // flags word = (segment << 3) | pad << 2 | s
 // of the encoder's layer-3 walk and a segment end is followed only by padding within its step.
 constexpr int kSegAlign = 16;
 __host__ __device__ constexpr int64_t seg_rows(int64_t kept) { return (kept + kSegAlign - 1) / kSegAlign * kSegAlign; }
+
+// Checked build (-DLOCC_CHECKED=1, `tools/checked_run.sh`): device-side bounds checks on the hot
+// kernels' global-memory indices — this pool's substitute for compute-sanitizer memcheck, which is
+// closed here.  A failed check prints the condition and traps (the call returns LOCC_E_CUDA).
+#ifndef LOCC_CHECKED
+#define LOCC_CHECKED 0
+#endif
+#if LOCC_CHECKED
+#define LOCC_CHECK(cond)                                                               \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      printf("LOCC_CHECK failed: %s (%s:%d, block %d thread %d)\n", #cond, __FILE__, \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+// ... and with two values of the failing case
+#define LOCC_CHECK_V(cond, u, v)                                                                        \
+  do {                                                                                                  \
+    if (!(cond)) {                                                                                      \
+      printf("LOCC_CHECK failed: %s [%s = %lld, %s = %lld] (%s:%d, block %d thread %d)\n", #cond, #u, \
+             (long long)(u), #v, (long long)(v), __FILE__, __LINE__, (int)blockIdx.x, (int)threadIdx.x);  \
+      __trap();                                                                                         \
+    }                                                                                                   \
+  } while (0)
+#else
+#define LOCC_CHECK_V(cond, u, v) \
+  do {                           \
+  } while (0)
+#define LOCC_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 // S0 output (one copy per context, resident for the context's lifetime).
 struct ShapeTable {
@@ -117,8 +152,10 @@ struct Batch {
   int want_occ;          // the caller asked for C_s (locc_query_debug)
   int64_t* offsets;      // [G+1] exclusive scan of counts
   uint2* rows;           // [sum pad16(n)] kept rows: (flags, point index k in the own shape's sorted table)
+  int64_t rows_cap;      // capacity of `rows` in rows (checked builds)
   const float4* pts;     // the shape table's sorted points [S][K] (the rows' coordinates: pts[own K + k])
   int K;
+  int S;                 // shapes in the table (checked builds)
   float* pooled;         // [G][H] mean over occupied cells of the cell-max features, or their SUM when
                          // cells_c is set (the tensor-core encoder; the predictor divides)
   int32_t* cells_c;      // [G] occupied cells C of each non-empty segment when pooled holds sums, else null

@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTa
     for (int f = lane; f < F; f += 32) e[f] = 0.f;
     return;
   }
+  LOCC_CHECK(nc <= 512 && (unsigned)own < (unsigned)T.S && (unsigned)other < (unsigned)T.S);
   float4 lo = T.lo[other];
   lo.w = T.lo[own].w;  // the own cell's half-diagonal squared as the margin
   const float4 hi = T.hi[other];

@@ -49,8 +49,11 @@ __global__ void __launch_bounds__(256) encoder_f32_kernel(DevParams P, Batch b) 
     if (f < TR) {
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (f < nr) {  // the row's coordinates from the shape table (own shape of the row's segment)
+        LOCC_CHECK(t0 + f < b.rows_cap);
         const uint2 rw = b.rows[t0 + f];
+        LOCC_CHECK((rw.x >> kRowSegShift) < b.G && rw.y < (uint32_t)b.K);
         const int own = __float_as_int(b.xf[4 * (int64_t)(rw.x >> kRowSegShift) + 3].x);
+        LOCC_CHECK((unsigned)own < (unsigned)b.S);
         const float4 p = b.pts[(int64_t)own * b.K + rw.y];
         v = make_float4(p.x, p.y, p.z, __uint_as_float(rw.x));
       }
@@ -73,6 +76,7 @@ __global__ void __launch_bounds__(256) encoder_f32_kernel(DevParams P, Batch b) 
           }
           if (fl & kRowFlagSegEnd) {
             const int64_t seg = fl >> kRowSegShift;
+            LOCC_CHECK(seg < b.G && run_cells > 0);
             b.pooled[seg * H + f] = __fdiv_rn(run_sum, (float)run_cells);
             run_sum = 0.f;
             run_cells = 0;

@@ -128,6 +128,8 @@ struct TcArgs {
   float* pooled;     // [G][256] cell sums (the predictor divides by cells_c)
   int32_t* cells_c;  // [G] occupied cells per segment
   int64_t G;
+  int S;             // shapes (checked builds)
+  int64_t rows_cap;  // rows capacity (checked builds)
   long long* trace;  // debug timeline (LOCC_TC_TRACE): [2 ranks][64 tiles][16 events] of cluster 0
 };
 
@@ -443,8 +445,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       if (ok && lt < 128) {
         const uint32_t trow = tile_row_of_local(rank, lt);
         if ((int)trow < nr) {
+          LOCC_CHECK(r0 + trow < a.offsets[a.G] && r0 + trow < a.rows_cap);
           const uint2 rw = a.rows[r0 + trow];
+          LOCC_CHECK((rw.x >> kRowSegShift) < a.G && rw.y < (uint32_t)a.K);
           const int own = __float_as_int(a.xf[4 * (int64_t)(rw.x >> kRowSegShift) + 3].x);
+          LOCC_CHECK((unsigned)own < (unsigned)a.S);
           p = a.pts[(int64_t)own * a.K + rw.y];
         }
       }
@@ -556,6 +561,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) encoder
       for (int h = 0; h < 2; ++h) {
         const int r = 128 * h + 32 * eg + lane;
         S.flags[r] = r < nrows ? a.rows[row0 + r].x : 0u;
+        LOCC_CHECK(r >= nrows || (row0 + r < a.offsets[a.G] && (S.flags[r] >> kRowSegShift) < a.G));
         const int r2 = interleaved_row(h, eg, lane);  // interleaved masks of step eg of part h
         const uint32_t fl = r2 < nrows ? a.rows[row0 + r2].x : 0u;
         const uint32_t ce = __ballot_sync(0xffffffffu, fl & kRowFlagCellEnd);
@@ -626,6 +632,8 @@ cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b
   args.cells_c = b.cells_c;
   if (!b.cells_c) return cudaErrorInvalidValue;
   args.G = b.G;
+  args.S = b.S;
+  args.rows_cap = b.rows_cap;
   args.trace = trace;
   const size_t smem = encoder_tc_smem_bytes();
   const cudaError_t attr = deterministic ? smem_optin(encoder_tc_kernel<true>, smem)

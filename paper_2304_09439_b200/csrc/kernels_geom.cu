@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(256) crop_count_kernel(ShapeTable T, Batch b, 
     }
     return;
   }
+  LOCC_CHECK((unsigned)own < (unsigned)T.S && (unsigned)other < (unsigned)T.S);
   const float4 lo = T.lo[other], hi = T.hi[other];
   const float4* pts = T.pts + (int64_t)own * T.K;
   const uint16_t* perm = T.perm + (int64_t)own * T.K;
@@ -240,6 +241,9 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
   const float4* pts = T.pts + (int64_t)own * T.K;
   const int nsteps = (T.K + 31) >> 5;
   const uint32_t* kb = b.kbits + g * nsteps;
+  LOCC_CHECK((unsigned)own < (unsigned)T.S);
+  LOCC_CHECK(b.offsets[g] >= 0 && b.offsets[g] + seg_rows(n) <= b.rows_cap &&
+             b.offsets[g + 1] - b.offsets[g] == seg_rows(n));
   uint2* out = b.rows + b.offsets[g];
   const uint32_t segbits = (uint32_t)g << kRowSegShift;
   int written = 0;        // kept rows before this step
@@ -272,12 +276,14 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
     const int next_cell = __shfl_sync(0xffffffffu, cell, nxt);
     const int first_cell = __shfl_sync(0xffffffffu, cell, first);
     if (pending && lane == 0) {
+      LOCC_CHECK(pidx >= 0 && pidx < n);
       const uint32_t f = segbits | (pcell != first_cell ? kRowFlagCellEnd : 0);
       out[pidx] = make_uint2(f, (uint32_t)pk);
     }
     const int idx = written + __popc(m & lanemask_lt());
     const int k = base + lane;
     if (keep && lane != last) {
+      LOCC_CHECK(idx < n);
       const uint32_t f = segbits | (cell != next_cell ? kRowFlagCellEnd : 0);
       out[idx] = make_uint2(f, (uint32_t)k);
     }

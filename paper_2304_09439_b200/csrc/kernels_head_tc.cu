@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
       const int npairs = (int)min((int64_t)kHP, b.B - i0);
       const bool live = r < 2 * npairs;
       const int64_t g = 2 * i0 + r;
+      LOCC_CHECK(!live || g < b.G);
       const int ns = live ? b.counts[g] : 0;
       S.nside[r] = ns;
       // ---- z = [e ; canonical q ; t ; 0...] (K = 96) for side r (e = 0 for an empty side)
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(kGrad ? 192 : 320, 1) head_tc_kernel(DevParams
         const float4* m4 = reinterpret_cast<const float4*>(b.pooled + g * 256);
         // the tensor-core encoder leaves cell sums: m = S / C (IEEE division)
         const float cnt = (b.cells_c && ns > 0) ? (float)b.cells_c[g] : 1.f, rcnt = __frcp_rn(cnt);
+        LOCC_CHECK_V(ns == 0 || (cnt >= 1.f && cnt <= (float)ns), g, (int64_t)ns * 100000 + (int64_t)cnt);  // 1 <= cells <= kept
         for (int h = 0; h < 2; ++h) {
           if (h == 1) {  // the first half has been consumed
             mbar_wait(&S.d_full, dph);

@@ -610,8 +610,13 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     b.want_occ = occ != nullptr;
     b.offsets = (set2 ? c->offsets2 : c->offsets).as<int64_t>();
     b.rows = (set2 ? c->rows2 : c->rows).as<uint2>();
+    b.rows_cap = 2 * (set2 ? c->cap_B2 : c->cap_B) * seg_rows(c->T.K);
+#if LOCC_CHECKED
+    if (getenv("LOCC_CHECK_SELFTEST")) b.rows_cap = 1;  // tools/checked_run.sh: a check must fire
+#endif
     b.pts = c->T.pts;
     b.K = c->T.K;
+    b.S = c->T.S;
     b.pooled = (set2 ? c->pooled2 : c->pooled).as<float>();
     // the tensor-core encoder leaves cell sums and counts (the predictor divides); fp32: means
     b.cells_c = (!cells && c->cfg.precision == LOCC_PREC_BF16) ? (set2 ? c->cellc2 : c->cellc).as<int32_t>() : nullptr;
