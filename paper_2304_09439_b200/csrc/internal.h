@@ -183,6 +183,12 @@ cudaError_t launch_crop_count(const ShapeTable& T, const Batch& b, int words, cu
 cudaError_t launch_scan(const int32_t* counts, int64_t G, int64_t* offsets, int64_t* block_tmp,
                         cudaStream_t st);
 cudaError_t launch_crop_emit(const ShapeTable& T, const Batch& b, cudaStream_t st);
+// S2-S3 fused (transform + crop + compaction with a decoupled look-back, one launch; K <= kFusedMaxK):
+// lb = crop_compact_lb_words(G) look-back words (zeroed by the launcher on `st`).
+constexpr int kFusedMaxK = 2048;  // eight warps' shared-memory row lists: 64 KB per block
+size_t crop_compact_lb_words(int64_t G);
+cudaError_t launch_crop_compact(const ShapeTable& T, const Batch& b, int words, unsigned long long* lb,
+                                cudaStream_t st);
 cudaError_t launch_encoder_f32(const DevParams& P, const Batch& b, cudaStream_t st);
 cudaError_t launch_encoder_tc(const DevParams& P, const TcL1& l1, const Batch& b, int num_sms, cudaStream_t st,
                               long long* trace = nullptr, bool deterministic = false);

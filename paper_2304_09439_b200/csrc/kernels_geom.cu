@@ -303,6 +303,192 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
   if (n + lane < pad_end) out[n + lane] = make_uint2(segbits | kRowFlagPad, 0u);
 }
 
+// ---------------------------------------------------------------- S2-S3 fused: transform + crop + compaction
+// One kernel for the whole crop (K <= kFusedMaxK).  A block of kCropWarps warps takes kCropWarps
+// consecutive segments (one per warp); blocks claim their segment ranges in order from a counter, so
+// every predecessor of a claimed range is already running.
+//   1. Per warp: float4 point loads (four 32-point steps in flight), the transform + eps test, a warp
+//      ballot; each kept point's sorted index k and its "last of cell" bit (the next kept point's cell
+//      differs) go to the warp's shared-memory list at its rank (ballot prefix count): the count pass
+//      and the row staging are one pass over the points.
+//   2. The block's footprints seg_rows(n) are scanned in shared memory; warp 0 runs a decoupled
+//      look-back over the blocks: it publishes the block's aggregate, sums its predecessors' (32 per
+//      round, lane-parallel) back to the first one that has published an inclusive prefix, and
+//      publishes its own.  lb[t] = flag << 62 | value, flag 1 = aggregate, 2 = inclusive prefix, 0 =
+//      not yet (lb zeroed before the launch; lb[nblocks] is the claim counter).
+//   3. Each warp's staged rows leave as the encoder's 8-byte rows at its offset (coalesced), then the
+//      padding.
+// Same keep decisions, counts, occupied cells, debug masks and row words as crop_count + scan +
+// crop_emit, which remain for K > kFusedMaxK (tests/test_parity_gpu.py checks the two bitwise equal).
+constexpr int kCropWarps = 8;
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbPre = 2ull << 62, kLbVal = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// keep_point with the x and y rows of the transform and of the box test as pairs (FFMA2/FADD2 with the
+// point's coordinates as broadcast operands): each element's arithmetic and rounding are keep_point's,
+// so the decisions are bitwise the same.  Rxy[j] = (R[j], R[3 + j]), txy = (t0, t1), loxy/hixy likewise.
+struct Xf2 {
+  float2 Rxy[3], txy, loxy, nhixy;  // nhixy = -(hi.x, hi.y)
+  float Rz[3], tz, loz, nhiz, eps2;
+};
+
+__device__ __forceinline__ bool keep_point_xy(const Xf2& Q, const float4& p) {
+  const float2 x = make_float2(p.x, p.x), y = make_float2(p.y, p.y), z = make_float2(p.z, p.z);
+  const float2 pxy = __ffma2_rn(Q.Rxy[0], x, __ffma2_rn(Q.Rxy[1], y, __ffma2_rn(Q.Rxy[2], z, Q.txy)));
+  const float pz = __fmaf_rn(Q.Rz[0], p.x, __fmaf_rn(Q.Rz[1], p.y, __fmaf_rn(Q.Rz[2], p.z, Q.tz)));
+  const float2 l = __fadd2_rn(Q.loxy, make_float2(-pxy.x, -pxy.y)), h = __fadd2_rn(pxy, Q.nhixy);
+  const float dx = fmaxf(fmaxf(l.x, h.x), 0.f), dy = fmaxf(fmaxf(l.y, h.y), 0.f);
+  const float dz = fmaxf(fmaxf(__fsub_rn(Q.loz, pz), __fadd_rn(pz, Q.nhiz)), 0.f);
+  return __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, __fmul_rn(dz, dz))) <= Q.eps2;
+}
+
+template <bool kOcc>
+__global__ void __launch_bounds__(32 * kCropWarps) crop_compact_kernel(ShapeTable T, Batch b, int words,
+                                                                      unsigned long long* __restrict__ lb,
+                                                                      int64_t nblocks) {
+  extern __shared__ uint32_t crop_list[];
+  __shared__ int64_t s_tile;
+  __shared__ uint32_t s_foot[kCropWarps];
+  __shared__ unsigned long long s_off[kCropWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int cap = (T.K + 31) & ~31;
+  uint32_t* list = crop_list + w * cap;  // each kept point in order: sorted index k | cell id << 16
+  const uint32_t list_sa = (uint32_t)__cvta_generic_to_shared(list);
+  if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(lb + nblocks, 1ull);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t g = tile * kCropWarps + w;
+  int own = 0, other = 0;
+  Xf X;
+  int n = 0, C = 0;
+  if (g < b.G && segment_load(b, g, own, other, X)) {
+    LOCC_CHECK((unsigned)own < (unsigned)T.S && (unsigned)other < (unsigned)T.S);
+    const float4 lo = T.lo[other], hi = T.hi[other];
+    Xf2 Q;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      Q.Rxy[j] = make_float2(X.R[j], X.R[3 + j]);
+      Q.Rz[j] = X.R[6 + j];
+    }
+    Q.txy = make_float2(X.t[0], X.t[1]);
+    Q.tz = X.t[2];
+    Q.loxy = make_float2(lo.x, lo.y);
+    Q.nhixy = make_float2(-hi.x, -hi.y);
+    Q.loz = lo.z;
+    Q.nhiz = -hi.z;
+    Q.eps2 = lo.w;
+    const float4* pts = T.pts + (int64_t)own * T.K;
+    const uint16_t* perm = T.perm + (int64_t)own * T.K;
+    uint32_t* mask = b.masks ? b.masks + g * words : nullptr;
+    int carry = -1;
+    for (int base0 = 0; base0 < T.K; base0 += 128) {
+      float4 pp[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = base0 + 32 * j + lane;
+        pp[j] = k < T.K ? pts[k] : make_float4(0.f, 0.f, 0.f, __int_as_float(-2));
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = base0 + 32 * j + lane;
+        const bool keep = k < T.K && keep_point_xy(Q, pp[j]);
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (m == 0) continue;
+        if (keep) {
+          const int idx = n + __popc(m & lanemask_lt());
+          LOCC_CHECK(idx < cap);
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(list_sa + 4u * idx),
+                       "r"((uint32_t)k | (uint32_t)__float_as_int(pp[j].w) << 16) : "memory");
+          if (mask) {
+            const int ck = perm[k];
+            atomicOr(mask + (ck >> 5), 1u << (ck & 31));
+          }
+        }
+        if (kOcc) {  // occupied cells: kept points whose cell differs from the previous kept point's
+          const int cell = __float_as_int(pp[j].w);
+          const unsigned before = m & lanemask_lt();
+          int prev = __shfl_sync(0xffffffffu, cell, before ? 31 - __clz(before) : lane);
+          if (!before) prev = carry;
+          C += __popc(__ballot_sync(0xffffffffu, keep && prev != cell));
+          carry = __shfl_sync(0xffffffffu, cell, 31 - __clz(m));
+        }
+        n += __popc(m);
+      }
+    }
+  }
+  if (lane == 0) s_foot[w] = (uint32_t)seg_rows(n);
+  __syncthreads();
+  // ---- 2. block scan + decoupled look-back over the blocks (warp 0)
+  if (w == 0) {
+    uint32_t f = lane < kCropWarps ? s_foot[lane] : 0u, x = f;
+#pragma unroll
+    for (int o = 1; o < kCropWarps; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    const unsigned long long agg = __shfl_sync(0xffffffffu, x, kCropWarps - 1);
+    if (lane == 0) st_relaxed_u64(lb + tile, (tile == 0 ? kLbPre : kLbAgg) | agg);
+    unsigned long long excl = 0;
+    if (tile > 0) {
+      for (int64_t hi = tile - 1;; hi -= 32) {
+        const int64_t i = hi - lane;
+        unsigned long long v = kLbPre;  // before block 0: prefix 0
+        if (i >= 0) {
+          v = ld_relaxed_u64(lb + i);
+          for (unsigned ns = 32; (v >> 62) == 0; ns = ns < 256 ? 2 * ns : ns) {
+            __nanosleep(ns);
+            v = ld_relaxed_u64(lb + i);
+          }
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        const int lim = pm ? __ffs(pm) - 1 : 31;  // lanes 0..lim: aggregates, then lim's inclusive prefix
+        unsigned long long y = lane <= lim ? (v & kLbVal) : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+        excl += y;
+        if (pm) break;
+      }
+      if (lane == 0) st_relaxed_u64(lb + tile, kLbPre | (excl + agg));
+    }
+    if (lane < kCropWarps) s_off[lane] = excl + x - f;
+    if (lane == 0 && (tile + 1) * kCropWarps >= b.G) b.offsets[b.G] = (int64_t)(excl + agg);
+  }
+  __syncthreads();
+  if (g >= b.G) return;
+  // ---- 3. rows out
+  const unsigned long long off = s_off[w], foot = s_foot[w];
+  if (lane == 0) {
+    b.offsets[g] = (int64_t)off;
+    b.counts[g] = n;
+    if (kOcc) b.occ[g] = C;
+    if (n) {
+      atomicAdd(&b.stats->kept_rows, (unsigned long long)n);
+      atomicAdd(&b.stats->nonempty_sides, 1ull);
+    }
+  }
+  LOCC_CHECK((int64_t)(off + foot) <= b.rows_cap);
+  __syncwarp();  // the list was written by every lane
+  uint2* out = b.rows + off;
+  const uint32_t segbits = (uint32_t)g << kRowSegShift;
+  // a row ends its cell iff the next kept row's cell differs (the last row ends cell and segment)
+  for (int i = lane; i < (int)foot; i += 32) {
+    uint2 r = make_uint2(segbits | kRowFlagPad, 0u);
+    if (i < n) {
+      const uint32_t e = list[i], nx = i + 1 < n ? list[i + 1] : 0xffff0000u;
+      r = make_uint2(segbits | ((e ^ nx) >> 16 ? kRowFlagCellEnd : 0) | (i == n - 1 ? kRowFlagSegEnd : 0), e & 0xffffu);
+    }
+    out[i] = r;
+  }
+}
+
 // ---------------------------------------------------------------- exclusive scan of segment footprints
 // Block size of the scan kernels: 256 threads, so that a scan block fits next to a persistent encoder
 // CTA (the overlapped crop pipeline).
@@ -415,6 +601,27 @@ cudaError_t launch_crop_emit(const ShapeTable& T, const Batch& b, cudaStream_t s
   if (b.G == 0) return cudaSuccess;
   const int64_t blocks = (b.G * 32 + 127) / 128;
   crop_emit_kernel<<<(unsigned)blocks, 128, 0, st>>>(T, b);
+  return cudaGetLastError();
+}
+
+size_t crop_compact_smem(int K) { return (size_t)kCropWarps * ((K + 31) & ~31) * sizeof(uint32_t); }
+
+size_t crop_compact_lb_words(int64_t G) { return (size_t)((G + kCropWarps - 1) / kCropWarps) + 1; }
+
+cudaError_t launch_crop_compact(const ShapeTable& T, const Batch& b, int words, unsigned long long* lb,
+                                cudaStream_t st) {
+  if (b.G == 0) return cudaMemsetAsync(b.offsets, 0, sizeof(int64_t), st);
+  if (T.K > kFusedMaxK) return cudaErrorInvalidValue;
+  const int64_t blocks = (b.G + kCropWarps - 1) / kCropWarps;
+  cudaError_t e = cudaMemsetAsync(lb, 0, sizeof(unsigned long long) * (size_t)(blocks + 1), st);
+  if (e != cudaSuccess) return e;
+  const size_t sm = crop_compact_smem(T.K);
+  e = b.want_occ ? smem_optin(crop_compact_kernel<true>, sm) : smem_optin(crop_compact_kernel<false>, sm);
+  if (e != cudaSuccess) return e;
+  if (b.want_occ)
+    crop_compact_kernel<true><<<(unsigned)blocks, 32 * kCropWarps, sm, st>>>(T, b, words, lb, blocks);
+  else
+    crop_compact_kernel<false><<<(unsigned)blocks, 32 * kCropWarps, sm, st>>>(T, b, words, lb, blocks);
   return cudaGetLastError();
 }
 

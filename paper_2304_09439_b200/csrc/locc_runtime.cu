@@ -3,7 +3,8 @@
 // Owns the per-context device state (parameters, shape table, scratch), validates inputs, splits a
 // query into sub-batches that bound the scratch memory, and launches the kernels of one pass of
 // the hot path on one stream:
-//   crop_count -> scan (3 launches) -> crop_emit -> encoder (fp32 or tcgen05) -> head
+//   segment_xf -> crop_compact (fused transform + crop + compaction; crop_count -> scan -> crop_emit
+//   for K > kFusedMaxK) -> encoder (fp32 or tcgen05) -> head
 // No exception crosses the ABI; every CUDA call is checked and mapped to a locc_status.
 #include <cuda_runtime.h>
 
@@ -139,11 +140,12 @@ struct locc_ctx {
   ShapeTable T{};
   // scratch for one sub-batch
   int64_t cap_B = 0;
+  bool force_2pass = false;  // LOCC_CROP_2PASS at creation: the two-pass crop at any K
   DevBuf trace;
   DevBuf in_pairs, in_poses, in_pairs2, in_poses2, counts, occ, offsets, scan_tmp, rows, pooled, stats, xf, kbits,
-      cellc;
+      cellc, lb;
   // second buffer set of the overlapped crop pipeline (sub-batches alternate between the two)
-  DevBuf counts2, offsets2, scan_tmp2, rows2, pooled2, xf2, kbits2, cellc2;
+  DevBuf counts2, offsets2, scan_tmp2, rows2, pooled2, xf2, kbits2, cellc2, lb2;
   int64_t cap_B2 = 0;
   DevBuf out_probs, out_labels, out_logits, out_kept, out_occ, out_masks, out_emb, out_grad;
   locc_stats last{};
@@ -408,6 +410,10 @@ locc_status upload_params(locc_ctx* c, const float* flat) {
   return LOCC_OK;
 }
 
+// The two-pass crop (crop_count -> scan -> crop_emit) for K > kFusedMaxK, or on request (LOCC_CROP_2PASS:
+// A/B timing and bitwise comparison of the fused kernel; read when the context is created).
+bool crop_2pass(const locc_ctx* c) { return c->T.K > kFusedMaxK || c->force_2pass; }
+
 // The second buffer set of the overlapped crop pipeline.
 locc_status ensure_scratch2(locc_ctx* c, int64_t B) {
   const int K = c->T.K;
@@ -415,12 +421,13 @@ locc_status ensure_scratch2(locc_ctx* c, int64_t B) {
   if (B > c->cap_B2) {
     CK(c->counts2.ensure(sizeof(int32_t) * G));
     CK(c->offsets2.ensure(sizeof(int64_t) * (G + 1)));
-    CK(c->scan_tmp2.ensure(sizeof(int64_t) * scan_tmp_elems(G)));
+    CK(c->lb2.ensure(sizeof(unsigned long long) * crop_compact_lb_words(G)));
+    if (crop_2pass(c)) CK(c->scan_tmp2.ensure(sizeof(int64_t) * scan_tmp_elems(G)));
     CK(c->rows2.ensure(sizeof(uint2) * (size_t)G * seg_rows(K)));
     CK(c->pooled2.ensure(sizeof(float) * (size_t)G * c->cfg.H));
     CK(c->cellc2.ensure(sizeof(int32_t) * G));
     CK(c->xf2.ensure(sizeof(float4) * 4 * G));
-    CK(c->kbits2.ensure(sizeof(uint32_t) * G * ((K + 31) / 32)));
+    if (crop_2pass(c)) CK(c->kbits2.ensure(sizeof(uint32_t) * G * ((K + 31) / 32)));
     c->cap_B2 = B;
   }
   return LOCC_OK;
@@ -436,10 +443,11 @@ locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks, bool need_gr
     CK(c->in_poses2.ensure(sizeof(float) * 14 * B));
     CK(c->counts.ensure(sizeof(int32_t) * G));
     CK(c->xf.ensure(sizeof(float4) * 4 * G));
-    CK(c->kbits.ensure(sizeof(uint32_t) * G * ((K + 31) / 32)));
+    if (crop_2pass(c)) CK(c->kbits.ensure(sizeof(uint32_t) * G * ((K + 31) / 32)));
+    CK(c->lb.ensure(sizeof(unsigned long long) * crop_compact_lb_words(G)));
     CK(c->occ.ensure(sizeof(int32_t) * G));
     CK(c->offsets.ensure(sizeof(int64_t) * (G + 1)));
-    CK(c->scan_tmp.ensure(sizeof(int64_t) * scan_tmp_elems(G)));
+    if (crop_2pass(c)) CK(c->scan_tmp.ensure(sizeof(int64_t) * scan_tmp_elems(G)));
     CK(c->rows.ensure(sizeof(uint2) * (size_t)G * seg_rows(K)));
     CK(c->pooled.ensure(sizeof(float) * (size_t)G * c->cfg.H));
     CK(c->cellc.ensure(sizeof(int32_t) * G));
@@ -455,6 +463,19 @@ locc_status ensure_scratch(locc_ctx* c, int64_t B, bool need_masks, bool need_gr
   if (need_masks) CK(c->out_masks.ensure(sizeof(uint32_t) * (size_t)G * ((K + 31) / 32)));
   if (need_grad) CK(c->out_grad.ensure(sizeof(float) * (size_t)14 * c->cap_B));
   return LOCC_OK;
+}
+
+// S1-S3 of one sub-batch on `st`: per-segment transforms, then the fused crop (crop_compact) or, for
+// K > kFusedMaxK (its shared-memory row list would not fit), crop_count -> scan -> crop_emit.
+cudaError_t launch_crop(locc_ctx* c, const Batch& b, int words, bool set2, cudaStream_t st) {
+  cudaError_t e = launch_segment_xf(c->T, b, st);
+  if (e != cudaSuccess) return e;
+  if (!crop_2pass(c))
+    return launch_crop_compact(c->T, b, words, (set2 ? c->lb2 : c->lb).as<unsigned long long>(), st);
+  if ((e = launch_crop_count(c->T, b, words, st)) != cudaSuccess) return e;
+  if ((e = launch_scan(b.counts, b.G, b.offsets, (set2 ? c->scan_tmp2 : c->scan_tmp).as<int64_t>(), st)) != cudaSuccess)
+    return e;
+  return launch_crop_emit(c->T, b, st);
 }
 
 // The predictor runs on the tensor cores (3xTF32, kernels_head_tc.cu) in LOCC_PREC_BF16 contexts; the
@@ -657,19 +678,13 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       cudaStream_t cs = c->crop_stream;
       if (subs >= 2) CK(cudaStreamWaitEvent(cs, c->ev_done[j], 0));  // sub-batch s - 2 done with set j
       if (c->timing && subs < 64) CK(cudaEventRecord(c->ev_cs[subs], cs));
-      CK(launch_segment_xf(c->T, b, cs));
-      CK(launch_crop_count(c->T, b, words, cs));
-      CK(launch_scan(b.counts, b.G, b.offsets, (set2 ? c->scan_tmp2 : c->scan_tmp).as<int64_t>(), cs));
-      CK(launch_crop_emit(c->T, b, cs));
+      CK(launch_crop(c, b, words, set2, cs));
       if (c->timing && subs < 64) CK(cudaEventRecord(c->ev_ce[subs], cs));
       CK(cudaEventRecord(c->ev_crop[j], cs));
       CK(cudaStreamWaitEvent(st, c->ev_crop[j], 0));
     } else {
       if (c->timing) CK(cudaEventRecord(c->crop_ev[subs], st));
-      CK(launch_segment_xf(c->T, b, st));
-      CK(launch_crop_count(c->T, b, words, st));
-      CK(launch_scan(b.counts, b.G, b.offsets, c->scan_tmp.as<int64_t>(), st));
-      CK(launch_crop_emit(c->T, b, st));
+      CK(launch_crop(c, b, words, false, st));
     }
     if (c->timing) CK(cudaEventRecord(c->enc_ev[2 * subs], st));
     if (c->cfg.precision == LOCC_PREC_BF16) {
@@ -706,7 +721,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
       CK(launch_head(c->P, b, d_probs, d_labels, d_logits, d_emb, d_grad, st));
     if (c->timing) CK(cudaEventRecord(c->head_ev[subs], st));
     if (overlap) CK(cudaEventRecord(c->ev_done[subs & 1], st));
-    launches += 8;
+    launches += crop_2pass(c) ? 8 : 4;
     }
     if (!dev) CK(cudaEventRecord(c->ev_free[subs & 1], st));  // the kernels are done with the inputs
     ++subs;
@@ -1089,6 +1104,7 @@ locc_status locc_create(const locc_config* cfg, locc_ctx** out) {
   c->cfg = *cfg;
   c->cfg.device_ids = nullptr;  // not owned (the group keeps its sub-contexts instead)
   c->device = dev;
+  c->force_2pass = getenv("LOCC_CROP_2PASS") != nullptr;
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) c->num_sms = prop.multiProcessorCount;
   cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);

@@ -331,6 +331,40 @@ def test_k_sweep_parity(locc_mod, oracle_mod, wflat, precision, K):
     assert (ref["kept"].sum(1) > 0).mean() > 0.8
 
 
+@pytest.mark.parametrize("K", [2048, 2049, 10000])
+def test_large_k_parity(locc_mod, oracle_mod, wflat, K):
+    """The fused crop at its largest K (kFusedMaxK = 2048: the shared-memory row lists of eight warps
+    are 64 KB) and the two-pass crop (crop_count -> scan -> crop_emit) that serves K above it."""
+    wl = ls.make_workload("C1", N=16, K=K, S=6)
+    ref = oracle_mod.query(wflat, wl.points, wl.pairs, wl.poses, bf16_emul=True)
+    with make_ctx(locc_mod, wflat, wl.points, 1) as ctx:
+        got = ctx.query_debug(wl.pairs, wl.poses)
+    assert_parity(got, ref, 1)
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_fused_crop_equals_two_pass(locc_mod, wflat, precision, monkeypatch):
+    """crop_compact (one kernel: crop, look-back offsets, rows) against crop_count -> scan -> crop_emit
+    (LOCC_CROP_2PASS, read at context creation): every output bitwise equal, over ragged sub-batches
+    (the overlapped crop pipeline's two buffer sets) and with the debug outputs (masks, C_s)."""
+    wl = ls.make_workload("C2", N=6000)
+    outs = []
+    for two_pass in (False, True):
+        if two_pass:
+            monkeypatch.setenv("LOCC_CROP_2PASS", "1")
+        with make_ctx(locc_mod, wflat, wl.points, precision, max_batch=1500) as ctx:
+            q = ctx.query(wl.pairs, wl.poses)
+            assert ctx.stats()["sub_batches"] == 4
+            d = ctx.query_debug(wl.pairs[:700], wl.poses[:700])
+        outs.append((q, d))
+        monkeypatch.delenv("LOCC_CROP_2PASS", raising=False)
+    (q0, d0), (q1, d1) = outs
+    for a, b in zip(q0, q1):
+        assert np.array_equal(a, b)
+    for k in d0:
+        assert np.array_equal(d0[k], d1[k]), k
+
+
 def test_c3_sharded_equals_unsharded_bf16(locc_mod, wflat):
     """pairs are independent, so the C3 batch split into 8 contiguous shards of
     ceil(N/8) pairs (each a separate query, as the 8 ranks of a multi-GPU run compute them) gives

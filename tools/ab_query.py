@@ -1,5 +1,6 @@
 """A/B timing of liblocc builds through the round-1 subset of the ABI (create, load weights, set
-shapes, locc_query on device buffers): C3 step time on the same box.  usage: python tools/ab_query.py a.so b.so ..."""
+shapes, locc_query on device buffers): C3 step time on the same box.  usage: python tools/ab_query.py a.so b.so ...
+A path may carry environment switches read at context creation: lib.so@LOCC_CROP_2PASS=1 (comma-separated)."""
 import ctypes as C
 import os
 import sys
@@ -16,7 +17,10 @@ class Cfg(C.Structure):
                 ("device_ids", C.c_void_p)]
 
 
-def run(path, pts, pairs, poses, flat, reps=4):
+def run(spec, pts, pairs, poses, flat, reps=4):
+    path, _, envs = spec.partition("@")
+    env = dict(e.split("=", 1) for e in envs.split(",") if e)
+    os.environ.update(env)
     L = C.CDLL(path)
     vp = C.c_void_p
     L.locc_create.argtypes = [C.POINTER(Cfg), C.POINTER(vp)]
@@ -48,6 +52,8 @@ def run(path, pts, pairs, poses, flat, reps=4):
         s.synchronize()
         ts.append(e0.elapsed_time(e1))
     L.locc_destroy(h)
+    for k in env:
+        del os.environ[k]
     return sum(ts) / len(ts), pr.cpu()
 
 
