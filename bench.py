@@ -431,7 +431,7 @@ def main():
         peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
         roof = {"bound": "alu", "unit": "TFLOP/s",
                 "peak_source": f"148 SM x 128 FP32 FMA/clk x 2 x {mhz:.0f} MHz (median SM clock under load)"}
-    traffic, crop_ncu = None, None
+    traffic, crop_ncu, tj = None, None, {}
     tp = os.path.join(ROOT, "profiles", "encoder_traffic.json")
     if os.path.exists(tp):
         try:
@@ -458,20 +458,28 @@ def main():
         hk["frac"] = hk["achieved"] / hk["peak"]
         roof["predictor"] = hk
     if st.get("crop_ms"):
-        # north_star's crop evidence: the algorithmic point bytes 2 K 12 B + 69 B of pair I/O per pair
-        # against HBM (the shape table itself is L2-resident, so this is an algorithmic rate)
+        # The crop (segment_xf + crop_compact) is issue-bound (ncu: DRAM ~12 %, L2 ~32 % of peak; the shape
+        # table is L2-resident): its roofline is warp-instruction issue, 4 per SM per cycle x 148 SMs at the
+        # median SM clock under load, with the ncu-counted warp instructions per pair of the round's
+        # capture.  north_star's HBM view (algorithmic point bytes 2 K 12 B + 69 B per pair per crop time)
+        # and the measured DRAM bytes per pair ride along.
         hbm = peaks.get("hbm_gbs", 6546.6)
         cb = (2 * a.K * 12 + 69) * N
-        roof["crop"] = {"bound": "hbm", "kernels": "segment_xf + crop_count + scan + crop_emit",
-                        "note": "timed serialised; in the measured steps it overlaps the encoder",
-                        "ms_per_step": st["crop_ms"], "unit": "GB/s",
-                        "achieved": cb / (st["crop_ms"] / 1e3) / 1e9, "peak": hbm,
-                        "frac": cb / (st["crop_ms"] / 1e3) / 1e9 / hbm,
+        crop_s = st["crop_ms"] / 1e3
+        ci = tj.get("crop_warp_instructions_per_pair")
+        issue_peak = 148 * 4 * mhz_load * 1e6 / 1e9  # G warp-instructions / s
+        roof["crop"] = {"bound": "alu", "kernels": "segment_xf + crop_compact (one launch: crop, look-back, rows)",
+                        "note": "timed with the crop serialised (LOCC_NO_OVERLAP); its blocks cannot run beside the "
+                                "encoder's CTAs, so in the measured steps its time is exposed",
+                        "ms_per_step": st["crop_ms"], "unit": "G warp-instructions/s",
+                        "achieved": (ci * N / crop_s / 1e9) if ci else None, "peak": issue_peak,
+                        "peak_source": f"148 SM x 4 schedulers x 1 warp-instruction/clk x {mhz_load:.0f} MHz",
+                        "frac": (ci * N / crop_s / 1e9 / issue_peak) if ci else None,
+                        "warp_instructions_per_pair_ncu": ci,
+                        "point_bytes_rate_gbs": cb / crop_s / 1e9, "point_bytes_frac_of_hbm": cb / crop_s / 1e9 / hbm,
                         "algorithmic_bytes_per_pair": 2 * a.K * 12 + 69,
-                        # DRAM bytes per pair of crop_count + crop_emit from ncu --set full (the
-                        # row-buffer write dominates; the point reads hit L2)
                         "dram_bytes_per_pair_ncu": crop_ncu,
-                        "dram_bytes_source": "profiles/encoder_traffic.json (from the round's ncu capture)"}
+                        "ncu_source": "profiles/encoder_traffic.json (from the round's ncu capture)"}
 
     line = {"metric": METRIC, "value": world * N / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

@@ -54,13 +54,14 @@ def launches(path):
 
 def main(tag="r1"):
     L = launches(os.path.join(OUT, f"launches_{tag}.csv"))
-    # one step = launches from the first crop_count to the head before the next crop_count
+    # one sub-batch = the launches up to and including the first predictor
+    nsub = next((i + 1 for i, (name, _) in enumerate(L) if "head" in name), 8)
     step, per = {}, {}
-    for name, t in L[:8]:
+    for name, t in L[:nsub]:
         step[name] = step.get(name, 0.0) + t
     tot = sum(step.values())
     kern = {}
-    for k in ("encoder_tc", "crop_count", "crop_emit", "head_tc", "head_tile"):
+    for k in ("encoder_tc", "crop_compact", "crop_count", "crop_emit", "head_tc", "head_tile"):
         p = os.path.join(OUT, f"raw_{tag}_{k}.csv")
         if os.path.exists(p):
             kern[k] = raw(p)
@@ -69,7 +70,7 @@ def main(tag="r1"):
              "the 1,048,576-pair step is four of these).  ncu 2025, `--clock-control none`, 1 x B200.", "",
              "## Launch list of one sub-batch (gpu__time_duration, serialised, cold cache)", "",
              "| kernel | ms | share |", "|---|---|---|"]
-    for name, t in L[:8]:
+    for name, t in L[:nsub]:
         lines.append(f"| {name} | {t * 1e3:.3f} | {100 * t / tot:.1f}% |")
     lines += ["", f"Total {tot * 1e3:.2f} ms.", "", "## `--set full` per kernel (one launch)", "",
               "| kernel | ms | DRAM read GB | DRAM write GB | tensor pipe active | SM throughput | regs | SM clock GHz |",
@@ -81,16 +82,18 @@ def main(tag="r1"):
     md = "\n".join(lines) + "\n"
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     open(os.path.join(ROOT, "profiles", f"{tag}_summary.md"), "w").write(md)
-    js = {"tag": tag, "launches_one_subbatch": [{"kernel": n, "ms": t * 1e3} for n, t in L[:8]], "kernels": kern}
+    js = {"tag": tag, "launches_one_subbatch": [{"kernel": n, "ms": t * 1e3} for n, t in L[:nsub]], "kernels": kern}
     json.dump(js, open(os.path.join(ROOT, "profiles", f"{tag}_summary.json"), "w"), indent=1)
     if "encoder_tc" in kern:
         e = kern["encoder_tc"]
         traffic = {"bf16": e.get("dram_read", 0) + e.get("dram_write", 0),
                    "source": f"profiles/{tag}_summary.json (ncu --set full, one 262,144-pair launch)",
                    "pairs_per_launch": 262144}
-        cr = [kern[k] for k in ("crop_count", "crop_emit") if k in kern]
-        if cr:  # the crop's measured DRAM bytes per pair (crop_count + crop_emit, one sub-batch)
+        cr = [kern[k] for k in ("crop_compact", "crop_count", "crop_emit") if k in kern]
+        if cr:  # the crop's measured DRAM bytes and warp instructions per pair (one sub-batch)
             traffic["crop_bytes_per_pair"] = sum(k.get("dram_read", 0) + k.get("dram_write", 0) for k in cr) / 262144
+            traffic["crop_warp_instructions_per_pair"] = sum(k.get("inst_executed", 0) for k in cr) / 262144
+            traffic["crop_kernels"] = [k for k in ("crop_compact", "crop_count", "crop_emit") if k in kern]
         json.dump(traffic, open(os.path.join(ROOT, "profiles", "encoder_traffic.json"), "w"), indent=1)
     print(md)
 
