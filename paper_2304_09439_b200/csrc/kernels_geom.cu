@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(256) crop_emit_kernel(ShapeTable T, Batch b) {
   }
   // padding up to the next multiple of kSegAlign rows
   const int pad_end = (int)seg_rows(n);
-  if (n + lane < pad_end) out[n + lane] = make_uint2(segbits | kRowFlagPad, 0u);
+  for (int i = n + lane; i < pad_end; i += 32) out[i] = make_uint2(segbits | kRowFlagPad, 0u);
 }
 
 // ---------------------------------------------------------------- S2-S3 fused: transform + crop + compaction

@@ -252,6 +252,34 @@ def test_invariances(locc_mod, c1, wflat, precision, det):
     assert_invariant(base, pp, precision, keys=("probs", "logits", "kept", "occ", "emb"), det=det)
 
 
+def test_batch_composition_bitwise_bf16_deterministic(locc_mod, wflat):
+    """A deterministic bf16 context at C2 scale: every pair's outputs are bitwise the same alone, in a
+    shuffled batch, in a batch tail, in ragged sub-batches (both crop buffer sets) — its segments land at
+    different tile positions in each."""
+    wl = ls.make_workload("C2", N=3000)
+    idx = (0, 7, 1500, 2999)
+    with make_ctx(locc_mod, wflat, wl.points, 1) as ctx:
+        ctx.set_deterministic(True)
+        base = ctx.query(wl.pairs, wl.poses)
+        perm = np.random.default_rng(5).permutation(len(wl.pairs))
+        pm = ctx.query(wl.pairs[perm], wl.poses[perm])
+        tail = ctx.query(wl.pairs[1234:], wl.poses[1234:])
+        singles = [ctx.query(wl.pairs[i:i + 1], wl.poses[i:i + 1]) for i in idx]
+    with make_ctx(locc_mod, wflat, wl.points, 1, max_batch=701) as ctx:
+        ctx.set_deterministic(True)
+        sub = ctx.query(wl.pairs, wl.poses)
+        assert ctx.stats()["sub_batches"] == 5
+    for a, b in zip(base, sub):
+        assert np.array_equal(a, b)
+    for a, b in zip(base, pm):
+        assert np.array_equal(a[perm], b)
+    for a, b in zip(base, tail):
+        assert np.array_equal(a[1234:], b)
+    for i, s in zip(idx, singles):
+        for a, b in zip(base, s):
+            assert np.array_equal(a[i:i + 1], b)
+
+
 # ----------------------------------------------------------------------------- full sizes
 @pytest.mark.parametrize("precision", [0, 1])
 def test_c2_sampled_parity(locc_mod, oracle_mod, wflat, precision):
