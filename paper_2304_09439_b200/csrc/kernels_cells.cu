@@ -38,7 +38,7 @@ using tc::ffma2;
 // One block per shape, thread f = feature f.  The shape's points are cell-sorted (S0), so the cell-wise
 // max is a running max closed at each cell change; ReLU(max + b3) = max of ReLU(acc + b3).  Empty cells
 // stay 0 (the buffer is cleared first).
-__global__ void __launch_bounds__(256) grid_encode_kernel(DevParams P, ShapeTable T, int M, float* __restrict__ G) {
+__global__ void __launch_bounds__(256, 2) grid_encode_kernel(DevParams P, ShapeTable T, int M, float* __restrict__ G) {
   extern __shared__ float4 smem4[];
   float4* rows_s = smem4;                                // [64]
   float* hT = reinterpret_cast<float*>(smem4 + kMlpTR);  // [H][kMlpLDH]
@@ -46,10 +46,9 @@ __global__ void __launch_bounds__(256) grid_encode_kernel(DevParams P, ShapeTabl
   const int H = P.H, f = threadIdx.x, s = blockIdx.x;
   const bool act = f < H;
   float4 w1 = make_float4(0.f, 0.f, 0.f, 0.f);
-  float b2 = 0.f, b3 = 0.f;
+  float b3 = 0.f;
   if (act) {
     w1 = P.w1b[f];
-    b2 = P.b2[f];
     b3 = P.b3[f];
   }
   const float4* pts = T.pts + (int64_t)s * T.K;
@@ -60,10 +59,10 @@ __global__ void __launch_bounds__(256) grid_encode_kernel(DevParams P, ShapeTabl
     if (f < kMlpTR) rows_s[f] = f < nr ? pts[t0 + f] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
     if (f == 0) next_cell = t0 + kMlpTR < T.K ? __float_as_int(pts[t0 + kMlpTR].w) : -1;
     __syncthreads();
-    float acc[kMlpTR];
-    point_mlp_tile(P, rows_s, hT, acc, w1, b2, f, act);
+    point_mlp_tile(P, rows_s, hT, w1, f, act);
+    const float* acc = hT + f * kMlpLDH;  // feature f's layer-3 accumulators of the tile's rows
     if (act) {
-#pragma unroll
+#pragma unroll 4
       for (int r = 0; r < kMlpTR; ++r) {
         if (r < nr) {
           run_max = fmaxf(run_max, acc[r]);
@@ -416,7 +415,7 @@ __global__ void __launch_bounds__(256) cells_select_kernel(ShapeTable T, CellsTa
 }  // namespace
 
 cudaError_t launch_grid_encode(const DevParams& P, const ShapeTable& T, int M, float* G, cudaStream_t st) {
-  const size_t sm = sizeof(float4) * kMlpTR + sizeof(float) * 256 * kMlpLDH;
+  const size_t sm = kMlpSmemBytes;
   const cudaError_t attr = smem_optin(grid_encode_kernel, sm);
   if (attr != cudaSuccess) return attr;
   cudaError_t e = cudaMemsetAsync(G, 0, sizeof(float) * (size_t)T.S * M * M * M * P.H, st);

@@ -22,7 +22,7 @@ namespace {
 constexpr int TR = kMlpTR;
 constexpr int LDH = kMlpLDH;
 
-__global__ void __launch_bounds__(256) encoder_f32_kernel(DevParams P, Batch b) {
+__global__ void __launch_bounds__(256, 2) encoder_f32_kernel(DevParams P, Batch b) {
   extern __shared__ float4 smem4[];
   float4* rows_s = smem4;                        // [TR]
   float* hT = reinterpret_cast<float*>(smem4 + TR);  // [H][LDH]
@@ -35,10 +35,9 @@ __global__ void __launch_bounds__(256) encoder_f32_kernel(DevParams P, Batch b) 
   if (r0 == r1) return;
 
   float4 w1 = make_float4(0.f, 0.f, 0.f, 0.f);
-  float b2 = 0.f, b3 = 0.f;
+  float b3 = 0.f;
   if (act) {
     w1 = P.w1b[f];
-    b2 = P.b2[f];
     b3 = P.b3[f];
   }
   float run_max = -INFINITY, run_sum = 0.f;
@@ -60,11 +59,11 @@ __global__ void __launch_bounds__(256) encoder_f32_kernel(DevParams P, Batch b) 
       rows_s[f] = v;
     }
     __syncthreads();
-    float acc[TR];
-    point_mlp_tile(P, rows_s, hT, acc, w1, b2, f, act);
+    point_mlp_tile(P, rows_s, hT, w1, f, act);
+    const float* acc = hT + f * LDH;  // feature f's layer-3 accumulators of the tile's rows
     // S6-S7: segmented cell max + occupied-cell sum over the tile's rows (row flags are uniform)
     if (act) {
-#pragma unroll
+#pragma unroll 4
       for (int r = 0; r < TR; ++r) {
         const uint32_t fl = __float_as_uint(rows_s[r].w);
         if (r < nr && !(fl & kRowFlagPad)) {
@@ -93,8 +92,8 @@ __global__ void __launch_bounds__(256) encoder_f32_kernel(DevParams P, Batch b) 
 cudaError_t launch_encoder_f32(const DevParams& P, const Batch& b, cudaStream_t st) {
   const int64_t chunks = (b.G + kSegPerChunk - 1) / kSegPerChunk;
   if (chunks == 0) return cudaSuccess;
-  const size_t sm = sizeof(float4) * TR + sizeof(float) * (size_t)P.H * LDH;
-  const cudaError_t attr = smem_optin(encoder_f32_kernel, sizeof(float4) * TR + sizeof(float) * 256 * LDH);
+  const size_t sm = kMlpSmemBytes;
+  const cudaError_t attr = smem_optin(encoder_f32_kernel, sm);
   if (attr != cudaSuccess) return attr;
   encoder_f32_kernel<<<(unsigned)chunks, 256, sm, st>>>(P, b);
   return cudaGetLastError();
