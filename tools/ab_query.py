@@ -29,7 +29,7 @@ def run(spec, pts, pairs, poses, flat, reps=4):
     L.locc_query.argtypes = [vp, vp, vp, C.c_int64, vp, vp, vp, vp]
     L.locc_destroy.argtypes = [vp]
     h = vp()
-    cfg = Cfg(6, 256, 64, 1, 0, 0, 0, None)
+    cfg = Cfg(6, 256, 64, 1, 0, 0, int(os.environ.get("AB_MAX_BATCH", "0")), None)  # AB_MAX_BATCH: sub-batch size
     assert L.locc_create(C.byref(cfg), C.byref(h)) == 0
     assert L.locc_load_weights_mem(h, flat.ctypes.data, flat.size) == 0
     assert L.locc_set_shapes(h, pts.ctypes.data, pts.shape[0], pts.shape[1]) == 0
