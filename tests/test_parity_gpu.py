@@ -280,6 +280,20 @@ def test_batch_composition_bitwise_bf16_deterministic(locc_mod, wflat):
             assert np.array_equal(a[i:i + 1], b)
 
 
+@pytest.mark.parametrize("H,F", [(96, 64), (160, 32)])
+def test_fp32_other_widths(locc_mod, oracle_mod, H, F):
+    """The fp32 crop path at point-MLP widths other than 256 (the register-tiled GEMM's partial feature
+    groups, point_mlp.cuh) and another F (the generic predictor) against the oracle."""
+    w = ls.flatten_weights(ls.make_weights("spread", H, F, calib=ls.load_calibration()), H, F)
+    wl = ls.make_workload("C1", N=40, S=8)
+    ref = oracle_mod.query(w, wl.points, wl.pairs, wl.poses, H=H, F=F)
+    with locc_mod.Locc(M=6, H=H, F=F, precision=0, device=0) as ctx:
+        ctx.load_weights_mem(w)
+        ctx.set_shapes(wl.points)
+        got = ctx.query_debug(wl.pairs, wl.poses)
+    assert_parity(got, ref, 0)
+
+
 # ----------------------------------------------------------------------------- full sizes
 @pytest.mark.parametrize("precision", [0, 1])
 def test_c2_sampled_parity(locc_mod, oracle_mod, wflat, precision):
