@@ -19,7 +19,7 @@ constexpr int kRowSegShift = 3;    // flags word = (segment << 3) | pad << 2 | s
 constexpr int kSegAlign = 16;
 __host__ __device__ constexpr int64_t seg_rows(int64_t kept) { return (kept + kSegAlign - 1) / kSegAlign * kSegAlign; }
 
-// Checked build (-DLOCC_CHECKED=1, `tools/checked_run.sh`): device-side bounds checks on the hot
+// Checked build (-DLOCC_CHECKED=1, `tools/checked_run.py`): device-side bounds checks on the hot
 // kernels' global-memory indices — this pool's substitute for compute-sanitizer memcheck, which is
 // closed here.  A failed check prints the condition and traps (the call returns LOCC_E_CUDA).
 #ifndef LOCC_CHECKED

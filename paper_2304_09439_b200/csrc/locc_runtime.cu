@@ -633,7 +633,7 @@ locc_status run_query(locc_ctx* c, const int32_t* pairs, const float* poses, int
     b.rows = (set2 ? c->rows2 : c->rows).as<uint2>();
     b.rows_cap = 2 * (set2 ? c->cap_B2 : c->cap_B) * seg_rows(c->T.K);
 #if LOCC_CHECKED
-    if (getenv("LOCC_CHECK_SELFTEST")) b.rows_cap = 1;  // tools/checked_run.sh: a check must fire
+    if (getenv("LOCC_CHECK_SELFTEST")) b.rows_cap = 1;  // tools/checked_run.py: a check must fire
 #endif
     b.pts = c->T.pts;
     b.K = c->T.K;
