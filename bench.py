@@ -15,7 +15,7 @@ over ranks; value = all pairs / that time.
 
 The N = 1 line also carries the BASELINE.json config table (`sweep`: C1/C2 in fp32 and bf16, C5's
 K x N grid with its roofline fractions, C4's closed-loop times, the oracle at 1 and all host threads)
-and the deterministic bf16 mode's throughput (`deterministic`).
+and the opt-in fast bf16 walk's throughput (`fast_walk`; the headline is the default deterministic walk).
 """
 import argparse
 import json
@@ -231,9 +231,8 @@ def run_sweep(a, locc, torch, stream, flush, peaks):
     peak_s = peaks.get("bf16_tflops_sustained", 1400.0)
     peak_b = peaks.get("bf16_tflops", 1640.0)
 
-    def one(points, pairs, poses, prec, det=False):
+    def one(points, pairs, poses, prec):
         ctx = locc.Locc(precision=prec, device=torch.cuda.current_device())
-        ctx.set_deterministic(det)
         ctx.load_weights_mem(flat)
         ctx.set_shapes(points)
         n = len(pairs)
@@ -686,14 +685,16 @@ def main():
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(pts, pairs, poses, flat)
     if world == 1:
-        # the deterministic bf16 mode (locc_set_deterministic: bitwise batch-composition invariance)
+        # the headline is the default (deterministic) bf16 walk; the opt-in fast walk (locc_set_
+        # deterministic(ctx, 0): ~5 % faster, batch composition moves probabilities by <= 1e-5)
         if prec == locc.LOCC_PREC_BF16:
-            ctx.set_deterministic(True)
-            dms = time_query(ctx, torch, stream, d_pairs, d_poses, d_probs, d_labels, reps=a.steps,
-                             warm=1, flush=flush)
             ctx.set_deterministic(False)
-            line["deterministic"] = {"value": N / (dms / 1e3), "unit": UNIT, "ms_per_step": dms,
-                                     "api": "locc_set_deterministic(ctx, 1)"}
+            fms = time_query(ctx, torch, stream, d_pairs, d_poses, d_probs, d_labels, reps=a.steps,
+                             warm=1, flush=flush)
+            ctx.set_deterministic(True)
+            line["fast_walk"] = {"value": N / (fms / 1e3), "unit": UNIT, "ms_per_step": fms,
+                                 "api": "locc_set_deterministic(ctx, 0)",
+                                 "note": "not bitwise invariant to batch composition (<= 1e-5 in probability)"}
         if not a.no_sweep:
             line["sweep"] = run_sweep(a, locc, torch, stream, flush, peaks)
     if rank == 0:

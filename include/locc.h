@@ -276,12 +276,12 @@ locc_status locc_query_allgather(locc_ctx* ctx, const int32_t* pairs, const floa
 /* Switch the encoder precision of an existing context (LOCC_PREC_FP32 / LOCC_PREC_BF16). */
 locc_status locc_set_precision(locc_ctx* ctx, int32_t precision);
 
-/* Bitwise reproducibility of LOCC_PREC_BF16 contexts (reading Q24).  0 (default): the
- * tensor-core encoder's layer-3 epilogue sums a segment's cell values in an order that depends on
- * where the segment falls in its 128-row part, so batch composition (N, pair order, sub-batching,
- * GPU count) can move a probability by a few fp32 ulps (<= 1e-5).  1: an order fixed by the segment's
- * own rows (16-row blocks), so every output is bitwise independent of batch composition; the
- * epilogue costs more.  FP32 contexts are always bitwise reproducible.
+/* Bitwise reproducibility of LOCC_PREC_BF16 contexts (reading Q24).  1 (default): the
+ * tensor-core encoder's layer-3 epilogue sums a segment's cell values in an order fixed by the
+ * segment's own rows (16-row blocks), so every output is bitwise independent of batch composition
+ * (N, pair order, sub-batching, GPU count).  0: a faster walk (~5 % at C3) whose order
+ * depends on where the segment falls in its 128-row part, so batch composition can move a probability
+ * by a few fp32 ulps (<= 1e-5).  FP32 contexts are always bitwise reproducible.
  * Errors: INVALID_ARG (null). */
 locc_status locc_set_deterministic(locc_ctx* ctx, int32_t enabled);
 

@@ -129,7 +129,7 @@ struct locc_ctx {
   std::vector<cudaEvent_t> head_ev;  // per sub-batch predictor stop (its start = the encoder stop)
   std::vector<cudaEvent_t> crop_ev;  // per sub-batch crop start (its stop = the encoder start)
   bool timing = false;
-  bool deterministic = false;  // bf16 encoder: the deterministic layer-3 walk (locc_set_deterministic)
+  bool deterministic = true;  // bf16 encoder: the deterministic layer-3 walk (default; locc_set_deterministic)
   bool has_weights = false, has_shapes = false;
   // parameters
   DevBuf params, tc_img, head_tc_img, grid_tc_img;

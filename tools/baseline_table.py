@@ -21,7 +21,7 @@ def main(path=os.path.join(ROOT, "profiles", "r2_bench_line.json")):
     print(f"| C2 16K pairs | 1 | fp32 / bf16 | {c2['bf16']['kept_rows_per_pair']:.0f} | {c2['fp32']['checks_per_s']:,.0f} / "
           f"{c2['bf16']['checks_per_s']:,.0f} | — / {pct(c2['bf16'])} | same |")
     print(f"| C3 1M pairs | 1 | bf16 | {sw['C5']['K=1500']['1048576']['kept_rows_per_pair']:.0f} | **{d['value']:,.0f}** (e2e from "
-          f"host buffers {d['e2e']['value']:,.0f}; deterministic mode {d['deterministic']['value']:,.0f}) | "
+          f"host buffers {d['e2e']['value']:,.0f}; " + (f"opt-in fast walk {d['fast_walk']['value']:,.0f}" if 'fast_walk' in d else f"deterministic mode {d['deterministic']['value']:,.0f}") + ") | "
           f"**{100 * d['roofline']['frac']:.0f} %** (encoder kernel) | same ({oc['sample'].split(' pairs')[0].replace('first ', '')}-pair sample) |")
     c4 = "; ".join(f"{int(e):,}: {v['ms_per_dt_encode_once']:.2f} / {v['ms_per_dt_crop_bf16']:.1f}" for e, v in sw["C4"].items())
     print(f"| C4 sim step, E envs × 3 pairs, 4 substeps per Δt | 1 | bf16 | — | ms per Δt (encode-once / crop detector): {c4} | — | — |")
